@@ -1,0 +1,214 @@
+/*
+ * tqd.h -- C ABI of the B200-native sharded state-vector forward + adjoint
+ * gradient path (arXiv 2511.19291, "TorchQuantumDistributed").
+ *
+ * The library (paper_2511_19291_b200/libtqd.so) applies a gate circuit to a
+ * complex 2^n state vector sharded over GPUs, computes Pauli expectation values,
+ * and computes their parameter gradients with the invertible reverse sweep.
+ * Every step runs in hand-written CUDA kernels for sm_100a plus NCCL for the
+ * qubit-remap exchange; there is no CPU fallback.
+ *
+ * Citations are PAPER.md line numbers with the
+ * section / algorithm / equation they fall in.  Readings of ambiguous passages
+ * (R1..R20) are listed in DESIGN.md.
+ *
+ * Conventions
+ *   - Status: every call returns int; 0 = TQD_OK, < 0 = error (enum below).
+ *     The message of the last error of the calling thread is returned by
+ *     tqd_last_error().  After a CUDA or NCCL error the context is poisoned:
+ *     every later call on it returns TQD_ERR_STATE.
+ *   - Qubits: logical qubit q in [0, n).  Canonical amplitude index: qubit q is
+ *     bit (n-1-q) (MSB-first, reading R1; qubit q is tensor
+ *     dimension q of X in C^{2x...x2}, row-major).
+ *   - Pauli masks: bit q of x_mask / z_mask <-> logical qubit q;
+ *     (x,z) = (0,0) I, (1,0) X, (0,1) Z, (1,1) Y.
+ *   - Ownership: handles are library-owned and freed with *_destroy / *_free.
+ *     Input arrays are copied and never retained.  Output arrays are
+ *     caller-owned HOST memory.  A caller-provided device buffer (dev_buf) stays
+ *     owned by the caller and must outlive the state.  The CUDA stream is
+ *     borrowed.
+ *   - Collectives: tqd_state_init, tqd_expval, tqd_adjoint_grad and
+ *     tqd_get_amplitudes are collective over the context's ranks: every rank
+ *     calls them in the same order with the same arguments (and records the
+ *     same gates).
+ *   - Laziness: tqd_apply_gate only records the gate on the state's tape (no
+ *     device work, like the deferred MoveDim^{-1} of Alg. 2).
+ *     Execution happens in tqd_expval, tqd_adjoint_grad, tqd_get_amplitudes.
+ */
+#ifndef TQD_ABI_H_
+#define TQD_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tqd_ctx tqd_ctx;     /* one per process = one GPU; owns NCCL comm + stream */
+typedef struct tqd_state tqd_state; /* sharded state + gate tape + qubit map pi          */
+
+/* Amplitude precision. Complex64 = interleaved float (re, im); complex128 = double. */
+typedef enum { TQD_C64 = 0, TQD_C128 = 1 } tqd_dtype;
+
+/* Gate kinds ("universal gate set using single-qubit Pauli rotation
+ * gates and the two-qubit CNOT", plus the fixed gates and custom unitaries it
+ * allows; north star adds CZ and U3).
+ *   1q fixed:  I X Y Z H S SDG T TDG                  (textbook matrices)
+ *   2q fixed:  CNOT (wires = [control, target], R3), CZ, SWAP
+ *   custom:    MAT1 (2x2), MAT2 (4x4): row-major (re, im) doubles; must be
+ *              unitary ("users should take care to ensure they are
+ *              unitary"): ||M M^dag - I||_max <= 1e-10 (C128) / 1e-5 (C64)
+ *   rotation:  RX RY RZ = exp(-i theta P / 2) (R4), 1 parameter
+ *              U3(theta, phi, lambda) = [[c, -e^{il} s], [e^{ip} s, e^{i(p+l)} c]]
+ *              (R5), 3 parameters.
+ * For 2q gates wires[0] is the more significant bit of the 4x4 index (R2). */
+typedef enum {
+    TQD_I = 0, TQD_X, TQD_Y, TQD_Z, TQD_H, TQD_S, TQD_SDG, TQD_T, TQD_TDG,
+    TQD_CNOT, TQD_CZ, TQD_SWAP,
+    TQD_MAT1, TQD_MAT2,
+    TQD_RX, TQD_RY, TQD_RZ, TQD_U3,
+    TQD_NUM_GATES
+} tqd_gate;
+
+enum {
+    TQD_OK = 0,
+    TQD_ERR_ARG = -1,         /* NULL pointer, bad wire / arity / parameter count / size */
+    TQD_ERR_QUBITS = -2,      /* n < log2(world) + 2, n > 62, or shard too large */
+    TQD_ERR_WORLD = -3,       /* world not a power of two, rank out of range */
+    TQD_ERR_NOT_UNITARY = -4, /* MAT1 / MAT2 fails the unitarity tolerance */
+    TQD_ERR_OOM = -5,         /* device allocation failed / dev_buf too small */
+    TQD_ERR_CUDA = -6,        /* CUDA runtime error (context poisoned) */
+    TQD_ERR_NCCL = -7,        /* NCCL error (context poisoned) */
+    TQD_ERR_UNSUPPORTED = -8, /* valid request this build does not implement */
+    TQD_ERR_STATE = -9        /* poisoned context, consumed state, wrong call order */
+};
+
+/* Options (tqd_state_set_option).  Defaults are tuned for B200. */
+typedef enum {
+    TQD_OPT_TILE_QUBITS = 0,  /* k: amplitudes per fused-sweep tile = 2^k (9..14; default 12) */
+    TQD_OPT_SMALL_MAX = 1,    /* n_loc <= this runs the single-CTA whole-state kernel (default 10) */
+    TQD_OPT_PROFILE = 2,      /* 1: time every kernel with CUDA events (see tqd_metrics) */
+    TQD_OPT_GRID_CTAS = 3,    /* persistent CTAs per launch (0 = auto: SMs x resident CTAs) */
+    TQD_OPT_USE_GRAPH = 4     /* 1: replay cached plans as CUDA graphs (default 0)      */
+} tqd_option;
+
+/* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.
+ * Byte counts are ALGORITHMIC (what the method must move, DESIGN.md section
+ * "Algorithmic bytes"), not DRAM counters. */
+typedef struct tqd_metrics {
+    uint64_t fwd_sweeps;        /* fused forward sweep launches                      */
+    uint64_t bwd_sweeps;        /* fused adjoint sweep launches                      */
+    uint64_t remaps;            /* global<->local qubit remaps (all-to-all rounds)   */
+    uint64_t gates_applied;     /* gates applied in forward sweeps                   */
+    uint64_t gates_unapplied;   /* gates un-applied in adjoint sweeps                */
+    uint64_t hbm_bytes;         /* algorithmic HBM bytes of all kernels              */
+    uint64_t a2a_bytes;         /* bytes this rank sent to other ranks               */
+    double   fwd_sweep_ms;      /* summed kernel time of forward sweeps (PROFILE=1)  */
+    double   bwd_sweep_ms;      /* summed kernel time of adjoint sweeps (PROFILE=1)  */
+    double   other_ms;          /* init / expval / lambda-init / gather (PROFILE=1)  */
+    double   a2a_ms;            /* remap exchange time (PROFILE=1)                   */
+    uint64_t fwd_sweep_bytes;   /* algorithmic bytes of forward sweeps               */
+    uint64_t bwd_sweep_bytes;   /* algorithmic bytes of adjoint sweeps               */
+    uint64_t peak_device_bytes; /* state buffers + scratch held by this state        */
+    uint64_t kernel_launches;   /* library kernels launched                          */
+} tqd_metrics;
+
+/* --- context ------------------------------------------------------------- */
+
+/* Writes a 128-byte NCCL unique id into out128 (call on rank 0, broadcast the
+ * bytes to the other ranks by any means, e.g. torch.distributed). */
+int tqd_nccl_unique_id(void *out128);
+
+/* Create the per-process context.  world must be a power of two (sharding
+ * log2 d qubits over d accelerators, §4.2); 0 <= rank < world.
+ * nccl_id: the 128 bytes from tqd_nccl_unique_id (ignored, may be NULL, iff
+ * world == 1).  cuda_stream: a cudaStream_t to run on (borrowed) or NULL for
+ * a library-created stream.  Collective over the world when world > 1. */
+int tqd_ctx_create(int world, int rank, int cuda_device, const void *nccl_id,
+                   void *cuda_stream, tqd_ctx **out);
+int tqd_ctx_destroy(tqd_ctx *ctx);
+
+/* --- state --------------------------------------------------------------- */
+
+/* Device bytes per rank for an n-qubit state of dtype dt on `world` ranks:
+ * the shard psi (2^{n - log2 world} amplitudes), plus lambda for the adjoint
+ * when with_adjoint != 0, plus the remap staging when world > 1. */
+int tqd_state_bytes(int n_qubits, tqd_dtype dt, int world, int with_adjoint, size_t *bytes_per_rank);
+
+/* Allocate and initialise |0...0> (reset_states):
+ * amplitude 1 at canonical index 0 on the rank that owns it.  The qubit map
+ * pi starts as the identity: logical qubit q at physical bit n-1-q, so logical
+ * qubits 0..g-1 (g = log2 world) are the sharded ("global") ones.
+ * dev_buf: NULL = the library allocates; else a device buffer of buf_bytes
+ * >= tqd_state_bytes(..., with_adjoint=1) that the library carves up.
+ * Errors: TQD_ERR_QUBITS when n < g + 2 ("at least two unsharded
+ * dimensions") or n > 62; TQD_ERR_OOM.  Collective. */
+int tqd_state_init(tqd_ctx *ctx, int n_qubits, tqd_dtype dt, void *dev_buf, size_t buf_bytes,
+                   tqd_state **out);
+/* Back to |0...0>, empty tape, pi = identity.  Collective (device memset). */
+int tqd_state_reset(tqd_state *st);
+int tqd_state_free(tqd_state *st);
+int tqd_state_set_option(tqd_state *st, int option, int64_t value);
+
+/* Record gate g on `wires` (n_wires = 1 or 2, distinct, < n).  params: 0, 1 or
+ * 3 angles (NULL iff 0).  matrix: MAT1 2x2 / MAT2 4x4 row-major (re, im)
+ * doubles, NULL otherwise.  trainable != 0 gives each angle a gradient slot in
+ * recording order.  No device work (lazy).  Errors: TQD_ERR_ARG,
+ * TQD_ERR_NOT_UNITARY, TQD_ERR_STATE (state consumed by tqd_adjoint_grad). */
+int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires,
+                   const double *params, const double *matrix, int trainable);
+
+/* Number of gradient slots recorded so far. */
+int tqd_num_params(const tqd_state *st, int *out);
+
+/* Execute pending gates, then out[t] = c_t <psi|P_t|psi> (
+ * measure_allZ), c_t = 1 when coeff is NULL.  Terms with X/Y
+ * on a sharded qubit: TQD_ERR_UNSUPPORTED.  Collective. */
+int tqd_expval(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_t *z_mask,
+               const double *coeff, double *out);
+
+/* Execute pending gates, then E = sum_t c_t <psi|P_t|psi> and
+ * out_grad[p] = dE/dtheta_p for every gradient slot p (n_grad must equal
+ * tqd_num_params), by the invertible reverse sweep of PAPER.md:220-236 (§4.4):
+ * lambda = H psi, then per gate in reverse: g += 2 Re <lambda|(dU)U^dag|psi>,
+ * psi <- U^dag psi (x = U^* y), lambda <- U^dag lambda
+ * (dx = U^T dy in the real representation, Eq. save_x).
+ * This is the VJP of any loss of the expectation values (choose c_t = dL/dE_t,
+ * e.g. sign(E_t) for Listing 2's out.abs().sum()).
+ * Z-only terms (x_mask == 0) in this build, else TQD_ERR_UNSUPPORTED.
+ * CONSUMES the state: afterwards only tqd_state_reset / tqd_state_free /
+ * tqd_get_metrics are allowed.  Collective. */
+int tqd_adjoint_grad(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_t *z_mask,
+                     const double *coeff, double *out_value, double *out_grad, int n_grad);
+
+/* Execute pending gates and copy amplitudes [first, first+count) in CANONICAL
+ * order (MoveDim^{-1} of PAPER.md:116-119 applied through pi) to host_out
+ * (count complex values of the state's dtype, interleaved re, im).  Every rank
+ * receives the values.  Collective. */
+int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host_out);
+
+int tqd_get_metrics(const tqd_state *st, tqd_metrics *out);
+int tqd_reset_metrics(tqd_state *st);
+
+/* Message of the calling thread's last error ("" if none). */
+const char *tqd_last_error(void);
+
+/* Library build string (arch, CUDA / NCCL versions). */
+const char *tqd_version(void);
+
+/* Diagnostic, host only (no GPU, no device work): run the planner on a circuit
+ * and write its stages (tile bits, layouts, ops, remaps, qubit map pi before /
+ * after each stage) as JSON into json_out (cap bytes, NUL-terminated).
+ * Circuit as parallel arrays of length G: kinds[G] (tqd_gate), wires[2G],
+ * params[3G], mats[32G] (MAT1/MAT2 row-major re,im), trainable[G].
+ * k: tile qubits; small_max: as TQD_OPT_SMALL_MAX; c128: dtype flag.
+ * *needed receives the JSON size + 1.  TQD_ERR_ARG if cap is too small. */
+int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, const int *kinds, const int *wires,
+                   const double *params, const double *mats, const int *trainable, char *json_out, size_t cap,
+                   size_t *needed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQD_ABI_H_ */

@@ -1,0 +1,336 @@
+"""Python binding of libtqd.so (include/tqd.h): argument marshalling only.
+
+Every step of the forward / expectation / adjoint path runs in the library's
+CUDA kernels (sm_100a) and NCCL; this module only converts Python arguments to
+the C ABI and raises on error.  There is no CPU fallback: if the library is
+missing and cannot be built, import of the binding fails loudly.
+
+Raw ABI names are exposed one-to-one (``tqd_state_init`` ...); the small
+``Context`` / ``State`` classes below wrap them for tests and bench.py.
+PyTorch is used only for plumbing: the current CUDA stream and, for world > 1,
+broadcasting the NCCL unique id over ``torch.distributed``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtqd.so")
+
+# this binding's own copy of the tqd_gate enum (include/tqd.h)
+GATES = {
+    "I": 0, "X": 1, "Y": 2, "Z": 3, "H": 4, "S": 5, "SDG": 6, "T": 7, "TDG": 8,
+    "CNOT": 9, "CZ": 10, "SWAP": 11, "MAT1": 12, "MAT2": 13,
+    "RX": 14, "RY": 15, "RZ": 16, "U3": 17,
+}
+C64, C128 = 0, 1
+OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH = 0, 1, 2, 3, 4
+ERRORS = {0: "TQD_OK", -1: "TQD_ERR_ARG", -2: "TQD_ERR_QUBITS", -3: "TQD_ERR_WORLD",
+          -4: "TQD_ERR_NOT_UNITARY", -5: "TQD_ERR_OOM", -6: "TQD_ERR_CUDA", -7: "TQD_ERR_NCCL",
+          -8: "TQD_ERR_UNSUPPORTED", -9: "TQD_ERR_STATE"}
+
+
+class TqdError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Metrics(ctypes.Structure):
+    _fields_ = [
+        ("fwd_sweeps", ctypes.c_uint64), ("bwd_sweeps", ctypes.c_uint64), ("remaps", ctypes.c_uint64),
+        ("gates_applied", ctypes.c_uint64), ("gates_unapplied", ctypes.c_uint64),
+        ("hbm_bytes", ctypes.c_uint64), ("a2a_bytes", ctypes.c_uint64),
+        ("fwd_sweep_ms", ctypes.c_double), ("bwd_sweep_ms", ctypes.c_double),
+        ("other_ms", ctypes.c_double), ("a2a_ms", ctypes.c_double),
+        ("fwd_sweep_bytes", ctypes.c_uint64), ("bwd_sweep_bytes", ctypes.c_uint64),
+        ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lock = threading.Lock()
+_lib = None
+
+_P = ctypes.c_void_p
+_SIG = {
+    "tqd_nccl_unique_id": [_P],
+    "tqd_ctx_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.POINTER(_P)],
+    "tqd_ctx_destroy": [_P],
+    "tqd_state_bytes": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)],
+    "tqd_state_init": [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, ctypes.POINTER(_P)],
+    "tqd_state_reset": [_P],
+    "tqd_state_free": [_P],
+    "tqd_state_set_option": [_P, ctypes.c_int, ctypes.c_int64],
+    "tqd_apply_gate": [_P, ctypes.c_int, _P, ctypes.c_int, _P, _P, ctypes.c_int],
+    "tqd_num_params": [_P, ctypes.POINTER(ctypes.c_int)],
+    "tqd_expval": [_P, ctypes.c_int, _P, _P, _P, _P],
+    "tqd_adjoint_grad": [_P, ctypes.c_int, _P, _P, _P, ctypes.POINTER(ctypes.c_double), _P, ctypes.c_int],
+    "tqd_get_amplitudes": [_P, ctypes.c_uint64, ctypes.c_uint64, _P],
+    "tqd_get_metrics": [_P, ctypes.POINTER(Metrics)],
+    "tqd_reset_metrics": [_P],
+    "tqd_debug_plan": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                       _P, _P, _P, _P, _P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
+}
+EXPORTS = list(_SIG) + ["tqd_last_error", "tqd_version"]
+
+
+def lib():
+    """Load libtqd.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            from . import build as _build
+            if not _build.up_to_date():
+                _build.build()
+            L = ctypes.CDLL(LIB_PATH)
+            for name, args in _SIG.items():
+                f = getattr(L, name)
+                f.argtypes = args
+                f.restype = ctypes.c_int
+            L.tqd_last_error.argtypes = []
+            L.tqd_last_error.restype = ctypes.c_char_p
+            L.tqd_version.argtypes = []
+            L.tqd_version.restype = ctypes.c_char_p
+            _lib = L
+    return _lib
+
+
+def _call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        raise TqdError(rc, lib().tqd_last_error().decode())
+    return rc
+
+
+def _arr(a, dtype):
+    return np.ascontiguousarray(np.asarray(a, dtype=dtype))
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+# ---- raw ABI (same names as include/tqd.h) ---------------------------------------
+def tqd_version() -> str:
+    return lib().tqd_version().decode()
+
+
+def tqd_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_char * 128)()
+    _call("tqd_nccl_unique_id", ctypes.cast(buf, _P))
+    return bytes(buf)
+
+
+def tqd_ctx_create(world: int, rank: int, device: int, nccl_id: bytes | None, stream: int | None):
+    out = _P()
+    idbuf = (ctypes.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
+    _call("tqd_ctx_create", world, rank, device, ctypes.cast(idbuf, _P) if idbuf is not None else None,
+          _P(stream) if stream else None, ctypes.byref(out))
+    return out
+
+
+def tqd_ctx_destroy(ctx):
+    _call("tqd_ctx_destroy", ctx)
+
+
+def tqd_state_bytes(n: int, dtype: int, world: int, with_adjoint: int) -> int:
+    out = ctypes.c_size_t()
+    _call("tqd_state_bytes", n, dtype, world, with_adjoint, ctypes.byref(out))
+    return out.value
+
+
+def tqd_state_init(ctx, n: int, dtype: int, dev_buf: int | None = None, buf_bytes: int = 0):
+    out = _P()
+    _call("tqd_state_init", ctx, n, dtype, _P(dev_buf) if dev_buf else None, buf_bytes, ctypes.byref(out))
+    return out
+
+
+def tqd_state_reset(st):
+    _call("tqd_state_reset", st)
+
+
+def tqd_state_free(st):
+    _call("tqd_state_free", st)
+
+
+def tqd_state_set_option(st, opt: int, value: int):
+    _call("tqd_state_set_option", st, opt, int(value))
+
+
+def tqd_apply_gate(st, gate, wires, params=(), matrix=None, trainable=True):
+    g = GATES[gate] if isinstance(gate, str) else int(gate)
+    w = _arr(wires, np.int32)
+    p = _arr(params, np.float64) if len(params) else None
+    m = None
+    if matrix is not None:
+        mm = np.asarray(matrix, dtype=np.complex128).reshape(-1)
+        m = np.empty(2 * mm.size, dtype=np.float64)
+        m[0::2], m[1::2] = mm.real, mm.imag
+    _call("tqd_apply_gate", st, g, _ptr(w), int(w.size), _ptr(p), _ptr(m), 1 if trainable else 0)
+
+
+def tqd_num_params(st) -> int:
+    out = ctypes.c_int()
+    _call("tqd_num_params", st, ctypes.byref(out))
+    return out.value
+
+
+def _terms(terms):
+    x = _arr([t[0] for t in terms] or [0], np.uint64)
+    z = _arr([t[1] for t in terms] or [0], np.uint64)
+    c = _arr([t[2] if len(t) > 2 else 1.0 for t in terms] or [0.0], np.float64)
+    return len(terms), x, z, c
+
+
+def tqd_expval(st, terms) -> np.ndarray:
+    T, x, z, c = _terms(terms)
+    out = np.zeros(max(T, 1), dtype=np.float64)
+    _call("tqd_expval", st, T, _ptr(x), _ptr(z), _ptr(c), _ptr(out))
+    return out[:T]
+
+
+def tqd_adjoint_grad(st, terms, n_grad: int | None = None):
+    T, x, z, c = _terms(terms)
+    if n_grad is None:
+        n_grad = tqd_num_params(st)
+    g = np.zeros(max(n_grad, 1), dtype=np.float64)
+    val = ctypes.c_double()
+    _call("tqd_adjoint_grad", st, T, _ptr(x), _ptr(z), _ptr(c), ctypes.byref(val), _ptr(g), n_grad)
+    return val.value, g[:n_grad]
+
+
+def tqd_get_amplitudes(st, first: int, count: int, dtype: int) -> np.ndarray:
+    out = np.zeros(count, dtype=np.complex128 if dtype == C128 else np.complex64)
+    _call("tqd_get_amplitudes", st, first, count, _ptr(out))
+    return out
+
+
+def tqd_get_metrics(st) -> dict:
+    m = Metrics()
+    _call("tqd_get_metrics", st, ctypes.byref(m))
+    return m.as_dict()
+
+
+def tqd_reset_metrics(st):
+    _call("tqd_reset_metrics", st)
+
+
+def tqd_last_error() -> str:
+    return lib().tqd_last_error().decode()
+
+
+def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 10, c128: bool = False) -> dict:
+    """Planner diagnostic (host only, no GPU): stages of `gates` as a dict."""
+    import json
+    G = len(gates)
+    kinds = np.zeros(max(G, 1), np.int32)
+    wires = np.zeros(2 * max(G, 1), np.int32)
+    params = np.zeros(3 * max(G, 1), np.float64)
+    mats = np.zeros(32 * max(G, 1), np.float64)
+    tr = np.zeros(max(G, 1), np.int32)
+    for i, g in enumerate(gates):
+        kinds[i] = GATES[g.name]
+        wires[2 * i:2 * i + len(g.wires)] = g.wires
+        params[3 * i:3 * i + len(g.params)] = g.params
+        if g.matrix is not None:
+            mm = np.asarray(g.matrix, np.complex128).reshape(-1)
+            mats[32 * i:32 * i + 2 * mm.size:2] = mm.real
+            mats[32 * i + 1:32 * i + 2 * mm.size:2] = mm.imag
+        tr[i] = 1 if g.trainable else 0
+    need = ctypes.c_size_t(0)
+    cap = 1 << 16
+    while True:
+        buf = ctypes.create_string_buffer(cap)
+        rc = lib().tqd_debug_plan(n, world, k, small_max, 1 if c128 else 0, G, _ptr(kinds), _ptr(wires),
+                                  _ptr(params), _ptr(mats), _ptr(tr), buf, cap, ctypes.byref(need))
+        if rc == 0:
+            return json.loads(buf.value.decode())
+        if need.value > cap:
+            cap = need.value
+            continue
+        raise TqdError(rc, tqd_last_error())
+
+
+# ---- convenience wrappers ----------------------------------------------------
+class Context:
+    """One per process = one GPU.  world > 1 bootstraps NCCL over torch.distributed."""
+
+    def __init__(self, world: int = 1, rank: int = 0, device: int = 0, nccl_id: bytes | None = None,
+                 stream: int | None = None):
+        self.world, self.rank, self.device = world, rank, device
+        self.handle = tqd_ctx_create(world, rank, device, nccl_id, stream)
+
+    @classmethod
+    def from_torch(cls, use_current_stream: bool = True):
+        """Context for this rank: RANK / WORLD_SIZE / LOCAL_RANK from torch.distributed / env."""
+        import torch
+        import torch.distributed as dist
+        world = dist.get_world_size() if dist.is_initialized() else 1
+        rank = dist.get_rank() if dist.is_initialized() else 0
+        device = int(os.environ.get("LOCAL_RANK", 0)) if world > 1 else torch.cuda.current_device()
+        torch.cuda.set_device(device)
+        nid = None
+        if world > 1:
+            obj = [tqd_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        stream = torch.cuda.current_stream(device).cuda_stream if use_current_stream else None
+        return cls(world, rank, device, nid, stream)
+
+    def close(self):
+        if self.handle:
+            tqd_ctx_destroy(self.handle)
+            self.handle = None
+
+
+class State:
+    def __init__(self, ctx: Context, n: int, dtype: str = "c64", dev_buf: int | None = None, buf_bytes: int = 0):
+        self.ctx, self.n = ctx, n
+        self.dtype = C128 if dtype in ("c128", C128) else C64
+        self.handle = tqd_state_init(ctx.handle, n, self.dtype, dev_buf, buf_bytes)
+
+    def set_option(self, opt: int, value: int):
+        tqd_state_set_option(self.handle, opt, value)
+
+    def reset(self):
+        tqd_state_reset(self.handle)
+
+    def apply(self, name, wires, params=(), matrix=None, trainable=True):
+        tqd_apply_gate(self.handle, name, wires, params, matrix, trainable)
+
+    def apply_circuit(self, gates):
+        for g in gates:
+            tqd_apply_gate(self.handle, g.name, g.wires, g.params, g.matrix, g.trainable)
+
+    @property
+    def n_params(self) -> int:
+        return tqd_num_params(self.handle)
+
+    def expval(self, terms) -> np.ndarray:
+        return tqd_expval(self.handle, terms)
+
+    def adjoint_grad(self, terms):
+        return tqd_adjoint_grad(self.handle, terms)
+
+    def amplitudes(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        if count is None:
+            count = (1 << self.n) - first
+        return tqd_get_amplitudes(self.handle, first, count, self.dtype)
+
+    def metrics(self) -> dict:
+        return tqd_get_metrics(self.handle)
+
+    def reset_metrics(self):
+        tqd_reset_metrics(self.handle)
+
+    def free(self):
+        if self.handle:
+            tqd_state_free(self.handle)
+            self.handle = None

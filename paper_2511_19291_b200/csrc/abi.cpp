@@ -1,0 +1,830 @@
+// abi.cpp -- the C ABI of include/tqd.h: contexts, states, the execution engine
+// (plan -> encode -> launch), the NCCL remap exchange and the reductions.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tqd.h"
+#include "plan.h"
+#include "tqd_internal.h"
+
+namespace tqd {
+// kernels.cu
+cudaError_t launch_sweep(bool dbl, int R, bool bwd, const DevStage *d_stage, const DevOp *d_ops, const int32_t *d_slots,
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int grid, cudaStream_t s);
+int sweep_max_ctas_per_sm(bool dbl, int R, bool bwd, int k, int W);
+cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
+                         uint64_t rank_hi, cudaStream_t s);
+cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
+                               double *eout, cudaStream_t s);
+cudaError_t launch_expval_z(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const uint64_t *d_z, int T,
+                            double *out, cudaStream_t s);
+cudaError_t launch_expval_xy(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, uint64_t xloc, const uint64_t *d_z,
+                             const int *d_ny, int T, double *out, cudaStream_t s);
+cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
+                          cudaStream_t s);
+cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
+cudaError_t launch_remap_pack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s);
+cudaError_t launch_remap_unpack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s);
+}  // namespace tqd
+
+using namespace tqd;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+struct tqd_ctx {
+    int world = 1, rank = 0, device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    bool poisoned = false;
+    int sms = 148;
+};
+
+enum Cat { CAT_FWD = 0, CAT_BWD = 1, CAT_OTHER = 2, CAT_A2A = 3 };
+
+struct tqd_state {
+    tqd_ctx *ctx = nullptr;
+    int n = 0, n_loc = 0, g = 0;
+    bool dbl = false;
+    size_t esz = 8;
+    void *psi = nullptr, *lam = nullptr, *sendb = nullptr, *recvb = nullptr;
+    bool own_psi = false, own_lam = false, own_xchg = false;
+    void *user_buf = nullptr;
+    size_t user_bytes = 0;
+    std::vector<GateRec> gates;
+    int n_params = 0;
+    size_t executed = 0;
+    std::vector<Stage> history;
+    std::vector<int> pos;
+    bool consumed = false;
+    // options
+    int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0;
+    tqd_metrics met;
+    // device scratch
+    void *d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    double *d_red = nullptr;  // reductions: values / grads
+    size_t red_count = 0;
+    // profiling
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, int>> ev_used;  // (start index, category); stop = start+1
+    size_t ev_next = 0;
+};
+
+#define CUDA_TRY(st, call)                                                                            \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess) {                                                                      \
+            (st)->ctx->poisoned = true;                                                               \
+            return fail(TQD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));            \
+        }                                                                                             \
+    } while (0)
+
+#define NCCL_TRY(st, call)                                                                            \
+    do {                                                                                              \
+        ncclResult_t r_ = (call);                                                                     \
+        if (r_ != ncclSuccess) {                                                                      \
+            (st)->ctx->poisoned = true;                                                               \
+            return fail(TQD_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));            \
+        }                                                                                             \
+    } while (0)
+
+static int check_live(const tqd_state *st) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    if (st->ctx->poisoned) return fail(TQD_ERR_STATE, "context poisoned by an earlier CUDA/NCCL error");
+    return TQD_OK;
+}
+
+// ---- profiling events ------------------------------------------------------
+static int ev_begin(tqd_state *st, int cat) {
+    if (!st->opt_profile) return -1;
+    if (st->ev_next + 2 > st->ev_pool.size()) {
+        for (int i = 0; i < 64; i++) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return -1;
+            st->ev_pool.push_back(e);
+        }
+    }
+    const int idx = (int)st->ev_next;
+    st->ev_next += 2;
+    cudaEventRecord(st->ev_pool[idx], st->ctx->stream);
+    st->ev_used.push_back({idx, cat});
+    return idx;
+}
+static void ev_end(tqd_state *st, int idx) {
+    if (idx < 0) return;
+    cudaEventRecord(st->ev_pool[idx + 1], st->ctx->stream);
+}
+static int ev_collect(tqd_state *st) {
+    if (st->ev_used.empty()) return TQD_OK;
+    CUDA_TRY(st, cudaEventSynchronize(st->ev_pool[st->ev_used.back().first + 1]));
+    for (auto &u : st->ev_used) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, st->ev_pool[u.first], st->ev_pool[u.first + 1]);
+        switch (u.second) {
+        case CAT_FWD: st->met.fwd_sweep_ms += ms; break;
+        case CAT_BWD: st->met.bwd_sweep_ms += ms; break;
+        case CAT_A2A: st->met.a2a_ms += ms; break;
+        default: st->met.other_ms += ms; break;
+        }
+    }
+    st->ev_used.clear();
+    st->ev_next = 0;
+    return TQD_OK;
+}
+
+static PlanConfig plan_cfg(const tqd_state *st) {
+    PlanConfig c;
+    c.n = st->n;
+    c.n_loc = st->n_loc;
+    c.k = st->opt_k;
+    c.R = 4;
+    c.small_max = st->opt_small;
+    c.c128 = st->dbl;
+    c.swz_bits = st->dbl ? 3 : 4;
+    // shared memory budget: the adjoint holds psi and lambda tiles
+    while (c.k > 9 && ((size_t)2 << c.k) * st->esz > 160 * 1024) c.k--;
+    if (c.k > c.n_loc) c.k = c.n_loc;
+    if (c.k - LANE_BITS - c.R > WMAX) c.k = LANE_BITS + c.R + WMAX;
+    return c;
+}
+
+static int ensure_scratch(tqd_state *st, size_t bytes) {
+    if (bytes <= st->scratch_bytes) return TQD_OK;
+    if (st->d_scratch) {
+        CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream));
+        cudaFree(st->d_scratch);
+        st->d_scratch = nullptr;
+    }
+    size_t nb = std::max(bytes, (size_t)1 << 20);
+    if (cudaMalloc(&st->d_scratch, nb) != cudaSuccess) {
+        cudaGetLastError();
+        st->scratch_bytes = 0;
+        return fail(TQD_ERR_OOM, "cannot allocate descriptor scratch");
+    }
+    st->scratch_bytes = nb;
+    return TQD_OK;
+}
+
+static int ensure_red(tqd_state *st, size_t count) {
+    if (count <= st->red_count) return TQD_OK;
+    if (st->d_red) {
+        CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream));
+        cudaFree(st->d_red);
+        st->d_red = nullptr;
+    }
+    size_t nc = std::max(count, (size_t)4096);
+    if (cudaMalloc(&st->d_red, nc * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        st->red_count = 0;
+        return fail(TQD_ERR_OOM, "cannot allocate reduction buffer");
+    }
+    st->red_count = nc;
+    return TQD_OK;
+}
+
+static uint64_t shard_bytes(const tqd_state *st) { return ((uint64_t)1 << st->n_loc) * st->esz; }
+
+static int ensure_xchg(tqd_state *st) {
+    if (st->sendb) return TQD_OK;
+    const size_t b = shard_bytes(st);
+    if (cudaMalloc(&st->sendb, b) != cudaSuccess || cudaMalloc(&st->recvb, b) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TQD_ERR_OOM, "cannot allocate remap staging buffers");
+    }
+    st->own_xchg = true;
+    st->met.peak_device_bytes += 2 * b;
+    return TQD_OK;
+}
+
+static int ensure_lambda(tqd_state *st) {
+    if (st->lam) return TQD_OK;
+    const size_t b = shard_bytes(st);
+    if (cudaMalloc(&st->lam, b) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TQD_ERR_OOM, "cannot allocate the adjoint state lambda");
+    }
+    st->own_lam = true;
+    st->met.peak_device_bytes += b;
+    return TQD_OK;
+}
+
+static uint64_t rank_hi(const tqd_state *st) { return (uint64_t)st->ctx->rank << st->n_loc; }
+
+// ---- remap exchange -------------------------------------
+static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
+    int rc = ensure_xchg(st);
+    if (rc) return rc;
+    tqd_ctx *c = st->ctx;
+    RemapMap rm;
+    memset(&rm, 0, sizeof(rm));
+    rm.m = rp.m;
+    rm.n_loc = st->n_loc;
+    std::vector<char> isl(st->n_loc, 0);
+    for (int i = 0; i < rp.m; i++) { rm.lpos[i] = (uint8_t)rp.lpos[i]; isl[rp.lpos[i]] = 1; }
+    int r = 0;
+    for (int p = 0; p < st->n_loc; p++) if (!isl[p]) rm.rest[r++] = (uint8_t)p;
+    const uint64_t blk = (uint64_t)1 << (st->n_loc - rp.m);
+    const int ev = ev_begin(st, CAT_A2A);
+    CUDA_TRY(st, launch_remap_pack(st->dbl, buf, st->sendb, rm, c->stream));
+    const size_t bb = blk * st->esz;
+    char *sb = (char *)st->sendb, *rb = (char *)st->recvb;
+    NCCL_TRY(st, ncclGroupStart());
+    for (uint64_t b = 0; b < ((uint64_t)1 << rp.m); b++) {
+        int peer = c->rank;
+        for (int i = 0; i < rp.m; i++) {
+            const int gb = rp.gpos[i] - st->n_loc;
+            peer = (peer & ~(1 << gb)) | ((int)((b >> i) & 1) << gb);
+        }
+        uint64_t u = 0;  // peer's global-bit values = where its block lands here
+        for (int i = 0; i < rp.m; i++) u |= (uint64_t)((peer >> (rp.gpos[i] - st->n_loc)) & 1) << i;
+        if (peer == c->rank) {
+            CUDA_TRY(st, cudaMemcpyAsync(rb + u * bb, sb + b * bb, bb, cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            const ncclDataType_t dt = st->dbl ? ncclDouble : ncclFloat;
+            NCCL_TRY(st, ncclSend(sb + b * bb, blk * 2, dt, peer, c->comm, c->stream));
+            NCCL_TRY(st, ncclRecv(rb + u * bb, blk * 2, dt, peer, c->comm, c->stream));
+            st->met.a2a_bytes += bb;
+        }
+    }
+    NCCL_TRY(st, ncclGroupEnd());
+    CUDA_TRY(st, launch_remap_unpack(st->dbl, st->recvb, buf, rm, c->stream));
+    ev_end(st, ev);
+    st->met.hbm_bytes += 4 * shard_bytes(st);
+    st->met.kernel_launches += 2;
+    return TQD_OK;
+}
+
+// ---- forward execution ------------------------------------------------------
+static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd) {
+    if (st->opt_grid > 0) return st->opt_grid;
+    int per = sweep_max_ctas_per_sm(st->dbl, sp.R, bwd, sp.k, sp.W);
+    if (per < 1) per = 1;
+    int64_t g = (int64_t)per * st->ctx->sms;
+    const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
+    if (g > tiles) g = tiles;
+    return (int)g;
+}
+
+// Encode stages [b, e) of `stages` (forward or backward order) into one upload
+// and launch them in order.
+static int run_stages(tqd_state *st, const std::vector<Stage> &stages, bool bwd, double *d_grad) {
+    std::vector<DevStage> dstages;
+    std::vector<DevOp> ops;
+    std::vector<int32_t> slots;
+    struct L { int type; int idx; int op_base; int n_ops; const Stage *s; };
+    std::vector<L> launches;
+    for (size_t ii = 0; ii < stages.size(); ii++) {
+        const Stage &s = stages[ii];
+        if (s.type == ST_SWEEP) {
+            if (s.sw.ops.empty()) continue;
+            DevStage ds;
+            encode_sweep(s.sw, st->gates, bwd, st->n_loc, ds, ops, slots);
+            launches.push_back({ST_SWEEP, (int)dstages.size(), 0, 0, &s});
+            dstages.push_back(ds);
+        } else if (s.type == ST_SMALL) {
+            if (s.sm.ops.empty()) continue;
+            const int b = (int)ops.size();
+            encode_small(s.sm, st->gates, bwd, ops);
+            launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, &s});
+        } else {
+            launches.push_back({ST_REMAP, -1, 0, 0, &s});
+        }
+    }
+    const size_t b_st = dstages.size() * sizeof(DevStage);
+    const size_t b_ops = ops.size() * sizeof(DevOp);
+    const size_t b_sl = slots.size() * sizeof(int32_t);
+    const size_t off_ops = (b_st + 255) & ~(size_t)255;
+    const size_t off_sl = (off_ops + b_ops + 255) & ~(size_t)255;
+    const size_t total = off_sl + b_sl + 256;
+    int rc = ensure_scratch(st, total);
+    if (rc) return rc;
+    std::vector<char> host(total, 0);
+    if (b_st) memcpy(host.data(), dstages.data(), b_st);
+    if (b_ops) memcpy(host.data() + off_ops, ops.data(), b_ops);
+    if (b_sl) memcpy(host.data() + off_sl, slots.data(), b_sl);
+    tqd_ctx *c = st->ctx;
+    CUDA_TRY(st, cudaMemcpyAsync(st->d_scratch, host.data(), total, cudaMemcpyHostToDevice, c->stream));
+    const DevStage *d_st = (const DevStage *)st->d_scratch;
+    const DevOp *d_ops = (const DevOp *)((char *)st->d_scratch + off_ops);
+    const int32_t *d_sl = (const int32_t *)((char *)st->d_scratch + off_sl);
+    const uint64_t sb = shard_bytes(st);
+    for (const L &l : launches) {
+        if (l.type == ST_SWEEP) {
+            const SweepPlan &sp = l.s->sw;
+            const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
+            CUDA_TRY(st, launch_sweep(st->dbl, sp.R, bwd, d_st + l.idx, d_ops, d_sl, st->psi, st->lam, d_grad,
+                                      rank_hi(st), sp.k, sp.W, sweep_grid(st, sp, bwd), c->stream));
+            ev_end(st, ev);
+            if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += sp.n_gates; }
+            else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
+            st->met.kernel_launches++;
+        } else if (l.type == ST_SMALL) {
+            const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
+            CUDA_TRY(st, launch_small(st->dbl, bwd, d_ops + l.op_base, l.n_ops, st->psi, st->lam, d_grad, st->n_loc,
+                                      rank_hi(st), c->stream));
+            ev_end(st, ev);
+            if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += l.s->sm.n_gates; }
+            else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += l.s->sm.n_gates; }
+            st->met.kernel_launches++;
+        } else {
+            rc = exec_remap(st, l.s->rm, st->psi);
+            if (rc) return rc;
+            if (bwd) { rc = exec_remap(st, l.s->rm, st->lam); if (rc) return rc; }
+            st->met.remaps++;
+        }
+    }
+    return TQD_OK;
+}
+
+static int execute_pending(tqd_state *st) {
+    if (st->executed == st->gates.size()) return TQD_OK;
+    std::vector<int> pending;
+    for (size_t i = st->executed; i < st->gates.size(); i++) pending.push_back((int)i);
+    std::vector<Stage> stages;
+    std::string err;
+    int rc = plan_circuit(st->gates, pending, st->pos, plan_cfg(st), stages, err);
+    if (rc) return fail(rc, err);
+    rc = run_stages(st, stages, false, nullptr);
+    if (rc) return rc;
+    for (auto &s : stages) st->history.push_back(std::move(s));
+    st->executed = st->gates.size();
+    return TQD_OK;
+}
+
+static int allreduce_sum(tqd_state *st, double *d, size_t count) {
+    if (st->ctx->world == 1 || count == 0) return TQD_OK;
+    NCCL_TRY(st, ncclAllReduce(d, d, count, ncclDouble, ncclSum, st->ctx->comm, st->ctx->stream));
+    return TQD_OK;
+}
+
+static uint64_t phys_mask(const tqd_state *st, uint64_t logical_mask) {
+    uint64_t m = 0;
+    for (int q = 0; q < st->n; q++)
+        if ((logical_mask >> q) & 1) m |= 1ull << st->pos[q];
+    return m;
+}
+
+static int check_terms(const tqd_state *st, int T, const uint64_t *x, const uint64_t *z) {
+    if (T < 0) return fail(TQD_ERR_ARG, "n_terms < 0");
+    if (T > 0 && (!x || !z)) return fail(TQD_ERR_ARG, "x_mask / z_mask is NULL");
+    const uint64_t lim = st->n >= 64 ? ~0ull : ((1ull << st->n) - 1);
+    for (int t = 0; t < T; t++)
+        if ((x[t] & ~lim) || (z[t] & ~lim)) return fail(TQD_ERR_ARG, "Pauli mask names a qubit >= n");
+    return TQD_OK;
+}
+
+// ============================================================================
+extern "C" {
+
+const char *tqd_last_error(void) { return g_err.c_str(); }
+
+const char *tqd_version(void) {
+    static std::string v;
+    if (v.empty()) {
+        char b[160];
+        snprintf(b, sizeof(b), "tqd-b200 sm_100a CUDA %d NCCL %d.%d.%d", CUDART_VERSION, NCCL_MAJOR, NCCL_MINOR, NCCL_PATCH);
+        v = b;
+    }
+    return v.c_str();
+}
+
+int tqd_nccl_unique_id(void *out128) {
+    if (!out128) return fail(TQD_ERR_ARG, "out128 is NULL");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(TQD_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "NCCL unique id is 128 bytes");
+    memcpy(out128, &id, 128);
+    return TQD_OK;
+}
+
+int tqd_ctx_create(int world, int rank, int cuda_device, const void *nccl_id, void *cuda_stream, tqd_ctx **out) {
+    if (!out) return fail(TQD_ERR_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || (world & (world - 1)) != 0) return fail(TQD_ERR_WORLD, "world size must be a power of two");
+    if (rank < 0 || rank >= world) return fail(TQD_ERR_WORLD, "rank out of range");
+    if (world > 1 && !nccl_id) return fail(TQD_ERR_ARG, "nccl_id is NULL for world > 1");
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) return fail(TQD_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    tqd_ctx *c = new tqd_ctx();
+    c->world = world;
+    c->rank = rank;
+    c->device = cuda_device;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cuda_device) == cudaSuccess) c->sms = prop.multiProcessorCount;
+    if (cuda_stream) {
+        c->stream = (cudaStream_t)cuda_stream;
+    } else {
+        e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { delete c; return fail(TQD_ERR_CUDA, std::string("cudaStreamCreate: ") + cudaGetErrorString(e)); }
+        c->own_stream = true;
+    }
+    if (world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, nccl_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            if (c->own_stream) cudaStreamDestroy(c->stream);
+            delete c;
+            return fail(TQD_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+    }
+    *out = c;
+    return TQD_OK;
+}
+
+int tqd_ctx_destroy(tqd_ctx *c) {
+    if (!c) return fail(TQD_ERR_ARG, "ctx is NULL");
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return TQD_OK;
+}
+
+int tqd_state_bytes(int n, tqd_dtype dt, int world, int with_adjoint, size_t *out) {
+    if (!out) return fail(TQD_ERR_ARG, "out is NULL");
+    if (world < 1 || (world & (world - 1))) return fail(TQD_ERR_WORLD, "world size must be a power of two");
+    int g = 0;
+    while ((1 << g) < world) g++;
+    if (n < g + 2 || n > 62) return fail(TQD_ERR_QUBITS, "need g + 2 <= n <= 62");
+    const size_t esz = dt == TQD_C128 ? 16 : 8;
+    const size_t shard = ((size_t)1 << (n - g)) * esz;
+    *out = shard * (with_adjoint ? 2 : 1) + (world > 1 ? 2 * shard : 0);
+    return TQD_OK;
+}
+
+int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_bytes, tqd_state **out) {
+    if (!c || !out) return fail(TQD_ERR_ARG, "ctx/out is NULL");
+    *out = nullptr;
+    if (c->poisoned) return fail(TQD_ERR_STATE, "context poisoned");
+    if (dt != TQD_C64 && dt != TQD_C128) return fail(TQD_ERR_ARG, "bad dtype");
+    int g = 0;
+    while ((1 << g) < c->world) g++;
+    if (n < g + 2 || n > 62)
+        return fail(TQD_ERR_QUBITS, "n must satisfy log2(world) + 2 <= n <= 62 (PAPER.md:162: at least two unsharded qubits)");
+    tqd_state *st = new tqd_state();
+    st->ctx = c;
+    st->n = n;
+    st->g = g;
+    st->n_loc = n - g;
+    st->dbl = dt == TQD_C128;
+    st->esz = st->dbl ? 16 : 8;
+    memset(&st->met, 0, sizeof(st->met));
+    const size_t sb = shard_bytes(st);
+    if (dev_buf) {
+        if (buf_bytes < sb) { delete st; return fail(TQD_ERR_OOM, "dev_buf smaller than one shard"); }
+        st->psi = dev_buf;
+        if (buf_bytes >= 2 * sb) st->lam = (char *)dev_buf + sb;
+        if (c->world > 1 && buf_bytes >= 4 * sb) {
+            st->sendb = (char *)dev_buf + 2 * sb;
+            st->recvb = (char *)dev_buf + 3 * sb;
+        }
+        st->met.peak_device_bytes = buf_bytes;
+    } else {
+        if (cudaMalloc(&st->psi, sb) != cudaSuccess) {
+            cudaGetLastError();
+            delete st;
+            return fail(TQD_ERR_OOM, "cannot allocate the state shard");
+        }
+        st->own_psi = true;
+        st->met.peak_device_bytes = sb;
+    }
+    int rc = tqd_state_reset(st);
+    if (rc) { tqd_state_free(st); return rc; }
+    *out = st;
+    return TQD_OK;
+}
+
+int tqd_state_reset(tqd_state *st) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    st->gates.clear();
+    st->history.clear();
+    st->n_params = 0;
+    st->executed = 0;
+    st->consumed = false;
+    st->pos.assign(st->n, 0);
+    for (int q = 0; q < st->n; q++) st->pos[q] = st->n - 1 - q;  // MSB-first identity (R1)
+    const int ev = ev_begin(st, CAT_OTHER);
+    CUDA_TRY(st, cudaMemsetAsync(st->psi, 0, shard_bytes(st), st->ctx->stream));
+    if (st->ctx->rank == 0) CUDA_TRY(st, launch_set_one(st->dbl, st->psi, st->ctx->stream));
+    ev_end(st, ev);
+    st->met.hbm_bytes += shard_bytes(st);
+    st->met.kernel_launches += 1;
+    return ev_collect(st);
+}
+
+int tqd_state_free(tqd_state *st) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    if (st->ctx && st->ctx->stream) cudaStreamSynchronize(st->ctx->stream);
+    if (st->own_psi) cudaFree(st->psi);
+    if (st->own_lam) cudaFree(st->lam);
+    if (st->own_xchg) { cudaFree(st->sendb); cudaFree(st->recvb); }
+    if (st->d_scratch) cudaFree(st->d_scratch);
+    if (st->d_red) cudaFree(st->d_red);
+    for (auto e : st->ev_pool) cudaEventDestroy(e);
+    delete st;
+    return TQD_OK;
+}
+
+int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    switch (option) {
+    case TQD_OPT_TILE_QUBITS:
+        if (v < 9 || v > 14) return fail(TQD_ERR_ARG, "tile qubits must be in [9, 14]");
+        st->opt_k = (int)v; return TQD_OK;
+    case TQD_OPT_SMALL_MAX:
+        if (v < 0 || v > 12) return fail(TQD_ERR_ARG, "small_max must be in [0, 12]");
+        if (st->dbl && v > 11) return fail(TQD_ERR_ARG, "small_max must be <= 11 for complex128");
+        st->opt_small = (int)v; return TQD_OK;
+    case TQD_OPT_PROFILE: st->opt_profile = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_GRID_CTAS:
+        if (v < 0) return fail(TQD_ERR_ARG, "grid must be >= 0");
+        st->opt_grid = (int)v; return TQD_OK;
+    case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
+    default: return fail(TQD_ERR_ARG, "unknown option");
+    }
+}
+
+int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires, const double *params,
+                   const double *matrix, int trainable) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (!wires) return fail(TQD_ERR_ARG, "wires is NULL");
+    if (n_wires < 1 || n_wires > 2) return fail(TQD_ERR_ARG, "n_wires must be 1 or 2");
+    for (int i = 0; i < n_wires; i++)
+        if (wires[i] < 0 || wires[i] >= st->n) return fail(TQD_ERR_ARG, "wire out of range");
+    if (n_wires == 2 && wires[0] == wires[1]) return fail(TQD_ERR_ARG, "duplicate wires");
+    GateRec rec;
+    std::string err;
+    int rc = make_gate((int)g, wires, n_wires, params, matrix, trainable, st->dbl, rec, err);
+    if (rc) return fail(rc, err);
+    if (rec.trainable) {
+        rec.slot0 = st->n_params;
+        st->n_params += gate_num_params((int)g);
+    }
+    st->gates.push_back(rec);
+    return TQD_OK;
+}
+
+int tqd_num_params(const tqd_state *st, int *out) {
+    if (!st || !out) return fail(TQD_ERR_ARG, "NULL argument");
+    *out = st->n_params;
+    return TQD_OK;
+}
+
+int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff, double *out) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (T > 0 && !out) return fail(TQD_ERR_ARG, "out is NULL");
+    rc = check_terms(st, T, x, z);
+    if (rc) return rc;
+    rc = execute_pending(st);
+    if (rc) return rc;
+    if (T == 0) return ev_collect(st);
+    // reject X/Y on sharded qubits before any device work
+    for (int t = 0; t < T; t++)
+        if (phys_mask(st, x[t]) >> st->n_loc)
+            return fail(TQD_ERR_UNSUPPORTED, "X/Y on a sharded qubit is not supported by tqd_expval in this build");
+    rc = ensure_red(st, (size_t)T + 2 * 64 + 64);
+    if (rc) return rc;
+    tqd_ctx *c = st->ctx;
+    double *d_out = st->d_red;
+    uint64_t *d_masks = (uint64_t *)(st->d_red + T);
+    int *d_ny = (int *)(st->d_red + T + 64);
+    const uint64_t N = 1ull << st->n_loc;
+    CUDA_TRY(st, cudaMemsetAsync(d_out, 0, T * sizeof(double), c->stream));
+    const int ev = ev_begin(st, CAT_OTHER);
+    // Z-only terms, 16 per launch; X/Y terms grouped by x mask
+    std::vector<int> zt;
+    for (int t = 0; t < T; t++) if (x[t] == 0) zt.push_back(t);
+    std::vector<char> done(T, 0);
+    for (size_t b = 0; b < zt.size();) {
+        // terms contiguous in the output? use a staging vector + scatter by index below
+        const int cnt = (int)std::min<size_t>(16, zt.size() - b);
+        uint64_t hm[16];
+        for (int i = 0; i < cnt; i++) hm[i] = phys_mask(st, z[zt[b + i]]);
+        CUDA_TRY(st, cudaMemcpyAsync(d_masks, hm, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        // results go to d_out[T..] scratch? simpler: accumulate into d_out at the term positions via a temp
+        double *tmp = st->d_red + T + 128;
+        CUDA_TRY(st, cudaMemsetAsync(tmp, 0, 16 * sizeof(double), c->stream));
+        CUDA_TRY(st, launch_expval_z(st->dbl, st->psi, N, rank_hi(st), d_masks, cnt, tmp, c->stream));
+        for (int i = 0; i < cnt; i++)
+            CUDA_TRY(st, cudaMemcpyAsync(d_out + zt[b + i], tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // hm lives on the host stack
+        st->met.hbm_bytes += N * st->esz;
+        st->met.kernel_launches++;
+        for (int i = 0; i < cnt; i++) done[zt[b + i]] = 1;
+        b += cnt;
+    }
+    for (int t0 = 0; t0 < T; t0++) {
+        if (done[t0]) continue;
+        std::vector<int> grp;
+        for (int t = t0; t < T; t++)
+            if (!done[t] && x[t] == x[t0] && grp.size() < 16) grp.push_back(t);
+        const uint64_t xl = phys_mask(st, x[t0]);
+        uint64_t hm[16];
+        int hn[16];
+        for (size_t i = 0; i < grp.size(); i++) {
+            hm[i] = phys_mask(st, z[grp[i]]);
+            hn[i] = __builtin_popcountll(x[grp[i]] & z[grp[i]]) & 3;
+        }
+        CUDA_TRY(st, cudaMemcpyAsync(d_masks, hm, grp.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(st, cudaMemcpyAsync(d_ny, hn, grp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        double *tmp = st->d_red + T + 128;
+        CUDA_TRY(st, cudaMemsetAsync(tmp, 0, 16 * sizeof(double), c->stream));
+        CUDA_TRY(st, launch_expval_xy(st->dbl, st->psi, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp, c->stream));
+        for (size_t i = 0; i < grp.size(); i++)
+            CUDA_TRY(st, cudaMemcpyAsync(d_out + grp[i], tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+        st->met.hbm_bytes += 2 * N * st->esz;
+        st->met.kernel_launches++;
+        for (int t : grp) done[t] = 1;
+    }
+    ev_end(st, ev);
+    rc = allreduce_sum(st, d_out, T);
+    if (rc) return rc;
+    std::vector<double> h(T);
+    CUDA_TRY(st, cudaMemcpyAsync(h.data(), d_out, T * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    for (int t = 0; t < T; t++) out[t] = (coeff ? coeff[t] : 1.0) * h[t];
+    return ev_collect(st);
+}
+
+int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff, double *out_value,
+                     double *out_grad, int n_grad) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (!out_value) return fail(TQD_ERR_ARG, "out_value is NULL");
+    if (n_grad != st->n_params) return fail(TQD_ERR_ARG, "n_grad != tqd_num_params");
+    if (n_grad > 0 && !out_grad) return fail(TQD_ERR_ARG, "out_grad is NULL");
+    rc = check_terms(st, T, x, z);
+    if (rc) return rc;
+    if (T > 64) return fail(TQD_ERR_UNSUPPORTED, "at most 64 observable terms in tqd_adjoint_grad");
+    for (int t = 0; t < T; t++)
+        if (x[t]) return fail(TQD_ERR_UNSUPPORTED, "tqd_adjoint_grad supports Z-string terms only (x_mask == 0) in this build");
+    rc = execute_pending(st);
+    if (rc) return rc;
+    rc = ensure_lambda(st);
+    if (rc) return rc;
+    rc = ensure_red(st, (size_t)n_grad + 1);
+    if (rc) return rc;
+    tqd_ctx *c = st->ctx;
+    double *d_val = st->d_red;
+    double *d_grad = st->d_red + 1;
+    CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, (n_grad + 1) * sizeof(double), c->stream));
+    ZTerms zt;
+    memset(&zt, 0, sizeof(zt));
+    zt.T = T;
+    for (int t = 0; t < T; t++) {
+        zt.z[t] = phys_mask(st, z[t]);
+        zt.c[t] = coeff ? coeff[t] : 1.0;
+    }
+    const uint64_t N = 1ull << st->n_loc;
+    {
+        const int ev = ev_begin(st, CAT_OTHER);
+        CUDA_TRY(st, launch_lambda_init(st->dbl, st->psi, st->lam, N, rank_hi(st), zt, d_val, c->stream));
+        ev_end(st, ev);
+        st->met.hbm_bytes += 2 * N * st->esz;
+        st->met.kernel_launches++;
+    }
+    // reverse sweep down to (and including) the earliest stage holding a trainable gate
+    int first = -1;
+    for (size_t i = 0; i < st->history.size() && first < 0; i++) {
+        const Stage &s = st->history[i];
+        const std::vector<POp> *ops = s.type == ST_SWEEP ? &s.sw.ops : s.type == ST_SMALL ? &s.sm.ops : nullptr;
+        if (!ops) continue;
+        for (const POp &o : *ops)
+            if (st->gates[o.gate].ngen) { first = (int)i; break; }
+    }
+    if (first >= 0) {
+        std::vector<Stage> rev;
+        for (int i = (int)st->history.size() - 1; i >= first; i--) rev.push_back(st->history[i]);
+        rc = run_stages(st, rev, true, d_grad);
+        if (rc) return rc;
+    }
+    rc = allreduce_sum(st, st->d_red, (size_t)n_grad + 1);
+    if (rc) return rc;
+    std::vector<double> h(n_grad + 1);
+    CUDA_TRY(st, cudaMemcpyAsync(h.data(), st->d_red, (n_grad + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    *out_value = h[0];
+    for (int p = 0; p < n_grad; p++) out_grad[p] = h[p + 1];
+    st->consumed = true;
+    return ev_collect(st);
+}
+
+int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host_out) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (count && !host_out) return fail(TQD_ERR_ARG, "host_out is NULL");
+    const uint64_t total = 1ull << st->n;
+    if (first > total || count > total - first) return fail(TQD_ERR_ARG, "amplitude range out of bounds");
+    rc = execute_pending(st);
+    if (rc) return rc;
+    if (count == 0) return ev_collect(st);
+    GatherMap gm;
+    memset(&gm, 0, sizeof(gm));
+    gm.n = st->n;
+    gm.n_loc = st->n_loc;
+    gm.rank = (uint64_t)st->ctx->rank;
+    for (int b = 0; b < st->n; b++) gm.phys_of_canon_bit[b] = (uint8_t)st->pos[st->n - 1 - b];
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 24);
+    void *tmp = nullptr;
+    if (cudaMalloc(&tmp, chunk * st->esz) != cudaSuccess) { cudaGetLastError(); return fail(TQD_ERR_OOM, "gather buffer"); }
+    tqd_ctx *c = st->ctx;
+    for (uint64_t o = 0; o < count; o += chunk) {
+        const uint64_t cnt = std::min(chunk, count - o);
+        cudaError_t e = launch_gather(st->dbl, st->psi, tmp, first + o, cnt, gm, c->stream);
+        if (e == cudaSuccess && c->world > 1) {
+            ncclResult_t r = ncclAllReduce(tmp, tmp, cnt * 2, st->dbl ? ncclDouble : ncclFloat, ncclSum, c->comm, c->stream);
+            if (r != ncclSuccess) { cudaFree(tmp); c->poisoned = true; return fail(TQD_ERR_NCCL, ncclGetErrorString(r)); }
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync((char *)host_out + o * st->esz, tmp, cnt * st->esz, cudaMemcpyDeviceToHost, c->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) { cudaFree(tmp); c->poisoned = true; return fail(TQD_ERR_CUDA, cudaGetErrorString(e)); }
+        st->met.kernel_launches++;
+    }
+    cudaFree(tmp);
+    return ev_collect(st);
+}
+
+int tqd_get_metrics(const tqd_state *st, tqd_metrics *out) {
+    if (!st || !out) return fail(TQD_ERR_ARG, "NULL argument");
+    *out = st->met;
+    return TQD_OK;
+}
+
+int tqd_reset_metrics(tqd_state *st) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    const uint64_t peak = st->met.peak_device_bytes;
+    memset(&st->met, 0, sizeof(st->met));
+    st->met.peak_device_bytes = peak;
+    return TQD_OK;
+}
+
+// Diagnostic (no GPU needed): plan a circuit and return the stages as JSON.
+// gates: parallel arrays as in tqd_apply_gate (kinds[G], wires[2G], params[3G],
+// mats[32G], trainable[G]).  Returns the needed size if cap is too small.
+int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, const int *kinds, const int *wires,
+                   const double *params, const double *mats, const int *trainable, char *json_out, size_t cap,
+                   size_t *needed) {
+    if (world < 1 || (world & (world - 1))) return fail(TQD_ERR_WORLD, "world size must be a power of two");
+    int g = 0;
+    while ((1 << g) < world) g++;
+    if (n < g + 2 || n > 62) return fail(TQD_ERR_QUBITS, "bad n");
+    std::vector<GateRec> gates;
+    int np = 0;
+    for (int i = 0; i < G; i++) {
+        GateRec r;
+        std::string err;
+        const int nw = gate_arity(kinds[i]);
+        for (int j = 0; j < nw; j++)
+            if (wires[2 * i + j] < 0 || wires[2 * i + j] >= n) return fail(TQD_ERR_ARG, "wire out of range");
+        if (nw == 2 && wires[2 * i] == wires[2 * i + 1]) return fail(TQD_ERR_ARG, "duplicate wires");
+        int rc = make_gate(kinds[i], wires + 2 * i, nw, params + 3 * i, mats + 32 * i, trainable[i], c128 != 0, r, err);
+        if (rc) return fail(rc, err);
+        if (r.trainable) { r.slot0 = np; np += gate_num_params(kinds[i]); }
+        gates.push_back(r);
+    }
+    PlanConfig cfg;
+    cfg.n = n;
+    cfg.n_loc = n - g;
+    cfg.k = std::min(k, n - g);
+    cfg.R = 4;
+    cfg.small_max = small_max;
+    cfg.c128 = c128 != 0;
+    cfg.swz_bits = c128 ? 3 : 4;
+    if (cfg.k - LANE_BITS - cfg.R > WMAX) cfg.k = LANE_BITS + cfg.R + WMAX;
+    std::vector<int> pos(n);
+    for (int q = 0; q < n; q++) pos[q] = n - 1 - q;
+    std::vector<int> pending;
+    for (int i = 0; i < G; i++) pending.push_back(i);
+    std::vector<Stage> stages;
+    std::string err;
+    int rc = plan_circuit(gates, pending, pos, cfg, stages, err);
+    if (rc) return fail(rc, err);
+    std::string js = plan_to_json(stages, cfg);
+    if (needed) *needed = js.size() + 1;
+    if (!json_out || cap < js.size() + 1) return fail(TQD_ERR_ARG, "json buffer too small");
+    memcpy(json_out, js.c_str(), js.size() + 1);
+    return TQD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,394 @@
+// kernels.cu -- sm_100a kernels of the forward + adjoint path.
+//
+//   sweep_kernel<Real, R, BWD>   fused gate sweep over 2^k-amplitude tiles
+//                                (forward: Alg. 1/2 contraction
+//                                Y = M x_Q X for every gate of the stage;
+//                                backward: PAPER.md:220-236 recompute x = U^* y
+//                                plus the gradient contraction, on psi and lambda)
+//   small_kernel<Real, BWD>      whole shard in one CTA's shared memory
+//   lambda_init_kernel           lambda = H psi, E = <psi|H|psi> (Z strings)
+//   expval_z_kernel / expval_xy_kernel   <psi|P_t|psi> partial sums
+//   gather_kernel                canonical-order readback through pi
+//   remap_pack / remap_unpack    qubit-remap staging for the NCCL exchange
+//
+// Data layout in HBM: the shard is an array of interleaved (re, im) complex
+// numbers (float2 for complex64, double2 for complex128), physical index =
+// local bits of the qubit map pi.  See DESIGN.md "Data layout".
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+#include "tqd_internal.h"
+
+namespace tqd {
+
+// ---------------------------------------------------------------------------
+// Small-state kernel: the whole 2^n_loc shard in shared memory, one CTA,
+// gate-by-gate (ops address PHYSICAL positions: t0/t1 local positions,
+// BitRefs are BK_BASE full-index positions).
+__device__ __forceinline__ uint64_t ins0(uint64_t i, int p) {  // insert a 0 bit at position p
+    return ((i >> p) << (p + 1)) | (i & ((1ull << p) - 1));
+}
+
+template <typename Real, bool BWD>
+__global__ void __launch_bounds__(512) small_kernel(const DevOp *__restrict__ ops, int n_ops,
+                                                    typename CT<Real>::C *__restrict__ psi,
+                                                    typename CT<Real>::C *__restrict__ lam,
+                                                    double *__restrict__ grad, int n_loc, uint64_t rank_hi) {
+    typedef typename CT<Real>::C C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[32];
+    const uint64_t N = 1ull << n_loc;
+    C *A = reinterpret_cast<C *>(smem_raw);
+    C *L = A + N;
+    for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        A[i] = psi[i];
+        if (BWD) L[i] = lam[i];
+    }
+    __syncthreads();
+    auto bit = [&](BitRef b, uint64_t idx) -> int { return (int)(((idx | rank_hi) >> b.idx) & 1ull); };
+
+    for (int oi = 0; oi < n_ops; oi++) {
+        const DevOp &op = ops[oi];
+        const int kind = op.kind;
+        if (BWD && op.ngen) {
+            for (int gi = 0; gi < op.ngen; gi++) {
+                Real part = 0;
+                const int gk = op.gkind[gi];
+                if (kind == OP_D1) {
+                    for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+                        Real v = im_cj(L[i], A[i]);
+                        part += bit(op.b0, i) ? -v : v;
+                    }
+                } else {
+                    const int p = op.t0;
+                    const C g00 = ldc<C>(op.g[gi], 0), g01 = ldc<C>(op.g[gi], 1), g10 = ldc<C>(op.g[gi], 2),
+                            g11 = ldc<C>(op.g[gi], 3);
+                    for (uint64_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                        const uint64_t i0 = ins0(i, p), i1 = i0 | (1ull << p);
+                        const C a0 = A[i0], a1 = A[i1], l0 = L[i0], l1 = L[i1];
+                        if (gk == GEN_Y) part += re_cj(l1, a0) - re_cj(l0, a1);
+                        else if (gk == GEN_X) part += im_cj(l0, a1) + im_cj(l1, a0);
+                        else part += 2 * (re_cj(l0, cmul2(g00, a0, g01, a1)) + re_cj(l1, cmul2(g10, a0, g11, a1)));
+                    }
+                }
+                double tot = block_sum<double>((double)part, red);
+                if (threadIdx.x == 0) atomicAdd(&grad[op.slot[gi]], tot);
+                __syncthreads();
+            }
+        }
+        for (int pass = 0; pass < (BWD ? 2 : 1); pass++) {
+            C *X = pass ? L : A;
+            switch (kind) {
+            case OP_U1: case OP_R1: case OP_P1: {
+                const int p = op.t0;
+                C m00, m01, m10, m11;
+                if (kind == OP_U1) { m00 = ldc<C>(op.m, 0); m01 = ldc<C>(op.m, 1); m10 = ldc<C>(op.m, 2); m11 = ldc<C>(op.m, 3); }
+                else if (kind == OP_R1) {
+                    m00 = mk<C>((Real)op.m[0], 0); m01 = mk<C>((Real)op.m[1], 0);
+                    m10 = mk<C>((Real)op.m[2], 0); m11 = mk<C>((Real)op.m[3], 0);
+                } else { m00 = mk<C>(0, 0); m01 = ldc<C>(op.m, 0); m10 = ldc<C>(op.m, 1); m11 = mk<C>(0, 0); }
+                for (uint64_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                    const uint64_t i0 = ins0(i, p), i1 = i0 | (1ull << p);
+                    if (op.ctrl.kind != BK_NONE && !bit(op.ctrl, i0)) continue;
+                    const C x0 = X[i0], x1 = X[i1];
+                    X[i0] = cmul2(m00, x0, m01, x1);
+                    X[i1] = cmul2(m10, x0, m11, x1);
+                }
+                break;
+            }
+            case OP_D1: {
+                const C d0 = ldc<C>(op.m, 0), d1 = ldc<C>(op.m, 1);
+                for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) X[i] = cmul(bit(op.b0, i) ? d1 : d0, X[i]);
+                break;
+            }
+            case OP_D2: {
+                for (uint64_t i = threadIdx.x; i < N; i += blockDim.x)
+                    X[i] = cmul(ldc<C>(op.m, 2 * bit(op.b0, i) + bit(op.b1, i)), X[i]);
+                break;
+            }
+            case OP_U2: {
+                const int p0 = op.t0, p1 = op.t1;
+                const int lo = p0 < p1 ? p0 : p1, hi = p0 < p1 ? p1 : p0;
+                for (uint64_t i = threadIdx.x; i < N / 4; i += blockDim.x) {
+                    const uint64_t b = ins0(ins0(i, lo), hi);
+                    const uint64_t idx[4] = {b, b | (1ull << p1), b | (1ull << p0), b | (1ull << p0) | (1ull << p1)};
+                    C v[4];
+                    for (int q = 0; q < 4; q++) v[q] = X[idx[q]];
+                    for (int r = 0; r < 4; r++) {
+                        C acc = mk<C>(0, 0);
+                        for (int q = 0; q < 4; q++) {
+                            C pr = cmul(ldc<C>(op.m, 4 * r + q), v[q]);
+                            acc.x += pr.x; acc.y += pr.y;
+                        }
+                        X[idx[r]] = acc;
+                    }
+                }
+                break;
+            }
+            default: break;
+            }
+        }
+        __syncthreads();
+    }
+    for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        psi[i] = A[i];
+        if (BWD) lam[i] = L[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Z-string observables in physical masks.
+
+// lambda = H psi with H = sum_t c_t Z_t (diagonal): h(b) = sum_t c_t (-1)^{popc(b & z_t)};
+// E partial = sum_b h(b) |psi_b|^2   (the seed dy of the reverse pass)
+template <typename Real>
+__global__ void __launch_bounds__(256) lambda_init_kernel(const typename CT<Real>::C *__restrict__ psi,
+                                                          typename CT<Real>::C *__restrict__ lam, uint64_t n,
+                                                          uint64_t rank_hi, ZTerms terms, double *__restrict__ eout) {
+    typedef typename CT<Real>::C C;
+    __shared__ double red[32];
+    double acc = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i | rank_hi;
+        Real h = 0;
+        for (int t = 0; t < terms.T; t++) {
+            const Real c = (Real)terms.c[t];
+            h += (__popcll(b & terms.z[t]) & 1) ? -c : c;
+        }
+        const C x = psi[i];
+        lam[i] = mk<C>(h * x.x, h * x.y);
+        acc += (double)(h * (x.x * x.x + x.y * x.y));
+    }
+    double tot = block_sum<double>(acc, red);
+    if (threadIdx.x == 0) atomicAdd(eout, tot);
+}
+
+// out[t] += sum_b |psi_b|^2 (-1)^{popc(b & z_t)}, up to 16 terms per launch
+template <typename Real>
+__global__ void __launch_bounds__(256) expval_z_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n,
+                                                       uint64_t rank_hi, const uint64_t *__restrict__ zmask, int T,
+                                                       double *__restrict__ out) {
+    typedef typename CT<Real>::C C;
+    __shared__ double red[32];
+    Real acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; t++) acc[t] = 0;
+    uint64_t z[16];
+#pragma unroll
+    for (int t = 0; t < 16; t++) z[t] = t < T ? zmask[t] : 0;
+    double dacc[16];
+#pragma unroll
+    for (int t = 0; t < 16; t++) dacc[t] = 0;
+    int cnt = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i | rank_hi;
+        const C x = psi[i];
+        const Real p = x.x * x.x + x.y * x.y;
+#pragma unroll
+        for (int t = 0; t < 16; t++)
+            if (t < T) acc[t] += (__popcll(b & z[t]) & 1) ? -p : p;
+        if (++cnt == 64) {
+#pragma unroll
+            for (int t = 0; t < 16; t++) { dacc[t] += acc[t]; acc[t] = 0; }
+            cnt = 0;
+        }
+    }
+    for (int t = 0; t < T; t++) {
+        double tot = block_sum<double>(dacc[t] + (double)acc[t], red);
+        if (threadIdx.x == 0) atomicAdd(&out[t], tot);
+    }
+}
+
+// out[t] += sum_b Re( i^{ny_t} (-1)^{popc(b & z_t)} conj(psi_{b^x}) psi_b ): one x mask, <= 16 terms
+template <typename Real>
+__global__ void __launch_bounds__(256) expval_xy_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n,
+                                                        uint64_t rank_hi, uint64_t xloc, const uint64_t *__restrict__ zmask,
+                                                        const int *__restrict__ ny, int T, double *__restrict__ out) {
+    typedef typename CT<Real>::C C;
+    __shared__ double red[32];
+    double acc[16];
+#pragma unroll
+    for (int t = 0; t < 16; t++) acc[t] = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i | rank_hi;
+        const C x = psi[i], y = psi[i ^ xloc];
+        const Real re = y.x * x.x + y.y * x.y;  // conj(y) x
+        const Real im = y.x * x.y - y.y * x.x;
+#pragma unroll
+        for (int t = 0; t < 16; t++) {
+            if (t < T) {
+                const int q = ny[t] & 3;  // i^q
+                Real v = q == 0 ? re : q == 1 ? -im : q == 2 ? -re : im;
+                acc[t] += (double)((__popcll(b & zmask[t]) & 1) ? -v : v);
+            }
+        }
+    }
+    for (int t = 0; t < T; t++) {
+        double tot = block_sum<double>(acc[t], red);
+        if (threadIdx.x == 0) atomicAdd(&out[t], tot);
+    }
+}
+
+// canonical index -> physical index through pi; amplitudes owned by other ranks -> 0
+template <typename Real>
+__global__ void gather_kernel(const typename CT<Real>::C *__restrict__ psi, typename CT<Real>::C *__restrict__ out,
+                              uint64_t first, uint64_t count, GatherMap gm) {
+    typedef typename CT<Real>::C C;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = first + i;
+        uint64_t p = 0;
+        for (int b = 0; b < gm.n; b++)
+            if ((c >> b) & 1) p |= 1ull << gm.phys_of_canon_bit[b];
+        const uint64_t r = p >> gm.n_loc;
+        out[i] = (r == gm.rank) ? psi[p & ((1ull << gm.n_loc) - 1)] : mk<C>(0, 0);
+    }
+}
+
+template <typename Real>
+__global__ void set_one_kernel(typename CT<Real>::C *psi) {
+    psi[0] = mk<typename CT<Real>::C>(1, 0);
+}
+
+// Remap staging.  The exchange swaps global positions gpos[i] (rank bit i of
+// the group) with local positions lpos[i], i < m.  pack: send block b (the
+// values of the local bits lpos) collects, in order of the remaining local
+// bits, every amplitude whose lpos-bits equal b.  unpack: the block received
+// from group peer s goes back with lpos-bits := s's rank bits.
+template <typename Real>
+__global__ void remap_pack_kernel(const typename CT<Real>::C *__restrict__ src, typename CT<Real>::C *__restrict__ dst,
+                                  RemapMap rm) {
+    const uint64_t blk = 1ull << (rm.n_loc - rm.m);
+    const uint64_t n = 1ull << rm.n_loc;
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = o / blk, r = o % blk;
+        uint64_t p = 0;
+        for (int i = 0; i < rm.n_loc - rm.m; i++)
+            if ((r >> i) & 1) p |= 1ull << rm.rest[i];
+        for (int i = 0; i < rm.m; i++)
+            if ((b >> i) & 1) p |= 1ull << rm.lpos[i];
+        dst[o] = src[p];
+    }
+}
+template <typename Real>
+__global__ void remap_unpack_kernel(const typename CT<Real>::C *__restrict__ src, typename CT<Real>::C *__restrict__ dst,
+                                    RemapMap rm) {
+    const uint64_t blk = 1ull << (rm.n_loc - rm.m);
+    const uint64_t n = 1ull << rm.n_loc;
+    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t s = o / blk, r = o % blk;
+        uint64_t p = 0;
+        for (int i = 0; i < rm.n_loc - rm.m; i++)
+            if ((r >> i) & 1) p |= 1ull << rm.rest[i];
+        for (int i = 0; i < rm.m; i++)
+            if ((s >> i) & 1) p |= 1ull << rm.lpos[i];
+        dst[p] = src[o];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Launchers (host side, called from engine.cpp)
+cudaError_t launch_sweep_f32_fwd(const DevStage *, const DevOp *, const int32_t *, void *, void *, double *, uint64_t, int, int, int, cudaStream_t);
+cudaError_t launch_sweep_f32_bwd(const DevStage *, const DevOp *, const int32_t *, void *, void *, double *, uint64_t, int, int, int, cudaStream_t);
+cudaError_t launch_sweep_f64_fwd(const DevStage *, const DevOp *, const int32_t *, void *, void *, double *, uint64_t, int, int, int, cudaStream_t);
+cudaError_t launch_sweep_f64_bwd(const DevStage *, const DevOp *, const int32_t *, void *, void *, double *, uint64_t, int, int, int, cudaStream_t);
+int sweep_occupancy_f32_fwd(int k, int W);
+int sweep_occupancy_f32_bwd(int k, int W);
+int sweep_occupancy_f64_fwd(int k, int W);
+int sweep_occupancy_f64_bwd(int k, int W);
+
+cudaError_t launch_sweep(bool dbl, int R, bool bwd, const DevStage *d_stage, const DevOp *d_ops,
+                         const int32_t *d_slots, void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W,
+                         int grid, cudaStream_t s) {
+    if (R != 4) return cudaErrorInvalidValue;
+    if (dbl) return bwd ? launch_sweep_f64_bwd(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, grid, s)
+                        : launch_sweep_f64_fwd(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, grid, s);
+    return bwd ? launch_sweep_f32_bwd(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, grid, s)
+               : launch_sweep_f32_fwd(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, grid, s);
+}
+
+int sweep_max_ctas_per_sm(bool dbl, int R, bool bwd, int k, int W) {
+    (void)R;
+    if (dbl) return bwd ? sweep_occupancy_f64_bwd(k, W) : sweep_occupancy_f64_fwd(k, W);
+    return bwd ? sweep_occupancy_f32_bwd(k, W) : sweep_occupancy_f32_fwd(k, W);
+}
+
+cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad,
+                         int n_loc, uint64_t rank_hi, cudaStream_t s) {
+    const size_t esz = dbl ? 16 : 8;
+    const size_t smem = (size_t)(bwd ? 2 : 1) * ((size_t)1 << n_loc) * esz;
+    const int threads = 512;
+#define TQD_S(T, BB)                                                                                   \
+    {                                                                                                   \
+        auto fn = small_kernel<T, BB>;                                                                  \
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+        if (e != cudaSuccess) return e;                                                                 \
+        fn<<<1, threads, smem, s>>>(d_ops, n_ops, (CT<T>::C *)psi, (CT<T>::C *)lam, grad, n_loc, rank_hi); \
+        return cudaGetLastError();                                                                      \
+    }
+    if (dbl) { if (bwd) TQD_S(double, true) else TQD_S(double, false) }
+    else { if (bwd) TQD_S(float, true) else TQD_S(float, false) }
+#undef TQD_S
+}
+
+static int grid_for(uint64_t n, int threads) {
+    uint64_t g = (n + threads - 1) / threads;
+    if (g > 148 * 8) g = 148 * 8;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
+                               double *eout, cudaStream_t s) {
+    const int th = 256;
+    if (dbl) lambda_init_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, (double2 *)lam, n, rank_hi, t, eout);
+    else lambda_init_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (float2 *)lam, n, rank_hi, t, eout);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expval_z(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const uint64_t *d_z, int T,
+                            double *out, cudaStream_t s) {
+    const int th = 256;
+    if (dbl) expval_z_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, n, rank_hi, d_z, T, out);
+    else expval_z_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, n, rank_hi, d_z, T, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expval_xy(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, uint64_t xloc, const uint64_t *d_z,
+                             const int *d_ny, int T, double *out, cudaStream_t s) {
+    const int th = 256;
+    if (dbl) expval_xy_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, n, rank_hi, xloc, d_z, d_ny, T, out);
+    else expval_xy_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, n, rank_hi, xloc, d_z, d_ny, T, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
+                          cudaStream_t s) {
+    const int th = 256;
+    if (dbl) gather_kernel<double><<<grid_for(count, th), th, 0, s>>>((const double2 *)psi, (double2 *)out, first, count, gm);
+    else gather_kernel<float><<<grid_for(count, th), th, 0, s>>>((const float2 *)psi, (float2 *)out, first, count, gm);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s) {
+    if (dbl) set_one_kernel<double><<<1, 1, 0, s>>>((double2 *)psi);
+    else set_one_kernel<float><<<1, 1, 0, s>>>((float2 *)psi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_remap_pack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s) {
+    const int th = 256;
+    const uint64_t n = 1ull << rm.n_loc;
+    if (dbl) remap_pack_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)src, (double2 *)dst, rm);
+    else remap_pack_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)src, (float2 *)dst, rm);
+    return cudaGetLastError();
+}
+cudaError_t launch_remap_unpack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s) {
+    const int th = 256;
+    const uint64_t n = 1ull << rm.n_loc;
+    if (dbl) remap_unpack_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)src, (double2 *)dst, rm);
+    else remap_unpack_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)src, (float2 *)dst, rm);
+    return cudaGetLastError();
+}
+
+}  // namespace tqd

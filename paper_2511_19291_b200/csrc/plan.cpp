@@ -1,0 +1,861 @@
+// plan.cpp -- gate records, fusion planner and device encoding (host only).
+//
+// See plan.h.  The planner's choices never change results, only the layout and
+// the number of HBM sweeps / exchanges.
+#include "plan.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+#include "../../include/tqd.h"
+
+namespace tqd {
+
+static const cd I1(0.0, 1.0);
+
+int gate_num_params(int kind) {
+    switch (kind) {
+    case TQD_RX: case TQD_RY: case TQD_RZ: return 1;
+    case TQD_U3: return 3;
+    default: return 0;
+    }
+}
+
+int gate_arity(int kind) {
+    switch (kind) {
+    case TQD_CNOT: case TQD_CZ: case TQD_SWAP: case TQD_MAT2: return 2;
+    default: return 1;
+    }
+}
+
+// Textbook matrices (readings R2-R5).
+static void base_matrix(int kind, const double *p, const double *mat, cd *M) {
+    for (int i = 0; i < 16; i++) M[i] = 0.0;
+    const double r2 = 1.0 / std::sqrt(2.0);
+    double c, s;
+    switch (kind) {
+    case TQD_I: M[0] = 1; M[3] = 1; break;
+    case TQD_X: M[1] = 1; M[2] = 1; break;
+    case TQD_Y: M[1] = -I1; M[2] = I1; break;
+    case TQD_Z: M[0] = 1; M[3] = -1; break;
+    case TQD_H: M[0] = r2; M[1] = r2; M[2] = r2; M[3] = -r2; break;
+    case TQD_S: M[0] = 1; M[3] = I1; break;
+    case TQD_SDG: M[0] = 1; M[3] = -I1; break;
+    case TQD_T: M[0] = 1; M[3] = std::polar(1.0, M_PI / 4); break;
+    case TQD_TDG: M[0] = 1; M[3] = std::polar(1.0, -M_PI / 4); break;
+    case TQD_RX: c = std::cos(p[0] / 2); s = std::sin(p[0] / 2);
+        M[0] = c; M[1] = -I1 * s; M[2] = -I1 * s; M[3] = c; break;
+    case TQD_RY: c = std::cos(p[0] / 2); s = std::sin(p[0] / 2);
+        M[0] = c; M[1] = -s; M[2] = s; M[3] = c; break;
+    case TQD_RZ: M[0] = std::polar(1.0, -p[0] / 2); M[3] = std::polar(1.0, p[0] / 2); break;
+    case TQD_U3: c = std::cos(p[0] / 2); s = std::sin(p[0] / 2);
+        M[0] = c; M[1] = -std::polar(1.0, p[2]) * s; M[2] = std::polar(1.0, p[1]) * s;
+        M[3] = std::polar(1.0, p[1] + p[2]) * c; break;
+    case TQD_CNOT: M[0] = 1; M[5] = 1; M[11] = 1; M[14] = 1; break;
+    case TQD_CZ: M[0] = 1; M[5] = 1; M[10] = 1; M[15] = -1; break;
+    case TQD_SWAP: M[0] = 1; M[6] = 1; M[9] = 1; M[15] = 1; break;
+    case TQD_MAT1: for (int i = 0; i < 4; i++) M[i] = cd(mat[2 * i], mat[2 * i + 1]); break;
+    case TQD_MAT2: for (int i = 0; i < 16; i++) M[i] = cd(mat[2 * i], mat[2 * i + 1]); break;
+    default: break;
+    }
+}
+
+// dU/dtheta_which for the parametric kinds
+static void dmatrix(int kind, const double *p, int which, cd *D) {
+    for (int i = 0; i < 4; i++) D[i] = 0.0;
+    double c, s;
+    switch (kind) {
+    case TQD_RX: c = std::cos(p[0] / 2); s = std::sin(p[0] / 2);
+        D[0] = -s / 2; D[1] = -I1 * c / 2.0; D[2] = -I1 * c / 2.0; D[3] = -s / 2; break;
+    case TQD_RY: c = std::cos(p[0] / 2); s = std::sin(p[0] / 2);
+        D[0] = -s / 2; D[1] = -c / 2; D[2] = c / 2; D[3] = -s / 2; break;
+    case TQD_RZ: D[0] = -I1 / 2.0 * std::polar(1.0, -p[0] / 2); D[3] = I1 / 2.0 * std::polar(1.0, p[0] / 2); break;
+    case TQD_U3: c = std::cos(p[0] / 2); s = std::sin(p[0] / 2);
+        if (which == 0) {
+            D[0] = -s / 2; D[1] = -std::polar(1.0, p[2]) * c / 2.0; D[2] = std::polar(1.0, p[1]) * c / 2.0;
+            D[3] = -std::polar(1.0, p[1] + p[2]) * s / 2.0;
+        } else if (which == 1) {
+            D[2] = I1 * std::polar(1.0, p[1]) * s; D[3] = I1 * std::polar(1.0, p[1] + p[2]) * c;
+        } else {
+            D[1] = -I1 * std::polar(1.0, p[2]) * s; D[3] = I1 * std::polar(1.0, p[1] + p[2]) * c;
+        }
+        break;
+    default: break;
+    }
+}
+
+static bool is_zero(cd z) { return z.real() == 0.0 && z.imag() == 0.0; }
+static bool is_one(cd z) { return z.real() == 1.0 && z.imag() == 0.0; }
+
+int make_gate(int kind, const int *wires, int n_wires, const double *params, const double *matrix, int trainable,
+              bool c128, GateRec &g, std::string &err) {
+    if (kind < 0 || kind >= TQD_NUM_GATES) { err = "unknown gate kind"; return TQD_ERR_ARG; }
+    if (n_wires != gate_arity(kind)) { err = "wrong number of wires for gate"; return TQD_ERR_ARG; }
+    if (!wires) { err = "wires is NULL"; return TQD_ERR_ARG; }
+    const int np = gate_num_params(kind);
+    if (np > 0 && !params) { err = "params is NULL for a parametric gate"; return TQD_ERR_ARG; }
+    if ((kind == TQD_MAT1 || kind == TQD_MAT2) && !matrix) { err = "matrix is NULL for MAT1/MAT2"; return TQD_ERR_ARG; }
+    g = GateRec();
+    g.kind = kind;
+    g.nw = n_wires;
+    for (int i = 0; i < n_wires; i++) g.w[i] = g.ow[i] = wires[i];
+    for (int i = 0; i < np; i++) {
+        g.p[i] = params[i];
+        if (!std::isfinite(params[i])) { err = "non-finite gate parameter"; return TQD_ERR_ARG; }
+    }
+    base_matrix(kind, g.p, matrix, g.M);
+    const int dim = n_wires == 2 ? 4 : 2;
+    if (kind == TQD_MAT1 || kind == TQD_MAT2) {
+        double worst = 0;
+        for (int r = 0; r < dim; r++)
+            for (int c = 0; c < dim; c++) {
+                cd acc = 0;
+                for (int q = 0; q < dim; q++) acc += g.M[dim * r + q] * std::conj(g.M[dim * c + q]);
+                if (r == c) acc -= 1.0;
+                if (!std::isfinite(acc.real()) || !std::isfinite(acc.imag())) worst = 1e300;
+                worst = std::max(worst, std::abs(acc));
+            }
+        const double tol = c128 ? 1e-10 : 1e-5;
+        if (worst > tol) {
+            err = "custom matrix is not unitary (||M M^dag - I||_max = " + std::to_string(worst) + ")";
+            return TQD_ERR_NOT_UNITARY;
+        }
+    }
+    g.trainable = (trainable && np > 0) ? 1 : 0;
+
+    // class
+    if (g.trainable) {
+        g.cls = kind == TQD_RZ ? CL_DIAG1 : CL_U1;
+    } else if (dim == 2) {
+        bool diag = is_zero(g.M[1]) && is_zero(g.M[2]);
+        if (diag && is_one(g.M[0]) && is_one(g.M[3])) g.cls = CL_IDENT;
+        else g.cls = diag ? CL_DIAG1 : CL_U1;
+    } else if (kind == TQD_SWAP) {
+        g.cls = CL_SWAP;
+    } else {
+        bool diag = true;
+        for (int r = 0; r < 4; r++)
+            for (int c = 0; c < 4; c++)
+                if (r != c && !is_zero(g.M[4 * r + c])) diag = false;
+        bool ident = diag;
+        for (int r = 0; r < 4; r++) if (!is_one(g.M[5 * r])) ident = false;
+        if (ident) g.cls = CL_IDENT;
+        else if (diag) g.cls = CL_DIAG2;
+        else {
+            // controlled on wires[0]: block diag(I, U) in the (w0 MSB) basis
+            bool c0 = is_one(g.M[0]) && is_one(g.M[5]) && is_zero(g.M[1]) && is_zero(g.M[4]);
+            for (int r = 0; r < 2 && c0; r++)
+                for (int c = 2; c < 4; c++)
+                    if (!is_zero(g.M[4 * r + c]) || !is_zero(g.M[4 * c + r])) c0 = false;
+            // controlled on wires[1]: indices {0,2} identity, {1,3} carry U
+            bool c1 = is_one(g.M[0]) && is_one(g.M[10]) && is_zero(g.M[2]) && is_zero(g.M[8]);
+            for (int r : {0, 2})
+                for (int c : {1, 3})
+                    if (!is_zero(g.M[4 * r + c]) || !is_zero(g.M[4 * c + r])) c1 = false;
+            if (c0) {
+                g.cls = CL_CTRL1;
+                g.sub[0] = g.M[10]; g.sub[1] = g.M[11]; g.sub[2] = g.M[14]; g.sub[3] = g.M[15];
+            } else if (c1) {
+                g.cls = CL_CTRL1;
+                g.sub[0] = g.M[5]; g.sub[1] = g.M[7]; g.sub[2] = g.M[13]; g.sub[3] = g.M[15];
+                std::swap(g.w[0], g.w[1]);  // store as [control, target]
+            } else {
+                g.cls = CL_U2;
+            }
+        }
+    }
+
+    // generators G_p = (dU/dtheta_p) U^dag (anti-Hermitian)
+    if (g.trainable) {
+        g.ngen = np;
+        for (int i = 0; i < np; i++) {
+            cd D[4];
+            dmatrix(kind, g.p, i, D);
+            for (int r = 0; r < 2; r++)
+                for (int c = 0; c < 2; c++) {
+                    cd acc = 0;
+                    for (int q = 0; q < 2; q++) acc += D[2 * r + q] * std::conj(g.M[2 * c + q]);
+                    g.G[i][2 * r + c] = acc;
+                }
+            g.gkind[i] = kind == TQD_RX ? GEN_X : kind == TQD_RY ? GEN_Y : kind == TQD_RZ ? GEN_Z : GEN_FULL;
+        }
+    }
+    return TQD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// planning helpers
+
+// logical wires with roles: targets (need register residency = non-diagonal
+// action) and diagonal wires (controls, diagonal gates)
+static void roles(const GateRec &g, int *tq, int &ntq, int *dq, int &ndq) {
+    ntq = ndq = 0;
+    switch (g.cls) {
+    case CL_U1: tq[ntq++] = g.w[0]; break;
+    case CL_CTRL1: tq[ntq++] = g.w[1]; dq[ndq++] = g.w[0]; break;
+    case CL_U2: tq[ntq++] = g.w[0]; tq[ntq++] = g.w[1]; break;
+    case CL_DIAG1: dq[ndq++] = g.w[0]; break;
+    case CL_DIAG2: dq[ndq++] = g.w[0]; dq[ndq++] = g.w[1]; break;
+    case CL_SWAP: tq[ntq++] = g.w[0]; tq[ntq++] = g.w[1]; break;  // roles only; relabel, no residency
+    default: break;
+    }
+}
+
+static bool real_mat(const cd *m, int n) {
+    for (int i = 0; i < n; i++) if (m[i].imag() != 0.0) return false;
+    return true;
+}
+
+// Build the op (physical positions) for a placed gate.
+static POp make_pop(const GateRec &g, int gi, const std::vector<int> &pos) {
+    POp o;
+    o.gate = gi;
+    o.wp0 = pos[g.ow[0]];
+    if (g.nw == 2) o.wp1 = pos[g.ow[1]];
+    auto set1 = [&](const cd *m, int trainable_kind) {
+        for (int i = 0; i < 4; i++) o.m[i] = m[i];
+        if (trainable_kind == TQD_RX || trainable_kind == TQD_U3) { o.kind = OP_U1; return; }
+        if (trainable_kind == TQD_RY) { o.kind = OP_R1; return; }
+        if (is_zero(m[0]) && is_zero(m[3])) {
+            o.kind = OP_P1;
+            o.plain = is_one(m[1]) && is_one(m[2]);
+        } else if (real_mat(m, 4)) {
+            o.kind = OP_R1;
+        } else {
+            o.kind = OP_U1;
+        }
+    };
+    switch (g.cls) {
+    case CL_U1:
+        o.tp0 = pos[g.w[0]];
+        set1(g.M, g.trainable ? g.kind : -1);
+        break;
+    case CL_CTRL1:
+        o.tp0 = pos[g.w[1]];
+        o.cp = pos[g.w[0]];
+        set1(g.sub, -1);
+        break;
+    case CL_U2:
+        o.kind = OP_U2;
+        o.tp0 = pos[g.w[0]];
+        o.tp1 = pos[g.w[1]];
+        for (int i = 0; i < 16; i++) o.m[i] = g.M[i];
+        break;
+    case CL_DIAG1:
+        o.kind = OP_D1;
+        o.dp0 = pos[g.w[0]];
+        o.m[0] = g.M[0];
+        o.m[1] = g.M[3];
+        break;
+    case CL_DIAG2:
+        o.kind = OP_D2;
+        o.dp0 = pos[g.w[0]];
+        o.dp1 = pos[g.w[1]];
+        for (int i = 0; i < 4; i++) o.m[i] = g.M[5 * i];
+        break;
+    default:
+        o.kind = OP_NONE;
+        break;
+    }
+    return o;
+}
+
+struct Item {      // placed gate (op or relabel) during sweep planning
+    int gate;
+    POp op;        // kind OP_NONE for relabel / identity
+    int relabel_a = -1, relabel_b = -1;  // physical positions swapped (SWAP relabel)
+    std::vector<int> npos;  // positions touched non-diagonally
+    std::vector<int> dpos;  // positions touched diagonally
+    std::vector<int> need;  // tile-local bits that must be register-resident
+};
+
+static int next_target_use(const std::vector<GateRec> &gates, const std::vector<int> &rest, int q) {
+    for (size_t i = 0; i < rest.size(); i++) {
+        const GateRec &g = gates[rest[i]];
+        int tq[2], dq[2], nt, nd;
+        roles(g, tq, nt, dq, nd);
+        if (g.cls == CL_SWAP) continue;
+        for (int j = 0; j < nt; j++)
+            if (tq[j] == q) return (int)i;
+    }
+    return 1 << 30;
+}
+
+static int gf2_rank(std::vector<uint32_t> v) {
+    int r = 0;
+    for (int bit = 31; bit >= 0; bit--) {
+        int piv = -1;
+        for (size_t i = r; i < v.size(); i++)
+            if ((v[i] >> bit) & 1) { piv = (int)i; break; }
+        if (piv < 0) continue;
+        std::swap(v[r], v[piv]);
+        for (size_t i = 0; i < v.size(); i++)
+            if ((int)i != r && ((v[i] >> bit) & 1)) v[i] ^= v[r];
+        r++;
+    }
+    return r;
+}
+
+static std::vector<uint32_t> choose_swizzle(int k, int SW, const std::vector<Layout> &lays) {
+    std::vector<uint32_t> best(k), cur(k);
+    int best_ok = -1;
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
+    for (int trial = 0; trial < 4000; trial++) {
+        for (int t = 0; t < k; t++) {
+            uint32_t f = 0;
+            if (t >= SW && trial > 0) f = (uint32_t)(next() & ((1u << SW) - 1));
+            cur[t] = (1u << t) ^ f;
+        }
+        int ok = 0;
+        for (const Layout &L : lays) {
+            std::vector<uint32_t> v;
+            for (int i = 0; i < SW; i++) v.push_back(cur[L.lane[i]] & ((1u << SW) - 1));
+            if (gf2_rank(v) == SW) ok++;
+        }
+        if (ok > best_ok) { best_ok = ok; best = cur; }
+        if (ok == (int)lays.size()) break;
+    }
+    return best;
+}
+
+// Plan one fused sweep stage.  Returns false if nothing could be placed.
+static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pending, std::vector<int> &pos,
+                       const PlanConfig &cfg, Stage &st) {
+    const int n = cfg.n, n_loc = cfg.n_loc;
+    const int k = std::min(cfg.k, n_loc);
+    const int R = cfg.R;
+    const int W = k - LANE_BITS - R;
+    if (W < 0 || W > WMAX) return false;
+
+    std::vector<int> tile_of(n_loc, -1), tphys;
+    for (int p = 0; p < LANE_BITS; p++) { tile_of[p] = p; tphys.push_back(p); }
+    std::vector<char> blocked(n, 0);
+    std::vector<int> wpos = pos;               // working map (relabels)
+    std::vector<int> wlq(n);
+    for (int q = 0; q < n; q++) wlq[wpos[q]] = q;
+    std::vector<Item> items;
+    std::vector<int> rest;
+    int n_nondiag = 0, n_slots = 0;
+    const int cap_nondiag = R * (MAXSEG - 6);
+
+    for (size_t ii = 0; ii < pending.size(); ii++) {
+        const int gi = pending[ii];
+        const GateRec &g = gates[gi];
+        bool blk = false;
+        for (int j = 0; j < g.nw; j++)
+            if (blocked[g.w[j]]) blk = true;
+        if (!blk && ((int)items.size() >= MAX_STAGE_OPS - 1 || n_slots + g.ngen > MAX_STAGE_SLOTS)) blk = true;
+        int tq[2], dq[2], nt, nd;
+        roles(g, tq, nt, dq, nd);
+        std::vector<int> newbits;
+        if (!blk && g.cls != CL_SWAP && nt > 0) {
+            if (n_nondiag >= cap_nondiag) blk = true;
+            for (int j = 0; j < nt && !blk; j++) {
+                const int p = wpos[tq[j]];
+                if (p >= n_loc) { blk = true; break; }
+                if (tile_of[p] < 0 && std::find(newbits.begin(), newbits.end(), p) == newbits.end()) newbits.push_back(p);
+            }
+            if (!blk && (int)(tphys.size() + newbits.size()) > k) blk = true;
+        }
+        if (blk) {
+            for (int j = 0; j < g.nw; j++) blocked[g.w[j]] = 1;
+            rest.push_back(gi);
+            continue;
+        }
+        for (int p : newbits) { tile_of[p] = (int)tphys.size(); tphys.push_back(p); }
+        Item it;
+        it.gate = gi;
+        if (g.cls == CL_SWAP) {
+            const int a = wpos[g.w[0]], b = wpos[g.w[1]];
+            it.relabel_a = a;
+            it.relabel_b = b;
+            it.npos = {a, b};
+            std::swap(wpos[g.w[0]], wpos[g.w[1]]);
+            wlq[wpos[g.w[0]]] = g.w[0];
+            wlq[wpos[g.w[1]]] = g.w[1];
+        } else {
+            it.op = make_pop(g, gi, wpos);
+            for (int j = 0; j < nt; j++) it.npos.push_back(wpos[tq[j]]);
+            for (int j = 0; j < nd; j++) it.dpos.push_back(wpos[dq[j]]);
+            for (int j = 0; j < nt; j++) it.need.push_back(tile_of[wpos[tq[j]]]);
+            if (nt) n_nondiag++;
+            n_slots += g.ngen;
+        }
+        items.push_back(it);
+    }
+    if (items.empty()) return false;
+
+    // fill the tile to k bits
+    for (int p = 0; p < n_loc && (int)tphys.size() < k; p++)
+        if (tile_of[p] < 0) { tile_of[p] = (int)tphys.size(); tphys.push_back(p); }
+
+    // ---- list scheduling into register layouts (segments) ----
+    const int m = (int)items.size();
+    std::vector<std::vector<int>> succ(m);
+    std::vector<int> indeg(m, 0);
+    for (int j = 0; j < m; j++)
+        for (int i = 0; i < j; i++) {
+            bool conflict = false;
+            for (int p : items[j].npos) {
+                if (std::count(items[i].npos.begin(), items[i].npos.end(), p) ||
+                    std::count(items[i].dpos.begin(), items[i].dpos.end(), p)) conflict = true;
+            }
+            for (int p : items[j].dpos)
+                if (std::count(items[i].npos.begin(), items[i].npos.end(), p)) conflict = true;
+            if (conflict) { succ[i].push_back(j); indeg[j]++; }
+        }
+    std::vector<char> done(m, 0);
+    std::vector<int> order, seg_of;
+    std::vector<std::vector<int>> segregs(1);
+    auto subset = [](const std::vector<int> &a, const std::vector<int> &b) {
+        for (int x : a) if (!std::count(b.begin(), b.end(), x)) return false;
+        return true;
+    };
+    int nseg = 1;
+    while ((int)order.size() < m) {
+        std::vector<int> &cur = segregs[nseg - 1];
+        int pick = -1;
+        for (int i = 0; i < m && pick < 0; i++)
+            if (!done[i] && indeg[i] == 0 && subset(items[i].need, cur)) pick = i;
+        if (pick < 0) {
+            for (int i = 0; i < m && pick < 0; i++) {
+                if (done[i] || indeg[i] != 0) continue;
+                std::vector<int> u = cur;
+                bool ok = true;
+                for (int x : items[i].need) {
+                    if (nseg == 1 && x < LANE_BITS) ok = false;
+                    if (!std::count(u.begin(), u.end(), x)) u.push_back(x);
+                }
+                if (ok && (int)u.size() <= R) { cur = u; pick = i; }
+            }
+        }
+        if (pick < 0) {
+            if (nseg == MAXSEG) break;
+            segregs.push_back({});
+            nseg++;
+            continue;
+        }
+        done[pick] = 1;
+        order.push_back(pick);
+        seg_of.push_back(nseg - 1);
+        for (int j : succ[pick]) indeg[j]--;
+    }
+    // drop empty trailing segment
+    while (nseg > 1 && (seg_of.empty() || seg_of.back() < nseg - 1)) { segregs.pop_back(); nseg--; }
+
+    // items not scheduled go back to pending (closed under successors)
+    std::vector<int> dropped;
+    for (int i = 0; i < m; i++)
+        if (!done[i]) dropped.push_back(items[i].gate);
+
+    // final qubit map after the kept relabels
+    std::vector<int> fpos = pos;
+    for (int oi : order) {
+        const Item &it = items[oi];
+        if (it.relabel_a >= 0) {
+            int qa = -1, qb = -1;
+            for (int q = 0; q < n; q++) {
+                if (fpos[q] == it.relabel_a) qa = q;
+                if (fpos[q] == it.relabel_b) qb = q;
+            }
+            std::swap(fpos[qa], fpos[qb]);
+        }
+    }
+
+    // remaining gates (dropped + blocked), in recording order
+    std::vector<int> remaining = rest;
+    remaining.insert(remaining.end(), dropped.begin(), dropped.end());
+    std::sort(remaining.begin(), remaining.end());
+
+    // ---- layouts ----
+    SweepPlan &sp = st.sw;
+    sp.k = k; sp.R = R; sp.W = W;
+    sp.ld_phys = tphys;
+    sp.lays.assign(nseg, Layout());
+    std::vector<int> fl(n_loc, -1);  // logical qubit at physical position after relabels
+    for (int q = 0; q < n; q++) if (fpos[q] < n_loc) fl[fpos[q]] = q;
+    for (int s = 0; s < nseg; s++) {
+        std::vector<int> regs = segregs[s];
+        for (int t = 0; t < k && (int)regs.size() < R; t++) {
+            if (s == 0 && t < LANE_BITS) continue;
+            if (!std::count(regs.begin(), regs.end(), t)) regs.push_back(t);
+        }
+        std::vector<int> others;
+        for (int t = 0; t < k; t++) if (!std::count(regs.begin(), regs.end(), t)) others.push_back(t);
+        std::vector<int> lanes;
+        if (s == 0) {
+            for (int t = 0; t < LANE_BITS; t++) lanes.push_back(t);
+        } else if (s == nseg - 1) {
+            // qubits used furthest in the future go to physical bits 0..4
+            std::vector<std::pair<long long, int>> cand;
+            for (int t : others) {
+                const int q = fl[tphys[t]];
+                cand.push_back({-(long long)next_target_use(gates, remaining, q), t});
+            }
+            std::sort(cand.begin(), cand.end());
+            for (int i = 0; i < LANE_BITS; i++) lanes.push_back(cand[i].second);
+            std::sort(lanes.begin(), lanes.end());
+        } else {
+            for (int i = 0; i < LANE_BITS; i++) lanes.push_back(others[i]);
+        }
+        std::vector<int> warps;
+        for (int t : others) if (!std::count(lanes.begin(), lanes.end(), t)) warps.push_back(t);
+        Layout &L = sp.lays[s];
+        for (int i = 0; i < R; i++) L.reg[i] = regs[i];
+        for (int i = 0; i < LANE_BITS; i++) L.lane[i] = lanes[i];
+        for (int i = 0; i < WMAX; i++) L.warp[i] = i < W ? warps[i] : 0;
+    }
+    // output permutation sigma: last layout's lanes land on physical 0..4
+    sp.st_phys.assign(k, -1);
+    {
+        const Layout &L = sp.lays[nseg - 1];
+        std::vector<char> used(n_loc, 0);
+        for (int i = 0; i < LANE_BITS; i++) { sp.st_phys[L.lane[i]] = i; used[i] = 1; }
+        std::vector<int> freep;
+        for (int t = LANE_BITS; t < k; t++) {
+            bool moved = sp.st_phys[t] >= 0;
+            if (!moved) { sp.st_phys[t] = tphys[t]; used[tphys[t]] = 1; }
+        }
+        for (int t = LANE_BITS; t < k; t++) if (!used[tphys[t]]) freep.push_back(tphys[t]);
+        size_t fi = 0;
+        for (int t = 0; t < LANE_BITS; t++)
+            if (sp.st_phys[t] < 0) sp.st_phys[t] = freep[fi++];
+    }
+    // ops in schedule order with segment ids
+    sp.seg_begin.assign(nseg + 1, 0);
+    sp.n_gates = 0;
+    for (size_t i = 0; i < order.size(); i++) {
+        const Item &it = items[order[i]];
+        sp.n_gates++;
+        if (it.op.kind == OP_NONE) continue;
+        POp o = it.op;
+        o.seg = seg_of[i];
+        sp.ops.push_back(o);
+    }
+    for (int s = 0, oi = 0; s <= nseg; s++) {
+        while (oi < (int)sp.ops.size() && sp.ops[oi].seg < s) oi++;
+        sp.seg_begin[s] = oi;
+    }
+    sp.seg_begin[nseg] = (int)sp.ops.size();
+    sp.swz = choose_swizzle(k, cfg.swz_bits, sp.lays);
+
+    // new qubit map: relabels, then sigma on the tile
+    st.pos_before = pos;
+    std::vector<int> npos = fpos;
+    for (int q = 0; q < n; q++) {
+        const int p = fpos[q];
+        if (p < n_loc && tile_of[p] >= 0) npos[q] = sp.st_phys[tile_of[p]];
+    }
+    if (sp.ops.empty()) npos = fpos;  // no launch: no sigma
+    pos = npos;
+    st.pos_after = npos;
+    pending = remaining;
+    return true;
+}
+
+static bool plan_small(const std::vector<GateRec> &gates, std::vector<int> &pending, std::vector<int> &pos,
+                       const PlanConfig &cfg, Stage &st) {
+    const int n = cfg.n, n_loc = cfg.n_loc;
+    std::vector<char> blocked(n, 0);
+    std::vector<int> rest;
+    st.pos_before = pos;
+    SmallPlan &sp = st.sm;
+    sp.n_gates = 0;
+    for (size_t ii = 0; ii < pending.size(); ii++) {
+        const int gi = pending[ii];
+        const GateRec &g = gates[gi];
+        bool blk = false;
+        for (int j = 0; j < g.nw; j++) if (blocked[g.w[j]]) blk = true;
+        int tq[2], dq[2], nt, nd;
+        roles(g, tq, nt, dq, nd);
+        if (!blk && g.cls != CL_SWAP)
+            for (int j = 0; j < nt; j++) if (pos[tq[j]] >= n_loc) blk = true;
+        if (blk) {
+            for (int j = 0; j < g.nw; j++) blocked[g.w[j]] = 1;
+            rest.push_back(gi);
+            continue;
+        }
+        sp.n_gates++;
+        if (g.cls == CL_SWAP) { std::swap(pos[g.w[0]], pos[g.w[1]]); continue; }
+        POp o = make_pop(g, gi, pos);
+        if (o.kind != OP_NONE) sp.ops.push_back(o);
+    }
+    if (sp.n_gates == 0) return false;
+    pending = rest;
+    st.pos_after = pos;
+    return true;
+}
+
+static void plan_remap(const std::vector<GateRec> &gates, const std::vector<int> &pending, std::vector<int> &pos,
+                       const PlanConfig &cfg, Stage &st) {
+    const int n = cfg.n, n_loc = cfg.n_loc;
+    std::vector<int> need;  // global physical positions needed as targets soon
+    for (size_t i = 0; i < pending.size() && i < (size_t)(4 * n); i++) {
+        const GateRec &g = gates[pending[i]];
+        if (g.cls == CL_SWAP) continue;
+        int tq[2], dq[2], nt, nd;
+        roles(g, tq, nt, dq, nd);
+        for (int j = 0; j < nt; j++) {
+            const int p = pos[tq[j]];
+            if (p >= n_loc && !std::count(need.begin(), need.end(), p)) need.push_back(p);
+        }
+    }
+    std::sort(need.begin(), need.end());
+    // Belady: evict the local qubits whose next target use is furthest away
+    std::vector<std::pair<long long, int>> cand;
+    std::vector<int> lq(n);
+    for (int q = 0; q < n; q++) lq[pos[q]] = q;
+    for (int p = 0; p < n_loc; p++)
+        cand.push_back({-(long long)next_target_use(gates, pending, lq[p]), -p});
+    std::sort(cand.begin(), cand.end());
+    RemapPlan &rm = st.rm;
+    rm.m = (int)need.size();
+    std::vector<int> lp;
+    for (int i = 0; i < rm.m; i++) lp.push_back(-cand[i].second);
+    std::sort(lp.begin(), lp.end());
+    st.pos_before = pos;
+    for (int i = 0; i < rm.m; i++) {
+        rm.gpos[i] = need[i];
+        rm.lpos[i] = lp[i];
+        const int qa = lq[need[i]], qb = lq[lp[i]];
+        std::swap(pos[qa], pos[qb]);
+        lq[pos[qa]] = qa;
+        lq[pos[qb]] = qb;
+    }
+    st.pos_after = pos;
+}
+
+int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,
+                 const PlanConfig &cfg, std::vector<Stage> &out, std::string &err) {
+    int guard = 0;
+    while (!pending.empty()) {
+        if (++guard > 1000000) { err = "planner did not converge"; return TQD_ERR_STATE; }
+        Stage st;
+        bool ok;
+        if (cfg.n_loc <= cfg.small_max) {
+            st.type = ST_SMALL;
+            ok = plan_small(gates, pending, pos, cfg, st);
+        } else {
+            st.type = ST_SWEEP;
+            ok = plan_sweep(gates, pending, pos, cfg, st);
+        }
+        if (ok) {
+            out.push_back(std::move(st));
+            continue;
+        }
+        if (cfg.n_loc == cfg.n) { err = "planner made no progress on a single-rank state"; return TQD_ERR_STATE; }
+        Stage rs;
+        rs.type = ST_REMAP;
+        plan_remap(gates, pending, pos, cfg, rs);
+        if (rs.rm.m == 0) { err = "planner made no progress"; return TQD_ERR_STATE; }
+        out.push_back(std::move(rs));
+    }
+    return TQD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device encoding
+
+static void put(double *m, int i, cd v) { m[2 * i] = v.real(); m[2 * i + 1] = v.imag(); }
+
+static void fill_matrix(DevOp &d, const POp &o, bool dag) {
+    switch (o.kind) {
+    case OP_U1:
+        if (!dag) for (int i = 0; i < 4; i++) put(d.m, i, o.m[i]);
+        else { put(d.m, 0, std::conj(o.m[0])); put(d.m, 1, std::conj(o.m[2])); put(d.m, 2, std::conj(o.m[1])); put(d.m, 3, std::conj(o.m[3])); }
+        break;
+    case OP_R1:
+        if (!dag) { d.m[0] = o.m[0].real(); d.m[1] = o.m[1].real(); d.m[2] = o.m[2].real(); d.m[3] = o.m[3].real(); }
+        else { d.m[0] = o.m[0].real(); d.m[1] = o.m[2].real(); d.m[2] = o.m[1].real(); d.m[3] = o.m[3].real(); }
+        break;
+    case OP_P1:  // [[0,a],[b,0]]^dag = [[0, conj b], [conj a, 0]]
+        if (!dag) { put(d.m, 0, o.m[1]); put(d.m, 1, o.m[2]); }
+        else { put(d.m, 0, std::conj(o.m[2])); put(d.m, 1, std::conj(o.m[1])); }
+        d.t1 = (uint8_t)o.plain;
+        break;
+    case OP_D1:
+        put(d.m, 0, dag ? std::conj(o.m[0]) : o.m[0]);
+        put(d.m, 1, dag ? std::conj(o.m[1]) : o.m[1]);
+        break;
+    case OP_U2:
+        for (int r = 0; r < 4; r++)
+            for (int c = 0; c < 4; c++) put(d.m, 4 * r + c, dag ? std::conj(o.m[4 * c + r]) : o.m[4 * r + c]);
+        break;
+    case OP_D2:
+        for (int i = 0; i < 4; i++) put(d.m, i, dag ? std::conj(o.m[i]) : o.m[i]);
+        break;
+    default: break;
+    }
+}
+
+static void fill_gens(DevOp &d, const GateRec &g) {
+    d.ngen = (uint8_t)g.ngen;
+    for (int i = 0; i < g.ngen; i++) {
+        d.gkind[i] = g.gkind[i];
+        for (int j = 0; j < 4; j++) put(d.g[i], j, g.G[i][j]);
+    }
+}
+
+void encode_sweep(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
+                  std::vector<DevOp> &ops, std::vector<int32_t> &slot_param) {
+    memset(&ds, 0, sizeof(ds));
+    const int nseg = (int)sp.lays.size();
+    ds.k = sp.k; ds.R = sp.R; ds.W = sp.W; ds.nseg = nseg;
+    ds.n_tiles = (int64_t)1 << (n_loc - sp.k);
+    std::vector<int> sorted = sp.ld_phys;
+    std::sort(sorted.begin(), sorted.end());
+    for (int t = 0; t < sp.k; t++) {
+        ds.ld_phys[t] = (uint8_t)(bwd ? sp.st_phys[t] : sp.ld_phys[t]);
+        ds.st_phys[t] = (uint8_t)(bwd ? sp.ld_phys[t] : sp.st_phys[t]);
+        ds.tile_sorted[t] = (uint8_t)sorted[t];
+        ds.swz[t] = sp.swz[t];
+    }
+    std::vector<int> tile_of(n_loc, -1);
+    for (int t = 0; t < sp.k; t++) tile_of[sp.ld_phys[t]] = t;
+    ds.op_base = (int)ops.size();
+    ds.slot_base = (int)slot_param.size();
+    int nslots = 0;
+    for (int s = 0; s < nseg; s++) {
+        const int fs = bwd ? nseg - 1 - s : s;  // forward segment index
+        const Layout &L = sp.lays[fs];
+        DevLayout &DL = ds.lay[s];
+        for (int i = 0; i < sp.R; i++) DL.reg[i] = (uint8_t)L.reg[i];
+        for (int i = 0; i < LANE_BITS; i++) DL.lane[i] = (uint8_t)L.lane[i];
+        for (int i = 0; i < WMAX; i++) DL.warp[i] = (uint8_t)L.warp[i];
+        ds.seg_begin[s] = (int)ops.size() - ds.op_base;
+        const int b = sp.seg_begin[fs], e = sp.seg_begin[fs + 1];
+        auto regidx = [&](int t) {
+            for (int i = 0; i < sp.R; i++) if (L.reg[i] == t) return i;
+            return -1;
+        };
+        auto bref = [&](int p) {
+            BitRef r;
+            r.kind = BK_NONE; r.idx = 0;
+            if (p < 0) return r;
+            const int t = p < n_loc ? tile_of[p] : -1;
+            if (t >= 0) {
+                const int ri = regidx(t);
+                if (ri >= 0) { r.kind = BK_REG; r.idx = (uint8_t)ri; }
+                else { r.kind = BK_TIX; r.idx = (uint8_t)t; }
+            } else {
+                r.kind = BK_BASE; r.idx = (uint8_t)p;
+            }
+            return r;
+        };
+        for (int jj = 0; jj < e - b; jj++) {
+            const POp &o = sp.ops[bwd ? e - 1 - jj : b + jj];
+            DevOp d;
+            memset(&d, 0, sizeof(d));
+            d.kind = (uint8_t)o.kind;
+            if (o.tp0 >= 0) d.t0 = (uint8_t)regidx(tile_of[o.tp0]);
+            if (o.tp1 >= 0) d.t1 = (uint8_t)regidx(tile_of[o.tp1]);
+            d.ctrl = bref(o.cp);
+            d.b0 = bref(o.dp0);
+            d.b1 = bref(o.dp1);
+            fill_matrix(d, o, bwd);
+            if (bwd && gates[o.gate].ngen) {
+                fill_gens(d, gates[o.gate]);
+                for (int i = 0; i < d.ngen; i++) {
+                    d.slot[i] = nslots++;
+                    slot_param.push_back(gates[o.gate].slot0 + i);
+                }
+            }
+            ops.push_back(d);
+        }
+    }
+    ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
+    ds.n_ops = (int)ops.size() - ds.op_base;
+    ds.n_slots = nslots;
+}
+
+void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops) {
+    const int m = (int)sp.ops.size();
+    for (int jj = 0; jj < m; jj++) {
+        const POp &o = sp.ops[bwd ? m - 1 - jj : jj];
+        DevOp d;
+        memset(&d, 0, sizeof(d));
+        d.kind = (uint8_t)o.kind;
+        if (o.tp0 >= 0) d.t0 = (uint8_t)o.tp0;
+        if (o.tp1 >= 0) d.t1 = (uint8_t)o.tp1;
+        auto bref = [&](int p) {
+            BitRef r;
+            r.kind = p < 0 ? BK_NONE : BK_BASE;
+            r.idx = (uint8_t)(p < 0 ? 0 : p);
+            return r;
+        };
+        d.ctrl = bref(o.cp);
+        d.b0 = bref(o.dp0);
+        d.b1 = bref(o.dp1);
+        fill_matrix(d, o, bwd);
+        if (o.kind == OP_P1) d.t1 = (uint8_t)o.tp1;  // small kernel ignores t1 for P1
+        if (bwd && gates[o.gate].ngen) {
+            fill_gens(d, gates[o.gate]);
+            for (int i = 0; i < d.ngen; i++) d.slot[i] = gates[o.gate].slot0 + i;
+        }
+        ops.push_back(d);
+    }
+}
+
+// ---------------------------------------------------------------------------
+std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg) {
+    std::ostringstream os;
+    os << "{\"n\":" << cfg.n << ",\"n_loc\":" << cfg.n_loc << ",\"k\":" << cfg.k << ",\"R\":" << cfg.R
+       << ",\"stages\":[";
+    for (size_t si = 0; si < stages.size(); si++) {
+        const Stage &st = stages[si];
+        if (si) os << ",";
+        os << "{\"type\":\"" << (st.type == ST_SWEEP ? "sweep" : st.type == ST_SMALL ? "small" : "remap") << "\"";
+        os << ",\"pos_before\":[";
+        for (size_t i = 0; i < st.pos_before.size(); i++) os << (i ? "," : "") << st.pos_before[i];
+        os << "],\"pos_after\":[";
+        for (size_t i = 0; i < st.pos_after.size(); i++) os << (i ? "," : "") << st.pos_after[i];
+        os << "]";
+        auto op_json = [&](const POp &o) {
+            os << "{\"gate\":" << o.gate << ",\"kind\":" << o.kind << ",\"tp0\":" << o.tp0 << ",\"tp1\":" << o.tp1
+               << ",\"cp\":" << o.cp << ",\"dp0\":" << o.dp0 << ",\"dp1\":" << o.dp1 << ",\"seg\":" << o.seg
+               << ",\"wp0\":" << o.wp0 << ",\"wp1\":" << o.wp1 << "}";
+        };
+        if (st.type == ST_SWEEP) {
+            const SweepPlan &sp = st.sw;
+            os << ",\"k\":" << sp.k << ",\"R\":" << sp.R << ",\"W\":" << sp.W << ",\"n_gates\":" << sp.n_gates;
+            os << ",\"ld_phys\":[";
+            for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.ld_phys[t];
+            os << "],\"st_phys\":[";
+            for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.st_phys[t];
+            os << "],\"swz\":[";
+            for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.swz[t];
+            os << "],\"layouts\":[";
+            for (size_t s = 0; s < sp.lays.size(); s++) {
+                const Layout &L = sp.lays[s];
+                os << (s ? "," : "") << "{\"reg\":[";
+                for (int i = 0; i < sp.R; i++) os << (i ? "," : "") << L.reg[i];
+                os << "],\"lane\":[";
+                for (int i = 0; i < LANE_BITS; i++) os << (i ? "," : "") << L.lane[i];
+                os << "],\"warp\":[";
+                for (int i = 0; i < sp.W; i++) os << (i ? "," : "") << L.warp[i];
+                os << "]}";
+            }
+            os << "],\"ops\":[";
+            for (size_t i = 0; i < sp.ops.size(); i++) { if (i) os << ","; op_json(sp.ops[i]); }
+            os << "]";
+        } else if (st.type == ST_SMALL) {
+            os << ",\"n_gates\":" << st.sm.n_gates << ",\"ops\":[";
+            for (size_t i = 0; i < st.sm.ops.size(); i++) { if (i) os << ","; op_json(st.sm.ops[i]); }
+            os << "]";
+        } else {
+            os << ",\"m\":" << st.rm.m << ",\"gpos\":[";
+            for (int i = 0; i < st.rm.m; i++) os << (i ? "," : "") << st.rm.gpos[i];
+            os << "],\"lpos\":[";
+            for (int i = 0; i < st.rm.m; i++) os << (i ? "," : "") << st.rm.lpos[i];
+            os << "]";
+        }
+        os << "}";
+    }
+    os << "]}";
+    return os.str();
+}
+
+}  // namespace tqd

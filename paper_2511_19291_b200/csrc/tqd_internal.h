@@ -1,0 +1,124 @@
+// tqd_internal.h -- descriptors shared by the host planner and the sm_100a kernels.
+//
+// A circuit is executed as a list of STAGES (Alg. 2 + §4.2 in
+// B200 form):
+//   SWEEP  one fused pass over the local shard.  The shard is cut into tiles of
+//          2^k amplitudes: the k "tile-local" bits t = 0..k-1 sit at physical
+//          positions ld_phys[t] (t = 0..4 are always physical bits 0..4 so that
+//          one warp instruction reads one 256 B run).  Inside a CTA the tile is
+//          distributed as   lanes (5 bits) x warps (W bits) x registers (R bits).
+//          A LAYOUT says which tile-local bit each lane / warp / register bit
+//          holds.  Gates run on register bits only (their targets); controls and
+//          diagonal gates may sit on any bit.  Between segments the CTA changes
+//          layout through shared memory (one STS + one LDS per amplitude).  The
+//          store may move tile bits to other tile positions (st_phys), which is
+//          how the qubit map pi changes for free.
+//   SMALL  the whole local shard in one CTA's shared memory (n_loc small);
+//          gate-by-gate, one launch for a whole run of local gates.
+//   REMAP  exchange of global (rank) qubit positions with local positions over
+//          NCCL ("interchanging qubit positions" +
+//          "redistribute across devices", the NCCL all-to-all).
+#pragma once
+#include <stdint.h>
+
+namespace tqd {
+
+constexpr int KMAX = 16;    // max tile bits
+constexpr int RMAX = 5;     // max register bits
+constexpr int WMAX = 3;     // max warp bits (8 warps = 256 threads)
+constexpr int LANE_BITS = 5;
+constexpr int MAXSEG = 24;  // layouts per sweep stage
+constexpr int MAX_STAGE_OPS = 384;
+constexpr int MAX_STAGE_SLOTS = 256;
+
+enum OpKind : uint8_t {
+    OP_NONE = 0,
+    OP_U1 = 1,  // general complex 2x2 on register bit t0 (optional control)
+    OP_R1 = 2,  // real 2x2 on register bit t0 (RY, H, ...) (optional control)
+    OP_P1 = 3,  // [[0, a], [b, 0]] on register bit t0 (X, Y, CNOT's target) (optional control)
+    OP_D1 = 4,  // diag(d0, d1) on bit b0 (any bit) (optional control)
+    OP_U2 = 5,  // general complex 4x4 on register bits (t0 = MSB, t1)
+    OP_D2 = 6,  // diag(d00, d01, d10, d11) on bits (b0 = MSB, b1)
+};
+
+enum BitKind : uint8_t {
+    BK_NONE = 0,
+    BK_REG = 1,   // register bit idx of the current layout
+    BK_TIX = 2,   // tile-local bit idx held by a lane or warp bit (per-thread constant)
+    BK_BASE = 3,  // physical position idx outside the tile (incl. global = rank bits)
+};
+
+enum GenKind : uint8_t {
+    GEN_NONE = 0,
+    GEN_X = 1,     // G = -(i/2) X   (RX)
+    GEN_Y = 2,     // G = -(i/2) Y   (RY)
+    GEN_Z = 3,     // G = -(i/2) Z   (RZ, on a D1 op)
+    GEN_FULL = 4,  // G = (dU/dtheta) U^dag, general 2x2 (U3)
+};
+
+struct BitRef {
+    uint8_t kind;
+    uint8_t idx;
+};
+
+// One gate in device form.  Matrices are float64; float kernels convert on use.
+// For backward ops the matrix is already U^dagger and g[] holds the generators
+// G_p = (dU/dtheta_p) U^dag of the ORIGINAL gate.
+struct alignas(16) DevOp {
+    uint8_t kind;       // OpKind
+    uint8_t t0, t1;     // SWEEP: register-bit indices; SMALL: physical positions
+    uint8_t ngen;       // generators (gradient slots) carried by this op
+    BitRef ctrl;        // control bit (must be 1) or BK_NONE
+    BitRef b0, b1;      // D1 / D2 bits
+    uint8_t gkind[3];   // GenKind per generator
+    uint8_t pad0[5];
+    int32_t slot[3];    // SWEEP: stage-local slot; SMALL: global parameter index
+    int32_t pad1;
+    double m[32];       // U1: 4 complex; R1: 4 real; P1: a, b; D1: d0, d1; U2: 16 complex; D2: 4 complex
+    double g[3][8];     // generator matrices (2x2 complex, row-major re,im)
+};
+
+struct DevLayout {
+    uint8_t reg[RMAX];
+    uint8_t lane[LANE_BITS];
+    uint8_t warp[WMAX];
+    uint8_t pad[2];
+};
+
+struct DevStage {
+    int32_t k, R, W, nseg;
+    int64_t n_tiles;
+    uint8_t ld_phys[KMAX];      // physical position of tile-local bit t at load
+    uint8_t st_phys[KMAX];      // physical position of tile-local bit t at store
+    uint8_t tile_sorted[KMAX];  // the tile's physical positions, ascending
+    uint32_t swz[KMAX];         // shared-memory address vector of tile-local bit t
+    int32_t seg_begin[MAXSEG + 1];
+    DevLayout lay[MAXSEG];
+    int32_t op_base, n_ops;     // into the launch's DevOp array
+    int32_t slot_base, n_slots; // into the launch's slot -> parameter table
+    int32_t lam_init;           // backward only: 1 = build lambda = H psi on load
+    int32_t pad;
+};
+
+// Z-string observable in PHYSICAL masks (full index incl. rank bits)
+struct ZTerms {
+    int T;
+    uint64_t z[64];
+    double c[64];
+};
+
+// canonical index -> physical index through pi (readback)
+struct GatherMap {
+    int n, n_loc;
+    uint64_t rank;
+    uint8_t phys_of_canon_bit[64];  // canonical bit b -> physical position
+};
+
+// remap staging: local positions swapped with the global ones, and the rest
+struct RemapMap {
+    int m, n_loc;
+    uint8_t lpos[8];
+    uint8_t rest[64];  // remaining local positions, ascending (n_loc - m of them)
+};
+
+}  // namespace tqd

@@ -1,0 +1,67 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol that
+include/tqd.h declares, and its host-only entry points validate arguments."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import workloads as W
+
+tqd = pytest.importorskip("paper_2511_19291_b200")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "tqd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tqd_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(tqd.LIB_PATH)
+    names = header_functions()
+    assert len(names) >= 18
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(tqd.EXPORTS)
+
+
+def test_version_string():
+    v = tqd.tqd_version()
+    assert "sm_100a" in v and "NCCL" in v
+
+
+def test_state_bytes():
+    assert tqd.tqd_state_bytes(30, tqd.C64, 1, 1) == 2 * 8 * (1 << 30)
+    assert tqd.tqd_state_bytes(36, tqd.C64, 8, 0) == 8 * (1 << 33) * 3
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_state_bytes(3, tqd.C64, 4, 0)        # n < log2(world) + 2
+    assert e.value.code == -2
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_state_bytes(10, tqd.C64, 3, 0)       # world not a power of two
+    assert e.value.code == -3
+
+
+def test_debug_plan_rejects_bad_gates():
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_debug_plan(4, [W.Gate("CNOT", (1, 1))])
+    assert e.value.code == -1
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_debug_plan(4, [W.Gate("RY", (7,), (0.1,))])
+    assert e.value.code == -1
+    import numpy as np
+    bad = np.array([[1, 1], [0, 1]], complex)
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_debug_plan(4, [W.Gate("MAT1", (0,), (), bad)])
+    assert e.value.code == -4
+
+
+def test_product_path_does_not_import_oracle():
+    """The CUDA path never routes through the oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2511_19291_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f

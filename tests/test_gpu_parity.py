@@ -1,0 +1,322 @@
+"""GPU <-> oracle parity through the C ABI (needs a B200).
+
+Tolerances (BASELINE.json north_star): expectation values and gradients within
+1e-4 absolute for complex64 and 1e-10 for complex128; amplitudes within 1e-5
+max-abs for complex64 (1e-12 for complex128).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": dict(amp=1e-5, val=1e-4), "c128": dict(amp=1e-12, val=1e-10)}
+
+
+@pytest.fixture(scope="module")
+def tqd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need CUDA (run with -m 'not gpu' on CPU)")
+    import paper_2511_19291_b200 as t
+    return t
+
+
+@pytest.fixture(scope="module")
+def ctx(tqd):
+    c = tqd.Context(1, 0, 0)
+    yield c
+    c.close()
+
+
+def make_state(tqd, ctx, n, dtype, k=None, small_max=None):
+    st = tqd.State(ctx, n, dtype)
+    if k is not None:
+        st.set_option(tqd.OPT_TILE_QUBITS, k)
+    if small_max is not None:
+        st.set_option(tqd.OPT_SMALL_MAX, small_max)
+    return st
+
+
+# ---------------------------------------------------------------- amplitudes
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 10])
+def test_small_path_amplitudes(tqd, ctx, orc, n, dtype):
+    for seed in range(3):
+        gates = W.random_circuit(n, 60, seed)
+        st = make_state(tqd, ctx, n, dtype)
+        st.apply_circuit(gates)
+        got = st.amplitudes()
+        st.free()
+        ref = orc.run(n, gates)
+        assert np.max(np.abs(got - ref)) < TOL[dtype]["amp"], (n, seed)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,k", [(9, 9), (11, 10), (12, 12), (13, 11), (15, 12), (17, 12), (18, 9)])
+def test_sweep_path_amplitudes(tqd, ctx, orc, n, k, dtype):
+    """Fused tiled sweeps (forced: small path off); several tiles and k values."""
+    for seed in range(2):
+        gates = W.random_circuit(n, 120, seed + 10 * n)
+        st = make_state(tqd, ctx, n, dtype, k=k, small_max=0)
+        st.apply_circuit(gates)
+        got = st.amplitudes()
+        m = st.metrics()
+        st.free()
+        assert m["fwd_sweeps"] >= 1
+        ref = orc.run(n, gates)
+        assert np.max(np.abs(got - ref)) < TOL[dtype]["amp"], (n, k, seed)
+
+
+def test_incremental_execution(tqd, ctx, orc):
+    """Gates recorded after an execution point continue from the permuted layout."""
+    n = 14
+    g1, g2 = W.random_circuit(n, 50, 1), W.hea(n, 2, 2)
+    st = make_state(tqd, ctx, n, "c64", small_max=0)
+    st.apply_circuit(g1)
+    a1 = st.amplitudes()
+    st.apply_circuit(g2)
+    a2 = st.amplitudes()
+    st.free()
+    assert np.max(np.abs(a1 - orc.run(n, g1))) < 1e-5
+    assert np.max(np.abs(a2 - orc.run(n, g1 + g2))) < 1e-5
+
+
+def test_qft_and_ghz(tqd, ctx, orc):
+    n = 16
+    x = 0xBEEF
+    st = make_state(tqd, ctx, n, "c128", small_max=0)
+    st.apply_circuit(W.basis_prep(n, x) + W.qft(n))
+    got = st.amplitudes()
+    st.free()
+    N = 1 << n
+    ref = np.exp(2j * np.pi * x * np.arange(N) / N) / math.sqrt(N)
+    assert np.max(np.abs(got - ref)) < 1e-12
+    st = make_state(tqd, ctx, n, "c64", small_max=0)
+    st.apply_circuit([W.Gate("H", (0,))] + [W.Gate("CNOT", (q, q + 1)) for q in range(n - 1)])
+    a = st.amplitudes()
+    zz = st.expval([(0, (1 << i) | (1 << j), 1.0) for i in range(0, n, 3) for j in range(i + 1, n, 4)])
+    st.free()
+    ref = np.zeros(N, complex)
+    ref[0] = ref[-1] = 1 / math.sqrt(2)
+    assert np.max(np.abs(a - ref)) < 1e-6
+    assert np.allclose(zz, 1.0, atol=1e-5)
+
+
+def test_amplitude_window(tqd, ctx, orc):
+    n = 13
+    gates = W.random_circuit(n, 80, 5)
+    st = make_state(tqd, ctx, n, "c128", small_max=0)
+    st.apply_circuit(gates)
+    part = st.amplitudes(1000, 777)
+    st.free()
+    assert np.max(np.abs(part - orc.run(n, gates)[1000:1777])) < 1e-12
+
+
+# ---------------------------------------------------------------- expval
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,small_max", [(6, 10), (10, 10), (13, 0), (16, 0)])
+def test_expval_pauli_strings(tqd, ctx, orc, n, small_max, dtype):
+    gates = W.random_circuit(n, 100, n)
+    terms = W.random_pauli_terms(n, 20, n) + W.random_z_terms(n, 20, n) + W.sum_z(n)
+    st = make_state(tqd, ctx, n, dtype, small_max=small_max)
+    st.apply_circuit(gates)
+    got = st.expval(terms)
+    st.free()
+    ref = orc.expval(orc.run(n, gates), n, terms)
+    assert np.max(np.abs(got - ref)) < TOL[dtype]["val"]
+
+
+def test_listing1(tqd, ctx):
+    """PAPER.md:291-308 Listing 1 -> [0.5, 0.5, 1, 1, 1, 1] (tests/golden)."""
+    import json, os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "listing1_measure_allZ.json")))
+    st = make_state(tqd, ctx, 6, "c128")
+    st.apply("Z", [0])
+    st.apply("RY", [0], [math.pi / 3])
+    st.apply("CNOT", [0, 1])
+    got = st.expval(W.sum_z(6))
+    st.free()
+    assert np.allclose(got, gold["expected"], atol=1e-12)
+
+
+# ---------------------------------------------------------------- gradients
+def _grad_check(tqd, ctx, orc, n, gates, terms, dtype, **opt):
+    st = make_state(tqd, ctx, n, dtype, **opt)
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(terms)
+    st.free()
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    tol = TOL[dtype]["val"]
+    assert abs(val - rval) < tol
+    assert grad.shape == rgrad.shape
+    err = np.max(np.abs(grad - rgrad)) if len(grad) else 0.0
+    assert err < tol, (err, np.max(np.abs(rgrad)))
+    return err
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,small_max,k", [(4, 10, None), (9, 10, None), (11, 0, 10), (14, 0, 12), (16, 0, 12)])
+def test_adjoint_random_circuits(tqd, ctx, orc, n, small_max, k, dtype):
+    for seed in range(2):
+        for small in (False, True):
+            gates = W.random_circuit(n, 80, seed + 3 * n, small=small)
+            terms = W.random_z_terms(n, 5, seed) + [(0, 1 << (n - 1), 0.5)]
+            _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=small_max, k=k)
+
+
+def test_cfg1_exact(tqd, ctx, orc):
+    """BASELINE.json configs[0]: 10q HEA depth 4, <Z0> and all 80 gradients, complex128."""
+    wl = W.config(1)
+    assert wl.n_params == 80 and len(wl.gates) == 120
+    _grad_check(tqd, ctx, orc, wl.n, wl.gates, wl.terms, "c128")
+
+
+@pytest.mark.parametrize("small", [False, True])
+def test_hea_sweep_grads(tqd, ctx, orc, small):
+    n = 18
+    gates = W.hea(n, 6, seed=1, small=small)
+    _grad_check(tqd, ctx, orc, n, gates, W.sum_z(n), "c64", small_max=0)
+
+
+def test_listing2_vjp(tqd, ctx, orc):
+    """encoder RY + 3 x (CX ring, RY layer); loss = sum |<Z_i>|:
+    dL/dtheta is one adjoint pass with coefficients sign(<Z_i>) (A22)."""
+    n = 12
+    rng = np.random.default_rng(0)
+    x = rng.uniform(0, math.pi / 3, n)
+    gates = [W.Gate("RY", (i,), (float(x[i]),)) for i in range(n)]
+    for _ in range(3):
+        gates += [W.Gate("CNOT", (i, (i + 1) % n), (), None, False) for i in range(n)]
+        gates += [W.Gate("RY", (i,), (float(rng.uniform(0, 2 * math.pi)),)) for i in range(n)]
+    st = make_state(tqd, ctx, n, "c64", small_max=0)
+    st.apply_circuit(gates)
+    ez = st.expval(W.sum_z(n))
+    st.free()
+    terms = [(0, 1 << q, float(np.sign(ez[q]))) for q in range(n)]
+    _grad_check(tqd, ctx, orc, n, gates, terms, "c64", small_max=0)
+
+
+def test_nontrainable_and_u3(tqd, ctx, orc):
+    n = 13
+    gates = W.random_circuit(n, 60, 9, kinds=["U3", "RX", "RY", "RZ", "CNOT", "CZ", "H"])
+    for g in gates[::3]:
+        g.trainable = False
+    _grad_check(tqd, ctx, orc, n, gates, W.sum_z(n), "c128", small_max=0)
+    _grad_check(tqd, ctx, orc, n, gates, W.sum_z(n), "c128")
+
+
+# ---------------------------------------------------------------- full-size properties
+def test_cfg3_entangler_free_factorization(tqd, ctx, orc):
+    """30q depth-20 RY/RZ ansatz (cfg 3 shape, same launch configuration as bench.py,
+    no CNOTs): E(sum Z_i) and every gradient factor into 1-qubit oracle runs (exact pin)."""
+    n, depth = 30, 20
+    gates = [g for g in W.hea(n, depth, seed=0, small=True) if g.name != "CNOT"]
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(W.sum_z(n))
+    st.free()
+    ref_val, ref_grad = 0.0, np.zeros(len(grad))
+    idx = {id(g): i for i, g in enumerate(gates)}
+    for q in range(n):
+        sub = [g for g in gates if g.wires[0] == q]
+        v, g1 = orc.adjoint(1, [W.Gate(g.name, (0,), g.params) for g in sub], [(0, 1, 1.0)])
+        ref_val += v
+        for g, d in zip(sub, g1):
+            ref_grad[idx[id(g)]] = d
+    assert abs(val - ref_val) < 1e-4
+    assert np.max(np.abs(grad - ref_grad)) < 1e-4
+
+
+def test_cfg3_mirror_circuit(tqd, ctx):
+    """U then U^dag at 30 qubits returns |0..0>: <Z_i> = 1 and psi_0 = 1."""
+    n = 30
+    gates = W.hea(n, 6, seed=4)
+    inv = []
+    for g in reversed(gates):
+        if g.name in ("RY", "RZ"):
+            inv.append(W.Gate(g.name, g.wires, (-g.params[0],)))
+        else:
+            inv.append(g)
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(gates + inv)
+    ez = st.expval(W.sum_z(n))
+    a0 = st.amplitudes(0, 4)
+    st.free()
+    assert np.allclose(ez, 1.0, atol=1e-4)
+    assert abs(a0[0] - 1) < 1e-4 and np.max(np.abs(a0[1:])) < 1e-4
+
+
+def test_cfg3_parameter_shift_spot(tqd, ctx):
+    """Full cfg-3 circuit: adjoint gradients vs parameter shift (two GPU forwards each)."""
+    n = 30
+    gates = W.hea(n, 20, seed=0, small=True)
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(W.sum_z(n))
+    st.free()
+    par = [i for i, g in enumerate(gates) if g.name in W.PARAMETRIC]
+    for pi in (0, 611, 1199):
+        gi = par[pi]
+        es = []
+        for sgn in (+1, -1):
+            gg = list(gates)
+            g = gg[gi]
+            gg[gi] = W.Gate(g.name, g.wires, (g.params[0] + sgn * math.pi / 2,))
+            st = make_state(tqd, ctx, n, "c64")
+            st.apply_circuit(gg)
+            es.append(st.expval(W.sum_z(n)).sum())
+            st.free()
+        assert abs((es[0] - es[1]) / 2 - grad[pi]) < 1e-3
+
+
+# ---------------------------------------------------------------- ABI errors
+def test_abi_errors(tqd, ctx):
+    st = tqd.State(ctx, 5, "c64")
+    with pytest.raises(tqd.TqdError) as e:
+        st.apply("CNOT", [1, 1])
+    assert e.value.code == -1
+    with pytest.raises(tqd.TqdError) as e:
+        st.apply("RY", [9], [0.1])
+    assert e.value.code == -1
+    with pytest.raises(tqd.TqdError) as e:
+        st.apply("MAT1", [0], (), np.array([[1, 1], [0, 1]]))
+    assert e.value.code == -4
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_apply_gate(st.handle, "RY", [0], ())  # missing parameter
+    assert e.value.code == -1
+    st.apply("RY", [0], [0.3])
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_adjoint_grad(st.handle, [(1, 0, 1.0)])  # X term: unsupported in the adjoint
+    assert e.value.code == -8
+    v, g = st.adjoint_grad([(0, 1, 1.0)])
+    assert abs(v - math.cos(0.3)) < 1e-6 and abs(g[0] + math.sin(0.3)) < 1e-6
+    with pytest.raises(tqd.TqdError) as e:
+        st.apply("X", [0])  # consumed
+    assert e.value.code == -9
+    st.reset()
+    st.apply("X", [0])
+    assert abs(st.expval([(0, 1, 1.0)])[0] + 1) < 1e-6
+    st.free()
+    with pytest.raises(tqd.TqdError) as e:
+        tqd.tqd_state_init(ctx.handle, 0, tqd.C64)
+    assert e.value.code == -2
+
+
+def test_metrics_account_bytes(tqd, ctx):
+    n = 20
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(W.hea(n, 3, 0))
+    st.reset_metrics()
+    st.adjoint_grad(W.sum_z(n))
+    m = st.metrics()
+    st.free()
+    sb = 8 << n
+    assert m["fwd_sweeps"] > 0 and m["bwd_sweeps"] == m["fwd_sweeps"]
+    assert m["fwd_sweep_bytes"] == 2 * sb * m["fwd_sweeps"]
+    assert m["bwd_sweep_bytes"] == 4 * sb * m["bwd_sweeps"]
+    assert m["gates_applied"] == 3 * 3 * n
+    assert m["a2a_bytes"] == 0 and m["remaps"] == 0
