@@ -112,6 +112,8 @@ typedef struct tqd_metrics {
     uint64_t bwd_sweep_bytes;   /* algorithmic bytes of adjoint sweeps               */
     uint64_t peak_device_bytes; /* state buffers + scratch held by this state        */
     uint64_t kernel_launches;   /* library kernels launched                          */
+    uint64_t h2d_bytes;         /* host->device bytes (plan descriptors, masks)      */
+    uint64_t d2h_bytes;         /* device->host bytes (values, gradients, amplitudes) */
 } tqd_metrics;
 
 /* --- context ------------------------------------------------------------- */
@@ -142,12 +144,18 @@ int tqd_state_bytes(int n_qubits, tqd_dtype dt, int world, int with_adjoint, siz
  * qubits 0..g-1 (g = log2 world) are the sharded ("global") ones.
  * dev_buf: NULL = the library allocates; else a device buffer of buf_bytes
  * >= tqd_state_bytes(..., with_adjoint=1) that the library carves up.
- * Errors: TQD_ERR_QUBITS when n < g + 2 ("at least two unsharded
- * dimensions") or n > 62; TQD_ERR_OOM.  Collective. */
+ * Errors: TQD_ERR_QUBITS when n > 62, or (world > 1) n < g + 2 (PAPER.md:162
+ * "at least two unsharded dimensions"); TQD_ERR_OOM.  Collective. */
 int tqd_state_init(tqd_ctx *ctx, int n_qubits, tqd_dtype dt, void *dev_buf, size_t buf_bytes,
                    tqd_state **out);
 /* Back to |0...0>, empty tape, pi = identity.  Collective (device memset). */
 int tqd_state_reset(tqd_state *st);
+/* Back to |0...0> and pi = identity but KEEP the recorded tape: the next
+ * tqd_expval / tqd_adjoint_grad re-executes the same circuit with the plan and
+ * device descriptors already resident (no re-planning, no upload).  For
+ * repeated evaluation of one circuit (benchmarks, optimisers that re-record
+ * only when parameters change).  Collective. */
+int tqd_state_rewind(tqd_state *st);
 int tqd_state_free(tqd_state *st);
 int tqd_state_set_option(tqd_state *st, int option, int64_t value);
 

@@ -49,6 +49,7 @@ class Metrics(ctypes.Structure):
         ("other_ms", ctypes.c_double), ("a2a_ms", ctypes.c_double),
         ("fwd_sweep_bytes", ctypes.c_uint64), ("bwd_sweep_bytes", ctypes.c_uint64),
         ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+        ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64),
     ]
 
     def as_dict(self):
@@ -66,6 +67,7 @@ _SIG = {
     "tqd_state_bytes": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)],
     "tqd_state_init": [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, ctypes.POINTER(_P)],
     "tqd_state_reset": [_P],
+    "tqd_state_rewind": [_P],
     "tqd_state_free": [_P],
     "tqd_state_set_option": [_P, ctypes.c_int, ctypes.c_int64],
     "tqd_apply_gate": [_P, ctypes.c_int, _P, ctypes.c_int, _P, _P, ctypes.c_int],
@@ -154,6 +156,10 @@ def tqd_state_init(ctx, n: int, dtype: int, dev_buf: int | None = None, buf_byte
 
 def tqd_state_reset(st):
     _call("tqd_state_reset", st)
+
+
+def tqd_state_rewind(st):
+    _call("tqd_state_rewind", st)
 
 
 def tqd_state_free(st):
@@ -301,6 +307,9 @@ class State:
 
     def reset(self):
         tqd_state_reset(self.handle)
+
+    def rewind(self):
+        tqd_state_rewind(self.handle)
 
     def apply(self, name, wires, params=(), matrix=None, trainable=True):
         tqd_apply_gate(self.handle, name, wires, params, matrix, trainable)

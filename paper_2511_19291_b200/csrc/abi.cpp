@@ -72,11 +72,15 @@ struct tqd_state {
     // options
     int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0;
     tqd_metrics met;
-    // device scratch
-    void *d_scratch = nullptr;
-    size_t scratch_bytes = 0;
     double *d_red = nullptr;  // reductions: values / grads
     size_t red_count = 0;
+    // plan / descriptor caches (tqd_state_rewind replays the same tape)
+    uint64_t tape_version = 1;
+    uint64_t fwd_cache_version = 0, bwd_cache_version = ~0ull;
+    bool history_cached = false;
+    std::vector<Stage> cached_stages, rev_stages;
+    std::vector<int> cached_pos;
+    struct Encoded *enc_fwd = nullptr, *enc_bwd = nullptr, *enc_tmp = nullptr;
     // profiling
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_used;  // (start index, category); stop = start+1
@@ -159,23 +163,6 @@ static PlanConfig plan_cfg(const tqd_state *st) {
     if (c.k > c.n_loc) c.k = c.n_loc;
     if (c.k - LANE_BITS - c.R > WMAX) c.k = LANE_BITS + c.R + WMAX;
     return c;
-}
-
-static int ensure_scratch(tqd_state *st, size_t bytes) {
-    if (bytes <= st->scratch_bytes) return TQD_OK;
-    if (st->d_scratch) {
-        CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream));
-        cudaFree(st->d_scratch);
-        st->d_scratch = nullptr;
-    }
-    size_t nb = std::max(bytes, (size_t)1 << 20);
-    if (cudaMalloc(&st->d_scratch, nb) != cudaSuccess) {
-        cudaGetLastError();
-        st->scratch_bytes = 0;
-        return fail(TQD_ERR_OOM, "cannot allocate descriptor scratch");
-    }
-    st->scratch_bytes = nb;
-    return TQD_OK;
 }
 
 static int ensure_red(tqd_state *st, size_t count) {
@@ -278,52 +265,29 @@ static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd) {
     return (int)g;
 }
 
-// Encode stages [b, e) of `stages` (forward or backward order) into one upload
-// and launch them in order.
-static int run_stages(tqd_state *st, const std::vector<Stage> &stages, bool bwd, double *d_grad) {
-    std::vector<DevStage> dstages;
-    std::vector<DevOp> ops;
-    std::vector<int32_t> slots;
-    struct L { int type; int idx; int op_base; int n_ops; const Stage *s; };
+// Encoded launch list: descriptors of a stage list, uploaded once to the device.
+struct Encoded {
+    void *dev = nullptr;
+    size_t cap = 0;
+    size_t off_ops = 0, off_sl = 0;
+    struct L { int type; int idx; int op_base; int n_ops; int stage; };
     std::vector<L> launches;
-    for (size_t ii = 0; ii < stages.size(); ii++) {
-        const Stage &s = stages[ii];
-        if (s.type == ST_SWEEP) {
-            if (s.sw.ops.empty()) continue;
-            DevStage ds;
-            encode_sweep(s.sw, st->gates, bwd, st->n_loc, ds, ops, slots);
-            launches.push_back({ST_SWEEP, (int)dstages.size(), 0, 0, &s});
-            dstages.push_back(ds);
-        } else if (s.type == ST_SMALL) {
-            if (s.sm.ops.empty()) continue;
-            const int b = (int)ops.size();
-            encode_small(s.sm, st->gates, bwd, ops);
-            launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, &s});
-        } else {
-            launches.push_back({ST_REMAP, -1, 0, 0, &s});
-        }
-    }
-    const size_t b_st = dstages.size() * sizeof(DevStage);
-    const size_t b_ops = ops.size() * sizeof(DevOp);
-    const size_t b_sl = slots.size() * sizeof(int32_t);
-    const size_t off_ops = (b_st + 255) & ~(size_t)255;
-    const size_t off_sl = (off_ops + b_ops + 255) & ~(size_t)255;
-    const size_t total = off_sl + b_sl + 256;
-    int rc = ensure_scratch(st, total);
-    if (rc) return rc;
-    std::vector<char> host(total, 0);
-    if (b_st) memcpy(host.data(), dstages.data(), b_st);
-    if (b_ops) memcpy(host.data() + off_ops, ops.data(), b_ops);
-    if (b_sl) memcpy(host.data() + off_sl, slots.data(), b_sl);
+    bool valid = false;
+};
+
+static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E);
+
+// Launch an encoded stage list (forward or backward) on the context stream.
+static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool bwd, const Encoded &E, double *d_grad) {
     tqd_ctx *c = st->ctx;
-    CUDA_TRY(st, cudaMemcpyAsync(st->d_scratch, host.data(), total, cudaMemcpyHostToDevice, c->stream));
-    const DevStage *d_st = (const DevStage *)st->d_scratch;
-    const DevOp *d_ops = (const DevOp *)((char *)st->d_scratch + off_ops);
-    const int32_t *d_sl = (const int32_t *)((char *)st->d_scratch + off_sl);
+    const DevStage *d_st = (const DevStage *)E.dev;
+    const DevOp *d_ops = (const DevOp *)((char *)E.dev + E.off_ops);
+    const int32_t *d_sl = (const int32_t *)((char *)E.dev + E.off_sl);
     const uint64_t sb = shard_bytes(st);
-    for (const L &l : launches) {
+    for (const Encoded::L &l : E.launches) {
+        const Stage &s = stages[l.stage];
         if (l.type == ST_SWEEP) {
-            const SweepPlan &sp = l.s->sw;
+            const SweepPlan &sp = s.sw;
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, sp.R, bwd, d_st + l.idx, d_ops, d_sl, st->psi, st->lam, d_grad,
                                       rank_hi(st), sp.k, sp.W, sweep_grid(st, sp, bwd), c->stream));
@@ -336,29 +300,114 @@ static int run_stages(tqd_state *st, const std::vector<Stage> &stages, bool bwd,
             CUDA_TRY(st, launch_small(st->dbl, bwd, d_ops + l.op_base, l.n_ops, st->psi, st->lam, d_grad, st->n_loc,
                                       rank_hi(st), c->stream));
             ev_end(st, ev);
-            if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += l.s->sm.n_gates; }
-            else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += l.s->sm.n_gates; }
+            if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += s.sm.n_gates; }
+            else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += s.sm.n_gates; }
             st->met.kernel_launches++;
         } else {
-            rc = exec_remap(st, l.s->rm, st->psi);
+            int rc = exec_remap(st, s.rm, st->psi);
             if (rc) return rc;
-            if (bwd) { rc = exec_remap(st, l.s->rm, st->lam); if (rc) return rc; }
+            if (bwd) { rc = exec_remap(st, s.rm, st->lam); if (rc) return rc; }
             st->met.remaps++;
         }
     }
     return TQD_OK;
 }
 
+static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E) {
+    std::vector<DevStage> dstages;
+    std::vector<DevOp> ops;
+    std::vector<int32_t> slots;
+    E.launches.clear();
+    E.valid = false;
+    for (size_t ii = 0; ii < stages.size(); ii++) {
+        const Stage &s = stages[ii];
+        if (s.type == ST_SWEEP) {
+            if (s.sw.ops.empty()) continue;
+            DevStage ds;
+            encode_sweep(s.sw, st->gates, bwd, st->n_loc, ds, ops, slots);
+            E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, 0, (int)ii});
+            dstages.push_back(ds);
+        } else if (s.type == ST_SMALL) {
+            if (s.sm.ops.empty()) continue;
+            const int b = (int)ops.size();
+            encode_small(s.sm, st->gates, bwd, ops);
+            E.launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, (int)ii});
+        } else {
+            E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii});
+        }
+    }
+    const size_t b_st = dstages.size() * sizeof(DevStage);
+    const size_t b_ops = ops.size() * sizeof(DevOp);
+    const size_t b_sl = slots.size() * sizeof(int32_t);
+    E.off_ops = (b_st + 255) & ~(size_t)255;
+    E.off_sl = (E.off_ops + b_ops + 255) & ~(size_t)255;
+    const size_t total = E.off_sl + b_sl + 256;
+    if (total > E.cap) {
+        if (E.dev) {
+            CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream));
+            cudaFree(E.dev);
+            E.dev = nullptr;
+        }
+        const size_t nb = std::max(total, (size_t)1 << 20);
+        if (cudaMalloc(&E.dev, nb) != cudaSuccess) {
+            cudaGetLastError();
+            E.cap = 0;
+            return fail(TQD_ERR_OOM, "cannot allocate descriptor buffer");
+        }
+        E.cap = nb;
+    }
+    std::vector<char> host(total, 0);
+    if (b_st) memcpy(host.data(), dstages.data(), b_st);
+    if (b_ops) memcpy(host.data() + E.off_ops, ops.data(), b_ops);
+    if (b_sl) memcpy(host.data() + E.off_sl, slots.data(), b_sl);
+    // pageable source: the copy is staged before cudaMemcpyAsync returns and is
+    // stream-ordered after earlier launches that may still read this buffer
+    CUDA_TRY(st, cudaMemcpyAsync(E.dev, host.data(), total, cudaMemcpyHostToDevice, st->ctx->stream));
+    st->met.h2d_bytes += total;
+    E.valid = true;
+    return TQD_OK;
+}
+
+static void free_encoded(Encoded &E) {
+    if (E.dev) cudaFree(E.dev);
+    E.dev = nullptr;
+    E.cap = 0;
+    E.valid = false;
+}
+
 static int execute_pending(tqd_state *st) {
     if (st->executed == st->gates.size()) return TQD_OK;
+    if (st->executed == 0 && st->fwd_cache_version == st->tape_version && st->enc_fwd->valid) {
+        // replay of the same tape from |0..0> (tqd_state_rewind): plan + descriptors are resident
+        st->history = st->cached_stages;
+        int rc = launch_encoded(st, st->history, false, *st->enc_fwd, nullptr);
+        if (rc) return rc;
+        st->pos = st->cached_pos;
+        st->executed = st->gates.size();
+        st->history_cached = true;
+        return TQD_OK;
+    }
     std::vector<int> pending;
     for (size_t i = st->executed; i < st->gates.size(); i++) pending.push_back((int)i);
     std::vector<Stage> stages;
     std::string err;
+    const bool from_zero = st->executed == 0;
     int rc = plan_circuit(st->gates, pending, st->pos, plan_cfg(st), stages, err);
     if (rc) return fail(rc, err);
-    rc = run_stages(st, stages, false, nullptr);
+    Encoded &E = from_zero ? *st->enc_fwd : *st->enc_tmp;
+    rc = encode_upload(st, stages, false, E);
     if (rc) return rc;
+    rc = launch_encoded(st, stages, false, E, nullptr);
+    if (rc) return rc;
+    if (from_zero) {
+        st->cached_stages = stages;
+        st->cached_pos = st->pos;
+        st->fwd_cache_version = st->tape_version;
+        st->bwd_cache_version = ~0ull;
+        st->history_cached = true;
+    } else {
+        st->history_cached = false;
+    }
     for (auto &s : stages) st->history.push_back(std::move(s));
     st->executed = st->gates.size();
     return TQD_OK;
@@ -459,7 +508,7 @@ int tqd_state_bytes(int n, tqd_dtype dt, int world, int with_adjoint, size_t *ou
     if (world < 1 || (world & (world - 1))) return fail(TQD_ERR_WORLD, "world size must be a power of two");
     int g = 0;
     while ((1 << g) < world) g++;
-    if (n < g + 2 || n > 62) return fail(TQD_ERR_QUBITS, "need g + 2 <= n <= 62");
+    if (n < (g ? g + 2 : 1) || n > 62) return fail(TQD_ERR_QUBITS, "need g + 2 <= n <= 62");
     const size_t esz = dt == TQD_C128 ? 16 : 8;
     const size_t shard = ((size_t)1 << (n - g)) * esz;
     *out = shard * (with_adjoint ? 2 : 1) + (world > 1 ? 2 * shard : 0);
@@ -473,7 +522,7 @@ int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_by
     if (dt != TQD_C64 && dt != TQD_C128) return fail(TQD_ERR_ARG, "bad dtype");
     int g = 0;
     while ((1 << g) < c->world) g++;
-    if (n < g + 2 || n > 62)
+    if (n < (g ? g + 2 : 1) || n > 62)
         return fail(TQD_ERR_QUBITS, "n must satisfy log2(world) + 2 <= n <= 62 (PAPER.md:162: at least two unsharded qubits)");
     tqd_state *st = new tqd_state();
     st->ctx = c;
@@ -483,6 +532,9 @@ int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_by
     st->dbl = dt == TQD_C128;
     st->esz = st->dbl ? 16 : 8;
     memset(&st->met, 0, sizeof(st->met));
+    st->enc_fwd = new Encoded();
+    st->enc_bwd = new Encoded();
+    st->enc_tmp = new Encoded();
     const size_t sb = shard_bytes(st);
     if (dev_buf) {
         if (buf_bytes < sb) { delete st; return fail(TQD_ERR_OOM, "dev_buf smaller than one shard"); }
@@ -513,6 +565,8 @@ int tqd_state_reset(tqd_state *st) {
     if (rc) return rc;
     st->gates.clear();
     st->history.clear();
+    st->tape_version++;
+    st->history_cached = false;
     st->n_params = 0;
     st->executed = 0;
     st->consumed = false;
@@ -527,13 +581,33 @@ int tqd_state_reset(tqd_state *st) {
     return ev_collect(st);
 }
 
+int tqd_state_rewind(tqd_state *st) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    st->history.clear();
+    st->history_cached = false;
+    st->executed = 0;
+    st->consumed = false;
+    st->pos.assign(st->n, 0);
+    for (int q = 0; q < st->n; q++) st->pos[q] = st->n - 1 - q;
+    const int ev = ev_begin(st, CAT_OTHER);
+    CUDA_TRY(st, cudaMemsetAsync(st->psi, 0, shard_bytes(st), st->ctx->stream));
+    if (st->ctx->rank == 0) CUDA_TRY(st, launch_set_one(st->dbl, st->psi, st->ctx->stream));
+    ev_end(st, ev);
+    st->met.hbm_bytes += shard_bytes(st);
+    st->met.kernel_launches += 1;
+    return TQD_OK;
+}
+
 int tqd_state_free(tqd_state *st) {
     if (!st) return fail(TQD_ERR_ARG, "state is NULL");
     if (st->ctx && st->ctx->stream) cudaStreamSynchronize(st->ctx->stream);
     if (st->own_psi) cudaFree(st->psi);
     if (st->own_lam) cudaFree(st->lam);
     if (st->own_xchg) { cudaFree(st->sendb); cudaFree(st->recvb); }
-    if (st->d_scratch) cudaFree(st->d_scratch);
+    for (Encoded *E : {st->enc_fwd, st->enc_bwd, st->enc_tmp}) {
+        if (E) { free_encoded(*E); delete E; }
+    }
     if (st->d_red) cudaFree(st->d_red);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
     delete st;
@@ -577,6 +651,7 @@ int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires, con
         st->n_params += gate_num_params((int)g);
     }
     st->gates.push_back(rec);
+    st->tape_version++;
     return TQD_OK;
 }
 
@@ -661,6 +736,7 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
     std::vector<double> h(T);
     CUDA_TRY(st, cudaMemcpyAsync(h.data(), d_out, T * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    st->met.d2h_bytes += T * sizeof(double);
     for (int t = 0; t < T; t++) out[t] = (coeff ? coeff[t] : 1.0) * h[t];
     return ev_collect(st);
 }
@@ -713,9 +789,20 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
             if (st->gates[o.gate].ngen) { first = (int)i; break; }
     }
     if (first >= 0) {
-        std::vector<Stage> rev;
-        for (int i = (int)st->history.size() - 1; i >= first; i--) rev.push_back(st->history[i]);
-        rc = run_stages(st, rev, true, d_grad);
+        // backward stage list = the forward history reversed; its descriptors are
+        // cached with the forward plan when the history is the cached one
+        const bool cacheable = st->history_cached && st->fwd_cache_version == st->tape_version;
+        if (!(cacheable && st->bwd_cache_version == st->tape_version && st->enc_bwd->valid)) {
+            st->rev_stages.clear();
+            for (int i = (int)st->history.size() - 1; i >= first; i--) st->rev_stages.push_back(st->history[i]);
+            Encoded &E = cacheable ? *st->enc_bwd : *st->enc_tmp;
+            rc = encode_upload(st, st->rev_stages, true, E);
+            if (rc) return rc;
+            st->bwd_cache_version = cacheable ? st->tape_version : ~0ull;
+            rc = launch_encoded(st, st->rev_stages, true, E, d_grad);
+        } else {
+            rc = launch_encoded(st, st->rev_stages, true, *st->enc_bwd, d_grad);
+        }
         if (rc) return rc;
     }
     rc = allreduce_sum(st, st->d_red, (size_t)n_grad + 1);
@@ -723,6 +810,7 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
     std::vector<double> h(n_grad + 1);
     CUDA_TRY(st, cudaMemcpyAsync(h.data(), st->d_red, (n_grad + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    st->met.d2h_bytes += (n_grad + 1) * sizeof(double);
     *out_value = h[0];
     for (int p = 0; p < n_grad; p++) out_grad[p] = h[p + 1];
     st->consumed = true;
@@ -757,6 +845,7 @@ int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host
             if (r != ncclSuccess) { cudaFree(tmp); c->poisoned = true; return fail(TQD_ERR_NCCL, ncclGetErrorString(r)); }
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync((char *)host_out + o * st->esz, tmp, cnt * st->esz, cudaMemcpyDeviceToHost, c->stream);
+        st->met.d2h_bytes += cnt * st->esz;
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e != cudaSuccess) { cudaFree(tmp); c->poisoned = true; return fail(TQD_ERR_CUDA, cudaGetErrorString(e)); }
         st->met.kernel_launches++;
