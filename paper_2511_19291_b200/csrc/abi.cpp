@@ -16,9 +16,10 @@
 
 namespace tqd {
 // kernels.cu
-cudaError_t launch_sweep(bool dbl, int R, bool bwd, const DevStage *d_stage, const DevOp *d_ops, const int32_t *d_slots,
-                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int grid, cudaStream_t s);
-int sweep_max_ctas_per_sm(bool dbl, int R, bool bwd, int k, int W);
+cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int grid,
+                         cudaStream_t s);
+int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
                          uint64_t rank_hi, cudaStream_t s);
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
@@ -255,9 +256,9 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
 }
 
 // ---- forward execution ------------------------------------------------------
-static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd) {
+static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops) {
     if (st->opt_grid > 0) return st->opt_grid;
-    int per = sweep_max_ctas_per_sm(st->dbl, sp.R, bwd, sp.k, sp.W);
+    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops);
     if (per < 1) per = 1;
     int64_t g = (int64_t)per * st->ctx->sms;
     const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
@@ -270,7 +271,8 @@ struct Encoded {
     void *dev = nullptr;
     size_t cap = 0;
     size_t off_ops = 0, off_sl = 0;
-    struct L { int type; int idx; int op_base; int n_ops; int stage; };
+    size_t off_kops = 0;
+    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; };
     std::vector<L> launches;
     bool valid = false;
 };
@@ -282,6 +284,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
     tqd_ctx *c = st->ctx;
     const DevStage *d_st = (const DevStage *)E.dev;
     const DevOp *d_ops = (const DevOp *)((char *)E.dev + E.off_ops);
+    const char *d_kops = (const char *)E.dev + E.off_kops;
     const int32_t *d_sl = (const int32_t *)((char *)E.dev + E.off_sl);
     const uint64_t sb = shard_bytes(st);
     for (const Encoded::L &l : E.launches) {
@@ -289,8 +292,8 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
         if (l.type == ST_SWEEP) {
             const SweepPlan &sp = s.sw;
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
-            CUDA_TRY(st, launch_sweep(st->dbl, sp.R, bwd, d_st + l.idx, d_ops, d_sl, st->psi, st->lam, d_grad,
-                                      rank_hi(st), sp.k, sp.W, sweep_grid(st, sp, bwd), c->stream));
+            CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
+                                      sp.k, sp.W, l.n_ops, l.grid, c->stream));
             ev_end(st, ev);
             if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += sp.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
@@ -313,34 +316,47 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
     return TQD_OK;
 }
 
-static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E) {
-    std::vector<DevStage> dstages;
-    std::vector<DevOp> ops;
-    std::vector<int32_t> slots;
-    E.launches.clear();
-    E.valid = false;
+template <typename Real>
+static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E,
+                       std::vector<DevStage> &dstages, std::vector<DevOp> &ops, std::vector<KOp<Real>> &kops,
+                       std::vector<int32_t> &slots) {
     for (size_t ii = 0; ii < stages.size(); ii++) {
         const Stage &s = stages[ii];
         if (s.type == ST_SWEEP) {
             if (s.sw.ops.empty()) continue;
             DevStage ds;
-            encode_sweep(s.sw, st->gates, bwd, st->n_loc, ds, ops, slots);
-            E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, 0, (int)ii});
+            encode_sweep_k<Real>(s.sw, st->gates, bwd, st->n_loc, ds, kops, slots);
+            E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
+                                  sweep_grid(st, s.sw, bwd, ds.n_ops)});
             dstages.push_back(ds);
         } else if (s.type == ST_SMALL) {
             if (s.sm.ops.empty()) continue;
             const int b = (int)ops.size();
             encode_small(s.sm, st->gates, bwd, ops);
-            E.launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, (int)ii});
+            E.launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, (int)ii, 1});
         } else {
-            E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii});
+            E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii, 0});
         }
     }
+}
+
+static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E) {
+    std::vector<DevStage> dstages;
+    std::vector<DevOp> ops;
+    std::vector<KOp<float>> kf;
+    std::vector<KOp<double>> kd;
+    std::vector<int32_t> slots;
+    E.launches.clear();
+    E.valid = false;
+    if (st->dbl) encode_all<double>(st, stages, bwd, E, dstages, ops, kd, slots);
+    else encode_all<float>(st, stages, bwd, E, dstages, ops, kf, slots);
     const size_t b_st = dstages.size() * sizeof(DevStage);
     const size_t b_ops = ops.size() * sizeof(DevOp);
+    const size_t b_k = st->dbl ? kd.size() * sizeof(KOp<double>) : kf.size() * sizeof(KOp<float>);
     const size_t b_sl = slots.size() * sizeof(int32_t);
     E.off_ops = (b_st + 255) & ~(size_t)255;
-    E.off_sl = (E.off_ops + b_ops + 255) & ~(size_t)255;
+    E.off_kops = (E.off_ops + b_ops + 255) & ~(size_t)255;
+    E.off_sl = (E.off_kops + b_k + 255) & ~(size_t)255;
     const size_t total = E.off_sl + b_sl + 256;
     if (total > E.cap) {
         if (E.dev) {
@@ -359,6 +375,7 @@ static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool b
     std::vector<char> host(total, 0);
     if (b_st) memcpy(host.data(), dstages.data(), b_st);
     if (b_ops) memcpy(host.data() + E.off_ops, ops.data(), b_ops);
+    if (b_k) memcpy(host.data() + E.off_kops, st->dbl ? (const void *)kd.data() : (const void *)kf.data(), b_k);
     if (b_sl) memcpy(host.data() + E.off_sl, slots.data(), b_sl);
     // pageable source: the copy is staged before cudaMemcpyAsync returns and is
     // stream-ordered after earlier launches that may still read this buffer

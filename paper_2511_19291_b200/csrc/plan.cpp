@@ -298,7 +298,48 @@ static int gf2_rank(std::vector<uint32_t> v) {
     return r;
 }
 
-static std::vector<uint32_t> choose_swizzle(int k, int SW, const std::vector<Layout> &lays) {
+bool TileMap::identity() const {
+    if (cst || !aff.empty()) return false;
+    for (int t = 0; t < KMAX; t++)
+        if (col[t] != (1u << t)) return false;
+    return true;
+}
+
+static TileMap identity_map() {
+    TileMap m;
+    for (int t = 0; t < KMAX; t++) m.col[t] = 1u << t;
+    return m;
+}
+
+// x_t ^= x_c (or ^= 1, or ^= a bit outside the tile), composed after m
+static void map_apply_perm(TileMap &m, int t, int c_tile, int c_pos) {
+    auto tr = [&](uint32_t v) { return (c_tile >= 0 && ((v >> c_tile) & 1)) ? v ^ (1u << t) : v; };
+    for (int j = 0; j < KMAX; j++) m.col[j] = tr(m.col[j]);
+    m.cst = tr(m.cst);
+    for (auto &a : m.aff) a.second = tr(a.second);
+    if (c_tile < 0) {
+        if (c_pos < 0) {
+            m.cst ^= 1u << t;
+        } else {
+            bool found = false;
+            for (auto &a : m.aff)
+                if (a.first == c_pos) { a.second ^= 1u << t; found = true; }
+            if (!found) m.aff.push_back({c_pos, 1u << t});
+        }
+    }
+}
+
+static uint32_t lin(const uint32_t *cols, uint32_t v) {
+    uint32_t r = 0;
+    for (int t = 0; v; t++, v >>= 1)
+        if (v & 1) r ^= cols[t];
+    return r;
+}
+
+// Shared-memory swizzle: address(y) = y ^ F(y's high bits) in the low SW bits.
+// Chosen so that, for every exchange, the lane bits 0..SW-1 of the write and of
+// the read side hit distinct banks (SW = 4 for 8 B elements, 3 for 16 B).
+static std::vector<uint32_t> choose_swizzle(int k, int SW, const std::vector<std::vector<uint32_t>> &sets) {
     std::vector<uint32_t> best(k), cur(k);
     int best_ok = -1;
     uint64_t rng = 0x9E3779B97F4A7C15ull;
@@ -310,13 +351,13 @@ static std::vector<uint32_t> choose_swizzle(int k, int SW, const std::vector<Lay
             cur[t] = (1u << t) ^ f;
         }
         int ok = 0;
-        for (const Layout &L : lays) {
+        for (const auto &set : sets) {
             std::vector<uint32_t> v;
-            for (int i = 0; i < SW; i++) v.push_back(cur[L.lane[i]] & ((1u << SW) - 1));
+            for (uint32_t y : set) v.push_back(lin(cur.data(), y) & ((1u << SW) - 1));
             if (gf2_rank(v) == SW) ok++;
         }
         if (ok > best_ok) { best_ok = ok; best = cur; }
-        if (ok == (int)lays.size()) break;
+        if (ok == (int)sets.size()) break;
     }
     return best;
 }
@@ -339,7 +380,8 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     std::vector<Item> items;
     std::vector<int> rest;
     int n_nondiag = 0, n_slots = 0;
-    const int cap_nondiag = R * (MAXSEG - 6);
+    const int cap_nondiag = R * (MAXSEG - 4);
+    std::vector<int> aff_pos;  // distinct control positions outside the tile of folded CNOTs
 
     for (size_t ii = 0; ii < pending.size(); ii++) {
         const int gi = pending[ii];
@@ -380,8 +422,20 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
             it.op = make_pop(g, gi, wpos);
             for (int j = 0; j < nt; j++) it.npos.push_back(wpos[tq[j]]);
             for (int j = 0; j < nd; j++) it.dpos.push_back(wpos[dq[j]]);
-            for (int j = 0; j < nt; j++) it.need.push_back(tile_of[wpos[tq[j]]]);
-            if (nt) n_nondiag++;
+            // X / CNOT with the target in the tile: a GF(2)-affine index map,
+            // folded into the next layout change (no register residency needed)
+            if (it.op.kind == OP_P1 && it.op.plain && !g.trainable) {
+                const int cpos = it.op.cp;
+                const bool outside = cpos >= 0 && (cpos >= n_loc || tile_of[cpos] < 0);
+                if (!outside) it.op.perm = 1;
+                else if (std::count(aff_pos.begin(), aff_pos.end(), cpos) || (int)aff_pos.size() < NAFF) {
+                    it.op.perm = 1;
+                    if (!std::count(aff_pos.begin(), aff_pos.end(), cpos)) aff_pos.push_back(cpos);
+                }
+            }
+            if (!it.op.perm)
+                for (int j = 0; j < nt; j++) it.need.push_back(tile_of[wpos[tq[j]]]);
+            if (nt && !it.op.perm) n_nondiag++;
             n_slots += g.ngen;
         }
         items.push_back(it);
@@ -394,8 +448,9 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
 
     // ---- list scheduling into register layouts (segments) ----
     const int m = (int)items.size();
+    auto is_perm = [&](int i) { return items[i].op.perm != 0; };
     std::vector<std::vector<int>> succ(m);
-    std::vector<int> indeg(m, 0);
+    std::vector<int> indeg(m, 0), ready_seg(m, 0);
     for (int j = 0; j < m; j++)
         for (int i = 0; i < j; i++) {
             bool conflict = false;
@@ -408,7 +463,7 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
             if (conflict) { succ[i].push_back(j); indeg[j]++; }
         }
     std::vector<char> done(m, 0);
-    std::vector<int> order, seg_of;
+    std::vector<int> order, seg_of(m, -1);
     std::vector<std::vector<int>> segregs(1);
     auto subset = [](const std::vector<int> &a, const std::vector<int> &b) {
         for (int x : a) if (!std::count(b.begin(), b.end(), x)) return false;
@@ -416,17 +471,22 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     };
     int nseg = 1;
     while ((int)order.size() < m) {
-        std::vector<int> &cur = segregs[nseg - 1];
+        const int cs = nseg - 1;
+        std::vector<int> &cur = segregs[cs];
+        auto eligible = [&](int i) { return !done[i] && indeg[i] == 0 && ready_seg[i] <= cs; };
         int pick = -1;
+        // permutation gates first (free), then ops whose targets are already resident
         for (int i = 0; i < m && pick < 0; i++)
-            if (!done[i] && indeg[i] == 0 && subset(items[i].need, cur)) pick = i;
+            if (eligible(i) && is_perm(i)) pick = i;
+        for (int i = 0; i < m && pick < 0; i++)
+            if (eligible(i) && subset(items[i].need, cur)) pick = i;
         if (pick < 0) {
             for (int i = 0; i < m && pick < 0; i++) {
-                if (done[i] || indeg[i] != 0) continue;
+                if (!eligible(i)) continue;
                 std::vector<int> u = cur;
                 bool ok = true;
                 for (int x : items[i].need) {
-                    if (nseg == 1 && x < LANE_BITS) ok = false;
+                    if (cs == 0 && x < LANE_BITS) ok = false;
                     if (!std::count(u.begin(), u.end(), x)) u.push_back(x);
                 }
                 if (ok && (int)u.size() <= R) { cur = u; pick = i; }
@@ -440,11 +500,41 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         }
         done[pick] = 1;
         order.push_back(pick);
-        seg_of.push_back(nseg - 1);
-        for (int j : succ[pick]) indeg[j]--;
+        seg_of[pick] = cs;
+        for (int j : succ[pick]) {
+            indeg[j]--;
+            const int rs = (is_perm(pick) && !is_perm(j)) ? cs + 1 : cs;
+            ready_seg[j] = std::max(ready_seg[j], rs);
+        }
     }
-    // drop empty trailing segment
-    while (nseg > 1 && (seg_of.empty() || seg_of.back() < nseg - 1)) { segregs.pop_back(); nseg--; }
+    // drop empty trailing segments
+    auto last_used = [&]() {
+        int ls = 0;
+        for (int i : order) ls = std::max(ls, seg_of[i]);
+        return ls;
+    };
+    // permutation gates left in the last segment would need a final map at the
+    // store (uncoalesced): hand them back to the next stage, unless the stage
+    // has nothing else (then a trailing empty segment realises them)
+    {
+        const int ls = last_used();
+        bool any_arith = false;
+        for (int i : order) if (!is_perm(i)) any_arith = true;
+        if (any_arith) {
+            std::vector<int> keep;
+            for (int i : order) {
+                if (is_perm(i) && seg_of[i] == ls) { done[i] = 0; seg_of[i] = -1; }
+                else keep.push_back(i);
+            }
+            order = keep;
+            nseg = last_used() + 1;
+        } else {
+            nseg = std::max(2, last_used() + 2);
+            if (nseg > MAXSEG) nseg = MAXSEG;
+        }
+        while ((int)segregs.size() < nseg) segregs.push_back({});
+        segregs.resize(nseg);
+    }
 
     // items not scheduled go back to pending (closed under successors)
     std::vector<int> dropped;
@@ -524,23 +614,49 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         for (int t = 0; t < LANE_BITS; t++)
             if (sp.st_phys[t] < 0) sp.st_phys[t] = freep[fi++];
     }
-    // ops in schedule order with segment ids
+    // ops in schedule order with segment ids; per-segment permutation maps
     sp.seg_begin.assign(nseg + 1, 0);
+    sp.maps.assign(nseg, identity_map());
     sp.n_gates = 0;
+    sp.n_arith = 0;
     for (size_t i = 0; i < order.size(); i++) {
         const Item &it = items[order[i]];
         sp.n_gates++;
         if (it.op.kind == OP_NONE) continue;
         POp o = it.op;
-        o.seg = seg_of[i];
+        o.seg = seg_of[order[i]];
+        if (o.perm) {
+            const int t = tile_of[o.tp0];
+            const int ct = (o.cp >= 0 && o.cp < n_loc) ? tile_of[o.cp] : -1;
+            map_apply_perm(sp.maps[o.seg], t, ct, ct >= 0 ? -1 : o.cp);
+        } else {
+            sp.n_arith++;
+        }
         sp.ops.push_back(o);
     }
+    // ops sorted by segment (stable: schedule order inside a segment)
+    std::stable_sort(sp.ops.begin(), sp.ops.end(), [](const POp &a, const POp &b) { return a.seg < b.seg; });
     for (int s = 0, oi = 0; s <= nseg; s++) {
         while (oi < (int)sp.ops.size() && sp.ops[oi].seg < s) oi++;
         sp.seg_begin[s] = oi;
     }
     sp.seg_begin[nseg] = (int)sp.ops.size();
-    sp.swz = choose_swizzle(k, cfg.swz_bits, sp.lays);
+    // swizzle: per exchange, the write side's lane vectors (through the map)
+    // and the read side's lane vectors must be bank-conflict free
+    {
+        std::vector<std::vector<uint32_t>> sets;
+        const int SW = cfg.swz_bits;
+        for (int s = 0; s + 1 < nseg; s++) {
+            std::vector<uint32_t> w, r;
+            for (int i = 0; i < SW; i++) {
+                w.push_back(sp.maps[s].col[sp.lays[s].lane[i]]);
+                r.push_back(1u << sp.lays[s + 1].lane[i]);
+            }
+            sets.push_back(w);
+            sets.push_back(r);
+        }
+        sp.swz = choose_swizzle(k, SW, sets);
+    }
 
     // new qubit map: relabels, then sigma on the tile
     st.pos_before = pos;
@@ -699,10 +815,25 @@ static void fill_gens(DevOp &d, const GateRec &g) {
     }
 }
 
-void encode_sweep(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
-                  std::vector<DevOp> &ops, std::vector<int32_t> &slot_param) {
+// The 2x2 an op applies to its target / diagonal bit (forward or adjoint form).
+static void op_matrix2(const POp &o, bool dag, cd *M) {
+    cd F[4];
+    switch (o.kind) {
+    case OP_U1: case OP_R1: F[0] = o.m[0]; F[1] = o.m[1]; F[2] = o.m[2]; F[3] = o.m[3]; break;
+    case OP_P1: F[0] = 0.0; F[1] = o.m[1]; F[2] = o.m[2]; F[3] = 0.0; break;
+    case OP_D1: F[0] = o.m[0]; F[1] = 0.0; F[2] = 0.0; F[3] = o.m[1]; break;
+    default: F[0] = 1.0; F[1] = 0.0; F[2] = 0.0; F[3] = 1.0; break;
+    }
+    if (!dag) { for (int i = 0; i < 4; i++) M[i] = F[i]; }
+    else { M[0] = std::conj(F[0]); M[1] = std::conj(F[2]); M[2] = std::conj(F[1]); M[3] = std::conj(F[3]); }
+}
+
+template <typename Real>
+void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
+                    std::vector<KOp<Real>> &ops, std::vector<int32_t> &slot_param) {
     memset(&ds, 0, sizeof(ds));
     const int nseg = (int)sp.lays.size();
+    const int R = sp.R;
     ds.k = sp.k; ds.R = sp.R; ds.W = sp.W; ds.nseg = nseg;
     ds.n_tiles = (int64_t)1 << (n_loc - sp.k);
     std::vector<int> sorted = sp.ld_phys;
@@ -718,17 +849,32 @@ void encode_sweep(const SweepPlan &sp, const std::vector<GateRec> &gates, bool b
     ds.op_base = (int)ops.size();
     ds.slot_base = (int)slot_param.size();
     int nslots = 0;
+    auto newop = [](int kind) {
+        KOp<Real> k;
+        memset(&k, 0, sizeof(k));
+        k.kind = (uint8_t)kind;
+        k.creg = 0xff;
+        return k;
+    };
+    auto add_gen = [&](KOp<Real> &k, const GateRec &g, int i, int bit) {
+        const int j = k.ngen++;
+        k.gbit[j] = (uint8_t)bit;
+        k.gkind[j] = g.gkind[i];
+        for (int q = 0; q < 4; q++) { k.g[j][2 * q] = (Real)g.G[i][q].real(); k.g[j][2 * q + 1] = (Real)g.G[i][q].imag(); }
+        k.slot[j] = (int16_t)nslots++;
+        slot_param.push_back(g.slot0 + i);
+    };
     for (int s = 0; s < nseg; s++) {
-        const int fs = bwd ? nseg - 1 - s : s;  // forward segment index
+        const int fs = bwd ? nseg - 1 - s : s;
         const Layout &L = sp.lays[fs];
         DevLayout &DL = ds.lay[s];
-        for (int i = 0; i < sp.R; i++) DL.reg[i] = (uint8_t)L.reg[i];
+        for (int i = 0; i < R; i++) DL.reg[i] = (uint8_t)L.reg[i];
         for (int i = 0; i < LANE_BITS; i++) DL.lane[i] = (uint8_t)L.lane[i];
         for (int i = 0; i < WMAX; i++) DL.warp[i] = (uint8_t)L.warp[i];
         ds.seg_begin[s] = (int)ops.size() - ds.op_base;
-        const int b = sp.seg_begin[fs], e = sp.seg_begin[fs + 1];
-        auto regidx = [&](int t) {
-            for (int i = 0; i < sp.R; i++) if (L.reg[i] == t) return i;
+        auto regidx = [&](int p) {
+            if (p < 0 || p >= n_loc || tile_of[p] < 0) return -1;
+            for (int i = 0; i < R; i++) if (L.reg[i] == tile_of[p]) return i;
             return -1;
         };
         auto bref = [&](int p) {
@@ -736,40 +882,157 @@ void encode_sweep(const SweepPlan &sp, const std::vector<GateRec> &gates, bool b
             r.kind = BK_NONE; r.idx = 0;
             if (p < 0) return r;
             const int t = p < n_loc ? tile_of[p] : -1;
-            if (t >= 0) {
-                const int ri = regidx(t);
-                if (ri >= 0) { r.kind = BK_REG; r.idx = (uint8_t)ri; }
-                else { r.kind = BK_TIX; r.idx = (uint8_t)t; }
-            } else {
-                r.kind = BK_BASE; r.idx = (uint8_t)p;
-            }
+            const int ri = regidx(p);
+            if (ri >= 0) { r.kind = BK_REG; r.idx = (uint8_t)ri; }
+            else if (t >= 0) { r.kind = BK_TIX; r.idx = (uint8_t)t; }
+            else { r.kind = BK_BASE; r.idx = (uint8_t)p; }
             return r;
         };
-        for (int jj = 0; jj < e - b; jj++) {
-            const POp &o = sp.ops[bwd ? e - 1 - jj : b + jj];
-            DevOp d;
-            memset(&d, 0, sizeof(d));
-            d.kind = (uint8_t)o.kind;
-            if (o.tp0 >= 0) d.t0 = (uint8_t)regidx(tile_of[o.tp0]);
-            if (o.tp1 >= 0) d.t1 = (uint8_t)regidx(tile_of[o.tp1]);
-            d.ctrl = bref(o.cp);
-            d.b0 = bref(o.dp0);
-            d.b1 = bref(o.dp1);
-            fill_matrix(d, o, bwd);
-            if (bwd && gates[o.gate].ngen) {
-                fill_gens(d, gates[o.gate]);
-                for (int i = 0; i < d.ngen; i++) {
-                    d.slot[i] = nslots++;
-                    slot_param.push_back(gates[o.gate].slot0 + i);
+        // current fused layer
+        bool active = false;
+        int mask = 0;
+        cd LM[RMAX][4];
+        KOp<Real> layer = newop(K_LAYER);
+        auto flush = [&]() {
+            if (!active) return;
+            bool real = true, diag = true;
+            for (int b = 0; b < R; b++) {
+                if (!((mask >> b) & 1)) continue;
+                for (int q = 0; q < 4; q++) if (LM[b][q].imag() != 0.0) real = false;
+                if (LM[b][1] != cd(0.0) || LM[b][2] != cd(0.0)) diag = false;
+            }
+            layer.mask = (uint8_t)mask;
+            layer.ltype = diag ? LT_DIAG : real ? LT_REAL : LT_GEN;
+            for (int b = 0; b < R; b++) {
+                if (!((mask >> b) & 1)) continue;
+                Real *m = layer.m + 8 * b;
+                if (layer.ltype == LT_REAL) {
+                    for (int q = 0; q < 4; q++) m[q] = (Real)LM[b][q].real();
+                } else if (layer.ltype == LT_DIAG) {
+                    m[0] = (Real)LM[b][0].real(); m[1] = (Real)LM[b][0].imag();
+                    m[2] = (Real)LM[b][3].real(); m[3] = (Real)LM[b][3].imag();
+                } else {
+                    for (int q = 0; q < 4; q++) { m[2 * q] = (Real)LM[b][q].real(); m[2 * q + 1] = (Real)LM[b][q].imag(); }
                 }
             }
-            ops.push_back(d);
+            ops.push_back(layer);
+            active = false;
+            mask = 0;
+            layer = newop(K_LAYER);
+        };
+        const int b = sp.seg_begin[fs], e = sp.seg_begin[fs + 1];
+        for (int jj = 0; jj < e - b; jj++) {
+            const POp &o = sp.ops[bwd ? e - 1 - jj : b + jj];
+            if (o.perm) continue;  // folded into the layout-change maps below
+            const GateRec &g = gates[o.gate];
+            const bool has_gen = bwd && g.ngen > 0;
+            int bit = -1;
+            if ((o.kind == OP_U1 || o.kind == OP_R1 || o.kind == OP_P1) && o.cp < 0) bit = regidx(o.tp0);
+            else if (o.kind == OP_D1 && o.cp < 0) bit = regidx(o.dp0);
+            if (bit >= 0) {
+                cd M[4];
+                op_matrix2(o, bwd, M);
+                const bool clash = active && ((mask >> bit) & 1);
+                if (active && (bwd ? (clash || layer.ngen + g.ngen > KOP_MAXGEN) : false)) flush();
+                if (active && clash && !bwd) {
+                    cd P[4];  // later op after earlier: M * LM
+                    P[0] = M[0] * LM[bit][0] + M[1] * LM[bit][2];
+                    P[1] = M[0] * LM[bit][1] + M[1] * LM[bit][3];
+                    P[2] = M[2] * LM[bit][0] + M[3] * LM[bit][2];
+                    P[3] = M[2] * LM[bit][1] + M[3] * LM[bit][3];
+                    for (int q = 0; q < 4; q++) LM[bit][q] = P[q];
+                } else {
+                    active = true;
+                    mask |= 1 << bit;
+                    for (int q = 0; q < 4; q++) LM[bit][q] = M[q];
+                }
+                if (has_gen)
+                    for (int i = 0; i < g.ngen; i++) add_gen(layer, g, i, bit);
+                continue;
+            }
+            flush();
+            KOp<Real> k = newop(K_NOP);
+            cd M[4];
+            switch (o.kind) {
+            case OP_U1: case OP_R1: case OP_P1: {
+                // controlled 1q (CNOT, controlled MAT2); targets are always register bits
+                op_matrix2(o, bwd, M);
+                k.kind = K_CU;
+                k.t0 = (uint8_t)regidx(o.tp0);
+                const int cr = regidx(o.cp);
+                if (cr >= 0) k.creg = (uint8_t)cr;
+                else if (o.cp >= 0) k.ctrl = bref(o.cp);
+                for (int q = 0; q < 4; q++) { k.m[2 * q] = (Real)M[q].real(); k.m[2 * q + 1] = (Real)M[q].imag(); }
+                break;
+            }
+            case OP_D1: {
+                op_matrix2(o, bwd, M);
+                k.kind = K_PHASE;
+                k.b0 = bref(o.dp0);
+                k.m[0] = (Real)M[0].real(); k.m[1] = (Real)M[0].imag();
+                k.m[2] = (Real)M[3].real(); k.m[3] = (Real)M[3].imag();
+                if (has_gen) add_gen(k, g, 0, 0);
+                break;
+            }
+            case OP_D2: {
+                k.kind = K_D2;
+                k.b0 = bref(o.dp0);
+                k.b1 = bref(o.dp1);
+                for (int q = 0; q < 4; q++) {
+                    const cd d = bwd ? std::conj(o.m[q]) : o.m[q];
+                    k.m[2 * q] = (Real)d.real(); k.m[2 * q + 1] = (Real)d.imag();
+                }
+                break;
+            }
+            case OP_U2: {
+                k.kind = K_U2;
+                k.t0 = (uint8_t)regidx(o.tp0);
+                k.t1 = (uint8_t)regidx(o.tp1);
+                for (int r = 0; r < 4; r++)
+                    for (int c = 0; c < 4; c++) {
+                        const cd v = bwd ? std::conj(o.m[4 * c + r]) : o.m[4 * r + c];
+                        k.m[8 * r + 2 * c] = (Real)v.real();
+                        k.m[8 * r + 2 * c + 1] = (Real)v.imag();
+                    }
+                break;
+            }
+            default: continue;
+            }
+            ops.push_back(k);
         }
+        flush();
     }
     ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
     ds.n_ops = (int)ops.size() - ds.op_base;
     ds.n_slots = nslots;
+    // layout changes: forward exchange s applies the map of forward segment s on
+    // the write side; the adjoint (exchange from forward layout f+1 to f) applies
+    // it on the read side (amp_pre[x] = amp_post[A x + b])
+    const uint32_t *swz = sp.swz.data();
+    for (int x = 0; x + 1 < nseg; x++) {
+        const int f = bwd ? nseg - 2 - x : x;
+        const TileMap &M = sp.maps[f];
+        uint32_t *mcol = bwd ? ds.rcol[x] : ds.wcol[x];
+        uint32_t *pcol = bwd ? ds.wcol[x] : ds.rcol[x];
+        for (int t = 0; t < sp.k; t++) {
+            mcol[t] = lin(swz, M.col[t]);
+            pcol[t] = swz[t];
+        }
+        (bwd ? ds.rcst[x] : ds.wcst[x]) = lin(swz, M.cst);
+        (bwd ? ds.wcst[x] : ds.rcst[x]) = 0;
+        ds.aff_read[x] = bwd ? 1 : 0;
+        ds.naff[x] = (uint8_t)M.aff.size();
+        for (size_t i = 0; i < M.aff.size() && i < (size_t)NAFF; i++) {
+            ds.aff_pos[x][i] = (uint8_t)M.aff[i].first;
+            ds.aff_vec[x][i] = lin(swz, M.aff[i].second);
+        }
+    }
 }
+
+template void encode_sweep_k<float>(const SweepPlan &, const std::vector<GateRec> &, bool, int, DevStage &,
+                                    std::vector<KOp<float>> &, std::vector<int32_t> &);
+template void encode_sweep_k<double>(const SweepPlan &, const std::vector<GateRec> &, bool, int, DevStage &,
+                                     std::vector<KOp<double>> &, std::vector<int32_t> &);
 
 void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops) {
     const int m = (int)sp.ops.size();
@@ -816,7 +1079,7 @@ std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg
         auto op_json = [&](const POp &o) {
             os << "{\"gate\":" << o.gate << ",\"kind\":" << o.kind << ",\"tp0\":" << o.tp0 << ",\"tp1\":" << o.tp1
                << ",\"cp\":" << o.cp << ",\"dp0\":" << o.dp0 << ",\"dp1\":" << o.dp1 << ",\"seg\":" << o.seg
-               << ",\"wp0\":" << o.wp0 << ",\"wp1\":" << o.wp1 << "}";
+               << ",\"wp0\":" << o.wp0 << ",\"wp1\":" << o.wp1 << ",\"perm\":" << o.perm << "}";
         };
         if (st.type == ST_SWEEP) {
             const SweepPlan &sp = st.sw;

@@ -62,6 +62,16 @@ struct POp {
     int plain = 0;           // OP_P1: plain swap
     int seg = 0;             // sweep segment
     int wp0 = -1, wp1 = -1;  // diagnostics: positions of the gate's wires[0], wires[1] at placement
+    int perm = 0;            // 1: CNOT / X on a tile bit, realised as an index map (no arithmetic)
+};
+
+// GF(2)-affine map on tile-local indices accumulated from the permutation gates
+// (CNOT, X) of one segment: x -> A x + c + sum_j [bit p_j of the full index] v_j
+struct TileMap {
+    uint32_t col[KMAX];               // A e_t
+    uint32_t cst = 0;                 // c
+    std::vector<std::pair<int, uint32_t>> aff;  // (physical position p_j outside the tile, v_j)
+    bool identity() const;
 };
 
 struct Layout {
@@ -77,7 +87,9 @@ struct SweepPlan {
     std::vector<int> seg_begin;         // size lays+1
     std::vector<POp> ops;               // in execution order, seg ascending
     std::vector<uint32_t> swz;
+    std::vector<TileMap> maps;          // per segment: permutation gates applied after its ops
     int n_gates = 0;                    // gates applied (incl. relabels / identities)
+    int n_arith = 0;                    // ops needing arithmetic (kernel launch needed if > 0 or maps)
 };
 
 struct SmallPlan {
@@ -116,8 +128,9 @@ int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, st
                  const PlanConfig &cfg, std::vector<Stage> &out, std::string &err);
 
 // Encode a sweep stage into device descriptors (forward or backward order).
-void encode_sweep(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
-                  std::vector<DevOp> &ops, std::vector<int32_t> &slot_param);
+template <typename Real>
+void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
+                    std::vector<KOp<Real>> &ops, std::vector<int32_t> &slot_param);
 void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops);
 
 std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg);

@@ -2,18 +2,24 @@
 //
 // Forward (BWD = false): for every 2^k-amplitude tile of the shard, load it
 // into registers (coalesced: lanes = physical bits 0..4), run the stage's gates
-// (Y = M x_Q X per gate, Alg. 2's lazy order record = the
-// layouts / qubit map pi), change register layout through shared memory where
-// the next gates need other target bits, store (optionally onto permuted tile
-// positions).  One HBM read + one HBM write per amplitude per stage.
+// (Y = M x_Q X per gate; Alg. 2's lazy order record = the
+// register layouts + qubit map pi), change register layout through shared
+// memory where the next gates need other target bits, store (optionally onto
+// permuted tile positions).  One HBM read + one HBM write per amplitude per
+// stage, whatever the number of gates in it.
 //
 // Adjoint (BWD = true): the same tile walk over psi and lambda together, gates
-// in reverse: first the gradient partial 2 Re <lam|G_p|psi> on the post-gate
+// in reverse: first the gradient partials 2 Re <lam|G_p|psi> on the post-gate
 // states, then psi <- U^dag psi (x = U^* y) and
 // lambda <- U^dag lambda (dx = U^T dy).
 //
-// Instantiated once per (precision, direction) in sweep_*.cu so nvcc compiles
-// the four variants in parallel.
+// Register file: each thread holds 2^R amplitudes (x2 in the adjoint) in TWO
+// buffers A and B; ops alternate A->B, B->A.  Every op therefore writes fresh
+// registers, so the runtime op dispatch needs no register shuffling at the
+// loop back-edge (the v1 kernel spent 28% of its instructions on MOVs there,
+// profiles/r01_v1_*_ncu.json).
+//
+// Instantiated once per (precision, direction) in sweep_*.cu.
 #pragma once
 #include "common.cuh"
 #include "tqd_internal.h"
@@ -21,309 +27,290 @@
 namespace tqd {
 
 constexpr int SWEEP_R = 4;  // register bits: 16 amplitudes (x2 states in the adjoint) per thread
+constexpr int NR = 1 << SWEEP_R;
+constexpr int MAX_WARPS = 1 << WMAX;
 
 template <int V> struct IC { static constexpr int value = V; };
 
-template <int R, typename F> __device__ __forceinline__ void dispatch1(int t, F &&f) {
+template <typename F> __device__ __forceinline__ void dispatch4(int t, F &&f) {
     switch (t) {
     case 0: f(IC<0>{}); break;
-    case 1: if constexpr (R > 1) f(IC<1>{}); break;
-    case 2: if constexpr (R > 2) f(IC<2>{}); break;
-    case 3: if constexpr (R > 3) f(IC<3>{}); break;
-    case 4: if constexpr (R > 4) f(IC<4>{}); break;
-    default: break;
+    case 1: f(IC<1>{}); break;
+    case 2: f(IC<2>{}); break;
+    default: f(IC<3>{}); break;
     }
 }
 
-// ---- register-level gates.  a[] = 2^R amplitudes; register index ri has bit i
-// = value of tile-local bit lay.reg[i].  TB is compile time.  CTRL: pair (ri, rj)
-// is updated only if (ri & cm) == cm and `on` (register / thread control).
+template <typename F> __device__ __forceinline__ void dispatch16(int t, F &&f) {
+    switch (t) {
+    case 0: f(IC<0>{}); break;   case 1: f(IC<1>{}); break;   case 2: f(IC<2>{}); break;
+    case 3: f(IC<3>{}); break;   case 4: f(IC<4>{}); break;   case 5: f(IC<5>{}); break;
+    case 6: f(IC<6>{}); break;   case 7: f(IC<7>{}); break;   case 8: f(IC<8>{}); break;
+    case 9: f(IC<9>{}); break;   case 10: f(IC<10>{}); break; case 11: f(IC<11>{}); break;
+    case 12: f(IC<12>{}); break; case 13: f(IC<13>{}); break; case 14: f(IC<14>{}); break;
+    default: f(IC<15>{}); break;
+    }
+}
 
-template <int R, int TB, bool CTRL, typename C>
-__device__ __forceinline__ void reg_u1(C *a, C m00, C m01, C m10, C m11, int cm, bool on) {
+// ---- layer ops: one 2x2 per active register bit, in place -------------------
+template <int MASK, typename C, typename Real>
+__device__ __forceinline__ void layer_gen(C *t, const Real *m) {
 #pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) {
-        if (ri & (1 << TB)) continue;
-        const int rj = ri | (1 << TB);
-        const C x0 = a[ri], x1 = a[rj];
+    for (int b = 0; b < SWEEP_R; b++) {
+        if (!((MASK >> b) & 1)) continue;
+        const Real *mb = m + 8 * b;
+        const C m00 = mk<C>(mb[0], mb[1]), m01 = mk<C>(mb[2], mb[3]), m10 = mk<C>(mb[4], mb[5]),
+                m11 = mk<C>(mb[6], mb[7]);
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            if (r & (1 << b)) continue;
+            const int s = r | (1 << b);
+            const C x0 = t[r], x1 = t[s];
+            t[r] = cmul2(m00, x0, m01, x1);
+            t[s] = cmul2(m10, x0, m11, x1);
+        }
+    }
+}
+
+template <int MASK, typename C, typename Real>
+__device__ __forceinline__ void layer_real(C *t, const Real *m) {
+#pragma unroll
+    for (int b = 0; b < SWEEP_R; b++) {
+        if (!((MASK >> b) & 1)) continue;
+        const Real *mb = m + 8 * b;
+        const Real m00 = mb[0], m01 = mb[1], m10 = mb[2], m11 = mb[3];
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            if (r & (1 << b)) continue;
+            const int s = r | (1 << b);
+            const C x0 = t[r], x1 = t[s];
+            t[r] = mk<C>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
+            t[s] = mk<C>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
+        }
+    }
+}
+
+constexpr int ctz4(int m) { return (m & 1) ? 0 : (m & 2) ? 1 : (m & 4) ? 2 : 3; }
+
+// diagonal layer: phase(r) = prod_b d_b[bit_b(r)], one complex multiply per amplitude
+template <int MASK, typename C, typename Real>
+__device__ __forceinline__ void layer_diag(C *t, const Real *m) {
+    if constexpr (MASK == 0) {
+        return;
+    } else {
+        constexpr int B0 = ctz4(MASK);
+        C ph[NR];
+        {
+            const C d0 = mk<C>(m[8 * B0 + 0], m[8 * B0 + 1]), d1 = mk<C>(m[8 * B0 + 2], m[8 * B0 + 3]);
+#pragma unroll
+            for (int r = 0; r < (2 << B0); r++) ph[r] = ((r >> B0) & 1) ? d1 : d0;
+        }
+#pragma unroll
+        for (int b = B0 + 1; b < SWEEP_R; b++) {
+            const int h = 1 << b;
+            if ((MASK >> b) & 1) {
+                const C d0 = mk<C>(m[8 * b + 0], m[8 * b + 1]), d1 = mk<C>(m[8 * b + 2], m[8 * b + 3]);
+#pragma unroll
+                for (int r = 0; r < h; r++) {
+                    ph[r + h] = cmul(ph[r], d1);
+                    ph[r] = cmul(ph[r], d0);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < h; r++) ph[r + h] = ph[r];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < NR; r++) t[r] = cmul(ph[r], t[r]);
+    }
+}
+
+// controlled general 2x2 (rare: controlled MAT2), in place; runtime control
+template <int T, typename C, typename Real>
+__device__ __forceinline__ void op_cu(C *a, const Real *m, int cm, bool on) {
+    const C m00 = mk<C>(m[0], m[1]), m01 = mk<C>(m[2], m[3]), m10 = mk<C>(m[4], m[5]), m11 = mk<C>(m[6], m[7]);
+#pragma unroll
+    for (int r = 0; r < NR; r++) {
+        if (r & (1 << T)) continue;
+        const int s = r | (1 << T);
+        const C x0 = a[r], x1 = a[s];
         const C y0 = cmul2(m00, x0, m01, x1), y1 = cmul2(m10, x0, m11, x1);
-        if (CTRL) {
-            const bool p = on && ((ri & cm) == cm);
-            a[ri] = p ? y0 : x0;
-            a[rj] = p ? y1 : x1;
-        } else {
-            a[ri] = y0;
-            a[rj] = y1;
-        }
+        const Real p = (on && ((r & cm) == cm)) ? (Real)1 : (Real)0;  // arithmetic blend: no register moves
+        a[r] = mk<C>(x0.x + p * (y0.x - x0.x), x0.y + p * (y0.y - x0.y));
+        a[s] = mk<C>(x1.x + p * (y1.x - x1.x), x1.y + p * (y1.y - x1.y));
     }
 }
 
-template <int R, int TB, bool CTRL, typename C, typename Real>
-__device__ __forceinline__ void reg_r1(C *a, Real m00, Real m01, Real m10, Real m11, int cm, bool on) {
+template <int T0, int T1, typename C, typename Real>
+__device__ __forceinline__ void op_u2(C *a, const Real *m) {
 #pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) {
-        if (ri & (1 << TB)) continue;
-        const int rj = ri | (1 << TB);
-        const C x0 = a[ri], x1 = a[rj];
-        const C y0 = mk<C>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
-        const C y1 = mk<C>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
-        if (CTRL) {
-            const bool p = on && ((ri & cm) == cm);
-            a[ri] = p ? y0 : x0;
-            a[rj] = p ? y1 : x1;
-        } else {
-            a[ri] = y0;
-            a[rj] = y1;
-        }
-    }
-}
-
-template <int R, int TB, bool CTRL, bool PLAIN, typename C>
-__device__ __forceinline__ void reg_p1(C *a, C pa, C pb, int cm, bool on) {
-#pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) {
-        if (ri & (1 << TB)) continue;
-        const int rj = ri | (1 << TB);
-        const C x0 = a[ri], x1 = a[rj];
-        const C y0 = PLAIN ? x1 : cmul(pa, x1);
-        const C y1 = PLAIN ? x0 : cmul(pb, x0);
-        if (CTRL) {
-            const bool p = on && ((ri & cm) == cm);
-            a[ri] = p ? y0 : x0;
-            a[rj] = p ? y1 : x1;
-        } else {
-            a[ri] = y0;
-            a[rj] = y1;
-        }
-    }
-}
-
-template <int R, int TB, typename C>
-__device__ __forceinline__ void reg_d1(C *a, C d0, C d1) {
-#pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) a[ri] = cmul((ri & (1 << TB)) ? d1 : d0, a[ri]);
-}
-
-template <int R, typename C>
-__device__ __forceinline__ void reg_scale(C *a, C d) {
-#pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) a[ri] = cmul(d, a[ri]);
-}
-
-// diagonal 2q: phase index 2*v0 + v1; v = register bit (mask m != 0) or thread value rv
-template <int R, typename C>
-__device__ __forceinline__ void reg_d2(C *a, const C *d, int m0, int rv0, int m1, int rv1) {
-#pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) {
-        const int v0 = m0 ? ((ri & m0) != 0) : rv0;
-        const int v1 = m1 ? ((ri & m1) != 0) : rv1;
-        const C e0 = v1 ? d[1] : d[0];
-        const C e1 = v1 ? d[3] : d[2];
-        a[ri] = cmul(v0 ? e1 : e0, a[ri]);
-    }
-}
-
-template <int R, int T0, int T1, typename C>
-__device__ __forceinline__ void reg_u2(C *a, const C *M) {
-#pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) {
-        if (ri & ((1 << T0) | (1 << T1))) continue;
-        const int idx[4] = {ri, ri | (1 << T1), ri | (1 << T0), ri | (1 << T0) | (1 << T1)};
+    for (int r = 0; r < NR; r++) {
+        if (r & ((1 << T0) | (1 << T1))) continue;
+        const int idx[4] = {r, r | (1 << T1), r | (1 << T0), r | (1 << T0) | (1 << T1)};
         C v[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) v[q] = a[idx[q]];
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-            C acc = cmul(M[4 * r], v[0]);
+        for (int i = 0; i < 4; i++) {
+            C acc = cmul(mk<C>(m[8 * i], m[8 * i + 1]), v[0]);
 #pragma unroll
             for (int q = 1; q < 4; q++) {
-                const C p = cmul(M[4 * r + q], v[q]);
+                const C p = cmul(mk<C>(m[8 * i + 2 * q], m[8 * i + 2 * q + 1]), v[q]);
                 acc.x += p.x;
                 acc.y += p.y;
             }
-            a[idx[r]] = acc;
+            a[idx[i]] = acc;
         }
     }
 }
 
-// ---- gradient partials: 2 Re <lam|G|psi> over this thread's amplitudes ----
-template <int R, int TB, typename C, typename Real>
-__device__ __forceinline__ Real grad_pair(const C *a, const C *l, int gk, const double *g) {
+// diagonal 2q on arbitrary bits: v = register bit (mask) or per-thread value
+template <typename C, typename Real>
+__device__ __forceinline__ void op_d2(C *a, const Real *m, int m0, int rv0, int m1, int rv1) {
+    const C d0 = mk<C>(m[0], m[1]), d1 = mk<C>(m[2], m[3]), d2 = mk<C>(m[4], m[5]), d3 = mk<C>(m[6], m[7]);
+#pragma unroll
+    for (int r = 0; r < NR; r++) {
+        const int v0 = m0 ? ((r & m0) != 0) : rv0;
+        const int v1 = m1 ? ((r & m1) != 0) : rv1;
+        const C e0 = v1 ? d1 : d0;
+        const C e1 = v1 ? d3 : d2;
+        a[r] = cmul(v0 ? e1 : e0, a[r]);
+    }
+}
+
+// ---- gradient partials on (psi, lambda): 2 Re <lam|G|psi> --------------------
+template <int T, typename C, typename Real>
+__device__ __forceinline__ Real grad_bit(const C *a, const C *l, int gk, const Real *g) {
     Real acc = 0;
     if (gk == GEN_Y) {  // G = -(i/2) Y = [[0, -1/2], [1/2, 0]]
 #pragma unroll
-        for (int ri = 0; ri < (1 << R); ri++) {
-            if (ri & (1 << TB)) continue;
-            const int rj = ri | (1 << TB);
-            acc += re_cj(l[rj], a[ri]) - re_cj(l[ri], a[rj]);
+        for (int r = 0; r < NR; r++) {
+            if (r & (1 << T)) continue;
+            const int s = r | (1 << T);
+            acc += re_cj(l[s], a[r]) - re_cj(l[r], a[s]);
         }
     } else if (gk == GEN_X) {  // G = -(i/2) X
 #pragma unroll
-        for (int ri = 0; ri < (1 << R); ri++) {
-            if (ri & (1 << TB)) continue;
-            const int rj = ri | (1 << TB);
-            acc += im_cj(l[ri], a[rj]) + im_cj(l[rj], a[ri]);
+        for (int r = 0; r < NR; r++) {
+            if (r & (1 << T)) continue;
+            const int s = r | (1 << T);
+            acc += im_cj(l[r], a[s]) + im_cj(l[s], a[r]);
+        }
+    } else if (gk == GEN_Z) {  // G = -(i/2) Z: sum_b z_b Im(conj(lam_b) psi_b)
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            const Real v = im_cj(l[r], a[r]);
+            acc += (r & (1 << T)) ? -v : v;
         }
     } else {  // general anti-Hermitian generator
-        const C g00 = ldc<C>(g, 0), g01 = ldc<C>(g, 1), g10 = ldc<C>(g, 2), g11 = ldc<C>(g, 3);
+        const C g00 = mk<C>(g[0], g[1]), g01 = mk<C>(g[2], g[3]), g10 = mk<C>(g[4], g[5]), g11 = mk<C>(g[6], g[7]);
 #pragma unroll
-        for (int ri = 0; ri < (1 << R); ri++) {
-            if (ri & (1 << TB)) continue;
-            const int rj = ri | (1 << TB);
-            const C v0 = cmul2(g00, a[ri], g01, a[rj]);
-            const C v1 = cmul2(g10, a[ri], g11, a[rj]);
-            acc += 2 * (re_cj(l[ri], v0) + re_cj(l[rj], v1));
+        for (int r = 0; r < NR; r++) {
+            if (r & (1 << T)) continue;
+            const int s = r | (1 << T);
+            const C v0 = cmul2(g00, a[r], g01, a[s]);
+            const C v1 = cmul2(g10, a[r], g11, a[s]);
+            acc += 2 * (re_cj(l[r], v0) + re_cj(l[s], v1));
         }
     }
     return acc;
 }
 
-// RZ generator G = -(i/2) Z on a register bit: sum_b z_b Im(conj(lam_b) psi_b)
-template <int R, int TB, typename C, typename Real>
-__device__ __forceinline__ Real grad_z_reg(const C *a, const C *l) {
-    Real acc = 0;
-#pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) {
-        const Real v = im_cj(l[ri], a[ri]);
-        acc += (ri & (1 << TB)) ? -v : v;
-    }
-    return acc;
-}
-
-template <int R, typename C, typename Real>
+template <typename C, typename Real>
 __device__ __forceinline__ Real grad_z_const(const C *a, const C *l, int bit) {
     Real acc = 0;
 #pragma unroll
-    for (int ri = 0; ri < (1 << R); ri++) acc += im_cj(l[ri], a[ri]);
+    for (int r = 0; r < NR; r++) acc += im_cj(l[r], a[r]);
     return bit ? -acc : acc;
 }
 
-// ---- one op on the register file ----
-template <typename Real, int R, bool BWD>
-__device__ __forceinline__ void run_op(const DevOp &op, typename CT<Real>::C *a, typename CT<Real>::C *l,
-                                       uint32_t tix, uint64_t basefull, double *sacc) {
+// ---- one op, in place on psi (and lambda in the adjoint) ----------------------
+template <typename Real, bool BWD>
+__device__ __forceinline__ void run_kop(const KOp<Real> &op, typename CT<Real>::C *a, typename CT<Real>::C *l,
+                                        uint32_t tix, uint64_t basefull, double *wacc) {
     typedef typename CT<Real>::C C;
     auto bitval = [&](BitRef b) -> int {
         return b.kind == BK_TIX ? (int)((tix >> b.idx) & 1u) : (int)((basefull >> b.idx) & 1ull);
     };
     const int kind = op.kind;
-
     if (BWD && op.ngen) {
+        // gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
         for (int gi = 0; gi < op.ngen; gi++) {
             Real part = 0;
-            const int gk = op.gkind[gi];
-            if (kind == OP_D1) {
-                if (op.b0.kind == BK_REG)
-                    dispatch1<R>(op.b0.idx, [&](auto tb) { part = grad_z_reg<R, decltype(tb)::value, C, Real>(a, l); });
-                else
-                    part = grad_z_const<R, C, Real>(a, l, bitval(op.b0));
+            if (kind == K_PHASE) {
+                part = grad_z_const<C, Real>(a, l, bitval(op.b0));
             } else {
-                dispatch1<R>(op.t0, [&](auto tb) { part = grad_pair<R, decltype(tb)::value, C, Real>(a, l, gk, op.g[gi]); });
+                const int gk = op.gkind[gi];
+                const Real *g = op.g[gi];
+                dispatch4(op.gbit[gi], [&](auto tb) { part = grad_bit<decltype(tb)::value, C, Real>(a, l, gk, g); });
             }
             part = warp_sum(part);
-            if ((threadIdx.x & 31) == 0) atomicAdd(&sacc[op.slot[gi]], (double)part);
+            if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
         }
     }
-
-    bool on = true;
-    int cm = 0;
-    if (op.ctrl.kind == BK_REG) cm = 1 << op.ctrl.idx;
-    else if (op.ctrl.kind != BK_NONE) on = bitval(op.ctrl) != 0;
-    const bool ctrl = (cm != 0) || (op.ctrl.kind != BK_NONE);
-
     switch (kind) {
-    case OP_U1: {
-        const C m00 = ldc<C>(op.m, 0), m01 = ldc<C>(op.m, 1), m10 = ldc<C>(op.m, 2), m11 = ldc<C>(op.m, 3);
-        dispatch1<R>(op.t0, [&](auto tb) {
-            constexpr int TB = decltype(tb)::value;
-            if (ctrl) {
-                reg_u1<R, TB, true>(a, m00, m01, m10, m11, cm, on);
-                if (BWD) reg_u1<R, TB, true>(l, m00, m01, m10, m11, cm, on);
+    case K_LAYER: {
+        const int lt = op.ltype;
+        dispatch16(op.mask, [&](auto mk_) {
+            constexpr int MASK = decltype(mk_)::value;
+            if (lt == LT_REAL) {
+                layer_real<MASK, C, Real>(a, op.m);
+                if (BWD) layer_real<MASK, C, Real>(l, op.m);
+            } else if (lt == LT_DIAG) {
+                layer_diag<MASK, C, Real>(a, op.m);
+                if (BWD) layer_diag<MASK, C, Real>(l, op.m);
             } else {
-                reg_u1<R, TB, false>(a, m00, m01, m10, m11, 0, true);
-                if (BWD) reg_u1<R, TB, false>(l, m00, m01, m10, m11, 0, true);
+                layer_gen<MASK, C, Real>(a, op.m);
+                if (BWD) layer_gen<MASK, C, Real>(l, op.m);
             }
         });
         break;
     }
-    case OP_R1: {
-        const Real m00 = (Real)op.m[0], m01 = (Real)op.m[1], m10 = (Real)op.m[2], m11 = (Real)op.m[3];
-        dispatch1<R>(op.t0, [&](auto tb) {
-            constexpr int TB = decltype(tb)::value;
-            if (ctrl) {
-                reg_r1<R, TB, true, C, Real>(a, m00, m01, m10, m11, cm, on);
-                if (BWD) reg_r1<R, TB, true, C, Real>(l, m00, m01, m10, m11, cm, on);
-            } else {
-                reg_r1<R, TB, false, C, Real>(a, m00, m01, m10, m11, 0, true);
-                if (BWD) reg_r1<R, TB, false, C, Real>(l, m00, m01, m10, m11, 0, true);
-            }
+    case K_CU: {
+        const bool on = op.ctrl.kind == BK_NONE ? true : bitval(op.ctrl) != 0;
+        const int cm = op.creg != 0xff ? (1 << op.creg) : 0;
+        dispatch4(op.t0, [&](auto tt) {
+            constexpr int T = decltype(tt)::value;
+            op_cu<T, C, Real>(a, op.m, cm, on);
+            if (BWD) op_cu<T, C, Real>(l, op.m, cm, on);
         });
         break;
     }
-    case OP_P1: {
-        const C pa = ldc<C>(op.m, 0), pb = ldc<C>(op.m, 1);
-        const bool plain = op.t1 != 0;
-        dispatch1<R>(op.t0, [&](auto tb) {
-            constexpr int TB = decltype(tb)::value;
-            if (plain) {
-                if (ctrl) {
-                    reg_p1<R, TB, true, true>(a, pa, pb, cm, on);
-                    if (BWD) reg_p1<R, TB, true, true>(l, pa, pb, cm, on);
-                } else {
-                    reg_p1<R, TB, false, true>(a, pa, pb, 0, true);
-                    if (BWD) reg_p1<R, TB, false, true>(l, pa, pb, 0, true);
-                }
-            } else {
-                if (ctrl) {
-                    reg_p1<R, TB, true, false>(a, pa, pb, cm, on);
-                    if (BWD) reg_p1<R, TB, true, false>(l, pa, pb, cm, on);
-                } else {
-                    reg_p1<R, TB, false, false>(a, pa, pb, 0, true);
-                    if (BWD) reg_p1<R, TB, false, false>(l, pa, pb, 0, true);
-                }
-            }
-        });
-        break;
-    }
-    case OP_D1: {
-        const C d0 = ldc<C>(op.m, 0), d1 = ldc<C>(op.m, 1);
-        if (op.b0.kind == BK_REG) {
-            dispatch1<R>(op.b0.idx, [&](auto tb) {
-                reg_d1<R, decltype(tb)::value>(a, d0, d1);
-                if (BWD) reg_d1<R, decltype(tb)::value>(l, d0, d1);
-            });
-        } else {
-            const C d = bitval(op.b0) ? d1 : d0;
-            reg_scale<R>(a, d);
-            if (BWD) reg_scale<R>(l, d);
+    case K_PHASE: {
+        const int v = bitval(op.b0);
+        const C d = v ? mk<C>(op.m[2], op.m[3]) : mk<C>(op.m[0], op.m[1]);
+#pragma unroll
+        for (int r = 0; r < NR; r++) a[r] = cmul(d, a[r]);
+        if (BWD) {
+#pragma unroll
+            for (int r = 0; r < NR; r++) l[r] = cmul(d, l[r]);
         }
         break;
     }
-    case OP_D2: {
-        C d[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) d[q] = ldc<C>(op.m, q);
+    case K_D2: {
         const int m0 = op.b0.kind == BK_REG ? (1 << op.b0.idx) : 0;
         const int m1 = op.b1.kind == BK_REG ? (1 << op.b1.idx) : 0;
         const int v0 = m0 ? 0 : bitval(op.b0);
         const int v1 = m1 ? 0 : bitval(op.b1);
-        reg_d2<R>(a, d, m0, v0, m1, v1);
-        if (BWD) reg_d2<R>(l, d, m0, v0, m1, v1);
+        op_d2<C, Real>(a, op.m, m0, v0, m1, v1);
+        if (BWD) op_d2<C, Real>(l, op.m, m0, v0, m1, v1);
         break;
     }
-    case OP_U2: {
-        C M[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) M[q] = ldc<C>(op.m, q);
-        dispatch1<R>(op.t0, [&](auto c0) {
-            dispatch1<R>(op.t1, [&](auto c1) {
-                constexpr int T0 = decltype(c0)::value, T1 = decltype(c1)::value;
-                if constexpr (T0 != T1) {
-                    reg_u2<R, T0, T1>(a, M);
-                    if (BWD) reg_u2<R, T0, T1>(l, M);
-                }
-            });
-        });
+    case K_U2: {
+        const int code = op.t0 * 4 + op.t1;
+        auto go = [&](auto c0, auto c1) {
+            constexpr int T0 = decltype(c0)::value, T1 = decltype(c1)::value;
+            op_u2<T0, T1, C, Real>(a, op.m);
+            if (BWD) op_u2<T0, T1, C, Real>(l, op.m);
+        };
+        switch (code) {
+        case 1: go(IC<0>{}, IC<1>{}); break;   case 2: go(IC<0>{}, IC<2>{}); break;
+        case 3: go(IC<0>{}, IC<3>{}); break;   case 4: go(IC<1>{}, IC<0>{}); break;
+        case 6: go(IC<1>{}, IC<2>{}); break;   case 7: go(IC<1>{}, IC<3>{}); break;
+        case 8: go(IC<2>{}, IC<0>{}); break;   case 9: go(IC<2>{}, IC<1>{}); break;
+        case 11: go(IC<2>{}, IC<3>{}); break;  case 12: go(IC<3>{}, IC<0>{}); break;
+        case 13: go(IC<3>{}, IC<1>{}); break;  default: go(IC<3>{}, IC<2>{}); break;
+        }
         break;
     }
     default: break;
@@ -331,8 +318,8 @@ __device__ __forceinline__ void run_op(const DevOp &op, typename CT<Real>::C *a,
 }
 
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
-template <typename Real, int R, bool BWD>
-__global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__ stg, const DevOp *__restrict__ ops,
+template <typename Real, bool BWD>
+__global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
@@ -340,25 +327,58 @@ __global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__
     typedef typename CT<Real>::C C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevStage S;
-    __shared__ double sacc[BWD ? MAX_STAGE_SLOTS : 1];
+    __shared__ uint64_t s_ldoff[NR], s_stoff[NR];
+    __shared__ uint32_t s_woff[MAXSEG][NR], s_roff[MAXSEG][NR];
+    __shared__ double s_acc[BWD ? MAX_WARPS : 1][BWD ? MAX_STAGE_SLOTS : 1];
 
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(stg);
         uint32_t *dst = reinterpret_cast<uint32_t *>(&S);
         for (int i = threadIdx.x; i < (int)(sizeof(DevStage) / 4); i += blockDim.x) dst[i] = src[i];
-        if (BWD)
-            for (int i = threadIdx.x; i < MAX_STAGE_SLOTS; i += blockDim.x) sacc[i] = 0.0;
     }
     __syncthreads();
-
     const int k = S.k;
     const int W = S.W;
     const int nseg = S.nseg;
+    // shared memory: [exchange psi (2^k)] [exchange lambda (2^k, adjoint)] [kernel ops]
     C *sm_a = reinterpret_cast<C *>(smem_raw);
     C *sm_l = sm_a + ((size_t)1 << k);
+    KOp<Real> *s_ops = reinterpret_cast<KOp<Real> *>(smem_raw + (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(C));
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base);
+        int4 *dst = reinterpret_cast<int4 *>(s_ops);
+        const int n16 = (int)(S.n_ops * sizeof(KOp<Real>) / 16);
+        for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x < NR) {
+            const int r = threadIdx.x;
+            uint64_t lo = 0, so = 0;
+            for (int i = 0; i < SWEEP_R; i++)
+                if ((r >> i) & 1) {
+                    lo |= 1ull << S.ld_phys[S.lay[0].reg[i]];
+                    so |= 1ull << S.st_phys[S.lay[nseg - 1].reg[i]];
+                }
+            s_ldoff[r] = lo;
+            s_stoff[r] = so;
+        }
+        for (int i = threadIdx.x; i < (nseg - 1) * NR; i += blockDim.x) {
+            const int s = i / NR, r = i % NR;
+            uint32_t w = 0, rd = 0;
+            for (int b = 0; b < SWEEP_R; b++)
+                if ((r >> b) & 1) {
+                    w ^= S.wcol[s][S.lay[s].reg[b]];
+                    rd ^= S.rcol[s][S.lay[s + 1].reg[b]];
+                }
+            s_woff[s][r] = w;
+            s_roff[s][r] = rd;
+        }
+        if (BWD)
+            for (int i = threadIdx.x; i < MAX_WARPS * MAX_STAGE_SLOTS; i += blockDim.x) (&s_acc[0][0])[i] = 0.0;
+    }
+    __syncthreads();
+
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const DevOp *sops = ops + S.op_base;
+    double *wacc = BWD ? &s_acc[warp][0] : nullptr;
 
     auto thr_phys_off = [&](const DevLayout &L, const uint8_t *phys) -> uint64_t {
         uint64_t off = 0;
@@ -376,15 +396,17 @@ __global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__
         for (int w = 0; w < W; w++) t |= (uint32_t)((warp >> w) & 1) << L.warp[w];
         return t;
     };
-    auto thr_sm = [&](const DevLayout &L) -> uint32_t {
+    auto thr_cols = [&](const uint32_t *cols, const DevLayout &L) -> uint32_t {
         uint32_t t = 0;
 #pragma unroll
         for (int i = 0; i < LANE_BITS; i++)
-            if ((lane >> i) & 1) t ^= S.swz[L.lane[i]];
+            if ((lane >> i) & 1) t ^= cols[L.lane[i]];
         for (int w = 0; w < W; w++)
-            if ((warp >> w) & 1) t ^= S.swz[L.warp[w]];
+            if ((warp >> w) & 1) t ^= cols[L.warp[w]];
         return t;
     };
+    const uint64_t ld_thr = thr_phys_off(S.lay[0], S.ld_phys);
+    const uint64_t st_thr = thr_phys_off(S.lay[nseg - 1], S.st_phys);
 
     for (int64_t tile = blockIdx.x; tile < S.n_tiles; tile += gridDim.x) {
         // deposit the tile index into the non-tile physical positions
@@ -395,111 +417,92 @@ __global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__
         }
         const uint64_t basefull = base | rank_hi;
 
-        C a[1 << R];
-        C l[BWD ? (1 << R) : 1];
+        C a[NR];
+        C l[BWD ? NR : 1];
         {
-            const DevLayout &L = S.lay[0];
-            const uint64_t off = base | thr_phys_off(L, S.ld_phys);
-            uint64_t roff[R];
+            const C *p = psi + (base | ld_thr);
+            const C *q = BWD ? lam + (base | ld_thr) : nullptr;
 #pragma unroll
-            for (int i = 0; i < R; i++) roff[i] = 1ull << S.ld_phys[L.reg[i]];
-#pragma unroll
-            for (int ri = 0; ri < (1 << R); ri++) {
-                uint64_t o = off;
-#pragma unroll
-                for (int i = 0; i < R; i++)
-                    if (ri & (1 << i)) o |= roff[i];
-                a[ri] = psi[o];
-                if (BWD) l[ri] = lam[o];
+            for (int r = 0; r < NR; r++) {
+                a[r] = p[s_ldoff[r]];
+                if (BWD) l[r] = q[s_ldoff[r]];
             }
         }
 
         for (int s = 0; s < nseg; s++) {
-            if (s > 0) {  // layout change through shared memory
-                const DevLayout &Lw = S.lay[s - 1];
-                const DevLayout &Lr = S.lay[s];
-                const uint32_t tw = thr_sm(Lw), tr = thr_sm(Lr);
-                uint32_t cw[R], cr[R];
+            if (s > 0) {
+                // layout change through shared memory; the permutation gates of the
+                // previous segment (CNOT / X: GF(2)-affine index maps) ride along
+                const int x = s - 1;
+                uint32_t aff = 0;
+                for (int i = 0; i < S.naff[x]; i++)
+                    if ((basefull >> S.aff_pos[x][i]) & 1ull) aff ^= S.aff_vec[x][i];
+                const uint32_t tw = thr_cols(S.wcol[x], S.lay[x]) ^ S.wcst[x] ^ (S.aff_read[x] ? 0u : aff);
+                const uint32_t tr = thr_cols(S.rcol[x], S.lay[s]) ^ S.rcst[x] ^ (S.aff_read[x] ? aff : 0u);
 #pragma unroll
-                for (int i = 0; i < R; i++) { cw[i] = S.swz[Lw.reg[i]]; cr[i] = S.swz[Lr.reg[i]]; }
-#pragma unroll
-                for (int ri = 0; ri < (1 << R); ri++) {
-                    uint32_t o = tw;
-#pragma unroll
-                    for (int i = 0; i < R; i++)
-                        if (ri & (1 << i)) o ^= cw[i];
-                    sm_a[o] = a[ri];
-                    if (BWD) sm_l[o] = l[ri];
+                for (int r = 0; r < NR; r++) {
+                    const uint32_t o = tw ^ s_woff[x][r];
+                    sm_a[o] = a[r];
+                    if (BWD) sm_l[o] = l[r];
                 }
                 __syncthreads();
 #pragma unroll
-                for (int ri = 0; ri < (1 << R); ri++) {
-                    uint32_t o = tr;
-#pragma unroll
-                    for (int i = 0; i < R; i++)
-                        if (ri & (1 << i)) o ^= cr[i];
-                    a[ri] = sm_a[o];
-                    if (BWD) l[ri] = sm_l[o];
+                for (int r = 0; r < NR; r++) {
+                    const uint32_t o = tr ^ s_roff[x][r];
+                    a[r] = sm_a[o];
+                    if (BWD) l[r] = sm_l[o];
                 }
                 __syncthreads();
             }
             const uint32_t tix = thr_tix(S.lay[s]);
             const int e = S.seg_begin[s + 1];
-            for (int oi = S.seg_begin[s]; oi < e; oi++) run_op<Real, R, BWD>(sops[oi], a, l, tix, basefull, sacc);
+            for (int oi = S.seg_begin[s]; oi < e; oi++) run_kop<Real, BWD>(s_ops[oi], a, l, tix, basefull, wacc);
         }
 
         {
-            const DevLayout &L = S.lay[nseg - 1];
-            const uint64_t off = base | thr_phys_off(L, S.st_phys);
-            uint64_t roff[R];
+            C *p = psi + (base | st_thr);
+            C *q = BWD ? lam + (base | st_thr) : nullptr;
 #pragma unroll
-            for (int i = 0; i < R; i++) roff[i] = 1ull << S.st_phys[L.reg[i]];
-#pragma unroll
-            for (int ri = 0; ri < (1 << R); ri++) {
-                uint64_t o = off;
-#pragma unroll
-                for (int i = 0; i < R; i++)
-                    if (ri & (1 << i)) o |= roff[i];
-                psi[o] = a[ri];
-                if (BWD) lam[o] = l[ri];
+            for (int r = 0; r < NR; r++) {
+                p[s_stoff[r]] = a[r];
+                if (BWD) q[s_stoff[r]] = l[r];
             }
         }
     }
 
     if (BWD) {
         __syncthreads();
+        const int nw = blockDim.x >> 5;
         for (int i = threadIdx.x; i < S.n_slots; i += blockDim.x) {
-            const double v = sacc[i];
+            double v = 0.0;
+            for (int w = 0; w < nw; w++) v += s_acc[w][i];
             if (v != 0.0) atomicAdd(&grad[slot_param[S.slot_base + i]], v);
         }
     }
 }
 
 template <typename Real, bool BWD>
-static size_t sweep_smem_bytes(int k) {
-    return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C);
+static size_t sweep_smem_bytes(int k, int n_ops) {
+    return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>);
 }
 
 template <typename Real, bool BWD>
-cudaError_t launch_sweep_impl(const DevStage *d_stage, const DevOp *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                              double *grad, uint64_t rank_hi, int k, int W, int grid, cudaStream_t s) {
+cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
+                              double *grad, uint64_t rank_hi, int k, int W, int n_ops, int grid, cudaStream_t s) {
     typedef typename CT<Real>::C C;
-    auto fn = sweep_kernel<Real, SWEEP_R, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
-    fn<<<grid, 32 << W, smem, s>>>(d_stage, d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi);
+    auto fn = sweep_kernel<Real, BWD>;
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops);
+    // set on every launch: the occupancy query may have lowered it
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi);
     return cudaGetLastError();
 }
 
 template <typename Real, bool BWD>
-int sweep_occupancy_impl(int k, int W) {
-    auto fn = sweep_kernel<Real, SWEEP_R, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k);
+int sweep_occupancy_impl(int k, int W, int n_ops) {
+    auto fn = sweep_kernel<Real, BWD>;
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 << W, smem) != cudaSuccess) {
@@ -513,10 +516,10 @@ int sweep_occupancy_impl(int k, int W) {
 
 #define TQD_INSTANTIATE_SWEEP(REAL, BWD, NAME)                                                                    \
     namespace tqd {                                                                                             \
-    cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const DevOp *d_ops, const int32_t *d_slots, void *psi, \
-                                    void *lam, double *grad, uint64_t rank_hi, int k, int W, int grid,             \
+    cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi,  \
+                                    void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int grid,  \
                                     cudaStream_t s) {                                                             \
-        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, grid, s);     \
+        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, grid, s); \
     }                                                                                                           \
-    int sweep_occupancy_##NAME(int k, int W) { return sweep_occupancy_impl<REAL, BWD>(k, W); }                  \
+    int sweep_occupancy_##NAME(int k, int W, int n_ops) { return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops); }    \
     }

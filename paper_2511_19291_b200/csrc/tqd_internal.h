@@ -27,8 +27,9 @@ constexpr int KMAX = 16;    // max tile bits
 constexpr int RMAX = 5;     // max register bits
 constexpr int WMAX = 3;     // max warp bits (8 warps = 256 threads)
 constexpr int LANE_BITS = 5;
-constexpr int MAXSEG = 24;  // layouts per sweep stage
-constexpr int MAX_STAGE_OPS = 384;
+constexpr int MAXSEG = 16;  // layouts per sweep stage
+constexpr int NAFF = 8;     // base-controlled affine terms per exchange
+constexpr int MAX_STAGE_OPS = 128;   // placed gates per sweep stage (bounds the kernel-op table in shared memory)
 constexpr int MAX_STAGE_SLOTS = 256;
 
 enum OpKind : uint8_t {
@@ -78,6 +79,40 @@ struct alignas(16) DevOp {
     double g[3][8];     // generator matrices (2x2 complex, row-major re,im)
 };
 
+// ---- sweep-kernel ops (v2): what the fused sweep kernel executes, staged in
+// shared memory in the kernel's precision.  Consecutive single-qubit gates on
+// register bits are fused into one K_LAYER op (one 2x2 per register bit, the
+// mask is a compile-time dispatch), so the runtime dispatch cost is paid once
+// per layer, not once per gate.
+enum KKind : uint8_t {
+    K_NOP = 0,
+    K_LAYER = 1,  // per active register bit b: 2x2 m[8b..8b+7] (type ltype)
+    K_CX = 2,     // X on register bit t0 (CNOT target), control creg / ctrl
+    K_CU = 3,     // general 2x2 on register bit t0, control creg / ctrl
+    K_PHASE = 4,  // diag(d0, d1) selected by a lane/warp/base bit b0 (+ RZ generator)
+    K_D2 = 5,     // diag 2q on bits b0 (MSB), b1 (any kind)
+    K_U2 = 6,     // 4x4 on register bits t0 (MSB), t1
+};
+enum LType : uint8_t { LT_GEN = 0, LT_REAL = 1, LT_DIAG = 2 };
+constexpr int KOP_MAXGEN = 4;
+
+template <typename Real> struct alignas(16) KOp {
+    uint8_t kind;
+    uint8_t mask;               // K_LAYER active register bits
+    uint8_t ltype;              // K_LAYER matrix type (LType)
+    uint8_t t0, t1;             // register-bit targets
+    uint8_t creg;               // register-bit control, 0xff = none
+    BitRef ctrl;                // lane / warp / base control, BK_NONE = none
+    BitRef b0, b1;              // K_PHASE / K_D2 bits
+    uint8_t ngen;               // backward: generators (gradient slots)
+    uint8_t gbit[KOP_MAXGEN];   // register bit of each generator (K_LAYER)
+    uint8_t gkind[KOP_MAXGEN];  // GenKind
+    uint8_t pad;
+    int16_t slot[KOP_MAXGEN];   // stage-local slot
+    Real m[32];
+    Real g[KOP_MAXGEN][8];      // generators (2x2 complex)
+};
+
 struct DevLayout {
     uint8_t reg[RMAX];
     uint8_t lane[LANE_BITS];
@@ -91,7 +126,17 @@ struct DevStage {
     uint8_t ld_phys[KMAX];      // physical position of tile-local bit t at load
     uint8_t st_phys[KMAX];      // physical position of tile-local bit t at store
     uint8_t tile_sorted[KMAX];  // the tile's physical positions, ascending
-    uint32_t swz[KMAX];         // shared-memory address vector of tile-local bit t
+    uint32_t swz[KMAX];         // shared-memory address vector of tile-local bit t (plain layouts)
+    // exchange s (segment s -> s+1): shared-memory address vectors of tile-local
+    // bit t on the write side (layout s) and the read side (layout s+1); the
+    // permutation gates of the stage (CNOT, X) are folded into these maps
+    uint32_t wcol[MAXSEG][KMAX];
+    uint32_t rcol[MAXSEG][KMAX];
+    uint32_t wcst[MAXSEG], rcst[MAXSEG];
+    uint8_t naff[MAXSEG];
+    uint8_t aff_read[MAXSEG];   // 1: affine terms apply to the read side
+    uint8_t aff_pos[MAXSEG][NAFF];
+    uint32_t aff_vec[MAXSEG][NAFF];
     int32_t seg_begin[MAXSEG + 1];
     DevLayout lay[MAXSEG];
     int32_t op_base, n_ops;     // into the launch's DevOp array

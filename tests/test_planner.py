@@ -95,6 +95,9 @@ def check_invariants(plan):
         segs = [op["seg"] for op in st["ops"]]
         assert segs == sorted(segs)
         for op in st["ops"]:
+            if op["perm"]:  # CNOT / X folded into a layout-change map: target only needs to be in the tile
+                assert op["tp0"] in ld
+                continue
             for key in ("tp0", "tp1"):
                 if op[key] >= 0:
                     assert ld.index(op[key]) in lays[op["seg"]]["reg"]
