@@ -888,31 +888,40 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             else { r.kind = BK_BASE; r.idx = (uint8_t)p; }
             return r;
         };
-        // current fused layer
+        // current fused layer: single-qubit gates on register bits, one matrix
+        // type per layer (real / diagonal / general) so the kernel's cheapest
+        // variant applies (real: packed f32x2 FMA, diagonal: one complex multiply
+        // per amplitude with the host-built table of 16 phase products)
         bool active = false;
-        int mask = 0;
+        int mask = 0, ltype = LT_GEN;
         cd LM[RMAX][4];
         KOp<Real> layer = newop(K_LAYER);
+        auto mtype = [](const cd *M) {
+            if (M[1] == cd(0.0) && M[2] == cd(0.0)) return (int)LT_DIAG;
+            for (int q = 0; q < 4; q++) if (M[q].imag() != 0.0) return (int)LT_GEN;
+            return (int)LT_REAL;
+        };
         auto flush = [&]() {
             if (!active) return;
-            bool real = true, diag = true;
-            for (int b = 0; b < R; b++) {
-                if (!((mask >> b) & 1)) continue;
-                for (int q = 0; q < 4; q++) if (LM[b][q].imag() != 0.0) real = false;
-                if (LM[b][1] != cd(0.0) || LM[b][2] != cd(0.0)) diag = false;
-            }
             layer.mask = (uint8_t)mask;
-            layer.ltype = diag ? LT_DIAG : real ? LT_REAL : LT_GEN;
-            for (int b = 0; b < R; b++) {
-                if (!((mask >> b) & 1)) continue;
-                Real *m = layer.m + 8 * b;
-                if (layer.ltype == LT_REAL) {
-                    for (int q = 0; q < 4; q++) m[q] = (Real)LM[b][q].real();
-                } else if (layer.ltype == LT_DIAG) {
-                    m[0] = (Real)LM[b][0].real(); m[1] = (Real)LM[b][0].imag();
-                    m[2] = (Real)LM[b][3].real(); m[3] = (Real)LM[b][3].imag();
-                } else {
-                    for (int q = 0; q < 4; q++) { m[2 * q] = (Real)LM[b][q].real(); m[2 * q + 1] = (Real)LM[b][q].imag(); }
+            layer.ltype = (uint8_t)ltype;
+            if (ltype == LT_DIAG) {
+                for (int r = 0; r < (1 << R); r++) {
+                    cd ph = 1.0;
+                    for (int bb = 0; bb < R; bb++)
+                        if ((mask >> bb) & 1) ph *= ((r >> bb) & 1) ? LM[bb][3] : LM[bb][0];
+                    layer.m[2 * r] = (Real)ph.real();
+                    layer.m[2 * r + 1] = (Real)ph.imag();
+                }
+            } else {
+                for (int bb = 0; bb < R; bb++) {
+                    if (!((mask >> bb) & 1)) continue;
+                    Real *m = layer.m + 8 * bb;
+                    if (ltype == LT_REAL) {
+                        for (int q = 0; q < 4; q++) m[q] = (Real)LM[bb][q].real();
+                    } else {
+                        for (int q = 0; q < 4; q++) { m[2 * q] = (Real)LM[bb][q].real(); m[2 * q + 1] = (Real)LM[bb][q].imag(); }
+                    }
                 }
             }
             ops.push_back(layer);
@@ -932,20 +941,24 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             if (bit >= 0) {
                 cd M[4];
                 op_matrix2(o, bwd, M);
+                int t = mtype(M);
+                if (g.trainable && g.kind == TQD_RZ) t = LT_DIAG;  // RZ gradients are batched on diagonal layers
                 const bool clash = active && ((mask >> bit) & 1);
-                if (active && (bwd ? (clash || layer.ngen + g.ngen > KOP_MAXGEN) : false)) flush();
-                if (active && clash && !bwd) {
-                    cd P[4];  // later op after earlier: M * LM
+                cd P[4];
+                if (clash && !bwd) {  // forward: compose later op after the earlier one on the same bit
                     P[0] = M[0] * LM[bit][0] + M[1] * LM[bit][2];
                     P[1] = M[0] * LM[bit][1] + M[1] * LM[bit][3];
                     P[2] = M[2] * LM[bit][0] + M[3] * LM[bit][2];
                     P[3] = M[2] * LM[bit][1] + M[3] * LM[bit][3];
-                    for (int q = 0; q < 4; q++) LM[bit][q] = P[q];
-                } else {
-                    active = true;
-                    mask |= 1 << bit;
-                    for (int q = 0; q < 4; q++) LM[bit][q] = M[q];
+                    if (mtype(P) == ltype) {
+                        for (int q = 0; q < 4; q++) LM[bit][q] = P[q];
+                        continue;
+                    }
                 }
+                if (active && (clash || t != ltype || (bwd && layer.ngen + g.ngen > KOP_MAXGEN))) flush();
+                if (!active) { active = true; ltype = t; }
+                mask |= 1 << bit;
+                for (int q = 0; q < 4; q++) LM[bit][q] = M[q];
                 if (has_gen)
                     for (int i = 0; i < g.ngen; i++) add_gen(layer, g, i, bit);
                 continue;

@@ -72,6 +72,15 @@ __device__ __forceinline__ void layer_gen(C *t, const Real *m) {
     }
 }
 
+// y = a*x + b*y for a complex pair with real coefficients: one packed f32x2
+// FMUL + FFMA per amplitude on sm_100a (fma.rn.f32x2), scalar in double
+__device__ __forceinline__ float2 raxpy(float a, float2 x, float b, float2 y) {
+    return __ffma2_rn(make_float2(b, b), y, __fmul2_rn(make_float2(a, a), x));
+}
+__device__ __forceinline__ double2 raxpy(double a, double2 x, double b, double2 y) {
+    return make_double2(a * x.x + b * y.x, a * x.y + b * y.y);
+}
+
 template <int MASK, typename C, typename Real>
 __device__ __forceinline__ void layer_real(C *t, const Real *m) {
 #pragma unroll
@@ -84,45 +93,18 @@ __device__ __forceinline__ void layer_real(C *t, const Real *m) {
             if (r & (1 << b)) continue;
             const int s = r | (1 << b);
             const C x0 = t[r], x1 = t[s];
-            t[r] = mk<C>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
-            t[s] = mk<C>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
+            t[r] = raxpy(m00, x0, m01, x1);
+            t[s] = raxpy(m10, x0, m11, x1);
         }
     }
 }
 
-constexpr int ctz4(int m) { return (m & 1) ? 0 : (m & 2) ? 1 : (m & 4) ? 2 : 3; }
-
-// diagonal layer: phase(r) = prod_b d_b[bit_b(r)], one complex multiply per amplitude
-template <int MASK, typename C, typename Real>
+// diagonal layer: m holds the 16 phase products ph[r] = prod_b d_b[bit_b(r)]
+// (built on the host): one complex multiply per amplitude for up to 4 gates
+template <typename C, typename Real>
 __device__ __forceinline__ void layer_diag(C *t, const Real *m) {
-    if constexpr (MASK == 0) {
-        return;
-    } else {
-        constexpr int B0 = ctz4(MASK);
-        C ph[NR];
-        {
-            const C d0 = mk<C>(m[8 * B0 + 0], m[8 * B0 + 1]), d1 = mk<C>(m[8 * B0 + 2], m[8 * B0 + 3]);
 #pragma unroll
-            for (int r = 0; r < (2 << B0); r++) ph[r] = ((r >> B0) & 1) ? d1 : d0;
-        }
-#pragma unroll
-        for (int b = B0 + 1; b < SWEEP_R; b++) {
-            const int h = 1 << b;
-            if ((MASK >> b) & 1) {
-                const C d0 = mk<C>(m[8 * b + 0], m[8 * b + 1]), d1 = mk<C>(m[8 * b + 2], m[8 * b + 3]);
-#pragma unroll
-                for (int r = 0; r < h; r++) {
-                    ph[r + h] = cmul(ph[r], d1);
-                    ph[r] = cmul(ph[r], d0);
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < h; r++) ph[r + h] = ph[r];
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < NR; r++) t[r] = cmul(ph[r], t[r]);
-    }
+    for (int r = 0; r < NR; r++) t[r] = cmul(mk<C>(m[2 * r], m[2 * r + 1]), t[r]);
 }
 
 // controlled general 2x2 (rare: controlled MAT2), in place; runtime control
@@ -179,16 +161,24 @@ __device__ __forceinline__ void op_d2(C *a, const Real *m, int m0, int rv0, int 
 }
 
 // ---- gradient partials on (psi, lambda): 2 Re <lam|G|psi> --------------------
+// element-wise x*y + z on the (re, im) pair (packed f32x2 FMA for float)
+__device__ __forceinline__ float2 cfma_elem(float2 x, float2 y, float2 z) { return __ffma2_rn(x, y, z); }
+__device__ __forceinline__ double2 cfma_elem(double2 x, double2 y, double2 z) {
+    return make_double2(fma(x.x, y.x, z.x), fma(x.y, y.y, z.y));
+}
 template <int T, typename C, typename Real>
 __device__ __forceinline__ Real grad_bit(const C *a, const C *l, int gk, const Real *g) {
     Real acc = 0;
-    if (gk == GEN_Y) {  // G = -(i/2) Y = [[0, -1/2], [1/2, 0]]
+    if (gk == GEN_Y) {  // G = -(i/2) Y = [[0, -1/2], [1/2, 0]]: Re(conj l1 a0) - Re(conj l0 a1)
+        C pos = mk<C>(0, 0), neg = mk<C>(0, 0);
 #pragma unroll
         for (int r = 0; r < NR; r++) {
             if (r & (1 << T)) continue;
             const int s = r | (1 << T);
-            acc += re_cj(l[s], a[r]) - re_cj(l[r], a[s]);
+            pos = cfma_elem(l[s], a[r], pos);
+            neg = cfma_elem(l[r], a[s], neg);
         }
+        acc = (pos.x + pos.y) - (neg.x + neg.y);
     } else if (gk == GEN_X) {  // G = -(i/2) X
 #pragma unroll
         for (int r = 0; r < NR; r++) {
@@ -233,7 +223,23 @@ __device__ __forceinline__ void run_kop(const KOp<Real> &op, typename CT<Real>::
         return b.kind == BK_TIX ? (int)((tix >> b.idx) & 1u) : (int)((basefull >> b.idx) & 1ull);
     };
     const int kind = op.kind;
-    if (BWD && op.ngen) {
+    if (BWD && op.ngen && kind == K_LAYER && op.ltype == LT_DIAG) {
+        // RZ generators of a diagonal layer, batched: w_r = Im(conj(lam_r) psi_r) once,
+        // g_b = sum_r (-1)^{bit_b(r)} w_r for every generator bit b
+        Real w[NR];
+#pragma unroll
+        for (int r = 0; r < NR; r++) w[r] = im_cj(l[r], a[r]);
+        for (int gi = 0; gi < op.ngen; gi++) {
+            Real part = 0;
+            dispatch4(op.gbit[gi], [&](auto tb) {
+                constexpr int T = decltype(tb)::value;
+#pragma unroll
+                for (int r = 0; r < NR; r++) part += ((r >> T) & 1) ? -w[r] : w[r];
+            });
+            part = warp_sum(part);
+            if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
+        }
+    } else if (BWD && op.ngen) {
         // gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
         for (int gi = 0; gi < op.ngen; gi++) {
             Real part = 0;
@@ -251,14 +257,16 @@ __device__ __forceinline__ void run_kop(const KOp<Real> &op, typename CT<Real>::
     switch (kind) {
     case K_LAYER: {
         const int lt = op.ltype;
+        if (lt == LT_DIAG) {
+            layer_diag<C, Real>(a, op.m);
+            if (BWD) layer_diag<C, Real>(l, op.m);
+            break;
+        }
         dispatch16(op.mask, [&](auto mk_) {
             constexpr int MASK = decltype(mk_)::value;
             if (lt == LT_REAL) {
                 layer_real<MASK, C, Real>(a, op.m);
                 if (BWD) layer_real<MASK, C, Real>(l, op.m);
-            } else if (lt == LT_DIAG) {
-                layer_diag<MASK, C, Real>(a, op.m);
-                if (BWD) layer_diag<MASK, C, Real>(l, op.m);
             } else {
                 layer_gen<MASK, C, Real>(a, op.m);
                 if (BWD) layer_gen<MASK, C, Real>(l, op.m);
@@ -319,7 +327,7 @@ __device__ __forceinline__ void run_kop(const KOp<Real> &op, typename CT<Real>::
 
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
 template <typename Real, bool BWD>
-__global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
+__global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
@@ -408,13 +416,19 @@ __global__ void __launch_bounds__(256) sweep_kernel(const DevStage *__restrict__
     const uint64_t ld_thr = thr_phys_off(S.lay[0], S.ld_phys);
     const uint64_t st_thr = thr_phys_off(S.lay[nseg - 1], S.st_phys);
 
-    for (int64_t tile = blockIdx.x; tile < S.n_tiles; tile += gridDim.x) {
-        // deposit the tile index into the non-tile physical positions
-        uint64_t base = (uint64_t)tile;
+    // tile index -> physical base: deposit into the non-tile positions once, then
+    // step by a masked add (carries propagate only through non-tile positions)
+    auto deposit = [&](uint64_t v) {
         for (int i = 0; i < k; i++) {
             const int p = S.tile_sorted[i];
-            base = ((base >> p) << (p + 1)) | (base & ((1ull << p) - 1));
+            v = ((v >> p) << (p + 1)) | (v & ((1ull << p) - 1));
         }
+        return v;
+    };
+    const uint64_t tmask = deposit(~0ull) & (S.n_tiles > 1 ? ~0ull : 0ull);
+    const uint64_t step = deposit((uint64_t)gridDim.x);
+    uint64_t base = deposit((uint64_t)blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < S.n_tiles; tile += gridDim.x, base = ((base | ~tmask) + step) & tmask) {
         const uint64_t basefull = base | rank_hi;
 
         C a[NR];
