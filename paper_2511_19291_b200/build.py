@@ -29,7 +29,7 @@ def _nccl_dirs():
 
 def _inputs():
     files = [os.path.join(CSRC, s) for s in SOURCES]
-    files += glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "tqd.h")]
+    files += glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "tqd.h")]
     return files
 
 

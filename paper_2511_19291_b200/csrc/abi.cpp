@@ -159,8 +159,8 @@ static PlanConfig plan_cfg(const tqd_state *st) {
     c.small_max = st->opt_small;
     c.c128 = st->dbl;
     c.swz_bits = st->dbl ? 3 : 4;
-    // shared memory budget: the adjoint holds psi and lambda tiles
-    while (c.k > 9 && ((size_t)2 << c.k) * st->esz > 160 * 1024) c.k--;
+    // shared memory budget: the adjoint exchanges psi and lambda tiles
+    while (c.k > 9 && ((size_t)2 << c.k) * st->esz > 144 * 1024) c.k--;
     if (c.k > c.n_loc) c.k = c.n_loc;
     if (c.k - LANE_BITS - c.R > WMAX) c.k = LANE_BITS + c.R + WMAX;
     return c;
