@@ -216,6 +216,16 @@ int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, cons
                    const double *params, const double *mats, const int *trainable, char *json_out, size_t cap,
                    size_t *needed);
 
+/* Diagnostic, host only: one rank's remap exchange schedule (PAPER.md:164, 261:
+ * interchange global qubit positions gpos[0..m) with local positions
+ * lpos[0..m) and redistribute).  Rank `rank` packs its local amplitudes into
+ * 2^m blocks by the values of the lpos-bits (block b, remaining local bits in
+ * ascending position order inside a block); block b goes to rank peer_out[b];
+ * the block received from that peer is unpacked as block recv_block_out[b]
+ * (its values become the lpos-bits).  Arrays of 2^m ints, caller-owned. */
+int tqd_debug_remap_schedule(int rank, int n_loc, int m, const int *gpos, const int *lpos, int *peer_out,
+                             int *recv_block_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,7 @@ _SIG = {
     "tqd_reset_metrics": [_P],
     "tqd_debug_plan": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                        _P, _P, _P, _P, _P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
+    "tqd_debug_remap_schedule": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P],
 }
 EXPORTS = list(_SIG) + ["tqd_last_error", "tqd_version"]
 
@@ -262,6 +263,17 @@ def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 
             cap = need.value
             continue
         raise TqdError(rc, tqd_last_error())
+
+
+def tqd_debug_remap_schedule(rank: int, n_loc: int, gpos, lpos):
+    """(peer[b], recv_block[b]) for every send block b of one rank's remap (host only)."""
+    m = len(gpos)
+    g = _arr(gpos or [0], np.int32)
+    l_ = _arr(lpos or [0], np.int32)
+    peer = np.zeros(1 << m, np.int32)
+    recv = np.zeros(1 << m, np.int32)
+    _call("tqd_debug_remap_schedule", rank, n_loc, m, _ptr(g), _ptr(l_), _ptr(peer), _ptr(recv))
+    return peer, recv
 
 
 # ---- convenience wrappers ----------------------------------------------------

@@ -212,6 +212,28 @@ static int ensure_lambda(tqd_state *st) {
 static uint64_t rank_hi(const tqd_state *st) { return (uint64_t)st->ctx->rank << st->n_loc; }
 
 // ---- remap exchange -------------------------------------
+// Swapping global positions gpos[i] with local positions lpos[i]: rank r sends
+// its block b (= the values of its lpos-bits) to the peer whose gpos-bits equal
+// b; the block received from a peer lands at block index u = that peer's
+// gpos-bits (the values the lpos-bits take after the swap).  Pure integer
+// schedule, shared by the device path and tqd_debug_remap_schedule.
+static void remap_schedule(int rank, int n_loc, const RemapPlan &rp, std::vector<int> &peer, std::vector<int> &recv_block) {
+    const int nb = 1 << rp.m;
+    peer.assign(nb, 0);
+    recv_block.assign(nb, 0);
+    for (int b = 0; b < nb; b++) {
+        int pr = rank;
+        for (int i = 0; i < rp.m; i++) {
+            const int gb = rp.gpos[i] - n_loc;
+            pr = (pr & ~(1 << gb)) | (((b >> i) & 1) << gb);
+        }
+        int u = 0;
+        for (int i = 0; i < rp.m; i++) u |= ((pr >> (rp.gpos[i] - n_loc)) & 1) << i;
+        peer[b] = pr;
+        recv_block[b] = u;
+    }
+}
+
 static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
     int rc = ensure_xchg(st);
     if (rc) return rc;
@@ -229,15 +251,12 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
     CUDA_TRY(st, launch_remap_pack(st->dbl, buf, st->sendb, rm, c->stream));
     const size_t bb = blk * st->esz;
     char *sb = (char *)st->sendb, *rb = (char *)st->recvb;
+    std::vector<int> peers, ublk;
+    remap_schedule(c->rank, st->n_loc, rp, peers, ublk);
     NCCL_TRY(st, ncclGroupStart());
     for (uint64_t b = 0; b < ((uint64_t)1 << rp.m); b++) {
-        int peer = c->rank;
-        for (int i = 0; i < rp.m; i++) {
-            const int gb = rp.gpos[i] - st->n_loc;
-            peer = (peer & ~(1 << gb)) | ((int)((b >> i) & 1) << gb);
-        }
-        uint64_t u = 0;  // peer's global-bit values = where its block lands here
-        for (int i = 0; i < rp.m; i++) u |= (uint64_t)((peer >> (rp.gpos[i] - st->n_loc)) & 1) << i;
+        const int peer = peers[b];
+        const uint64_t u = (uint64_t)ublk[b];
         if (peer == c->rank) {
             CUDA_TRY(st, cudaMemcpyAsync(rb + u * bb, sb + b * bb, bb, cudaMemcpyDeviceToDevice, c->stream));
         } else {
@@ -930,6 +949,28 @@ int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, cons
     if (needed) *needed = js.size() + 1;
     if (!json_out || cap < js.size() + 1) return fail(TQD_ERR_ARG, "json buffer too small");
     memcpy(json_out, js.c_str(), js.size() + 1);
+    return TQD_OK;
+}
+
+// Diagnostic, host only: the remap exchange schedule of one rank.  For each
+// send block b in [0, 2^m): peer_out[b] = destination rank, recv_block_out[b] =
+// block index where the data received from that peer is placed.
+int tqd_debug_remap_schedule(int rank, int n_loc, int m, const int *gpos, const int *lpos, int *peer_out,
+                             int *recv_block_out) {
+    if (m < 0 || m > 8 || !gpos || !lpos || !peer_out || !recv_block_out) return fail(TQD_ERR_ARG, "bad arguments");
+    RemapPlan rp;
+    rp.m = m;
+    for (int i = 0; i < m; i++) {
+        if (gpos[i] < n_loc || lpos[i] < 0 || lpos[i] >= n_loc) return fail(TQD_ERR_ARG, "bad positions");
+        rp.gpos[i] = gpos[i];
+        rp.lpos[i] = lpos[i];
+    }
+    std::vector<int> pr, ub;
+    remap_schedule(rank, n_loc, rp, pr, ub);
+    for (int b = 0; b < (1 << m); b++) {
+        peer_out[b] = pr[b];
+        recv_block_out[b] = ub[b];
+    }
     return TQD_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <sstream>
 
 #include "../../include/tqd.h"
@@ -849,6 +850,24 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     ds.op_base = (int)ops.size();
     ds.slot_base = (int)slot_param.size();
     int nslots = 0;
+    auto finalize = [](KOp<Real> &k) {
+        switch (k.kind) {
+        case K_LAYER:
+            k.code = (uint8_t)(k.ltype == LT_DIAG ? KC_DIAG : k.ltype == LT_REAL ? KC_REAL + k.mask : KC_GEN + k.mask);
+            break;
+        case K_CU: k.code = (uint8_t)(KC_CU + k.t0); break;
+        case K_PHASE: k.code = KC_PHASE; break;
+        case K_D2: k.code = KC_D2; break;
+        case K_U2: k.code = (uint8_t)(KC_U2 + u2_index(k.t0, k.t1)); break;
+        default: k.code = KC_NOP; break;
+        }
+        k.gbits = 0;
+        k.gkinds = 0;
+        for (int i = 0; i < k.ngen; i++) {
+            k.gbits |= (uint8_t)((k.gbit[i] & 3) << (2 * i));
+            k.gkinds |= (uint16_t)((k.gkind[i] & 15) << (4 * i));
+        }
+    };
     auto newop = [](int kind) {
         KOp<Real> k;
         memset(&k, 0, sizeof(k));
@@ -924,13 +943,15 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                     }
                 }
             }
+            finalize(layer);
             ops.push_back(layer);
             active = false;
             mask = 0;
             layer = newop(K_LAYER);
         };
         const int b = sp.seg_begin[fs], e = sp.seg_begin[fs + 1];
-        for (int jj = 0; jj < e - b; jj++) {
+        static const bool skip_ops = getenv("TQD_EXPERIMENT_SKIP_OPS") != nullptr;  // timing experiment only
+        for (int jj = 0; jj < e - b && !skip_ops; jj++) {
             const POp &o = sp.ops[bwd ? e - 1 - jj : b + jj];
             if (o.perm) continue;  // folded into the layout-change maps below
             const GateRec &g = gates[o.gate];
@@ -1011,6 +1032,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             }
             default: continue;
             }
+            finalize(k);
             ops.push_back(k);
         }
         flush();

@@ -215,77 +215,109 @@ __device__ __forceinline__ Real grad_z_const(const C *a, const C *l, int bit) {
 }
 
 // ---- one op, in place on psi (and lambda in the adjoint) ----------------------
+// h = the op's 16-byte dispatch header (already in registers: prefetched while
+// the previous op ran), op = the full op in shared memory (coefficients).
 template <typename Real, bool BWD>
-__device__ __forceinline__ void run_kop(const KOp<Real> &op, typename CT<Real>::C *a, typename CT<Real>::C *l,
-                                        uint32_t tix, uint64_t basefull, double *wacc) {
+__device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
+                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, double *wacc) {
     typedef typename CT<Real>::C C;
-    auto bitval = [&](BitRef b) -> int {
-        return b.kind == BK_TIX ? (int)((tix >> b.idx) & 1u) : (int)((basefull >> b.idx) & 1ull);
+    auto bitval = [&](uint32_t kind, uint32_t idx) -> int {
+        return kind == BK_TIX ? (int)((tix >> idx) & 1u) : (int)((basefull >> idx) & 1ull);
     };
-    const int kind = op.kind;
-    if (BWD && op.ngen && kind == K_LAYER && op.ltype == LT_DIAG) {
-        // RZ generators of a diagonal layer, batched: w_r = Im(conj(lam_r) psi_r) once,
-        // g_b = sum_r (-1)^{bit_b(r)} w_r for every generator bit b
-        Real w[NR];
+    const int code = h.x & 0xff;
+    if (BWD) {
+        const int ngen = (h.x >> 8) & 0xff;
+        if (ngen) {
+            const uint32_t gbits = h.y & 0xff;
+            const uint32_t gkinds = h.w & 0xffff;
+            if (code == KC_DIAG) {
+                // RZ generators of a diagonal layer, batched: w_r = Im(conj(lam_r) psi_r),
+                // g_b = sum_r (-1)^{bit_b(r)} w_r for every generator bit b
+                Real w[NR];
 #pragma unroll
-        for (int r = 0; r < NR; r++) w[r] = im_cj(l[r], a[r]);
-        for (int gi = 0; gi < op.ngen; gi++) {
-            Real part = 0;
-            dispatch4(op.gbit[gi], [&](auto tb) {
-                constexpr int T = decltype(tb)::value;
+                for (int r = 0; r < NR; r++) w[r] = im_cj(l[r], a[r]);
+                for (int gi = 0; gi < ngen; gi++) {
+                    Real part = 0;
+                    dispatch4((gbits >> (2 * gi)) & 3, [&](auto tb) {
+                        constexpr int T = decltype(tb)::value;
 #pragma unroll
-                for (int r = 0; r < NR; r++) part += ((r >> T) & 1) ? -w[r] : w[r];
-            });
-            part = warp_sum(part);
-            if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
-        }
-    } else if (BWD && op.ngen) {
-        // gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
-        for (int gi = 0; gi < op.ngen; gi++) {
-            Real part = 0;
-            if (kind == K_PHASE) {
-                part = grad_z_const<C, Real>(a, l, bitval(op.b0));
+                        for (int r = 0; r < NR; r++) part += ((r >> T) & 1) ? -w[r] : w[r];
+                    });
+                    part = warp_sum(part);
+                    if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
+                }
             } else {
-                const int gk = op.gkind[gi];
-                const Real *g = op.g[gi];
-                dispatch4(op.gbit[gi], [&](auto tb) { part = grad_bit<decltype(tb)::value, C, Real>(a, l, gk, g); });
+                // gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
+                for (int gi = 0; gi < ngen; gi++) {
+                    Real part = 0;
+                    if (code == KC_PHASE) {
+                        part = grad_z_const<C, Real>(a, l, bitval((h.z) & 0xff, (h.z >> 8) & 0xff));
+                    } else {
+                        const int gk = (gkinds >> (4 * gi)) & 15;
+                        const Real *g = op.g[gi];
+                        dispatch4((gbits >> (2 * gi)) & 3,
+                                  [&](auto tb) { part = grad_bit<decltype(tb)::value, C, Real>(a, l, gk, g); });
+                    }
+                    part = warp_sum(part);
+                    if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
+                }
             }
-            part = warp_sum(part);
-            if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
         }
     }
-    switch (kind) {
-    case K_LAYER: {
-        const int lt = op.ltype;
-        if (lt == LT_DIAG) {
-            layer_diag<C, Real>(a, op.m);
-            if (BWD) layer_diag<C, Real>(l, op.m);
-            break;
-        }
-        dispatch16(op.mask, [&](auto mk_) {
-            constexpr int MASK = decltype(mk_)::value;
-            if (lt == LT_REAL) {
-                layer_real<MASK, C, Real>(a, op.m);
-                if (BWD) layer_real<MASK, C, Real>(l, op.m);
-            } else {
-                layer_gen<MASK, C, Real>(a, op.m);
-                if (BWD) layer_gen<MASK, C, Real>(l, op.m);
-            }
-        });
-        break;
-    }
-    case K_CU: {
-        const bool on = op.ctrl.kind == BK_NONE ? true : bitval(op.ctrl) != 0;
-        const int cm = op.creg != 0xff ? (1 << op.creg) : 0;
-        dispatch4(op.t0, [&](auto tt) {
-            constexpr int T = decltype(tt)::value;
-            op_cu<T, C, Real>(a, op.m, cm, on);
-            if (BWD) op_cu<T, C, Real>(l, op.m, cm, on);
-        });
-        break;
-    }
-    case K_PHASE: {
-        const int v = bitval(op.b0);
+    const uint32_t creg = (h.x >> 16) & 0xff;
+    const uint32_t ck = (h.y >> 16) & 0xff, ci = h.y >> 24;
+    const bool on = ck == BK_NONE ? true : bitval(ck, ci) != 0;
+    const int cm = creg != 0xff ? (1 << creg) : 0;
+    switch (code) {
+    case 1: layer_real<1, C, Real>(a, op.m); if (BWD) layer_real<1, C, Real>(l, op.m); break;
+    case 2: layer_real<2, C, Real>(a, op.m); if (BWD) layer_real<2, C, Real>(l, op.m); break;
+    case 3: layer_real<3, C, Real>(a, op.m); if (BWD) layer_real<3, C, Real>(l, op.m); break;
+    case 4: layer_real<4, C, Real>(a, op.m); if (BWD) layer_real<4, C, Real>(l, op.m); break;
+    case 5: layer_real<5, C, Real>(a, op.m); if (BWD) layer_real<5, C, Real>(l, op.m); break;
+    case 6: layer_real<6, C, Real>(a, op.m); if (BWD) layer_real<6, C, Real>(l, op.m); break;
+    case 7: layer_real<7, C, Real>(a, op.m); if (BWD) layer_real<7, C, Real>(l, op.m); break;
+    case 8: layer_real<8, C, Real>(a, op.m); if (BWD) layer_real<8, C, Real>(l, op.m); break;
+    case 9: layer_real<9, C, Real>(a, op.m); if (BWD) layer_real<9, C, Real>(l, op.m); break;
+    case 10: layer_real<10, C, Real>(a, op.m); if (BWD) layer_real<10, C, Real>(l, op.m); break;
+    case 11: layer_real<11, C, Real>(a, op.m); if (BWD) layer_real<11, C, Real>(l, op.m); break;
+    case 12: layer_real<12, C, Real>(a, op.m); if (BWD) layer_real<12, C, Real>(l, op.m); break;
+    case 13: layer_real<13, C, Real>(a, op.m); if (BWD) layer_real<13, C, Real>(l, op.m); break;
+    case 14: layer_real<14, C, Real>(a, op.m); if (BWD) layer_real<14, C, Real>(l, op.m); break;
+    case 15: layer_real<15, C, Real>(a, op.m); if (BWD) layer_real<15, C, Real>(l, op.m); break;
+    case 16: layer_gen<1, C, Real>(a, op.m); if (BWD) layer_gen<1, C, Real>(l, op.m); break;
+    case 17: layer_gen<2, C, Real>(a, op.m); if (BWD) layer_gen<2, C, Real>(l, op.m); break;
+    case 18: layer_gen<3, C, Real>(a, op.m); if (BWD) layer_gen<3, C, Real>(l, op.m); break;
+    case 19: layer_gen<4, C, Real>(a, op.m); if (BWD) layer_gen<4, C, Real>(l, op.m); break;
+    case 20: layer_gen<5, C, Real>(a, op.m); if (BWD) layer_gen<5, C, Real>(l, op.m); break;
+    case 21: layer_gen<6, C, Real>(a, op.m); if (BWD) layer_gen<6, C, Real>(l, op.m); break;
+    case 22: layer_gen<7, C, Real>(a, op.m); if (BWD) layer_gen<7, C, Real>(l, op.m); break;
+    case 23: layer_gen<8, C, Real>(a, op.m); if (BWD) layer_gen<8, C, Real>(l, op.m); break;
+    case 24: layer_gen<9, C, Real>(a, op.m); if (BWD) layer_gen<9, C, Real>(l, op.m); break;
+    case 25: layer_gen<10, C, Real>(a, op.m); if (BWD) layer_gen<10, C, Real>(l, op.m); break;
+    case 26: layer_gen<11, C, Real>(a, op.m); if (BWD) layer_gen<11, C, Real>(l, op.m); break;
+    case 27: layer_gen<12, C, Real>(a, op.m); if (BWD) layer_gen<12, C, Real>(l, op.m); break;
+    case 28: layer_gen<13, C, Real>(a, op.m); if (BWD) layer_gen<13, C, Real>(l, op.m); break;
+    case 29: layer_gen<14, C, Real>(a, op.m); if (BWD) layer_gen<14, C, Real>(l, op.m); break;
+    case 30: layer_gen<15, C, Real>(a, op.m); if (BWD) layer_gen<15, C, Real>(l, op.m); break;
+    case KC_DIAG: layer_diag<C, Real>(a, op.m); if (BWD) layer_diag<C, Real>(l, op.m); break;
+    case 32: op_cu<0, C, Real>(a, op.m, cm, on); if (BWD) op_cu<0, C, Real>(l, op.m, cm, on); break;
+    case 33: op_cu<1, C, Real>(a, op.m, cm, on); if (BWD) op_cu<1, C, Real>(l, op.m, cm, on); break;
+    case 34: op_cu<2, C, Real>(a, op.m, cm, on); if (BWD) op_cu<2, C, Real>(l, op.m, cm, on); break;
+    case 35: op_cu<3, C, Real>(a, op.m, cm, on); if (BWD) op_cu<3, C, Real>(l, op.m, cm, on); break;
+    case 38: op_u2<0, 1, C, Real>(a, op.m); if (BWD) op_u2<0, 1, C, Real>(l, op.m); break;
+    case 39: op_u2<0, 2, C, Real>(a, op.m); if (BWD) op_u2<0, 2, C, Real>(l, op.m); break;
+    case 40: op_u2<0, 3, C, Real>(a, op.m); if (BWD) op_u2<0, 3, C, Real>(l, op.m); break;
+    case 41: op_u2<1, 0, C, Real>(a, op.m); if (BWD) op_u2<1, 0, C, Real>(l, op.m); break;
+    case 42: op_u2<1, 2, C, Real>(a, op.m); if (BWD) op_u2<1, 2, C, Real>(l, op.m); break;
+    case 43: op_u2<1, 3, C, Real>(a, op.m); if (BWD) op_u2<1, 3, C, Real>(l, op.m); break;
+    case 44: op_u2<2, 0, C, Real>(a, op.m); if (BWD) op_u2<2, 0, C, Real>(l, op.m); break;
+    case 45: op_u2<2, 1, C, Real>(a, op.m); if (BWD) op_u2<2, 1, C, Real>(l, op.m); break;
+    case 46: op_u2<2, 3, C, Real>(a, op.m); if (BWD) op_u2<2, 3, C, Real>(l, op.m); break;
+    case 47: op_u2<3, 0, C, Real>(a, op.m); if (BWD) op_u2<3, 0, C, Real>(l, op.m); break;
+    case 48: op_u2<3, 1, C, Real>(a, op.m); if (BWD) op_u2<3, 1, C, Real>(l, op.m); break;
+    case 49: op_u2<3, 2, C, Real>(a, op.m); if (BWD) op_u2<3, 2, C, Real>(l, op.m); break;
+    case KC_PHASE: {
+        const int v = bitval(h.z & 0xff, (h.z >> 8) & 0xff);
         const C d = v ? mk<C>(op.m[2], op.m[3]) : mk<C>(op.m[0], op.m[1]);
 #pragma unroll
         for (int r = 0; r < NR; r++) a[r] = cmul(d, a[r]);
@@ -295,30 +327,14 @@ __device__ __forceinline__ void run_kop(const KOp<Real> &op, typename CT<Real>::
         }
         break;
     }
-    case K_D2: {
-        const int m0 = op.b0.kind == BK_REG ? (1 << op.b0.idx) : 0;
-        const int m1 = op.b1.kind == BK_REG ? (1 << op.b1.idx) : 0;
-        const int v0 = m0 ? 0 : bitval(op.b0);
-        const int v1 = m1 ? 0 : bitval(op.b1);
+    case KC_D2: {
+        const uint32_t k0 = h.z & 0xff, i0 = (h.z >> 8) & 0xff, k1 = (h.z >> 16) & 0xff, i1 = h.z >> 24;
+        const int m0 = k0 == BK_REG ? (1 << i0) : 0;
+        const int m1 = k1 == BK_REG ? (1 << i1) : 0;
+        const int v0 = m0 ? 0 : bitval(k0, i0);
+        const int v1 = m1 ? 0 : bitval(k1, i1);
         op_d2<C, Real>(a, op.m, m0, v0, m1, v1);
         if (BWD) op_d2<C, Real>(l, op.m, m0, v0, m1, v1);
-        break;
-    }
-    case K_U2: {
-        const int code = op.t0 * 4 + op.t1;
-        auto go = [&](auto c0, auto c1) {
-            constexpr int T0 = decltype(c0)::value, T1 = decltype(c1)::value;
-            op_u2<T0, T1, C, Real>(a, op.m);
-            if (BWD) op_u2<T0, T1, C, Real>(l, op.m);
-        };
-        switch (code) {
-        case 1: go(IC<0>{}, IC<1>{}); break;   case 2: go(IC<0>{}, IC<2>{}); break;
-        case 3: go(IC<0>{}, IC<3>{}); break;   case 4: go(IC<1>{}, IC<0>{}); break;
-        case 6: go(IC<1>{}, IC<2>{}); break;   case 7: go(IC<1>{}, IC<3>{}); break;
-        case 8: go(IC<2>{}, IC<0>{}); break;   case 9: go(IC<2>{}, IC<1>{}); break;
-        case 11: go(IC<2>{}, IC<3>{}); break;  case 12: go(IC<3>{}, IC<0>{}); break;
-        case 13: go(IC<3>{}, IC<1>{}); break;  default: go(IC<3>{}, IC<2>{}); break;
-        }
         break;
     }
     default: break;
@@ -470,7 +486,14 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
             }
             const uint32_t tix = thr_tix(S.lay[s]);
             const int e = S.seg_begin[s + 1];
-            for (int oi = S.seg_begin[s]; oi < e; oi++) run_kop<Real, BWD>(s_ops[oi], a, l, tix, basefull, wacc);
+            int oi = S.seg_begin[s];
+            uint4 h = oi < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi]) : make_uint4(0, 0, 0, 0);
+            for (; oi < e; oi++) {
+                // header of the next op loads while this one runs
+                const uint4 hn = oi + 1 < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi + 1]) : h;
+                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, wacc);
+                h = hn;
+            }
         }
 
         {

@@ -96,20 +96,38 @@ enum KKind : uint8_t {
 enum LType : uint8_t { LT_GEN = 0, LT_REAL = 1, LT_DIAG = 2 };
 constexpr int KOP_MAXGEN = 4;
 
+// dense dispatch codes: one flat switch (jump table) in the kernel
+enum KCode : uint8_t {
+    KC_NOP = 0,
+    KC_REAL = 0,    // KC_REAL + mask (1..15): real 2x2 per active register bit
+    KC_GEN = 15,    // KC_GEN + mask (16..30): complex 2x2 per active register bit
+    KC_DIAG = 31,   // 16-phase table
+    KC_CU = 32,     // KC_CU + t0 (32..35)
+    KC_PHASE = 36,
+    KC_D2 = 37,
+    KC_U2 = 38,     // KC_U2 + u2_index(t0, t1) (38..49)
+    KC_COUNT = 50,
+};
+inline int u2_index(int t0, int t1) { return t0 * 3 + (t1 > t0 ? t1 - 1 : t1); }
+
+// The first 16 bytes are the dispatch header (prefetched one op ahead).
 template <typename Real> struct alignas(16) KOp {
-    uint8_t kind;
-    uint8_t mask;               // K_LAYER active register bits
-    uint8_t ltype;              // K_LAYER matrix type (LType)
-    uint8_t t0, t1;             // register-bit targets
+    uint8_t code;               // KCode
+    uint8_t ngen;               // backward: generators (gradient slots)
     uint8_t creg;               // register-bit control, 0xff = none
+    uint8_t t0;                 // K_CU target register bit
+    uint8_t gbits;              // generator register bits, 2 bits each
+    uint8_t pad0;
     BitRef ctrl;                // lane / warp / base control, BK_NONE = none
     BitRef b0, b1;              // K_PHASE / K_D2 bits
-    uint8_t ngen;               // backward: generators (gradient slots)
-    uint8_t gbit[KOP_MAXGEN];   // register bit of each generator (K_LAYER)
-    uint8_t gkind[KOP_MAXGEN];  // GenKind
-    uint8_t pad;
+    uint16_t gkinds;            // GenKind of each generator, 4 bits each
+    uint8_t kind, ltype;        // host / debug only
     int16_t slot[KOP_MAXGEN];   // stage-local slot
-    Real m[32];
+    uint8_t mask, t1;           // host / debug only
+    uint8_t gbit[KOP_MAXGEN];   // host view of gbits
+    uint8_t gkind[KOP_MAXGEN];  // host view of gkinds
+    uint8_t pad1[14];
+    Real m[32];                 // 16-byte aligned (offset 48)
     Real g[KOP_MAXGEN][8];      // generators (2x2 complex)
 };
 
