@@ -17,9 +17,9 @@
 namespace tqd {
 // kernels.cu
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
-                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int grid,
-                         cudaStream_t s);
-int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops);
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots,
+                         int grid, cudaStream_t s);
+int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
                          uint64_t rank_hi, cudaStream_t s);
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
@@ -275,9 +275,9 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
 }
 
 // ---- forward execution ------------------------------------------------------
-static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops) {
+static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops, int n_slots) {
     if (st->opt_grid > 0) return st->opt_grid;
-    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops);
+    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots);
     if (per < 1) per = 1;
     int64_t g = (int64_t)per * st->ctx->sms;
     const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
@@ -291,7 +291,7 @@ struct Encoded {
     size_t cap = 0;
     size_t off_ops = 0, off_sl = 0;
     size_t off_kops = 0;
-    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; };
+    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; int n_slots; };
     std::vector<L> launches;
     bool valid = false;
 };
@@ -312,7 +312,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
             const SweepPlan &sp = s.sw;
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
-                                      sp.k, sp.W, l.n_ops, l.grid, c->stream));
+                                      sp.k, sp.W, l.n_ops, l.n_slots, l.grid, c->stream));
             ev_end(st, ev);
             if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += sp.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
@@ -346,15 +346,15 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
             DevStage ds;
             encode_sweep_k<Real>(s.sw, st->gates, bwd, st->n_loc, ds, kops, slots);
             E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
-                                  sweep_grid(st, s.sw, bwd, ds.n_ops)});
+                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots), ds.n_slots});
             dstages.push_back(ds);
         } else if (s.type == ST_SMALL) {
             if (s.sm.ops.empty()) continue;
             const int b = (int)ops.size();
             encode_small(s.sm, st->gates, bwd, ops);
-            E.launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, (int)ii, 1});
+            E.launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, (int)ii, 1, 0});
         } else {
-            E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii, 0});
+            E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii, 0, 0});
         }
     }
 }

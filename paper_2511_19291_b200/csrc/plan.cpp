@@ -850,6 +850,14 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     ds.op_base = (int)ops.size();
     ds.slot_base = (int)slot_param.size();
     int nslots = 0;
+    // complex coefficient e at m[4i..4i+3] as (re, 0, im, im): the kernel does a
+    // complex multiply with one packed FMUL2 + one FFMA2 (swapped / negated halves)
+    auto pute = [](KOp<Real> &k, int i, cd v) {
+        k.m[4 * i] = (Real)v.real();
+        k.m[4 * i + 1] = 0;
+        k.m[4 * i + 2] = (Real)v.imag();
+        k.m[4 * i + 3] = (Real)v.imag();
+    };
     auto finalize = [](KOp<Real> &k) {
         switch (k.kind) {
         case K_LAYER:
@@ -929,8 +937,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                     cd ph = 1.0;
                     for (int bb = 0; bb < R; bb++)
                         if ((mask >> bb) & 1) ph *= ((r >> bb) & 1) ? LM[bb][3] : LM[bb][0];
-                    layer.m[2 * r] = (Real)ph.real();
-                    layer.m[2 * r + 1] = (Real)ph.imag();
+                    pute(layer, r, ph);
                 }
             } else {
                 for (int bb = 0; bb < R; bb++) {
@@ -939,7 +946,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                     if (ltype == LT_REAL) {
                         for (int q = 0; q < 4; q++) m[q] = (Real)LM[bb][q].real();
                     } else {
-                        for (int q = 0; q < 4; q++) { m[2 * q] = (Real)LM[bb][q].real(); m[2 * q + 1] = (Real)LM[bb][q].imag(); }
+                        for (int q = 0; q < 4; q++) pute(layer, 4 * bb + q, LM[bb][q]);
                     }
                 }
             }
@@ -996,15 +1003,15 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 const int cr = regidx(o.cp);
                 if (cr >= 0) k.creg = (uint8_t)cr;
                 else if (o.cp >= 0) k.ctrl = bref(o.cp);
-                for (int q = 0; q < 4; q++) { k.m[2 * q] = (Real)M[q].real(); k.m[2 * q + 1] = (Real)M[q].imag(); }
+                for (int q = 0; q < 4; q++) pute(k, q, M[q]);
                 break;
             }
             case OP_D1: {
                 op_matrix2(o, bwd, M);
                 k.kind = K_PHASE;
                 k.b0 = bref(o.dp0);
-                k.m[0] = (Real)M[0].real(); k.m[1] = (Real)M[0].imag();
-                k.m[2] = (Real)M[3].real(); k.m[3] = (Real)M[3].imag();
+                pute(k, 0, M[0]);
+                pute(k, 1, M[3]);
                 if (has_gen) add_gen(k, g, 0, 0);
                 break;
             }
@@ -1012,10 +1019,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 k.kind = K_D2;
                 k.b0 = bref(o.dp0);
                 k.b1 = bref(o.dp1);
-                for (int q = 0; q < 4; q++) {
-                    const cd d = bwd ? std::conj(o.m[q]) : o.m[q];
-                    k.m[2 * q] = (Real)d.real(); k.m[2 * q + 1] = (Real)d.imag();
-                }
+                for (int q = 0; q < 4; q++) pute(k, q, bwd ? std::conj(o.m[q]) : o.m[q]);
                 break;
             }
             case OP_U2: {
@@ -1023,11 +1027,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 k.t0 = (uint8_t)regidx(o.tp0);
                 k.t1 = (uint8_t)regidx(o.tp1);
                 for (int r = 0; r < 4; r++)
-                    for (int c = 0; c < 4; c++) {
-                        const cd v = bwd ? std::conj(o.m[4 * c + r]) : o.m[4 * r + c];
-                        k.m[8 * r + 2 * c] = (Real)v.real();
-                        k.m[8 * r + 2 * c + 1] = (Real)v.imag();
-                    }
+                    for (int c = 0; c < 4; c++) pute(k, 4 * r + c, bwd ? std::conj(o.m[4 * c + r]) : o.m[4 * r + c]);
                 break;
             }
             default: continue;

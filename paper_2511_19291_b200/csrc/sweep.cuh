@@ -52,22 +52,40 @@ template <typename F> __device__ __forceinline__ void dispatch16(int t, F &&f) {
     }
 }
 
+// ---- complex helpers on packed coefficients --------------------------------
+// complex coefficient stored as (re, 0, im, im) at e[0..3]:
+//   cmul_e(e, x) = e * x,  cfma_e(e, x, acc) = acc + e * x
+// float: a packed FMUL2/FFMA2 with the real part broadcast + one FFMA2 with the
+// halves of x swapped and the (im, im) pair half-negated; double: scalar.
+__device__ __forceinline__ float2 cmul_e(const float *e, float2 x) {
+    const float4 v = *reinterpret_cast<const float4 *>(e);
+    return __ffma2_rn(make_float2(-v.z, v.w), make_float2(x.y, x.x), __fmul2_rn(make_float2(v.x, v.x), x));
+}
+__device__ __forceinline__ float2 cfma_e(const float *e, float2 x, float2 acc) {
+    const float4 v = *reinterpret_cast<const float4 *>(e);
+    return __ffma2_rn(make_float2(-v.z, v.w), make_float2(x.y, x.x), __ffma2_rn(make_float2(v.x, v.x), x, acc));
+}
+__device__ __forceinline__ double2 cmul_e(const double *e, double2 x) {
+    return make_double2(e[0] * x.x - e[2] * x.y, e[0] * x.y + e[2] * x.x);
+}
+__device__ __forceinline__ double2 cfma_e(const double *e, double2 x, double2 acc) {
+    return make_double2(acc.x + e[0] * x.x - e[2] * x.y, acc.y + e[0] * x.y + e[2] * x.x);
+}
+
 // ---- layer ops: one 2x2 per active register bit, in place -------------------
 template <int MASK, typename C, typename Real>
 __device__ __forceinline__ void layer_gen(C *t, const Real *m) {
 #pragma unroll
     for (int b = 0; b < SWEEP_R; b++) {
         if (!((MASK >> b) & 1)) continue;
-        const Real *mb = m + 8 * b;
-        const C m00 = mk<C>(mb[0], mb[1]), m01 = mk<C>(mb[2], mb[3]), m10 = mk<C>(mb[4], mb[5]),
-                m11 = mk<C>(mb[6], mb[7]);
+        const Real *mb = m + 16 * b;  // entries 00, 01, 10, 11
 #pragma unroll
         for (int r = 0; r < NR; r++) {
             if (r & (1 << b)) continue;
             const int s = r | (1 << b);
             const C x0 = t[r], x1 = t[s];
-            t[r] = cmul2(m00, x0, m01, x1);
-            t[s] = cmul2(m10, x0, m11, x1);
+            t[r] = cfma_e(mb + 4, x1, cmul_e(mb, x0));
+            t[s] = cfma_e(mb + 12, x1, cmul_e(mb + 8, x0));
         }
     }
 }
@@ -104,19 +122,18 @@ __device__ __forceinline__ void layer_real(C *t, const Real *m) {
 template <typename C, typename Real>
 __device__ __forceinline__ void layer_diag(C *t, const Real *m) {
 #pragma unroll
-    for (int r = 0; r < NR; r++) t[r] = cmul(mk<C>(m[2 * r], m[2 * r + 1]), t[r]);
+    for (int r = 0; r < NR; r++) t[r] = cmul_e(m + 4 * r, t[r]);
 }
 
 // controlled general 2x2 (rare: controlled MAT2), in place; runtime control
 template <int T, typename C, typename Real>
 __device__ __forceinline__ void op_cu(C *a, const Real *m, int cm, bool on) {
-    const C m00 = mk<C>(m[0], m[1]), m01 = mk<C>(m[2], m[3]), m10 = mk<C>(m[4], m[5]), m11 = mk<C>(m[6], m[7]);
 #pragma unroll
     for (int r = 0; r < NR; r++) {
         if (r & (1 << T)) continue;
         const int s = r | (1 << T);
         const C x0 = a[r], x1 = a[s];
-        const C y0 = cmul2(m00, x0, m01, x1), y1 = cmul2(m10, x0, m11, x1);
+        const C y0 = cfma_e(m + 4, x1, cmul_e(m, x0)), y1 = cfma_e(m + 12, x1, cmul_e(m + 8, x0));
         const Real p = (on && ((r & cm) == cm)) ? (Real)1 : (Real)0;  // arithmetic blend: no register moves
         a[r] = mk<C>(x0.x + p * (y0.x - x0.x), x0.y + p * (y0.y - x0.y));
         a[s] = mk<C>(x1.x + p * (y1.x - x1.x), x1.y + p * (y1.y - x1.y));
@@ -134,13 +151,9 @@ __device__ __forceinline__ void op_u2(C *a, const Real *m) {
         for (int q = 0; q < 4; q++) v[q] = a[idx[q]];
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            C acc = cmul(mk<C>(m[8 * i], m[8 * i + 1]), v[0]);
+            C acc = cmul_e(m + 16 * i, v[0]);
 #pragma unroll
-            for (int q = 1; q < 4; q++) {
-                const C p = cmul(mk<C>(m[8 * i + 2 * q], m[8 * i + 2 * q + 1]), v[q]);
-                acc.x += p.x;
-                acc.y += p.y;
-            }
+            for (int q = 1; q < 4; q++) acc = cfma_e(m + 16 * i + 4 * q, v[q], acc);
             a[idx[i]] = acc;
         }
     }
@@ -149,14 +162,11 @@ __device__ __forceinline__ void op_u2(C *a, const Real *m) {
 // diagonal 2q on arbitrary bits: v = register bit (mask) or per-thread value
 template <typename C, typename Real>
 __device__ __forceinline__ void op_d2(C *a, const Real *m, int m0, int rv0, int m1, int rv1) {
-    const C d0 = mk<C>(m[0], m[1]), d1 = mk<C>(m[2], m[3]), d2 = mk<C>(m[4], m[5]), d3 = mk<C>(m[6], m[7]);
 #pragma unroll
     for (int r = 0; r < NR; r++) {
         const int v0 = m0 ? ((r & m0) != 0) : rv0;
         const int v1 = m1 ? ((r & m1) != 0) : rv1;
-        const C e0 = v1 ? d1 : d0;
-        const C e1 = v1 ? d3 : d2;
-        a[r] = cmul(v0 ? e1 : e0, a[r]);
+        a[r] = cmul_e(m + 4 * (2 * v0 + v1), a[r]);
     }
 }
 
@@ -219,7 +229,7 @@ __device__ __forceinline__ Real grad_z_const(const C *a, const C *l, int bit) {
 // the previous op ran), op = the full op in shared memory (coefficients).
 template <typename Real, bool BWD>
 __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
-                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, double *wacc) {
+                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, Real *tacc) {
     typedef typename CT<Real>::C C;
     auto bitval = [&](uint32_t kind, uint32_t idx) -> int {
         return kind == BK_TIX ? (int)((tix >> idx) & 1u) : (int)((basefull >> idx) & 1ull);
@@ -243,8 +253,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
 #pragma unroll
                         for (int r = 0; r < NR; r++) part += ((r >> T) & 1) ? -w[r] : w[r];
                     });
-                    part = warp_sum(part);
-                    if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
+                    tacc[op.slot[gi] * blockDim.x + threadIdx.x] += part;
                 }
             } else {
                 // gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
@@ -258,8 +267,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
                         dispatch4((gbits >> (2 * gi)) & 3,
                                   [&](auto tb) { part = grad_bit<decltype(tb)::value, C, Real>(a, l, gk, g); });
                     }
-                    part = warp_sum(part);
-                    if ((threadIdx.x & 31) == 0) wacc[op.slot[gi]] += (double)part;
+                    tacc[op.slot[gi] * blockDim.x + threadIdx.x] += part;
                 }
             }
         }
@@ -317,13 +325,12 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
     case 48: op_u2<3, 1, C, Real>(a, op.m); if (BWD) op_u2<3, 1, C, Real>(l, op.m); break;
     case 49: op_u2<3, 2, C, Real>(a, op.m); if (BWD) op_u2<3, 2, C, Real>(l, op.m); break;
     case KC_PHASE: {
-        const int v = bitval(h.z & 0xff, (h.z >> 8) & 0xff);
-        const C d = v ? mk<C>(op.m[2], op.m[3]) : mk<C>(op.m[0], op.m[1]);
+        const Real *d = op.m + 4 * bitval(h.z & 0xff, (h.z >> 8) & 0xff);
 #pragma unroll
-        for (int r = 0; r < NR; r++) a[r] = cmul(d, a[r]);
+        for (int r = 0; r < NR; r++) a[r] = cmul_e(d, a[r]);
         if (BWD) {
 #pragma unroll
-            for (int r = 0; r < NR; r++) l[r] = cmul(d, l[r]);
+            for (int r = 0; r < NR; r++) l[r] = cmul_e(d, l[r]);
         }
         break;
     }
@@ -353,7 +360,6 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     __shared__ DevStage S;
     __shared__ uint64_t s_ldoff[NR], s_stoff[NR];
     __shared__ uint32_t s_woff[MAXSEG][NR], s_roff[MAXSEG][NR];
-    __shared__ double s_acc[BWD ? MAX_WARPS : 1][BWD ? MAX_STAGE_SLOTS : 1];
 
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(stg);
@@ -368,6 +374,8 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     C *sm_a = reinterpret_cast<C *>(smem_raw);
     C *sm_l = sm_a + ((size_t)1 << k);
     KOp<Real> *s_ops = reinterpret_cast<KOp<Real> *>(smem_raw + (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(C));
+    // adjoint: per-thread gradient accumulators [slot][thread] (no per-tile reductions)
+    Real *tacc = reinterpret_cast<Real *>(s_ops + S.n_ops);
     {
         const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
@@ -396,13 +404,12 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
             s_roff[s][r] = rd;
         }
         if (BWD)
-            for (int i = threadIdx.x; i < MAX_WARPS * MAX_STAGE_SLOTS; i += blockDim.x) (&s_acc[0][0])[i] = 0.0;
+            for (int i = threadIdx.x; i < S.n_slots * (int)blockDim.x; i += blockDim.x) tacc[i] = 0;
     }
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    double *wacc = BWD ? &s_acc[warp][0] : nullptr;
 
     auto thr_phys_off = [&](const DevLayout &L, const uint8_t *phys) -> uint64_t {
         uint64_t off = 0;
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
             for (; oi < e; oi++) {
                 // header of the next op loads while this one runs
                 const uint4 hn = oi + 1 < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi + 1]) : h;
-                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, wacc);
+                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, tacc);
                 h = hn;
             }
         }
@@ -510,25 +517,28 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     if (BWD) {
         __syncthreads();
         const int nw = blockDim.x >> 5;
-        for (int i = threadIdx.x; i < S.n_slots; i += blockDim.x) {
+        for (int i = warp; i < S.n_slots; i += nw) {
             double v = 0.0;
-            for (int w = 0; w < nw; w++) v += s_acc[w][i];
-            if (v != 0.0) atomicAdd(&grad[slot_param[S.slot_base + i]], v);
+            for (int t = lane; t < (int)blockDim.x; t += 32) v += (double)tacc[i * blockDim.x + t];
+            v = warp_sum(v);
+            if (lane == 0 && v != 0.0) atomicAdd(&grad[slot_param[S.slot_base + i]], v);
         }
     }
 }
 
 template <typename Real, bool BWD>
-static size_t sweep_smem_bytes(int k, int n_ops) {
-    return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>);
+static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads) {
+    return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
+           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0);
 }
 
 template <typename Real, bool BWD>
 cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                              double *grad, uint64_t rank_hi, int k, int W, int n_ops, int grid, cudaStream_t s) {
+                              double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, int grid,
+                              cudaStream_t s) {
     typedef typename CT<Real>::C C;
     auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops);
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W);
     // set on every launch: the occupancy query may have lowered it
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -537,9 +547,9 @@ cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const 
 }
 
 template <typename Real, bool BWD>
-int sweep_occupancy_impl(int k, int W, int n_ops) {
+int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots) {
     auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops);
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 << W, smem) != cudaSuccess) {
@@ -554,9 +564,12 @@ int sweep_occupancy_impl(int k, int W, int n_ops) {
 #define TQD_INSTANTIATE_SWEEP(REAL, BWD, NAME)                                                                    \
     namespace tqd {                                                                                             \
     cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi,  \
-                                    void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int grid,  \
-                                    cudaStream_t s) {                                                             \
-        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, grid, s); \
+                                    void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, \
+                                    int grid, cudaStream_t s) {                                                   \
+        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, \
+                                            grid, s);                                                           \
     }                                                                                                           \
-    int sweep_occupancy_##NAME(int k, int W, int n_ops) { return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops); }    \
+    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots) {                                           \
+        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots);                                            \
+    }                                                                                                           \
     }

@@ -30,7 +30,7 @@ constexpr int LANE_BITS = 5;
 constexpr int MAXSEG = 16;  // layouts per sweep stage
 constexpr int NAFF = 8;     // base-controlled affine terms per exchange
 constexpr int MAX_STAGE_OPS = 128;   // placed gates per sweep stage (bounds the kernel-op table in shared memory)
-constexpr int MAX_STAGE_SLOTS = 256;
+constexpr int MAX_STAGE_SLOTS = 32;   // gradient slots per stage (per-thread fp32 accumulators in shared memory)
 
 enum OpKind : uint8_t {
     OP_NONE = 0,
@@ -127,7 +127,7 @@ template <typename Real> struct alignas(16) KOp {
     uint8_t gbit[KOP_MAXGEN];   // host view of gbits
     uint8_t gkind[KOP_MAXGEN];  // host view of gkinds
     uint8_t pad1[14];
-    Real m[32];                 // 16-byte aligned (offset 48)
+    Real m[64];                 // 16-byte aligned (offset 48); complex entries as (re, 0, im, im)
     Real g[KOP_MAXGEN][8];      // generators (2x2 complex)
 };
 
