@@ -18,8 +18,8 @@ namespace tqd {
 // kernels.cu
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
                          void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots,
-                         int grid, cudaStream_t s);
-int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots);
+                         int nseg, int grid, cudaStream_t s);
+int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
                          uint64_t rank_hi, cudaStream_t s);
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
@@ -150,20 +150,37 @@ static int ev_collect(tqd_state *st) {
     return TQD_OK;
 }
 
-static PlanConfig plan_cfg(const tqd_state *st) {
+static PlanConfig make_plan_cfg(int n, int n_loc, int k, int small_max, bool dbl) {
     PlanConfig c;
-    c.n = st->n;
-    c.n_loc = st->n_loc;
-    c.k = st->opt_k;
+    const size_t esz = dbl ? 16 : 8;
+    c.n = n;
+    c.n_loc = n_loc;
+    c.k = k;
     c.R = 4;
-    c.small_max = st->opt_small;
-    c.c128 = st->dbl;
-    c.swz_bits = st->dbl ? 3 : 4;
-    // shared memory budget: the adjoint exchanges psi and lambda tiles
-    while (c.k > 9 && ((size_t)2 << c.k) * st->esz > 144 * 1024) c.k--;
+    c.small_max = small_max;
+    c.c128 = dbl;
+    c.swz_bits = dbl ? 3 : 4;
+    // shared-memory budget of the adjoint sweep kernel (the larger of the two):
+    // psi + lambda exchange tiles, the stage's kernel ops, per-thread gradient
+    // accumulators and per-thread layout constants, within ~200 KB per CTA
+    if (dbl && c.k > 11) c.k = 11;
     if (c.k > c.n_loc) c.k = c.n_loc;
     if (c.k - LANE_BITS - c.R > WMAX) c.k = LANE_BITS + c.R + WMAX;
+    const size_t threads = (size_t)32 << std::max(0, c.k - LANE_BITS - c.R);
+    const size_t exch = ((size_t)2 << c.k) * esz;
+    const size_t tables = (size_t)3 * MAXSEG * threads * 4;
+    const size_t kop = dbl ? sizeof(KOp<double>) : sizeof(KOp<float>);
+    const size_t real = esz / 2;
+    const size_t budget = (size_t)200 * 1024 - std::min((size_t)200 * 1024 - 32 * 1024, exch + tables);
+    c.max_slots = (int)std::min<size_t>(MAX_STAGE_SLOTS, (budget / 3) / (threads * real));
+    c.max_slots = std::max(c.max_slots, 3);
+    c.max_ops = (int)std::min<size_t>(MAX_STAGE_OPS, (budget - (size_t)c.max_slots * threads * real) / kop);
+    c.max_ops = std::max(c.max_ops, 8);
     return c;
+}
+
+static PlanConfig plan_cfg(const tqd_state *st) {
+    return make_plan_cfg(st->n, st->n_loc, st->opt_k, st->opt_small, st->dbl);
 }
 
 static int ensure_red(tqd_state *st, size_t count) {
@@ -277,7 +294,7 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
 // ---- forward execution ------------------------------------------------------
 static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops, int n_slots) {
     if (st->opt_grid > 0) return st->opt_grid;
-    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots);
+    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots, (int)sp.lays.size());
     if (per < 1) per = 1;
     int64_t g = (int64_t)per * st->ctx->sms;
     const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
@@ -312,7 +329,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
             const SweepPlan &sp = s.sw;
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
-                                      sp.k, sp.W, l.n_ops, l.n_slots, l.grid, c->stream));
+                                      sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(), l.grid, c->stream));
             ev_end(st, ev);
             if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += sp.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
@@ -928,15 +945,7 @@ int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, cons
         if (r.trainable) { r.slot0 = np; np += gate_num_params(kinds[i]); }
         gates.push_back(r);
     }
-    PlanConfig cfg;
-    cfg.n = n;
-    cfg.n_loc = n - g;
-    cfg.k = std::min(k, n - g);
-    cfg.R = 4;
-    cfg.small_max = small_max;
-    cfg.c128 = c128 != 0;
-    cfg.swz_bits = c128 ? 3 : 4;
-    if (cfg.k - LANE_BITS - cfg.R > WMAX) cfg.k = LANE_BITS + cfg.R + WMAX;
+    PlanConfig cfg = make_plan_cfg(n, n - g, k, small_max, c128 != 0);
     std::vector<int> pos(n);
     for (int q = 0; q < n; q++) pos[q] = n - 1 - q;
     std::vector<int> pending;

@@ -381,7 +381,7 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     std::vector<Item> items;
     std::vector<int> rest;
     int n_nondiag = 0, n_slots = 0;
-    const int cap_nondiag = R * (MAXSEG - 4);
+    const int cap_nondiag = R * (MAXSEG - 2);
     std::vector<int> aff_pos;  // distinct control positions outside the tile of folded CNOTs
 
     for (size_t ii = 0; ii < pending.size(); ii++) {
@@ -390,7 +390,7 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         bool blk = false;
         for (int j = 0; j < g.nw; j++)
             if (blocked[g.w[j]]) blk = true;
-        if (!blk && ((int)items.size() >= MAX_STAGE_OPS - 1 || n_slots + g.ngen > MAX_STAGE_SLOTS)) blk = true;
+        if (!blk && ((int)items.size() >= cfg.max_ops - 1 || n_slots + g.ngen > cfg.max_slots)) blk = true;
         int tq[2], dq[2], nt, nd;
         roles(g, tq, nt, dq, nd);
         std::vector<int> newbits;
@@ -958,6 +958,52 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
         };
         const int b = sp.seg_begin[fs], e = sp.seg_begin[fs + 1];
         static const bool skip_ops = getenv("TQD_EXPERIMENT_SKIP_OPS") != nullptr;  // timing experiment only
+        // Single-qubit gates on register bits are queued per bit and emitted as
+        // layers: each layer takes the front gate of every bit whose front has the
+        // chosen type (gates on different bits commute, same-bit order is kept);
+        // the forward also composes consecutive same-type gates on one bit.  Any
+        // other op (controlled / 2q / phase on a non-register bit) drains the queues.
+        struct QG { cd M[4]; int t; int gate; };
+        std::vector<QG> q[RMAX];
+        size_t qh[RMAX] = {0, 0, 0, 0, 0};
+        auto drain = [&]() {
+            for (;;) {
+                int cnt[3] = {0, 0, 0};
+                for (int bb = 0; bb < R; bb++)
+                    if (qh[bb] < q[bb].size()) cnt[q[bb][qh[bb]].t]++;
+                if (!cnt[0] && !cnt[1] && !cnt[2]) break;
+                int T = LT_REAL;
+                for (int tt : {LT_DIAG, LT_GEN})
+                    if (cnt[tt] > cnt[T]) T = tt;
+                if (!cnt[T]) T = cnt[LT_DIAG] ? LT_DIAG : LT_GEN;
+                active = true;
+                ltype = T;
+                for (int bb = 0; bb < R; bb++) {
+                    if (qh[bb] >= q[bb].size() || q[bb][qh[bb]].t != T) continue;
+                    const GateRec &gg = gates[q[bb][qh[bb]].gate];
+                    if (bwd && layer.ngen + gg.ngen > KOP_MAXGEN) continue;
+                    for (int c = 0; c < 4; c++) LM[bb][c] = q[bb][qh[bb]].M[c];
+                    mask |= 1 << bb;
+                    if (bwd && gg.ngen)
+                        for (int i = 0; i < gg.ngen; i++) add_gen(layer, gg, i, bb);
+                    qh[bb]++;
+                    // forward: fold following gates on this bit while the product keeps the type
+                    while (!bwd && qh[bb] < q[bb].size()) {
+                        const cd *Mn = q[bb][qh[bb]].M;
+                        cd Pm[4];
+                        Pm[0] = Mn[0] * LM[bb][0] + Mn[1] * LM[bb][2];
+                        Pm[1] = Mn[0] * LM[bb][1] + Mn[1] * LM[bb][3];
+                        Pm[2] = Mn[2] * LM[bb][0] + Mn[3] * LM[bb][2];
+                        Pm[3] = Mn[2] * LM[bb][1] + Mn[3] * LM[bb][3];
+                        if (mtype(Pm) != T) break;
+                        for (int c = 0; c < 4; c++) LM[bb][c] = Pm[c];
+                        qh[bb]++;
+                    }
+                }
+                flush();
+            }
+            for (int bb = 0; bb < R; bb++) { q[bb].clear(); qh[bb] = 0; }
+        };
         for (int jj = 0; jj < e - b && !skip_ops; jj++) {
             const POp &o = sp.ops[bwd ? e - 1 - jj : b + jj];
             if (o.perm) continue;  // folded into the layout-change maps below
@@ -967,31 +1013,15 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             if ((o.kind == OP_U1 || o.kind == OP_R1 || o.kind == OP_P1) && o.cp < 0) bit = regidx(o.tp0);
             else if (o.kind == OP_D1 && o.cp < 0) bit = regidx(o.dp0);
             if (bit >= 0) {
-                cd M[4];
-                op_matrix2(o, bwd, M);
-                int t = mtype(M);
-                if (g.trainable && g.kind == TQD_RZ) t = LT_DIAG;  // RZ gradients are batched on diagonal layers
-                const bool clash = active && ((mask >> bit) & 1);
-                cd P[4];
-                if (clash && !bwd) {  // forward: compose later op after the earlier one on the same bit
-                    P[0] = M[0] * LM[bit][0] + M[1] * LM[bit][2];
-                    P[1] = M[0] * LM[bit][1] + M[1] * LM[bit][3];
-                    P[2] = M[2] * LM[bit][0] + M[3] * LM[bit][2];
-                    P[3] = M[2] * LM[bit][1] + M[3] * LM[bit][3];
-                    if (mtype(P) == ltype) {
-                        for (int q = 0; q < 4; q++) LM[bit][q] = P[q];
-                        continue;
-                    }
-                }
-                if (active && (clash || t != ltype || (bwd && layer.ngen + g.ngen > KOP_MAXGEN))) flush();
-                if (!active) { active = true; ltype = t; }
-                mask |= 1 << bit;
-                for (int q = 0; q < 4; q++) LM[bit][q] = M[q];
-                if (has_gen)
-                    for (int i = 0; i < g.ngen; i++) add_gen(layer, g, i, bit);
+                QG qg;
+                op_matrix2(o, bwd, qg.M);
+                qg.t = mtype(qg.M);
+                if (g.trainable && g.kind == TQD_RZ) qg.t = LT_DIAG;  // RZ gradients are batched on diagonal layers
+                qg.gate = o.gate;
+                q[bit].push_back(qg);
                 continue;
             }
-            flush();
+            drain();
             KOp<Real> k = newop(K_NOP);
             cd M[4];
             switch (o.kind) {
@@ -1035,7 +1065,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             finalize(k);
             ops.push_back(k);
         }
-        flush();
+        drain();
     }
     ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
     ds.n_ops = (int)ops.size() - ds.op_base;

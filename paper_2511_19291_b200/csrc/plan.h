@@ -120,6 +120,8 @@ struct PlanConfig {
     int small_max = 10;
     bool c128 = false;
     int swz_bits = 4;  // shared-memory conflict-free bits (4 for 8 B elems, 3 for 16 B)
+    int max_ops = MAX_STAGE_OPS;      // per sweep stage (shared-memory budget of the kernel)
+    int max_slots = MAX_STAGE_SLOTS;  // gradient slots per sweep stage
 };
 
 // Plan the gates `pending` (indices into gates, in recording order) starting

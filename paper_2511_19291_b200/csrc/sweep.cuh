@@ -31,6 +31,7 @@ constexpr int NR = 1 << SWEEP_R;
 constexpr int MAX_WARPS = 1 << WMAX;
 
 template <int V> struct IC { static constexpr int value = V; };
+__host__ __device__ constexpr int ctz4(int m) { return (m & 1) ? 0 : (m & 2) ? 1 : (m & 4) ? 2 : 3; }
 
 template <typename F> __device__ __forceinline__ void dispatch4(int t, F &&f) {
     switch (t) {
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevStage S;
     __shared__ uint64_t s_ldoff[NR], s_stoff[NR];
-    __shared__ uint32_t s_woff[MAXSEG][NR], s_roff[MAXSEG][NR];
+    __shared__ uint32_t s_wc[MAXSEG][SWEEP_R], s_rc[MAXSEG][SWEEP_R];  // byte address vectors of the register bits
 
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(stg);
@@ -376,6 +377,10 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     KOp<Real> *s_ops = reinterpret_cast<KOp<Real> *>(smem_raw + (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(C));
     // adjoint: per-thread gradient accumulators [slot][thread] (no per-tile reductions)
     Real *tacc = reinterpret_cast<Real *>(s_ops + S.n_ops);
+    // per-thread constants, computed once per kernel: tix[seg], write / read base of each exchange
+    uint32_t *s_tix = reinterpret_cast<uint32_t *>(tacc + (BWD ? S.n_slots * blockDim.x : 0));
+    uint32_t *s_tw = s_tix + nseg * blockDim.x;
+    uint32_t *s_tr = s_tw + (nseg - 1) * blockDim.x;
     {
         const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
@@ -392,16 +397,10 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
             s_ldoff[r] = lo;
             s_stoff[r] = so;
         }
-        for (int i = threadIdx.x; i < (nseg - 1) * NR; i += blockDim.x) {
-            const int s = i / NR, r = i % NR;
-            uint32_t w = 0, rd = 0;
-            for (int b = 0; b < SWEEP_R; b++)
-                if ((r >> b) & 1) {
-                    w ^= S.wcol[s][S.lay[s].reg[b]];
-                    rd ^= S.rcol[s][S.lay[s + 1].reg[b]];
-                }
-            s_woff[s][r] = w;
-            s_roff[s][r] = rd;
+        for (int i = threadIdx.x; i < (nseg - 1) * SWEEP_R; i += blockDim.x) {
+            const int x = i / SWEEP_R, b = i % SWEEP_R;
+            s_wc[x][b] = S.wcol[x][S.lay[x].reg[b]] * (uint32_t)sizeof(C);
+            s_rc[x][b] = S.rcol[x][S.lay[x + 1].reg[b]] * (uint32_t)sizeof(C);
         }
         if (BWD)
             for (int i = threadIdx.x; i < S.n_slots * (int)blockDim.x; i += blockDim.x) tacc[i] = 0;
@@ -438,6 +437,15 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     };
     const uint64_t ld_thr = thr_phys_off(S.lay[0], S.ld_phys);
     const uint64_t st_thr = thr_phys_off(S.lay[nseg - 1], S.st_phys);
+    {
+        const int T = blockDim.x, tid = threadIdx.x;
+        for (int s = 0; s < nseg; s++) s_tix[s * T + tid] = thr_tix(S.lay[s]);
+        for (int x = 0; x + 1 < nseg; x++) {
+            s_tw[x * T + tid] = (thr_cols(S.wcol[x], S.lay[x]) ^ S.wcst[x]) * (uint32_t)sizeof(C);
+            s_tr[x * T + tid] = (thr_cols(S.rcol[x], S.lay[x + 1]) ^ S.rcst[x]) * (uint32_t)sizeof(C);
+        }
+    }
+    __syncthreads();
 
     // tile index -> physical base: deposit into the non-tile positions once, then
     // step by a masked add (carries propagate only through non-tile positions)
@@ -474,24 +482,40 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
                 uint32_t aff = 0;
                 for (int i = 0; i < S.naff[x]; i++)
                     if ((basefull >> S.aff_pos[x][i]) & 1ull) aff ^= S.aff_vec[x][i];
-                const uint32_t tw = thr_cols(S.wcol[x], S.lay[x]) ^ S.wcst[x] ^ (S.aff_read[x] ? 0u : aff);
-                const uint32_t tr = thr_cols(S.rcol[x], S.lay[s]) ^ S.rcst[x] ^ (S.aff_read[x] ? aff : 0u);
+                aff *= (uint32_t)sizeof(C);
+                const uint32_t tw = s_tw[x * blockDim.x + threadIdx.x] ^ (S.aff_read[x] ? 0u : aff);
+                const uint32_t tr = s_tr[x * blockDim.x + threadIdx.x] ^ (S.aff_read[x] ? aff : 0u);
+                {
+                    // Gray-code walk: one XOR per register address
+                    uint32_t c[SWEEP_R], o[NR];
 #pragma unroll
-                for (int r = 0; r < NR; r++) {
-                    const uint32_t o = tw ^ s_woff[x][r];
-                    sm_a[o] = a[r];
-                    if (BWD) sm_l[o] = l[r];
+                    for (int b = 0; b < SWEEP_R; b++) c[b] = s_wc[x][b];
+                    o[0] = tw;
+#pragma unroll
+                    for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] ^ c[ctz4(r)];
+#pragma unroll
+                    for (int r = 0; r < NR; r++) {
+                        *reinterpret_cast<C *>(reinterpret_cast<char *>(sm_a) + o[r]) = a[r];
+                        if (BWD) *reinterpret_cast<C *>(reinterpret_cast<char *>(sm_l) + o[r]) = l[r];
+                    }
                 }
                 __syncthreads();
+                {
+                    uint32_t c[SWEEP_R], o[NR];
 #pragma unroll
-                for (int r = 0; r < NR; r++) {
-                    const uint32_t o = tr ^ s_roff[x][r];
-                    a[r] = sm_a[o];
-                    if (BWD) l[r] = sm_l[o];
+                    for (int b = 0; b < SWEEP_R; b++) c[b] = s_rc[x][b];
+                    o[0] = tr;
+#pragma unroll
+                    for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] ^ c[ctz4(r)];
+#pragma unroll
+                    for (int r = 0; r < NR; r++) {
+                        a[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_a) + o[r]);
+                        if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_l) + o[r]);
+                    }
                 }
                 __syncthreads();
             }
-            const uint32_t tix = thr_tix(S.lay[s]);
+            const uint32_t tix = s_tix[s * blockDim.x + threadIdx.x];
             const int e = S.seg_begin[s + 1];
             int oi = S.seg_begin[s];
             uint4 h = oi < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi]) : make_uint4(0, 0, 0, 0);
@@ -527,18 +551,18 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
 }
 
 template <typename Real, bool BWD>
-static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads) {
+static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int nseg) {
     return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
-           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0);
+           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t);
 }
 
 template <typename Real, bool BWD>
 cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                              double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, int grid,
-                              cudaStream_t s) {
+                              double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, int nseg,
+                              int grid, cudaStream_t s) {
     typedef typename CT<Real>::C C;
     auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W);
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
     // set on every launch: the occupancy query may have lowered it
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -547,9 +571,9 @@ cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const 
 }
 
 template <typename Real, bool BWD>
-int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots) {
+int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg) {
     auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W);
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 << W, smem) != cudaSuccess) {
@@ -565,11 +589,11 @@ int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots) {
     namespace tqd {                                                                                             \
     cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi,  \
                                     void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, \
-                                    int grid, cudaStream_t s) {                                                   \
+                                    int nseg, int grid, cudaStream_t s) {                                         \
         return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, \
-                                            grid, s);                                                           \
+                                            nseg, grid, s);                                                     \
     }                                                                                                           \
-    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots) {                                           \
-        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots);                                            \
+    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg) {                                 \
+        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots, nseg);                                      \
     }                                                                                                           \
     }

@@ -27,7 +27,7 @@ constexpr int KMAX = 16;    // max tile bits
 constexpr int RMAX = 5;     // max register bits
 constexpr int WMAX = 3;     // max warp bits (8 warps = 256 threads)
 constexpr int LANE_BITS = 5;
-constexpr int MAXSEG = 16;  // layouts per sweep stage
+constexpr int MAXSEG = 8;   // layouts per sweep stage
 constexpr int NAFF = 8;     // base-controlled affine terms per exchange
 constexpr int MAX_STAGE_OPS = 128;   // placed gates per sweep stage (bounds the kernel-op table in shared memory)
 constexpr int MAX_STAGE_SLOTS = 32;   // gradient slots per stage (per-thread fp32 accumulators in shared memory)
