@@ -819,10 +819,17 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
     CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, (n_grad + 1) * sizeof(double), c->stream));
     ZTerms zt;
     memset(&zt, 0, sizeof(zt));
-    zt.T = T;
     for (int t = 0; t < T; t++) {
-        zt.z[t] = phys_mask(st, z[t]);
-        zt.c[t] = coeff ? coeff[t] : 1.0;
+        const uint64_t zp = phys_mask(st, z[t]);
+        const double ct = coeff ? coeff[t] : 1.0;
+        if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
+            zt.cst += ct;
+            zt.w[__builtin_ctzll(zp)] += ct;
+        } else {
+            zt.z[zt.T] = zp;
+            zt.c[zt.T] = ct;
+            zt.T++;
+        }
     }
     const uint64_t N = 1ull << st->n_loc;
     {

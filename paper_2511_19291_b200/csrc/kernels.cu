@@ -148,10 +148,31 @@ __global__ void __launch_bounds__(256) lambda_init_kernel(const typename CT<Real
                                                           uint64_t rank_hi, ZTerms terms, double *__restrict__ eout) {
     typedef typename CT<Real>::C C;
     __shared__ double red[32];
+    // byte tables: tab[j][v] = sum_{i<8} w[8j + i] * bit_i(v)
+    __shared__ Real tab[8][256];
+    __shared__ int nbytes;
+    if (threadIdx.x == 0) {
+        int nb = 0;
+        for (int p = 0; p < 64; p++)
+            if (terms.w[p] != 0.0) nb = p / 8 + 1;
+        nbytes = nb;
+    }
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+        const int j = i >> 8, v = i & 255;
+        double s = 0;
+        for (int q = 0; q < 8; q++)
+            if ((v >> q) & 1) s += terms.w[8 * j + q];
+        tab[j][v] = (Real)s;
+    }
+    __syncthreads();
+    const int nb = nbytes;
+    const Real cst = (Real)terms.cst;
     double acc = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = i | rank_hi;
-        Real h = 0;
+        Real s = 0;
+        for (int j = 0; j < nb; j++) s += tab[j][(b >> (8 * j)) & 255];
+        Real h = cst - 2 * s;
         for (int t = 0; t < terms.T; t++) {
             const Real c = (Real)terms.c[t];
             h += (__popcll(b & terms.z[t]) & 1) ? -c : c;

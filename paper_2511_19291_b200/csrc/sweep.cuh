@@ -247,13 +247,26 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
                 Real w[NR];
 #pragma unroll
                 for (int r = 0; r < NR; r++) w[r] = im_cj(l[r], a[r]);
-                for (int gi = 0; gi < ngen; gi++) {
-                    Real part = 0;
-                    dispatch4((gbits >> (2 * gi)) & 3, [&](auto tb) {
-                        constexpr int T = decltype(tb)::value;
+                // single-bit Walsh sums g_b = sum_r (-1)^{bit_b(r)} w_r for b = 0..3 by a
+                // butterfly: differences at each level, sums carried up (40 adds)
+                Real gb[SWEEP_R];
+                {
+                    Real p[NR / 2];
+                    Real d = 0;
 #pragma unroll
-                        for (int r = 0; r < NR; r++) part += ((r >> T) & 1) ? -w[r] : w[r];
-                    });
+                    for (int j = 0; j < NR / 2; j++) { p[j] = w[2 * j] + w[2 * j + 1]; d += w[2 * j] - w[2 * j + 1]; }
+                    gb[0] = d;
+                    Real q2[NR / 4];
+                    d = 0;
+#pragma unroll
+                    for (int j = 0; j < NR / 4; j++) { q2[j] = p[2 * j] + p[2 * j + 1]; d += p[2 * j] - p[2 * j + 1]; }
+                    gb[1] = d;
+                    gb[2] = (q2[0] - q2[1]) + (q2[2] - q2[3]);
+                    gb[3] = (q2[0] + q2[1]) - (q2[2] + q2[3]);
+                }
+                for (int gi = 0; gi < ngen; gi++) {
+                    const int bb = (gbits >> (2 * gi)) & 3;
+                    const Real part = bb == 0 ? gb[0] : bb == 1 ? gb[1] : bb == 2 ? gb[2] : gb[3];
                     tacc[op.slot[gi] * blockDim.x + threadIdx.x] += part;
                 }
             } else {
@@ -351,7 +364,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
 
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
 template <typename Real, bool BWD>
-__global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
+__global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
@@ -359,7 +372,7 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
     typedef typename CT<Real>::C C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevStage S;
-    __shared__ uint64_t s_ldoff[NR], s_stoff[NR];
+    __shared__ uint64_t s_ldc[SWEEP_R], s_stc[SWEEP_R];  // element offsets of the register bits (load / store)
     __shared__ uint32_t s_wc[MAXSEG][SWEEP_R], s_rc[MAXSEG][SWEEP_R];  // byte address vectors of the register bits
 
     {
@@ -386,16 +399,10 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
         const int n16 = (int)(S.n_ops * sizeof(KOp<Real>) / 16);
         for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
-        if (threadIdx.x < NR) {
-            const int r = threadIdx.x;
-            uint64_t lo = 0, so = 0;
-            for (int i = 0; i < SWEEP_R; i++)
-                if ((r >> i) & 1) {
-                    lo |= 1ull << S.ld_phys[S.lay[0].reg[i]];
-                    so |= 1ull << S.st_phys[S.lay[nseg - 1].reg[i]];
-                }
-            s_ldoff[r] = lo;
-            s_stoff[r] = so;
+        if (threadIdx.x < SWEEP_R) {
+            const int i = threadIdx.x;
+            s_ldc[i] = 1ull << S.ld_phys[S.lay[0].reg[i]];
+            s_stc[i] = 1ull << S.st_phys[S.lay[nseg - 1].reg[i]];
         }
         for (int i = threadIdx.x; i < (nseg - 1) * SWEEP_R; i += blockDim.x) {
             const int x = i / SWEEP_R, b = i % SWEEP_R;
@@ -465,12 +472,18 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
         C a[NR];
         C l[BWD ? NR : 1];
         {
-            const C *p = psi + (base | ld_thr);
-            const C *q = BWD ? lam + (base | ld_thr) : nullptr;
+            // Gray-code walk over the register offsets: one 64-bit add per address
+            const uint64_t b0 = base | ld_thr;
+            uint64_t o[NR], c[SWEEP_R];
+#pragma unroll
+            for (int i = 0; i < SWEEP_R; i++) c[i] = s_ldc[i];
+            o[0] = b0;
+#pragma unroll
+            for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] + c[ctz4(r)];
 #pragma unroll
             for (int r = 0; r < NR; r++) {
-                a[r] = p[s_ldoff[r]];
-                if (BWD) l[r] = q[s_ldoff[r]];
+                a[r] = psi[o[r]];
+                if (BWD) l[r] = lam[o[r]];
             }
         }
 
@@ -528,12 +541,17 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? 2 : 1) sweep_kernel(c
         }
 
         {
-            C *p = psi + (base | st_thr);
-            C *q = BWD ? lam + (base | st_thr) : nullptr;
+            const uint64_t b0 = base | st_thr;
+            uint64_t o[NR], c[SWEEP_R];
+#pragma unroll
+            for (int i = 0; i < SWEEP_R; i++) c[i] = s_stc[i];
+            o[0] = b0;
+#pragma unroll
+            for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] + c[ctz4(r)];
 #pragma unroll
             for (int r = 0; r < NR; r++) {
-                p[s_stoff[r]] = a[r];
-                if (BWD) q[s_stoff[r]] = l[r];
+                psi[o[r]] = a[r];
+                if (BWD) lam[o[r]] = l[r];
             }
         }
     }

@@ -164,10 +164,14 @@ struct DevStage {
 };
 
 // Z-string observable in PHYSICAL masks (full index incl. rank bits)
+// lambda-init form: h(b) = cst - 2 sum_p w[p] bit_p(b) + sum_t c_t (-1)^{popc(b & z_t)}
+// (single-qubit Z terms folded into per-position weights, the rest listed)
 struct ZTerms {
     int T;
     uint64_t z[64];
     double c[64];
+    double w[64];
+    double cst;
 };
 
 // canonical index -> physical index through pi (readback)
