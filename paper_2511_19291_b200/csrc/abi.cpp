@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -160,6 +161,11 @@ static PlanConfig make_plan_cfg(int n, int n_loc, int k, int small_max, bool dbl
     c.small_max = small_max;
     c.c128 = dbl;
     c.swz_bits = dbl ? 3 : 4;
+    {
+        // pinned low bits: 2^c amplitudes per contiguous run = one 128 B line (c64: 4, c128: 3)
+        const char *e = getenv("TQD_C_LOW");
+        c.c_low = e ? std::max(1, std::min(5, atoi(e))) : (dbl ? 3 : 4);
+    }
     // shared-memory budget of the adjoint sweep kernel (the larger of the two):
     // psi + lambda exchange tiles, the stage's kernel ops, per-thread gradient
     // accumulators and per-thread layout constants, within ~200 KB per CTA

@@ -363,6 +363,41 @@ static std::vector<uint32_t> choose_swizzle(int k, int SW, const std::vector<std
     return best;
 }
 
+// Dry run of the next stage's placement (phase 1 of plan_sweep, logical qubits):
+// how many gates it would place if `lanes` (logical qubits) sit at physical bits
+// 0..4.  Used to choose which qubits a stage leaves on the always-resident bits.
+static int simulate_next_stage(const std::vector<GateRec> &gates, const std::vector<int> &remaining,
+                               const std::vector<int> &pos, int n_loc, int k, const int *lanes, int nl, int max_items) {
+    const int n = (int)pos.size();
+    std::vector<char> in_tile(n, 0), blocked(n, 0);
+    int tsize = 0;
+    for (int i = 0; i < nl; i++) { in_tile[lanes[i]] = 1; tsize++; }
+    int placed = 0, scanned = 0;
+    for (int gi : remaining) {
+        if (++scanned > 4 * n + 64) break;
+        const GateRec &g = gates[gi];
+        bool blk = false;
+        for (int j = 0; j < g.nw; j++) if (blocked[g.w[j]]) blk = true;
+        int tq[2], dq[2], nt, nd;
+        roles(g, tq, nt, dq, nd);
+        int add[2], na = 0;
+        if (!blk && g.cls != CL_SWAP)
+            for (int j = 0; j < nt && !blk; j++) {
+                const int qq = tq[j];
+                if (pos[qq] >= n_loc) blk = true;
+                else if (!in_tile[qq]) add[na++] = qq;
+            }
+        if (!blk && tsize + na > k) blk = true;
+        if (blk) {
+            for (int j = 0; j < g.nw; j++) blocked[g.w[j]] = 1;
+            continue;
+        }
+        for (int j = 0; j < na; j++) { in_tile[add[j]] = 1; tsize++; }
+        if (++placed >= max_items) break;
+    }
+    return placed;
+}
+
 // Plan one fused sweep stage.  Returns false if nothing could be placed.
 static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pending, std::vector<int> &pos,
                        const PlanConfig &cfg, Stage &st) {
@@ -373,7 +408,8 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     if (W < 0 || W > WMAX) return false;
 
     std::vector<int> tile_of(n_loc, -1), tphys;
-    for (int p = 0; p < LANE_BITS; p++) { tile_of[p] = p; tphys.push_back(p); }
+    const int C = cfg.c_low;  // physical bits 0..C-1 are in every tile (contiguous 2^C-amplitude runs)
+    for (int p = 0; p < C; p++) { tile_of[p] = p; tphys.push_back(p); }
     std::vector<char> blocked(n, 0);
     std::vector<int> wpos = pos;               // working map (relabels)
     std::vector<int> wlq(n);
@@ -487,7 +523,7 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
                 std::vector<int> u = cur;
                 bool ok = true;
                 for (int x : items[i].need) {
-                    if (cs == 0 && x < LANE_BITS) ok = false;
+                    if (cs == 0 && x < C) ok = false;
                     if (!std::count(u.begin(), u.end(), x)) u.push_back(x);
                 }
                 if (ok && (int)u.size() <= R) { cur = u; pick = i; }
@@ -571,24 +607,50 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     for (int s = 0; s < nseg; s++) {
         std::vector<int> regs = segregs[s];
         for (int t = 0; t < k && (int)regs.size() < R; t++) {
-            if (s == 0 && t < LANE_BITS) continue;
+            if (s == 0 && t < C) continue;
             if (!std::count(regs.begin(), regs.end(), t)) regs.push_back(t);
         }
         std::vector<int> others;
         for (int t = 0; t < k; t++) if (!std::count(regs.begin(), regs.end(), t)) others.push_back(t);
+        // lanes 0..C-1 hold the pinned low bits at load (layout 0) and the bits that
+        // land on physical 0..C-1 at store (last layout); lanes C..4 are free
         std::vector<int> lanes;
-        if (s == 0) {
-            for (int t = 0; t < LANE_BITS; t++) lanes.push_back(t);
-        } else if (s == nseg - 1) {
-            // qubits used furthest in the future go to physical bits 0..4
+        if (s == nseg - 1) {
+            // choose the C qubits left on the pinned bits so that the NEXT stage
+            // places the most gates (dry run over all C-subsets of the free bits);
+            // with one segment the pinned bits stay put
             std::vector<std::pair<long long, int>> cand;
             for (int t : others) {
+                if (nseg == 1 && t < C) continue;
                 const int q = fl[tphys[t]];
-                cand.push_back({-(long long)next_target_use(gates, remaining, q), t});
+                cand.push_back({(long long)next_target_use(gates, remaining, q), t});
             }
             std::sort(cand.begin(), cand.end());
-            for (int i = 0; i < LANE_BITS; i++) lanes.push_back(cand[i].second);
-            std::sort(lanes.begin(), lanes.end());
+            if (nseg == 1) {
+                for (int t = 0; t < C; t++) lanes.push_back(t);
+            } else {
+                const int no = (int)cand.size();
+                std::vector<int> best_pick;
+                int best = -1;
+                for (int m = 0; m < (1 << no); m++) {
+                    if (__builtin_popcount(m) != C) continue;
+                    int lqc[LANE_BITS], c = 0;
+                    std::vector<int> pick;
+                    for (int i = 0; i < no; i++)
+                        if ((m >> i) & 1) { lqc[c++] = fl[tphys[cand[i].second]]; pick.push_back(i); }
+                    const int sc = simulate_next_stage(gates, remaining, fpos, n_loc, k, lqc, C, cfg.max_ops - 1);
+                    if (sc > best) { best = sc; best_pick = pick; }
+                }
+                for (int i : best_pick) lanes.push_back(cand[i].second);
+                std::vector<std::pair<long long, int>> rest_c;
+                for (size_t i = 0; i < cand.size(); i++)
+                    if (!std::count(best_pick.begin(), best_pick.end(), (int)i)) rest_c.push_back(cand[i]);
+                cand = rest_c;
+            }
+            for (size_t i = 0; (int)lanes.size() < LANE_BITS && i < cand.size(); i++) lanes.push_back(cand[i].second);
+        } else if (s == 0) {
+            for (int t = 0; t < C; t++) lanes.push_back(t);
+            for (int t : others) if ((int)lanes.size() < LANE_BITS && t >= C) lanes.push_back(t);
         } else {
             for (int i = 0; i < LANE_BITS; i++) lanes.push_back(others[i]);
         }
@@ -604,15 +666,15 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     {
         const Layout &L = sp.lays[nseg - 1];
         std::vector<char> used(n_loc, 0);
-        for (int i = 0; i < LANE_BITS; i++) { sp.st_phys[L.lane[i]] = i; used[i] = 1; }
+        for (int i = 0; i < C; i++) { sp.st_phys[L.lane[i]] = i; used[i] = 1; }
         std::vector<int> freep;
-        for (int t = LANE_BITS; t < k; t++) {
+        for (int t = C; t < k; t++) {
             bool moved = sp.st_phys[t] >= 0;
             if (!moved) { sp.st_phys[t] = tphys[t]; used[tphys[t]] = 1; }
         }
-        for (int t = LANE_BITS; t < k; t++) if (!used[tphys[t]]) freep.push_back(tphys[t]);
+        for (int t = C; t < k; t++) if (!used[tphys[t]]) freep.push_back(tphys[t]);
         size_t fi = 0;
-        for (int t = 0; t < LANE_BITS; t++)
+        for (int t = 0; t < C; t++)
             if (sp.st_phys[t] < 0) sp.st_phys[t] = freep[fi++];
     }
     // ops in schedule order with segment ids; per-segment permutation maps
@@ -1148,7 +1210,8 @@ std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg
         };
         if (st.type == ST_SWEEP) {
             const SweepPlan &sp = st.sw;
-            os << ",\"k\":" << sp.k << ",\"R\":" << sp.R << ",\"W\":" << sp.W << ",\"n_gates\":" << sp.n_gates;
+            os << ",\"k\":" << sp.k << ",\"R\":" << sp.R << ",\"W\":" << sp.W << ",\"n_gates\":" << sp.n_gates
+               << ",\"c_low\":" << cfg.c_low;
             os << ",\"ld_phys\":[";
             for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.ld_phys[t];
             os << "],\"st_phys\":[";

@@ -120,6 +120,7 @@ struct PlanConfig {
     int small_max = 10;
     bool c128 = false;
     int swz_bits = 4;  // shared-memory conflict-free bits (4 for 8 B elems, 3 for 16 B)
+    int c_low = 4;     // physical bits 0..c_low-1 pinned in every tile (2^c_low-amplitude runs)
     int max_ops = MAX_STAGE_OPS;      // per sweep stage (shared-memory budget of the kernel)
     int max_slots = MAX_STAGE_SLOTS;  // gradient slots per sweep stage
 };

@@ -82,16 +82,16 @@ def check_invariants(plan):
     for st in plan["stages"]:
         if st["type"] != "sweep":
             continue
-        k, R, Wb = st["k"], st["R"], st["W"]
+        k, R, Wb, C = st["k"], st["R"], st["W"], st["c_low"]
         ld, stp, lays = st["ld_phys"], st["st_phys"], st["layouts"]
-        assert ld[:5] == [0, 1, 2, 3, 4]
+        assert ld[:C] == list(range(C))
+        assert lays[0]["lane"][:C] == list(range(C))
         assert sorted(ld) == sorted(stp) and len(set(ld)) == k
-        assert lays[0]["lane"] == [0, 1, 2, 3, 4]
         for L in lays:
             bits = L["reg"] + L["lane"] + L["warp"]
             assert sorted(bits) == list(range(k)) and len(L["reg"]) == R and len(L["warp"]) == Wb
         last = lays[-1]["lane"]
-        assert [stp[t] for t in last] == [0, 1, 2, 3, 4]
+        assert [stp[t] for t in last[:C]] == list(range(C))
         segs = [op["seg"] for op in st["ops"]]
         assert segs == sorted(segs)
         for op in st["ops"]:
