@@ -920,7 +920,8 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
         k.m[4 * i + 2] = (Real)v.imag();
         k.m[4 * i + 3] = (Real)v.imag();
     };
-    auto finalize = [](KOp<Real> &k) {
+    const int threads = 32 << sp.W;
+    auto finalize = [threads](KOp<Real> &k) {
         switch (k.kind) {
         case K_LAYER:
             k.code = (uint8_t)(k.ltype == LT_DIAG ? KC_DIAG : k.ltype == LT_REAL ? KC_REAL + k.mask : KC_GEN + k.mask);
@@ -937,6 +938,22 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             k.gbits |= (uint8_t)((k.gbit[i] & 3) << (2 * i));
             k.gkinds |= (uint16_t)((k.gkind[i] & 15) << (4 * i));
         }
+        // layer fast path: every generator is the layer type's own (RY on a real
+        // layer, RZ on a diagonal layer), at most one per register bit
+        k.gmask = 0;
+        if (k.kind == K_LAYER && k.ngen > 0 && (k.ltype == LT_REAL || k.ltype == LT_DIAG)) {
+            const int want = k.ltype == LT_REAL ? GEN_Y : GEN_Z;
+            int gm = 0;
+            bool ok = true;
+            for (int i = 0; i < k.ngen; i++) {
+                if (k.gkind[i] != want || ((gm >> k.gbit[i]) & 1)) ok = false;
+                gm |= 1 << k.gbit[i];
+            }
+            if (ok) k.gmask = (uint8_t)gm;
+        }
+        for (int i = 0; i < KOP_MAXGEN; i++) k.soff[i] = 0;
+        for (int i = 0; i < k.ngen; i++)
+            k.soff[k.gmask ? k.gbit[i] : i] = (uint16_t)(k.slot[i] * threads);
     };
     auto newop = [](int kind) {
         KOp<Real> k;

@@ -225,64 +225,98 @@ __device__ __forceinline__ Real grad_z_const(const C *a, const C *l, int bit) {
     return bit ? -acc : acc;
 }
 
+// ---- layer fast paths (adjoint): gradients of every RY / RZ of a layer ----------
+// packed helpers: (x.x + y.x, x.y + y.y) and (x.x - y.x, x.y - y.y)
+__device__ __forceinline__ float2 padd(float2 x, float2 y) { return __fadd2_rn(x, y); }
+__device__ __forceinline__ float2 psub(float2 x, float2 y) { return __fadd2_rn(x, make_float2(-y.x, -y.y)); }
+__device__ __forceinline__ double2 padd(double2 x, double2 y) { return make_double2(x.x + y.x, x.y + y.y); }
+__device__ __forceinline__ double2 psub(double2 x, double2 y) { return make_double2(x.x - y.x, x.y - y.y); }
+template <typename C> __device__ __forceinline__ C pneg(C x) { return mk<C>(-x.x, -x.y); }
+template <typename C> __device__ __forceinline__ C pswap(C x) { return mk<C>(x.y, x.x); }
+__device__ __forceinline__ float2 pmul(float2 x, float2 y) { return __fmul2_rn(x, y); }
+__device__ __forceinline__ double2 pmul(double2 x, double2 y) { return make_double2(x.x * y.x, x.y * y.y); }
+
+// RY generator G = -(i/2) Y on register bit T:
+//   2 Re <lam|G|psi> = sum_pairs Re(conj l1 a0) - Re(conj l0 a1)
+// two packed accumulators (independent FFMA2 chains), one final add
+template <int T, typename C, typename Real>
+__device__ __forceinline__ Real grad_y(const C *a, const C *l) {
+    C acc[2] = {mk<C>(0, 0), mk<C>(0, 0)};
+    int i = 0;
+#pragma unroll
+    for (int r = 0; r < NR; r++) {
+        if (r & (1 << T)) continue;
+        const int s = r | (1 << T);
+        acc[i & 1] = cfma_elem(l[s], a[r], acc[i & 1]);
+        acc[i & 1] = cfma_elem(pneg(l[r]), a[s], acc[i & 1]);
+        i++;
+    }
+    const C t = padd(acc[0], acc[1]);
+    return t.x + t.y;
+}
+
+template <int MASK, typename C, typename Real>
+__device__ __forceinline__ void grad_y_layer(const C *a, const C *l, uint32_t gm, const uint16_t *soff, Real *tt) {
+    if constexpr ((MASK & 1) != 0) if (gm & 1) tt[soff[0]] += grad_y<0, C, Real>(a, l);
+    if constexpr ((MASK & 2) != 0) if (gm & 2) tt[soff[1]] += grad_y<1, C, Real>(a, l);
+    if constexpr ((MASK & 4) != 0) if (gm & 4) tt[soff[2]] += grad_y<2, C, Real>(a, l);
+    if constexpr ((MASK & 8) != 0) if (gm & 8) tt[soff[3]] += grad_y<3, C, Real>(a, l);
+}
+
+// RZ generators G = -(i/2) Z on the register bits of a diagonal layer:
+//   g_b = sum_r (-1)^{bit_b(r)} w_r,  w_r = Im(conj(lam_r) psi_r) = p_r.x - p_r.y
+// with p_r = lam_r * swap(psi_r) (packed); single-bit Walsh sums by a packed
+// butterfly (differences at each level, sums carried up)
+template <typename C, typename Real>
+__device__ __forceinline__ void grad_z_layer(const C *a, const C *l, uint32_t gm, const uint16_t *soff, Real *tt) {
+    C p[NR];
+#pragma unroll
+    for (int r = 0; r < NR; r++) p[r] = pmul(l[r], pswap(a[r]));
+    C P[NR / 2], m[NR / 2];
+#pragma unroll
+    for (int j = 0; j < NR / 2; j++) { P[j] = padd(p[2 * j], p[2 * j + 1]); m[j] = psub(p[2 * j], p[2 * j + 1]); }
+    const C d0 = padd(padd(padd(m[0], m[1]), padd(m[2], m[3])), padd(padd(m[4], m[5]), padd(m[6], m[7])));
+    C Q[NR / 4], n[NR / 4];
+#pragma unroll
+    for (int j = 0; j < NR / 4; j++) { Q[j] = padd(P[2 * j], P[2 * j + 1]); n[j] = psub(P[2 * j], P[2 * j + 1]); }
+    const C d1 = padd(padd(n[0], n[1]), padd(n[2], n[3]));
+    const C d2 = padd(psub(Q[0], Q[1]), psub(Q[2], Q[3]));
+    const C d3 = psub(padd(Q[0], Q[1]), padd(Q[2], Q[3]));
+    if (gm & 1) tt[soff[0]] += d0.x - d0.y;
+    if (gm & 2) tt[soff[1]] += d1.x - d1.y;
+    if (gm & 4) tt[soff[2]] += d2.x - d2.y;
+    if (gm & 8) tt[soff[3]] += d3.x - d3.y;
+}
+
 // ---- one op, in place on psi (and lambda in the adjoint) ----------------------
 // h = the op's 16-byte dispatch header (already in registers: prefetched while
 // the previous op ran), op = the full op in shared memory (coefficients).
 template <typename Real, bool BWD>
 __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
-                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, Real *tacc) {
+                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, Real *tt) {
     typedef typename CT<Real>::C C;
     auto bitval = [&](uint32_t kind, uint32_t idx) -> int {
         return kind == BK_TIX ? (int)((tix >> idx) & 1u) : (int)((basefull >> idx) & 1ull);
     };
     const int code = h.x & 0xff;
+    const uint32_t gm = (h.y >> 8) & 0xff;  // layer fast path (grad_y_layer / grad_z_layer in the switch)
     if (BWD) {
         const int ngen = (h.x >> 8) & 0xff;
-        if (ngen) {
+        if (ngen && !gm) {
+            // general path: gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
             const uint32_t gbits = h.y & 0xff;
             const uint32_t gkinds = h.w & 0xffff;
-            if (code == KC_DIAG) {
-                // RZ generators of a diagonal layer, batched: w_r = Im(conj(lam_r) psi_r),
-                // g_b = sum_r (-1)^{bit_b(r)} w_r for every generator bit b
-                Real w[NR];
-#pragma unroll
-                for (int r = 0; r < NR; r++) w[r] = im_cj(l[r], a[r]);
-                // single-bit Walsh sums g_b = sum_r (-1)^{bit_b(r)} w_r for b = 0..3 by a
-                // butterfly: differences at each level, sums carried up (40 adds)
-                Real gb[SWEEP_R];
-                {
-                    Real p[NR / 2];
-                    Real d = 0;
-#pragma unroll
-                    for (int j = 0; j < NR / 2; j++) { p[j] = w[2 * j] + w[2 * j + 1]; d += w[2 * j] - w[2 * j + 1]; }
-                    gb[0] = d;
-                    Real q2[NR / 4];
-                    d = 0;
-#pragma unroll
-                    for (int j = 0; j < NR / 4; j++) { q2[j] = p[2 * j] + p[2 * j + 1]; d += p[2 * j] - p[2 * j + 1]; }
-                    gb[1] = d;
-                    gb[2] = (q2[0] - q2[1]) + (q2[2] - q2[3]);
-                    gb[3] = (q2[0] + q2[1]) - (q2[2] + q2[3]);
+            for (int gi = 0; gi < ngen; gi++) {
+                Real part = 0;
+                if (code == KC_PHASE) {
+                    part = grad_z_const<C, Real>(a, l, bitval((h.z) & 0xff, (h.z >> 8) & 0xff));
+                } else {
+                    const int gk = (gkinds >> (4 * gi)) & 15;
+                    const Real *g = op.g[gi];
+                    dispatch4((gbits >> (2 * gi)) & 3,
+                              [&](auto tb) { part = grad_bit<decltype(tb)::value, C, Real>(a, l, gk, g); });
                 }
-                for (int gi = 0; gi < ngen; gi++) {
-                    const int bb = (gbits >> (2 * gi)) & 3;
-                    const Real part = bb == 0 ? gb[0] : bb == 1 ? gb[1] : bb == 2 ? gb[2] : gb[3];
-                    tacc[op.slot[gi] * blockDim.x + threadIdx.x] += part;
-                }
-            } else {
-                // gradients on the post-gate states (R7): g_p += 2 Re <lam|G_p|psi>
-                for (int gi = 0; gi < ngen; gi++) {
-                    Real part = 0;
-                    if (code == KC_PHASE) {
-                        part = grad_z_const<C, Real>(a, l, bitval((h.z) & 0xff, (h.z >> 8) & 0xff));
-                    } else {
-                        const int gk = (gkinds >> (4 * gi)) & 15;
-                        const Real *g = op.g[gi];
-                        dispatch4((gbits >> (2 * gi)) & 3,
-                                  [&](auto tb) { part = grad_bit<decltype(tb)::value, C, Real>(a, l, gk, g); });
-                    }
-                    tacc[op.slot[gi] * blockDim.x + threadIdx.x] += part;
-                }
+                tt[op.soff[gi]] += part;
             }
         }
     }
@@ -291,21 +325,21 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
     const bool on = ck == BK_NONE ? true : bitval(ck, ci) != 0;
     const int cm = creg != 0xff ? (1 << creg) : 0;
     switch (code) {
-    case 1: layer_real<1, C, Real>(a, op.m); if (BWD) layer_real<1, C, Real>(l, op.m); break;
-    case 2: layer_real<2, C, Real>(a, op.m); if (BWD) layer_real<2, C, Real>(l, op.m); break;
-    case 3: layer_real<3, C, Real>(a, op.m); if (BWD) layer_real<3, C, Real>(l, op.m); break;
-    case 4: layer_real<4, C, Real>(a, op.m); if (BWD) layer_real<4, C, Real>(l, op.m); break;
-    case 5: layer_real<5, C, Real>(a, op.m); if (BWD) layer_real<5, C, Real>(l, op.m); break;
-    case 6: layer_real<6, C, Real>(a, op.m); if (BWD) layer_real<6, C, Real>(l, op.m); break;
-    case 7: layer_real<7, C, Real>(a, op.m); if (BWD) layer_real<7, C, Real>(l, op.m); break;
-    case 8: layer_real<8, C, Real>(a, op.m); if (BWD) layer_real<8, C, Real>(l, op.m); break;
-    case 9: layer_real<9, C, Real>(a, op.m); if (BWD) layer_real<9, C, Real>(l, op.m); break;
-    case 10: layer_real<10, C, Real>(a, op.m); if (BWD) layer_real<10, C, Real>(l, op.m); break;
-    case 11: layer_real<11, C, Real>(a, op.m); if (BWD) layer_real<11, C, Real>(l, op.m); break;
-    case 12: layer_real<12, C, Real>(a, op.m); if (BWD) layer_real<12, C, Real>(l, op.m); break;
-    case 13: layer_real<13, C, Real>(a, op.m); if (BWD) layer_real<13, C, Real>(l, op.m); break;
-    case 14: layer_real<14, C, Real>(a, op.m); if (BWD) layer_real<14, C, Real>(l, op.m); break;
-    case 15: layer_real<15, C, Real>(a, op.m); if (BWD) layer_real<15, C, Real>(l, op.m); break;
+    case 1: if (BWD && gm) grad_y_layer<1, C, Real>(a, l, gm, op.soff, tt); layer_real<1, C, Real>(a, op.m); if (BWD) layer_real<1, C, Real>(l, op.m); break;
+    case 2: if (BWD && gm) grad_y_layer<2, C, Real>(a, l, gm, op.soff, tt); layer_real<2, C, Real>(a, op.m); if (BWD) layer_real<2, C, Real>(l, op.m); break;
+    case 3: if (BWD && gm) grad_y_layer<3, C, Real>(a, l, gm, op.soff, tt); layer_real<3, C, Real>(a, op.m); if (BWD) layer_real<3, C, Real>(l, op.m); break;
+    case 4: if (BWD && gm) grad_y_layer<4, C, Real>(a, l, gm, op.soff, tt); layer_real<4, C, Real>(a, op.m); if (BWD) layer_real<4, C, Real>(l, op.m); break;
+    case 5: if (BWD && gm) grad_y_layer<5, C, Real>(a, l, gm, op.soff, tt); layer_real<5, C, Real>(a, op.m); if (BWD) layer_real<5, C, Real>(l, op.m); break;
+    case 6: if (BWD && gm) grad_y_layer<6, C, Real>(a, l, gm, op.soff, tt); layer_real<6, C, Real>(a, op.m); if (BWD) layer_real<6, C, Real>(l, op.m); break;
+    case 7: if (BWD && gm) grad_y_layer<7, C, Real>(a, l, gm, op.soff, tt); layer_real<7, C, Real>(a, op.m); if (BWD) layer_real<7, C, Real>(l, op.m); break;
+    case 8: if (BWD && gm) grad_y_layer<8, C, Real>(a, l, gm, op.soff, tt); layer_real<8, C, Real>(a, op.m); if (BWD) layer_real<8, C, Real>(l, op.m); break;
+    case 9: if (BWD && gm) grad_y_layer<9, C, Real>(a, l, gm, op.soff, tt); layer_real<9, C, Real>(a, op.m); if (BWD) layer_real<9, C, Real>(l, op.m); break;
+    case 10: if (BWD && gm) grad_y_layer<10, C, Real>(a, l, gm, op.soff, tt); layer_real<10, C, Real>(a, op.m); if (BWD) layer_real<10, C, Real>(l, op.m); break;
+    case 11: if (BWD && gm) grad_y_layer<11, C, Real>(a, l, gm, op.soff, tt); layer_real<11, C, Real>(a, op.m); if (BWD) layer_real<11, C, Real>(l, op.m); break;
+    case 12: if (BWD && gm) grad_y_layer<12, C, Real>(a, l, gm, op.soff, tt); layer_real<12, C, Real>(a, op.m); if (BWD) layer_real<12, C, Real>(l, op.m); break;
+    case 13: if (BWD && gm) grad_y_layer<13, C, Real>(a, l, gm, op.soff, tt); layer_real<13, C, Real>(a, op.m); if (BWD) layer_real<13, C, Real>(l, op.m); break;
+    case 14: if (BWD && gm) grad_y_layer<14, C, Real>(a, l, gm, op.soff, tt); layer_real<14, C, Real>(a, op.m); if (BWD) layer_real<14, C, Real>(l, op.m); break;
+    case 15: if (BWD && gm) grad_y_layer<15, C, Real>(a, l, gm, op.soff, tt); layer_real<15, C, Real>(a, op.m); if (BWD) layer_real<15, C, Real>(l, op.m); break;
     case 16: layer_gen<1, C, Real>(a, op.m); if (BWD) layer_gen<1, C, Real>(l, op.m); break;
     case 17: layer_gen<2, C, Real>(a, op.m); if (BWD) layer_gen<2, C, Real>(l, op.m); break;
     case 18: layer_gen<3, C, Real>(a, op.m); if (BWD) layer_gen<3, C, Real>(l, op.m); break;
@@ -321,7 +355,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
     case 28: layer_gen<13, C, Real>(a, op.m); if (BWD) layer_gen<13, C, Real>(l, op.m); break;
     case 29: layer_gen<14, C, Real>(a, op.m); if (BWD) layer_gen<14, C, Real>(l, op.m); break;
     case 30: layer_gen<15, C, Real>(a, op.m); if (BWD) layer_gen<15, C, Real>(l, op.m); break;
-    case KC_DIAG: layer_diag<C, Real>(a, op.m); if (BWD) layer_diag<C, Real>(l, op.m); break;
+    case KC_DIAG: if (BWD && gm) grad_z_layer<C, Real>(a, l, gm, op.soff, tt); layer_diag<C, Real>(a, op.m); if (BWD) layer_diag<C, Real>(l, op.m); break;
     case 32: op_cu<0, C, Real>(a, op.m, cm, on); if (BWD) op_cu<0, C, Real>(l, op.m, cm, on); break;
     case 33: op_cu<1, C, Real>(a, op.m, cm, on); if (BWD) op_cu<1, C, Real>(l, op.m, cm, on); break;
     case 34: op_cu<2, C, Real>(a, op.m, cm, on); if (BWD) op_cu<2, C, Real>(l, op.m, cm, on); break;
@@ -535,7 +569,7 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
             for (; oi < e; oi++) {
                 // header of the next op loads while this one runs
                 const uint4 hn = oi + 1 < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi + 1]) : h;
-                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, tacc);
+                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, tacc + threadIdx.x);
                 h = hn;
             }
         }

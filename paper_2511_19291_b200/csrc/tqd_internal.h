@@ -117,7 +117,8 @@ template <typename Real> struct alignas(16) KOp {
     uint8_t creg;               // register-bit control, 0xff = none
     uint8_t t0;                 // K_CU target register bit
     uint8_t gbits;              // generator register bits, 2 bits each
-    uint8_t pad0;
+    uint8_t gmask;              // layer fast path: register bits carrying the layer's own generator
+                                // (real layer: -(i/2) Y per bit, diagonal layer: -(i/2) Z per bit)
     BitRef ctrl;                // lane / warp / base control, BK_NONE = none
     BitRef b0, b1;              // K_PHASE / K_D2 bits
     uint16_t gkinds;            // GenKind of each generator, 4 bits each
@@ -126,7 +127,9 @@ template <typename Real> struct alignas(16) KOp {
     uint8_t mask, t1;           // host / debug only
     uint8_t gbit[KOP_MAXGEN];   // host view of gbits
     uint8_t gkind[KOP_MAXGEN];  // host view of gkinds
-    uint8_t pad1[14];
+    uint16_t soff[KOP_MAXGEN];  // gradient accumulator offsets slot * threads; indexed by register
+                                // bit when gmask != 0, else by generator
+    uint8_t pad1[6];
     Real m[64];                 // 16-byte aligned (offset 48); complex entries as (re, 0, im, im)
     Real g[KOP_MAXGEN][8];      // generators (2x2 complex)
 };

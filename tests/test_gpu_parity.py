@@ -209,6 +209,26 @@ def test_nontrainable_and_u3(tqd, ctx, orc):
     _grad_check(tqd, ctx, orc, n, gates, W.sum_z(n), "c128")
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_degenerate_trainable_angles(tqd, ctx, orc, dtype):
+    """Trainable gates whose matrix at these angles has another type than their
+    generator: U3(0, phi, lam) is diagonal, RX(0) = RY(0) = I are real, RZ(0) = I.
+    The gradients must still use each gate's own generator (not the layer type's)."""
+    n = 13
+    base = W.hea(n, 2, seed=5)
+    gates = []
+    for i, g in enumerate(base):
+        gates.append(g)
+        if i % 4 == 0:
+            w = g.wires[:1]
+            gates.append(W.Gate("U3", w, (0.0, 0.3 + 0.1 * i, -0.2), None, True))
+            gates.append(W.Gate("RX", w, (0.0,), None, True))
+            gates.append(W.Gate("RZ", w, (0.0,), None, True))
+            gates.append(W.Gate("RY", w, (0.0,), None, True))
+    terms = W.random_z_terms(n, 4, 1) + W.sum_z(n)
+    _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=0)
+
+
 # ---------------------------------------------------------------- full-size properties
 def test_cfg3_entangler_free_factorization(tqd, ctx, orc):
     """30q depth-20 RY/RZ ansatz (cfg 3 shape, same launch configuration as bench.py,
