@@ -174,7 +174,7 @@ static PlanConfig make_plan_cfg(int n, int n_loc, int k, int small_max, bool dbl
     if (c.k - LANE_BITS - c.R > WMAX) c.k = LANE_BITS + c.R + WMAX;
     const size_t threads = (size_t)32 << std::max(0, c.k - LANE_BITS - c.R);
     const size_t exch = ((size_t)2 << c.k) * esz;
-    const size_t tables = (size_t)3 * MAXSEG * threads * 4;
+    const size_t tables = (size_t)3 * MAXSEG * threads * 4 + (size_t)3 * threads * 8;  // layout constants + prefetch offsets
     const size_t kop = dbl ? sizeof(KOp<double>) : sizeof(KOp<float>);
     const size_t real = esz / 2;
     const size_t budget = (size_t)200 * 1024 - std::min((size_t)200 * 1024 - 32 * 1024, exch + tables);

@@ -428,6 +428,8 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
     uint32_t *s_tix = reinterpret_cast<uint32_t *>(tacc + (BWD ? S.n_slots * blockDim.x : 0));
     uint32_t *s_tw = s_tix + nseg * blockDim.x;
     uint32_t *s_tr = s_tw + (nseg - 1) * blockDim.x;
+    // per-thread L2-prefetch offsets (element offsets within a tile, up to 2 per thread)
+    uint64_t *s_pf = reinterpret_cast<uint64_t *>(s_tr + (nseg - 1) * blockDim.x);  // 8 B aligned (threads * 4 B is)
     {
         const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
@@ -486,6 +488,31 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
             s_tr[x * T + tid] = (thr_cols(S.rcol[x], S.lay[x + 1]) ^ S.rcst[x]) * (uint32_t)sizeof(C);
         }
     }
+    // L2 prefetch of the NEXT tile (issued while this one computes): the tile's
+    // load set is 2^(5-C) x 16 lines of 128 B per warp (C = the pinned low bits that
+    // fill a line); lane j of the warp covers line i*32 + j with one prefetch per i
+    int n_pf = 0;
+    {
+        const DevLayout &L = S.lay[0];
+        int C = 0;
+        while (C < LANE_BITS && S.ld_phys[L.lane[C]] == C) C++;
+        const int lbits = LANE_BITS - C;                // lane bits outside the line
+        const int nlines = 16 << lbits;                 // lines per warp load set
+        n_pf = nlines >= 64 ? 2 : 1;
+        uint64_t wpart = 0;
+        for (int w = 0; w < W; w++)
+            if ((warp >> w) & 1) wpart |= 1ull << S.ld_phys[L.warp[w]];
+        for (int i = 0; i < n_pf; i++) {
+            const int idx = (i * 32 + lane) % nlines;
+            uint64_t off = wpart;
+            for (int t = 0; t < lbits; t++)
+                if ((idx >> t) & 1) off |= 1ull << S.ld_phys[L.lane[C + t]];
+            const int r = (idx >> lbits) & (NR - 1);
+            for (int b = 0; b < SWEEP_R; b++)
+                if ((r >> b) & 1) off |= 1ull << S.ld_phys[L.reg[b]];
+            s_pf[i * blockDim.x + threadIdx.x] = off;
+        }
+    }
     __syncthreads();
 
     // tile index -> physical base: deposit into the non-tile positions once, then
@@ -518,6 +545,14 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
             for (int r = 0; r < NR; r++) {
                 a[r] = psi[o[r]];
                 if (BWD) l[r] = lam[o[r]];
+            }
+        }
+        if (tile + gridDim.x < S.n_tiles) {
+            const uint64_t nb = ((base | ~tmask) + step) & tmask;
+            for (int i = 0; i < n_pf; i++) {
+                const uint64_t e = nb + s_pf[i * blockDim.x + threadIdx.x];
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(psi + e));
+                if (BWD) asm volatile("prefetch.global.L2 [%0];" ::"l"(lam + e));
             }
         }
 
@@ -605,7 +640,8 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
 template <typename Real, bool BWD>
 static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int nseg) {
     return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
-           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t);
+           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t) +
+           (size_t)2 * threads * sizeof(uint64_t);
 }
 
 template <typename Real, bool BWD>
