@@ -122,10 +122,20 @@ typedef struct tqd_metrics {
  * bytes to the other ranks by any means, e.g. torch.distributed). */
 int tqd_nccl_unique_id(void *out128);
 
+/* Writes a 128-byte LOOPBACK id: a world of W ranks emulated inside one
+ * process on one device (test facility for 1-GPU machines).  Every rank calls
+ * tqd_ctx_create(W, rank, device, id, ...) from its own host thread; the remap
+ * blocks then move by device-to-device copies between the ranks' buffers after
+ * host barriers, and sums are reduced on the host in rank order.  No kernel of
+ * one rank waits on another rank's kernel.  The device work of every rank (rank-
+ * bit conditioned sweeps, remap pack / unpack, sharded reductions, readback) is
+ * the same as with NCCL; only the transport differs. */
+int tqd_loopback_id(void *out128);
+
 /* Create the per-process context.  world must be a power of two (sharding
  * log2 d qubits over d accelerators, §4.2); 0 <= rank < world.
- * nccl_id: the 128 bytes from tqd_nccl_unique_id (ignored, may be NULL, iff
- * world == 1).  cuda_stream: a cudaStream_t to run on (borrowed) or NULL for
+ * nccl_id: the 128 bytes from tqd_nccl_unique_id or tqd_loopback_id
+ * (ignored, may be NULL, iff world == 1).  cuda_stream: a cudaStream_t to run on (borrowed) or NULL for
  * a library-created stream.  Collective over the world when world > 1. */
 int tqd_ctx_create(int world, int rank, int cuda_device, const void *nccl_id,
                    void *cuda_stream, tqd_ctx **out);
@@ -171,8 +181,11 @@ int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires,
 int tqd_num_params(const tqd_state *st, int *out);
 
 /* Execute pending gates, then out[t] = c_t <psi|P_t|psi> (
- * measure_allZ), c_t = 1 when coeff is NULL.  Terms with X/Y
- * on a sharded qubit: TQD_ERR_UNSUPPORTED.  Collective. */
+ * measure_allZ), c_t = 1 when coeff is NULL.  Pauli string
+ * t: X on the qubits of x_mask[t], Z on z_mask[t], Y where both bits are set
+ * (bit q = logical qubit q).  A term whose X/Y part touches sharded qubits pairs
+ * this shard with the partner rank's (rank XOR those rank bits): one whole-shard
+ * exchange per distinct such x mask.  Collective. */
 int tqd_expval(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_t *z_mask,
                const double *coeff, double *out);
 

@@ -62,6 +62,7 @@ _lib = None
 _P = ctypes.c_void_p
 _SIG = {
     "tqd_nccl_unique_id": [_P],
+    "tqd_loopback_id": [_P],
     "tqd_ctx_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.POINTER(_P)],
     "tqd_ctx_destroy": [_P],
     "tqd_state_bytes": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)],
@@ -123,6 +124,13 @@ def _ptr(a):
 # ---- raw ABI (same names as include/tqd.h) ---------------------------------------
 def tqd_version() -> str:
     return lib().tqd_version().decode()
+
+
+def tqd_loopback_id() -> bytes:
+    """128-byte id of an in-process loopback world (W ranks on one device, one thread each)."""
+    buf = ctypes.create_string_buffer(128)
+    _call("tqd_loopback_id", ctypes.cast(buf, _P))
+    return buf.raw
 
 
 def tqd_nccl_unique_id() -> bytes:

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtqd.so")
 SOURCES = ["kernels.cu", "sweep_f32_fwd.cu", "sweep_f32_bwd.cu", "sweep_f64_fwd.cu", "sweep_f64_bwd.cu",
-           "plan.cpp", "abi.cpp"]
+           "plan.cpp", "comm.cpp", "abi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -29,7 +29,7 @@ def _nccl_dirs():
 
 def _inputs():
     files = [os.path.join(CSRC, s) for s in SOURCES]
-    files += glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "tqd.h")]
+    files += glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.cpp")) + [os.path.join(ROOT, "include", "tqd.h")]
     return files
 
 

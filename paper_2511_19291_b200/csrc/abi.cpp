@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/tqd.h"
+#include "comm.h"
 #include "plan.h"
 #include "tqd_internal.h"
 
@@ -27,8 +28,8 @@ cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n,
                                double *eout, cudaStream_t s);
 cudaError_t launch_expval_z(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const uint64_t *d_z, int T,
                             double *out, cudaStream_t s);
-cudaError_t launch_expval_xy(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, uint64_t xloc, const uint64_t *d_z,
-                             const int *d_ny, int T, double *out, cudaStream_t s);
+cudaError_t launch_expval_xy(bool dbl, const void *psi, const void *peer, uint64_t n, uint64_t rank_hi, uint64_t xloc,
+                             const uint64_t *d_z, const int *d_ny, int T, double *out, cudaStream_t s);
 cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
                           cudaStream_t s);
 cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
@@ -49,7 +50,7 @@ struct tqd_ctx {
     int world = 1, rank = 0, device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    ncclComm_t comm = nullptr;
+    Comm *comm = nullptr;  // world > 1: NCCL, or the in-process loopback (comm.h)
     bool poisoned = false;
     int sms = 148;
 };
@@ -98,12 +99,11 @@ struct tqd_state {
         }                                                                                             \
     } while (0)
 
-#define NCCL_TRY(st, call)                                                                            \
+#define COMM_TRY(st, call)                                                                            \
     do {                                                                                              \
-        ncclResult_t r_ = (call);                                                                     \
-        if (r_ != ncclSuccess) {                                                                      \
+        if ((call) != 0) {                                                                            \
             (st)->ctx->poisoned = true;                                                               \
-            return fail(TQD_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));            \
+            return fail(TQD_ERR_NCCL, (st)->ctx->comm->err);                                          \
         }                                                                                             \
     } while (0)
 
@@ -276,20 +276,19 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
     char *sb = (char *)st->sendb, *rb = (char *)st->recvb;
     std::vector<int> peers, ublk;
     remap_schedule(c->rank, st->n_loc, rp, peers, ublk);
-    NCCL_TRY(st, ncclGroupStart());
+    COMM_TRY(st, c->comm->group_start());
     for (uint64_t b = 0; b < ((uint64_t)1 << rp.m); b++) {
         const int peer = peers[b];
         const uint64_t u = (uint64_t)ublk[b];
         if (peer == c->rank) {
             CUDA_TRY(st, cudaMemcpyAsync(rb + u * bb, sb + b * bb, bb, cudaMemcpyDeviceToDevice, c->stream));
         } else {
-            const ncclDataType_t dt = st->dbl ? ncclDouble : ncclFloat;
-            NCCL_TRY(st, ncclSend(sb + b * bb, blk * 2, dt, peer, c->comm, c->stream));
-            NCCL_TRY(st, ncclRecv(rb + u * bb, blk * 2, dt, peer, c->comm, c->stream));
+            COMM_TRY(st, c->comm->send(sb + b * bb, bb, peer, c->stream));
+            COMM_TRY(st, c->comm->recv(rb + u * bb, bb, peer, c->stream));
             st->met.a2a_bytes += bb;
         }
     }
-    NCCL_TRY(st, ncclGroupEnd());
+    COMM_TRY(st, c->comm->group_end(c->stream));
     CUDA_TRY(st, launch_remap_unpack(st->dbl, st->recvb, buf, rm, c->stream));
     ev_end(st, ev);
     st->met.hbm_bytes += 4 * shard_bytes(st);
@@ -474,7 +473,7 @@ static int execute_pending(tqd_state *st) {
 
 static int allreduce_sum(tqd_state *st, double *d, size_t count) {
     if (st->ctx->world == 1 || count == 0) return TQD_OK;
-    NCCL_TRY(st, ncclAllReduce(d, d, count, ncclDouble, ncclSum, st->ctx->comm, st->ctx->stream));
+    COMM_TRY(st, st->ctx->comm->allreduce_sum(d, count, CE_F64, st->ctx->stream));
     return TQD_OK;
 }
 
@@ -519,6 +518,12 @@ int tqd_nccl_unique_id(void *out128) {
     return TQD_OK;
 }
 
+int tqd_loopback_id(void *out128) {
+    if (!out128) return fail(TQD_ERR_ARG, "out128 is NULL");
+    comm_make_loopback_id(out128);
+    return TQD_OK;
+}
+
 int tqd_ctx_create(int world, int rank, int cuda_device, const void *nccl_id, void *cuda_stream, tqd_ctx **out) {
     if (!out) return fail(TQD_ERR_ARG, "out is NULL");
     *out = nullptr;
@@ -541,13 +546,12 @@ int tqd_ctx_create(int world, int rank, int cuda_device, const void *nccl_id, vo
         c->own_stream = true;
     }
     if (world > 1) {
-        ncclUniqueId id;
-        memcpy(&id, nccl_id, sizeof(id));
-        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
-        if (r != ncclSuccess) {
+        std::string err;
+        c->comm = comm_create(nccl_id, world, rank, err);
+        if (!c->comm) {
             if (c->own_stream) cudaStreamDestroy(c->stream);
             delete c;
-            return fail(TQD_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+            return fail(TQD_ERR_NCCL, err);
         }
     }
     *out = c;
@@ -556,7 +560,7 @@ int tqd_ctx_create(int world, int rank, int cuda_device, const void *nccl_id, vo
 
 int tqd_ctx_destroy(tqd_ctx *c) {
     if (!c) return fail(TQD_ERR_ARG, "ctx is NULL");
-    if (c->comm) ncclCommDestroy(c->comm);
+    delete c->comm;
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return TQD_OK;
@@ -730,10 +734,6 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
     rc = execute_pending(st);
     if (rc) return rc;
     if (T == 0) return ev_collect(st);
-    // reject X/Y on sharded qubits before any device work
-    for (int t = 0; t < T; t++)
-        if (phys_mask(st, x[t]) >> st->n_loc)
-            return fail(TQD_ERR_UNSUPPORTED, "X/Y on a sharded qubit is not supported by tqd_expval in this build");
     rc = ensure_red(st, (size_t)T + 2 * 64 + 64);
     if (rc) return rc;
     tqd_ctx *c = st->ctx;
@@ -770,7 +770,23 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         std::vector<int> grp;
         for (int t = t0; t < T; t++)
             if (!done[t] && x[t] == x[t0] && grp.size() < 16) grp.push_back(t);
-        const uint64_t xl = phys_mask(st, x[t0]);
+        const uint64_t xp = phys_mask(st, x[t0]);
+        const uint64_t xl = xp & ((1ull << st->n_loc) - 1);
+        const int gx = (int)(xp >> st->n_loc);
+        const void *peer = st->psi;
+        if (gx) {
+            // X / Y on rank bits: <psi|P|psi> pairs this shard with rank ^ gx's shard
+            // (a whole-shard swap with that partner)
+            rc = ensure_xchg(st);
+            if (rc) return rc;
+            const int partner = c->rank ^ gx;
+            COMM_TRY(st, c->comm->group_start());
+            COMM_TRY(st, c->comm->send(st->psi, shard_bytes(st), partner, c->stream));
+            COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
+            COMM_TRY(st, c->comm->group_end(c->stream));
+            st->met.a2a_bytes += shard_bytes(st);
+            peer = st->recvb;
+        }
         uint64_t hm[16];
         int hn[16];
         for (size_t i = 0; i < grp.size(); i++) {
@@ -781,7 +797,7 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         CUDA_TRY(st, cudaMemcpyAsync(d_ny, hn, grp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
         double *tmp = st->d_red + T + 128;
         CUDA_TRY(st, cudaMemsetAsync(tmp, 0, 16 * sizeof(double), c->stream));
-        CUDA_TRY(st, launch_expval_xy(st->dbl, st->psi, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp, c->stream));
+        CUDA_TRY(st, launch_expval_xy(st->dbl, st->psi, peer, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp, c->stream));
         for (size_t i = 0; i < grp.size(); i++)
             CUDA_TRY(st, cudaMemcpyAsync(d_out + grp[i], tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         CUDA_TRY(st, cudaStreamSynchronize(c->stream));
@@ -907,8 +923,11 @@ int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host
         const uint64_t cnt = std::min(chunk, count - o);
         cudaError_t e = launch_gather(st->dbl, st->psi, tmp, first + o, cnt, gm, c->stream);
         if (e == cudaSuccess && c->world > 1) {
-            ncclResult_t r = ncclAllReduce(tmp, tmp, cnt * 2, st->dbl ? ncclDouble : ncclFloat, ncclSum, c->comm, c->stream);
-            if (r != ncclSuccess) { cudaFree(tmp); c->poisoned = true; return fail(TQD_ERR_NCCL, ncclGetErrorString(r)); }
+            if (c->comm->allreduce_sum(tmp, cnt * 2, st->dbl ? CE_F64 : CE_F32, c->stream) != 0) {
+                cudaFree(tmp);
+                c->poisoned = true;
+                return fail(TQD_ERR_NCCL, c->comm->err);
+            }
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync((char *)host_out + o * st->esz, tmp, cnt * st->esz, cudaMemcpyDeviceToHost, c->stream);
         st->met.d2h_bytes += cnt * st->esz;

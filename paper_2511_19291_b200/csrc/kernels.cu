@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(256) expval_z_kernel(const typename CT<Real>::
 
 // out[t] += sum_b Re( i^{ny_t} (-1)^{popc(b & z_t)} conj(psi_{b^x}) psi_b ): one x mask, <= 16 terms
 template <typename Real>
-__global__ void __launch_bounds__(256) expval_xy_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n,
+__global__ void __launch_bounds__(256) expval_xy_kernel(const typename CT<Real>::C *__restrict__ psi,
+                                                        const typename CT<Real>::C *__restrict__ peer, uint64_t n,
                                                         uint64_t rank_hi, uint64_t xloc, const uint64_t *__restrict__ zmask,
                                                         const int *__restrict__ ny, int T, double *__restrict__ out) {
     typedef typename CT<Real>::C C;
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(256) expval_xy_kernel(const typename CT<Real>:
     for (int t = 0; t < 16; t++) acc[t] = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t b = i | rank_hi;
-        const C x = psi[i], y = psi[i ^ xloc];
+        const C x = psi[i], y = peer[i ^ xloc];  // peer: this shard, or the partner rank's (X on rank bits)
         const Real re = y.x * x.x + y.y * x.y;  // conj(y) x
         const Real im = y.x * x.y - y.y * x.x;
 #pragma unroll
@@ -376,11 +377,15 @@ cudaError_t launch_expval_z(bool dbl, const void *psi, uint64_t n, uint64_t rank
     return cudaGetLastError();
 }
 
-cudaError_t launch_expval_xy(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, uint64_t xloc, const uint64_t *d_z,
-                             const int *d_ny, int T, double *out, cudaStream_t s) {
+cudaError_t launch_expval_xy(bool dbl, const void *psi, const void *peer, uint64_t n, uint64_t rank_hi, uint64_t xloc,
+                             const uint64_t *d_z, const int *d_ny, int T, double *out, cudaStream_t s) {
     const int th = 256;
-    if (dbl) expval_xy_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, n, rank_hi, xloc, d_z, d_ny, T, out);
-    else expval_xy_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, n, rank_hi, xloc, d_z, d_ny, T, out);
+    if (dbl)
+        expval_xy_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, (const double2 *)peer, n, rank_hi,
+                                                                xloc, d_z, d_ny, T, out);
+    else
+        expval_xy_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (const float2 *)peer, n, rank_hi, xloc,
+                                                               d_z, d_ny, T, out);
     return cudaGetLastError();
 }
 

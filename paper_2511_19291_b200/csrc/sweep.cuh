@@ -21,6 +21,8 @@
 //
 // Instantiated once per (precision, direction) in sweep_*.cu.
 #pragma once
+#include <atomic>
+
 #include "common.cuh"
 #include "tqd_internal.h"
 
@@ -644,6 +646,32 @@ static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int n
            (size_t)2 * threads * sizeof(uint64_t);
 }
 
+// The dynamic shared-memory cap is a per-function attribute shared by every host
+// thread: raise it ONCE per device to the opt-in maximum (a per-launch value would
+// race between threads driving different states, e.g. emulated ranks), and let
+// each launch / occupancy query pass its own size.
+template <typename F> static cudaError_t raise_smem_cap_once(F fn, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    int mx = 0;
+    e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
+
+template <typename Real, bool BWD> static std::atomic<uint64_t> &sweep_cap_flag() {
+    static std::atomic<uint64_t> f{0};
+    return f;
+}
+
 template <typename Real, bool BWD>
 cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
                               double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, int nseg,
@@ -651,8 +679,7 @@ cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const 
     typedef typename CT<Real>::C C;
     auto fn = sweep_kernel<Real, BWD>;
     const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
-    // set on every launch: the occupancy query may have lowered it
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>());
     if (e != cudaSuccess) return e;
     fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi);
     return cudaGetLastError();
@@ -662,7 +689,10 @@ template <typename Real, bool BWD>
 int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg) {
     auto fn = sweep_kernel<Real, BWD>;
     const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>()) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 << W, smem) != cudaSuccess) {
         cudaGetLastError();

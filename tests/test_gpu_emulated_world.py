@@ -1,0 +1,172 @@
+"""Multi-rank DEVICE path on one GPU: W ranks emulated in one process (one host
+thread + one stream + one shard per rank) through the loopback transport
+(include/tqd.h tqd_loopback_id).  Everything the ranks run on the device is the
+product path for world > 1 -- rank-bit conditioned sweeps (diagonal gates and
+controls on global qubits), remap pack / unpack around the
+block exchange, sharded expval / lambda-init / adjoint partials and their sums,
+the sharded readback -- only the transport between the shards is host-driven
+copies instead of NCCL (no kernel waits on another rank's kernel).
+
+Every rank's result is compared with the float64 oracle of the whole circuit.
+"""
+import threading
+import traceback
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": dict(amp=1e-5, val=1e-4), "c128": dict(amp=1e-12, val=1e-10)}
+
+
+@pytest.fixture(scope="module")
+def tqd():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need CUDA (run with -m 'not gpu' on CPU)")
+    import paper_2511_19291_b200 as t
+    return t
+
+
+def run_world(tqd, world, fn, timeout=600):
+    """fn(rank, ctx) on `world` threads sharing one loopback id; returns per-rank results."""
+    lid = tqd.tqd_loopback_id()
+    res, err = [None] * world, [None] * world
+
+    def worker(r):
+        try:
+            ctx = tqd.Context(world, r, 0, lid)
+            try:
+                res[r] = fn(r, ctx)
+            finally:
+                ctx.close()
+        except Exception:
+            err[r] = traceback.format_exc()
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+    assert not any(t.is_alive() for t in th), "emulated world hung"
+    bad = [f"rank {r}:\n{e}" for r, e in enumerate(err) if e is not None]
+    assert not bad, "\n".join(bad)
+    return res
+
+
+def mixed_circuit(n, seed):
+    return W.random_circuit(n, 120, seed) + W.hea(n, 2, seed) + W.qft(n)[:30]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n,k", [(2, 12, 9), (4, 13, 9), (8, 14, 9), (2, 16, 12), (4, 17, 12)])
+def test_world_amplitudes(tqd, orc, world, n, k, dtype):
+    gates = mixed_circuit(n, world + n)
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_TILE_QUBITS, k)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.apply_circuit(gates)
+        amp = st.amplitudes()
+        m = st.metrics()
+        st.free()
+        return amp, m
+    out = run_world(tqd, world, fn)
+    ref = orc.run(n, gates)
+    for amp, m in out:
+        assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"]
+        assert m["remaps"] > 0 and m["a2a_bytes"] > 0  # the exchange really ran
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n", [(2, 12), (4, 14), (8, 15)])
+def test_world_expval_pauli(tqd, orc, world, n, dtype):
+    """Z strings and X/Y strings, including strings acting on the global qubits."""
+    gates = mixed_circuit(n, 3 * world)
+    terms = W.random_pauli_terms(n, 16, n) + W.random_z_terms(n, 16, n) + W.sum_z(n)
+    # logical qubits 0..log2(world)-1 start on the rank bits (MSB-first)
+    terms += [(1, 0, 0.7), (0, 1, -0.4), (3, 4, 1.1), (2, 1 | (1 << (n - 1)), 0.3)]
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.apply_circuit(gates)
+        v = st.expval(terms)
+        st.free()
+        return v
+    out = run_world(tqd, world, fn)
+    ref = orc.expval(orc.run(n, gates), n, terms)
+    for v in out:
+        assert np.max(np.abs(v - ref)) < TOL[dtype]["val"]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n,k,small", [(2, 12, 9, False), (4, 14, 10, True), (8, 15, 9, True), (2, 17, 12, True)])
+def test_world_adjoint(tqd, orc, world, n, k, small, dtype):
+    """Adjoint gradients with remaps replayed on psi and lambda."""
+    gates = W.random_circuit(n, 80, 5 + world, small=small) + W.hea(n, 3, world, small=small)
+    terms = W.random_z_terms(n, 5, world) + W.sum_z(n)
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_TILE_QUBITS, k)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(terms)
+        st.free()
+        return val, grad
+    out = run_world(tqd, world, fn)
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    for val, grad in out:
+        assert abs(val - rval) < TOL[dtype]["val"]
+        assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]
+
+
+def test_world_ghz_global_targets(tqd, orc):
+    """GHZ with CNOT targets on the global qubits (forces remaps), read back on every rank."""
+    n, world = 14, 4
+    gates = [W.Gate("H", (n - 1,), (), None, True)] + [W.Gate("CNOT", (q + 1, q), (), None, True) for q in range(n - 2, -1, -1)]
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, "c128")
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.apply_circuit(gates)
+        amp = st.amplitudes()
+        zz = st.expval([(0, 1 | (1 << (n - 1)), 1.0), (0, 1, 1.0)])
+        st.free()
+        return amp, zz
+    for amp, zz in run_world(tqd, world, fn):
+        ref = orc.run(n, gates)
+        assert np.max(np.abs(amp - ref)) < 1e-12
+        assert abs(amp[0] - 2 ** -0.5) < 1e-12 and abs(amp[-1] - 2 ** -0.5) < 1e-12
+        assert abs(zz[0] - 1.0) < 1e-12 and abs(zz[1]) < 1e-12
+
+
+def test_world_matches_single_rank(tqd, orc):
+    """World 1 vs 2 vs 4 vs 8 give the same gradients (SPEC-style sharding invariance)."""
+    n = 13
+    gates = W.hea(n, 4, 11, small=True)
+    terms = W.sum_z(n)
+    vals = {}
+    for world in (1, 2, 4, 8):
+        def fn(r, ctx):
+            st = tqd.State(ctx, n, "c128")
+            st.set_option(tqd.OPT_TILE_QUBITS, 9)
+            st.apply_circuit(gates)
+            v = st.adjoint_grad(terms)
+            st.free()
+            return v
+        if world == 1:
+            ctx = tqd.Context(1, 0, 0)
+            vals[world] = fn(0, ctx)
+            ctx.close()
+        else:
+            vals[world] = run_world(tqd, world, fn)[0]
+    for world in (2, 4, 8):
+        assert abs(vals[world][0] - vals[1][0]) < 1e-11
+        assert np.max(np.abs(vals[world][1] - vals[1][1])) < 1e-11
