@@ -197,7 +197,9 @@ int tqd_expval(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_
  * (dx = U^T dy in the real representation, Eq. save_x).
  * This is the VJP of any loss of the expectation values (choose c_t = dL/dE_t,
  * e.g. sign(E_t) for Listing 2's out.abs().sum()).
- * Z-only terms (x_mask == 0) in this build, else TQD_ERR_UNSUPPORTED.
+ * General Pauli strings (as tqd_expval), at most 64 terms: Z strings seed
+ * lambda in one pass; X / Y strings add c_t P_t psi per x mask (with the partner
+ * rank's shard when the x mask has rank bits).
  * CONSUMES the state: afterwards only tqd_state_reset / tqd_state_free /
  * tqd_get_metrics are allowed.  Collective. */
 int tqd_adjoint_grad(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_t *z_mask,

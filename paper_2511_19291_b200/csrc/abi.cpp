@@ -30,6 +30,9 @@ cudaError_t launch_expval_z(bool dbl, const void *psi, uint64_t n, uint64_t rank
                             double *out, cudaStream_t s);
 cudaError_t launch_expval_xy(bool dbl, const void *psi, const void *peer, uint64_t n, uint64_t rank_hi, uint64_t xloc,
                              const uint64_t *d_z, const int *d_ny, int T, double *out, cudaStream_t s);
+cudaError_t launch_lambda_add_xy(bool dbl, const void *psi, const void *peer, void *lam, uint64_t n, uint64_t rank_hi,
+                                 uint64_t xloc, uint64_t xfull, const uint64_t *d_z, const int *d_ny, const double *d_c,
+                                 int T, double *eout, cudaStream_t s);
 cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
                           cudaStream_t s);
 cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
@@ -76,6 +79,7 @@ struct tqd_state {
     int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0;
     tqd_metrics met;
     double *d_red = nullptr;  // reductions: values / grads
+    uint64_t *d_xy = nullptr;  // X/Y adjoint-seed term scratch: z masks, coefficients, #Y
     size_t red_count = 0;
     // plan / descriptor caches (tqd_state_rewind replays the same tape)
     uint64_t tape_version = 1;
@@ -217,6 +221,15 @@ static int ensure_xchg(tqd_state *st) {
     }
     st->own_xchg = true;
     st->met.peak_device_bytes += 2 * b;
+    return TQD_OK;
+}
+
+static int ensure_xy_scratch(tqd_state *st) {
+    if (st->d_xy) return TQD_OK;
+    if (cudaMalloc(&st->d_xy, 48 * sizeof(uint64_t)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TQD_ERR_OOM, "cannot allocate the X/Y term scratch");
+    }
     return TQD_OK;
 }
 
@@ -672,6 +685,7 @@ int tqd_state_free(tqd_state *st) {
         if (E) { free_encoded(*E); delete E; }
     }
     if (st->d_red) cudaFree(st->d_red);
+    if (st->d_xy) cudaFree(st->d_xy);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
     delete st;
     return TQD_OK;
@@ -827,8 +841,6 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
     rc = check_terms(st, T, x, z);
     if (rc) return rc;
     if (T > 64) return fail(TQD_ERR_UNSUPPORTED, "at most 64 observable terms in tqd_adjoint_grad");
-    for (int t = 0; t < T; t++)
-        if (x[t]) return fail(TQD_ERR_UNSUPPORTED, "tqd_adjoint_grad supports Z-string terms only (x_mask == 0) in this build");
     rc = execute_pending(st);
     if (rc) return rc;
     rc = ensure_lambda(st);
@@ -842,6 +854,7 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
     ZTerms zt;
     memset(&zt, 0, sizeof(zt));
     for (int t = 0; t < T; t++) {
+        if (x && x[t]) continue;  // X / Y strings: lambda_add_xy below
         const uint64_t zp = phys_mask(st, z[t]);
         const double ct = coeff ? coeff[t] : 1.0;
         if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
@@ -860,6 +873,58 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
         ev_end(st, ev);
         st->met.hbm_bytes += 2 * N * st->esz;
         st->met.kernel_launches++;
+    }
+    // X / Y strings: lambda += c_t P_t psi, grouped by x mask (<= 16 terms per launch);
+    // x masks with rank bits pair the shard with the partner rank's (as in tqd_expval)
+    if (x) {
+        std::vector<char> done(T, 0);
+        std::vector<uint64_t> hz;
+        std::vector<int> hn;
+        std::vector<double> hc;
+        for (int t0 = 0; t0 < T; t0++) {
+            if (done[t0] || !x[t0]) continue;
+            std::vector<int> grp;
+            for (int t = t0; t < T; t++)
+                if (!done[t] && x[t] == x[t0] && grp.size() < 16) grp.push_back(t);
+            const uint64_t xp = phys_mask(st, x[t0]);
+            const uint64_t xl = xp & (N - 1);
+            const int gx = (int)(xp >> st->n_loc);
+            const void *peer = st->psi;
+            if (gx) {
+                rc = ensure_xchg(st);
+                if (rc) return rc;
+                const int partner = c->rank ^ gx;
+                COMM_TRY(st, c->comm->group_start());
+                COMM_TRY(st, c->comm->send(st->psi, shard_bytes(st), partner, c->stream));
+                COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
+                COMM_TRY(st, c->comm->group_end(c->stream));
+                st->met.a2a_bytes += shard_bytes(st);
+                peer = st->recvb;
+            }
+            hz.assign(16, 0);
+            hn.assign(16, 0);
+            hc.assign(16, 0.0);
+            for (size_t i = 0; i < grp.size(); i++) {
+                hz[i] = phys_mask(st, z[grp[i]]);
+                hn[i] = __builtin_popcountll(x[grp[i]] & z[grp[i]]) & 3;
+                hc[i] = coeff ? coeff[grp[i]] : 1.0;
+            }
+            rc = ensure_xy_scratch(st);
+            if (rc) return rc;
+            CUDA_TRY(st, cudaMemcpyAsync(st->d_xy, hz.data(), 16 * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 16, hc.data(), 16 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 32, hn.data(), 16 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+            const int ev = ev_begin(st, CAT_OTHER);
+            CUDA_TRY(st, launch_lambda_add_xy(st->dbl, st->psi, peer, st->lam, N, rank_hi(st), xl, xp, st->d_xy,
+                                              (const int *)(st->d_xy + 32), (const double *)(st->d_xy + 16),
+                                              (int)grp.size(), d_val, c->stream));
+            ev_end(st, ev);
+            CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host staging vectors are reused
+            st->met.h2d_bytes += 16 * (8 + 8 + 4);
+            st->met.hbm_bytes += 4 * N * st->esz;
+            st->met.kernel_launches++;
+            for (int t : grp) done[t] = 1;
+        }
     }
     // reverse sweep down to (and including) the earliest stage holding a trainable gate
     int first = -1;

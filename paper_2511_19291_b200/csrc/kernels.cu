@@ -7,6 +7,7 @@
 //                                plus the gradient contraction, on psi and lambda)
 //   small_kernel<Real, BWD>      whole shard in one CTA's shared memory
 //   lambda_init_kernel           lambda = H psi, E = <psi|H|psi> (Z strings)
+//   lambda_add_xy_kernel         lambda += c P psi, E += c <psi|P|psi> (X / Y strings)
 //   expval_z_kernel / expval_xy_kernel   <psi|P_t|psi> partial sums
 //   gather_kernel                canonical-order readback through pi
 //   remap_pack / remap_unpack    qubit-remap staging for the NCCL exchange
@@ -180,6 +181,46 @@ __global__ void __launch_bounds__(256) lambda_init_kernel(const typename CT<Real
         const C x = psi[i];
         lam[i] = mk<C>(h * x.x, h * x.y);
         acc += (double)(h * (x.x * x.x + x.y * x.y));
+    }
+    double tot = block_sum<double>(acc, red);
+    if (threadIdx.x == 0) atomicAdd(eout, tot);
+}
+
+// X / Y strings in the adjoint seed (PAPER.md:226-231 with H = sum_t c_t P_t):
+// lambda_j += sum_t c_t (P_t psi)_j for terms sharing one x mask, where
+// (P psi)_j = i^{q} (-1)^{popc((b_j ^ x) & z)} psi_{j ^ x}   (q = #Y mod 4; the same
+// convention as expval_xy_kernel), psi_{j ^ x} read from `peer` (this shard, or
+// the partner rank's when x has rank bits).  E partial += Re(conj(psi_j) * that).
+template <typename Real>
+__global__ void __launch_bounds__(256) lambda_add_xy_kernel(const typename CT<Real>::C *__restrict__ psi,
+                                                            const typename CT<Real>::C *__restrict__ peer,
+                                                            typename CT<Real>::C *__restrict__ lam, uint64_t n,
+                                                            uint64_t rank_hi, uint64_t xloc, uint64_t xfull,
+                                                            const uint64_t *__restrict__ zmask, const int *__restrict__ ny,
+                                                            const double *__restrict__ coef, int T,
+                                                            double *__restrict__ eout) {
+    typedef typename CT<Real>::C C;
+    __shared__ double red[32];
+    double acc = 0;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t bsrc = (j | rank_hi) ^ xfull;
+        const C y = peer[j ^ xloc];
+        Real ar = 0, ai = 0;  // sum_t c_t s_t, complex (s_t = i^q (-1)^parity)
+        for (int t = 0; t < T; t++) {
+            Real c = (Real)coef[t];
+            if (__popcll(bsrc & zmask[t]) & 1) c = -c;
+            switch (ny[t] & 3) {
+            case 0: ar += c; break;
+            case 1: ai += c; break;
+            case 2: ar -= c; break;
+            default: ai -= c; break;
+            }
+        }
+        const C v = mk<C>(ar * y.x - ai * y.y, ar * y.y + ai * y.x);
+        const C l = lam[j];
+        lam[j] = mk<C>(l.x + v.x, l.y + v.y);
+        const C x = psi[j];
+        acc += (double)(x.x * v.x + x.y * v.y);
     }
     double tot = block_sum<double>(acc, red);
     if (threadIdx.x == 0) atomicAdd(eout, tot);
@@ -386,6 +427,21 @@ cudaError_t launch_expval_xy(bool dbl, const void *psi, const void *peer, uint64
     else
         expval_xy_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (const float2 *)peer, n, rank_hi, xloc,
                                                                d_z, d_ny, T, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lambda_add_xy(bool dbl, const void *psi, const void *peer, void *lam, uint64_t n, uint64_t rank_hi,
+                                 uint64_t xloc, uint64_t xfull, const uint64_t *d_z, const int *d_ny, const double *d_c,
+                                 int T, double *eout, cudaStream_t s) {
+    const int th = 256;
+    if (dbl)
+        lambda_add_xy_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, (const double2 *)peer,
+                                                                    (double2 *)lam, n, rank_hi, xloc, xfull, d_z, d_ny,
+                                                                    d_c, T, eout);
+    else
+        lambda_add_xy_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (const float2 *)peer,
+                                                                   (float2 *)lam, n, rank_hi, xloc, xfull, d_z, d_ny,
+                                                                   d_c, T, eout);
     return cudaGetLastError();
 }
 

@@ -127,6 +127,27 @@ def test_world_adjoint(tqd, orc, world, n, k, small, dtype):
         assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n", [(2, 12), (4, 14), (8, 15)])
+def test_world_adjoint_pauli(tqd, orc, world, n, dtype):
+    """X / Y strings in the adjoint seed, including X / Y on the rank bits (partner-shard exchange)."""
+    gates = W.random_circuit(n, 60, 7 * world, small=True) + W.hea(n, 2, world, small=True)
+    terms = W.random_pauli_terms(n, 10, world) + [(1, 0, 0.7), (3, 4, -1.1), (2, 1 | (1 << (n - 1)), 0.3)]
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.apply_circuit(gates)
+        v = st.adjoint_grad(terms)
+        st.free()
+        return v
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    for val, grad in run_world(tqd, world, fn):
+        assert abs(val - rval) < TOL[dtype]["val"]
+        assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]
+
+
 def test_world_ghz_global_targets(tqd, orc):
     """GHZ with CNOT targets on the global qubits (forces remaps), read back on every rank."""
     n, world = 14, 4

@@ -168,6 +168,16 @@ def test_adjoint_random_circuits(tqd, ctx, orc, n, small_max, k, dtype):
             _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=small_max, k=k)
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,small_max,k", [(5, 10, None), (12, 0, 10), (15, 0, 12)])
+def test_adjoint_pauli_terms(tqd, ctx, orc, n, small_max, k, dtype):
+    """X / Y / Z strings in the adjoint seed lambda = sum_t c_t P_t psi."""
+    for seed in range(2):
+        gates = W.random_circuit(n, 70, 40 + seed, small=True) + W.hea(n, 2, seed, small=True)
+        terms = W.random_pauli_terms(n, 12, seed) + W.random_z_terms(n, 3, seed) + [(1, 2, 0.5), (3, 0, -0.25)]
+        _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=small_max, k=k)
+
+
 def test_cfg1_exact(tqd, ctx, orc):
     """BASELINE.json configs[0]: 10q HEA depth 4, <Z0> and all 80 gradients, complex128."""
     wl = W.config(1)
@@ -310,7 +320,7 @@ def test_abi_errors(tqd, ctx):
     assert e.value.code == -1
     st.apply("RY", [0], [0.3])
     with pytest.raises(tqd.TqdError) as e:
-        tqd.tqd_adjoint_grad(st.handle, [(1, 0, 1.0)])  # X term: unsupported in the adjoint
+        tqd.tqd_adjoint_grad(st.handle, [(0, 1, 1.0)] * 65)  # more than 64 terms
     assert e.value.code == -8
     v, g = st.adjoint_grad([(0, 1, 1.0)])
     assert abs(v - math.cos(0.3)) < 1e-6 and abs(g[0] + math.sin(0.3)) < 1e-6
