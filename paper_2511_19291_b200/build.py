@@ -53,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
               "-Xcompiler", "-fPIC,-O3", f"-I{inc}"]
     if verbose:
         common.append("-Xptxas=-v")
+    common += os.environ.get("TQD_NVCC_EXTRA", "").split()  # experiment knobs, e.g. -DTQD_SWEEP_R=3
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")

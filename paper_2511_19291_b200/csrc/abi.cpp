@@ -161,7 +161,7 @@ static PlanConfig make_plan_cfg(int n, int n_loc, int k, int small_max, bool dbl
     c.n = n;
     c.n_loc = n_loc;
     c.k = k;
-    c.R = 4;
+    c.R = TQD_SWEEP_R;
     c.small_max = small_max;
     c.c128 = dbl;
     c.swz_bits = dbl ? 3 : 4;
@@ -181,7 +181,9 @@ static PlanConfig make_plan_cfg(int n, int n_loc, int k, int small_max, bool dbl
     const size_t tables = (size_t)3 * MAXSEG * threads * 4 + (size_t)3 * threads * 8;  // layout constants + prefetch offsets
     const size_t kop = dbl ? sizeof(KOp<double>) : sizeof(KOp<float>);
     const size_t real = esz / 2;
-    const size_t budget = (size_t)200 * 1024 - std::min((size_t)200 * 1024 - 32 * 1024, exch + tables);
+    static const char *bkb = getenv("TQD_EXPERIMENT_SMEM_KB");  // timing experiments only
+    const size_t cap = (size_t)(bkb ? atoi(bkb) : 200) * 1024;
+    const size_t budget = cap - std::min(cap - 32 * 1024, exch + tables);
     c.max_slots = (int)std::min<size_t>(MAX_STAGE_SLOTS, (budget / 3) / (threads * real));
     c.max_slots = std::max(c.max_slots, 3);
     c.max_ops = (int)std::min<size_t>(MAX_STAGE_OPS, (budget - (size_t)c.max_slots * threads * real) / kop);

@@ -604,63 +604,121 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     sp.lays.assign(nseg, Layout());
     std::vector<int> fl(n_loc, -1);  // logical qubit at physical position after relabels
     for (int q = 0; q < n; q++) if (fpos[q] < n_loc) fl[fpos[q]] = q;
+    // register bits of every layout
+    std::vector<std::vector<int>> regs_of(nseg);
     for (int s = 0; s < nseg; s++) {
         std::vector<int> regs = segregs[s];
         for (int t = 0; t < k && (int)regs.size() < R; t++) {
             if (s == 0 && t < C) continue;
             if (!std::count(regs.begin(), regs.end(), t)) regs.push_back(t);
         }
-        std::vector<int> others;
-        for (int t = 0; t < k; t++) if (!std::count(regs.begin(), regs.end(), t)) others.push_back(t);
-        // lanes 0..C-1 hold the pinned low bits at load (layout 0) and the bits that
-        // land on physical 0..C-1 at store (last layout); lanes C..4 are free
-        std::vector<int> lanes;
-        if (s == nseg - 1) {
-            // choose the C qubits left on the pinned bits so that the NEXT stage
-            // places the most gates (dry run over all C-subsets of the free bits);
-            // with one segment the pinned bits stay put
-            std::vector<std::pair<long long, int>> cand;
-            for (int t : others) {
-                if (nseg == 1 && t < C) continue;
-                const int q = fl[tphys[t]];
-                cand.push_back({(long long)next_target_use(gates, remaining, q), t});
-            }
-            std::sort(cand.begin(), cand.end());
-            if (nseg == 1) {
-                for (int t = 0; t < C; t++) lanes.push_back(t);
-            } else {
-                const int no = (int)cand.size();
-                std::vector<int> best_pick;
-                int best = -1;
-                for (int m = 0; m < (1 << no); m++) {
-                    if (__builtin_popcount(m) != C) continue;
-                    int lqc[LANE_BITS], c = 0;
-                    std::vector<int> pick;
-                    for (int i = 0; i < no; i++)
-                        if ((m >> i) & 1) { lqc[c++] = fl[tphys[cand[i].second]]; pick.push_back(i); }
-                    const int sc = simulate_next_stage(gates, remaining, fpos, n_loc, k, lqc, C, cfg.max_ops - 1);
-                    if (sc > best) { best = sc; best_pick = pick; }
-                }
-                for (int i : best_pick) lanes.push_back(cand[i].second);
-                std::vector<std::pair<long long, int>> rest_c;
-                for (size_t i = 0; i < cand.size(); i++)
-                    if (!std::count(best_pick.begin(), best_pick.end(), (int)i)) rest_c.push_back(cand[i]);
-                cand = rest_c;
-            }
-            for (size_t i = 0; (int)lanes.size() < LANE_BITS && i < cand.size(); i++) lanes.push_back(cand[i].second);
-        } else if (s == 0) {
-            for (int t = 0; t < C; t++) lanes.push_back(t);
-            for (int t : others) if ((int)lanes.size() < LANE_BITS && t >= C) lanes.push_back(t);
-        } else {
-            for (int i = 0; i < LANE_BITS; i++) lanes.push_back(others[i]);
+        regs_of[s] = regs;
+    }
+    auto others_of = [&](int s) {
+        std::vector<int> o;
+        for (int t = 0; t < k; t++) if (!std::count(regs_of[s].begin(), regs_of[s].end(), t)) o.push_back(t);
+        return o;
+    };
+    // lanes 0..C-1 hold the pinned low bits at load (layout 0) and the bits that
+    // land on physical 0..C-1 at store (last layout): choose the latter so that the
+    // NEXT stage places the most gates (dry run over all C-subsets of the free bits);
+    // with one segment the pinned bits stay put
+    std::vector<int> last_pin, last_pref;  // pinned lanes of the last layout, then preferred order
+    {
+        const int s = nseg - 1;
+        std::vector<std::pair<long long, int>> cand;
+        for (int t : others_of(s)) {
+            if (nseg == 1 && t < C) continue;
+            const int q = fl[tphys[t]];
+            cand.push_back({(long long)next_target_use(gates, remaining, q), t});
         }
-        std::vector<int> warps;
-        for (int t : others) if (!std::count(lanes.begin(), lanes.end(), t)) warps.push_back(t);
+        std::sort(cand.begin(), cand.end());
+        if (nseg == 1) {
+            for (int t = 0; t < C; t++) last_pin.push_back(t);
+        } else {
+            const int no = (int)cand.size();
+            std::vector<int> best_pick;
+            int best = -1;
+            for (int m = 0; m < (1 << no); m++) {
+                if (__builtin_popcount(m) != C) continue;
+                int lqc[LANE_BITS], c = 0;
+                std::vector<int> pick;
+                for (int i = 0; i < no; i++)
+                    if ((m >> i) & 1) { lqc[c++] = fl[tphys[cand[i].second]]; pick.push_back(i); }
+                const int sc = simulate_next_stage(gates, remaining, fpos, n_loc, k, lqc, C, cfg.max_ops - 1);
+                if (sc > best) { best = sc; best_pick = pick; }
+            }
+            for (int i : best_pick) last_pin.push_back(cand[i].second);
+            for (size_t i = 0; i < cand.size(); i++)
+                if (!std::count(best_pick.begin(), best_pick.end(), (int)i)) last_pref.push_back(cand[i].second);
+        }
+    }
+    // Warp bits per layout, chosen so that as many layout changes as possible keep
+    // the SAME warp bits: such an exchange moves data only inside each warp
+    // (__syncwarp instead of a CTA barrier).  Exchange s is
+    // warp-local iff W_s == W_{s+1} and no permutation gate of segment s targets a
+    // warp bit (its map then preserves the warp bits).  Dynamic programme over the
+    // layouts; candidates = W-subsets of the non-register, non-pinned bits.
+    std::vector<uint32_t> perm_tgt(nseg, 0);
+    for (int oi : order)
+        if (is_perm(oi) && seg_of[oi] >= 0 && tile_of[items[oi].op.tp0] >= 0)
+            perm_tgt[seg_of[oi]] |= 1u << tile_of[items[oi].op.tp0];
+    std::vector<std::vector<uint32_t>> wc(nseg);
+    for (int s = 0; s < nseg; s++) {
+        uint32_t avail = 0;
+        for (int t : others_of(s)) avail |= 1u << t;
+        if (s == 0) avail &= ~((1u << C) - 1);
+        if (s == nseg - 1) for (int t : last_pin) avail &= ~(1u << t);
+        for (uint32_t m = 0; m < (1u << k); m++)
+            if ((m & ~avail) == 0 && __builtin_popcount(m) == W) wc[s].push_back(m);
+        if (wc[s].empty()) wc[s].push_back(0);  // unreachable for W <= k - R - 5
+    }
+    std::vector<std::vector<int>> cost(nseg), from(nseg);
+    for (int s = 0; s < nseg; s++) {
+        cost[s].assign(wc[s].size(), 0);
+        from[s].assign(wc[s].size(), 0);
+        if (s == 0) continue;
+        for (size_t b = 0; b < wc[s].size(); b++) {
+            int bc = 1 << 30, bf = 0;
+            for (size_t a = 0; a < wc[s - 1].size(); a++) {
+                const bool local = wc[s - 1][a] == wc[s][b] && !(perm_tgt[s - 1] & wc[s][b]);
+                const int c = cost[s - 1][a] + (local ? 0 : 1);
+                if (c < bc) { bc = c; bf = (int)a; }
+            }
+            cost[s][b] = bc;
+            from[s][b] = bf;
+        }
+    }
+    std::vector<uint32_t> wsel(nseg, 0);
+    {
+        int b = 0;
+        for (size_t i = 1; i < cost[nseg - 1].size(); i++)
+            if (cost[nseg - 1][i] < cost[nseg - 1][b]) b = (int)i;
+        for (int s = nseg - 1; s >= 0; s--) {
+            wsel[s] = wc[s][b];
+            b = from[s][b];
+        }
+    }
+    for (int s = 0; s < nseg; s++) {
+        const std::vector<int> &regs = regs_of[s];
+        std::vector<int> warps, lanes;
+        for (int t = 0; t < k; t++) if ((wsel[s] >> t) & 1) warps.push_back(t);
+        if (s == 0) for (int t = 0; t < C; t++) lanes.push_back(t);
+        if (s == nseg - 1 && s != 0) lanes = last_pin;
+        if (s == nseg - 1 && s != 0)
+            for (int t : last_pref)
+                if ((int)lanes.size() < LANE_BITS && !((wsel[s] >> t) & 1)) lanes.push_back(t);
+        for (int t : others_of(s))
+            if ((int)lanes.size() < LANE_BITS && !((wsel[s] >> t) & 1) && !std::count(lanes.begin(), lanes.end(), t))
+                lanes.push_back(t);
         Layout &L = sp.lays[s];
         for (int i = 0; i < R; i++) L.reg[i] = regs[i];
         for (int i = 0; i < LANE_BITS; i++) L.lane[i] = lanes[i];
         for (int i = 0; i < WMAX; i++) L.warp[i] = i < W ? warps[i] : 0;
     }
+    sp.xwarp.assign(nseg, 0);
+    for (int s = 0; s + 1 < nseg; s++)
+        sp.xwarp[s] = (wsel[s] == wsel[s + 1] && !(perm_tgt[s] & wsel[s])) ? 1 : 0;
     // output permutation sigma: last layout's lanes land on physical 0..4
     sp.st_phys.assign(k, -1);
     {
@@ -898,6 +956,10 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     const int nseg = (int)sp.lays.size();
     const int R = sp.R;
     ds.k = sp.k; ds.R = sp.R; ds.W = sp.W; ds.nseg = nseg;
+    {
+        static const char *fe = getenv("TQD_EXPERIMENT_FLAGS");  // timing experiments only
+        ds.flags = fe ? atoi(fe) : 0;
+    }
     ds.n_tiles = (int64_t)1 << (n_loc - sp.k);
     std::vector<int> sorted = sp.ld_phys;
     std::sort(sorted.begin(), sorted.end());
@@ -1149,6 +1211,30 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
     ds.n_ops = (int)ops.size() - ds.op_base;
     ds.n_slots = nslots;
+    // exchange synchronisation (kernel order): warp-local exchanges need only
+    // __syncwarp; the sync after an exchange's reads protects the next exchange's
+    // writes, so it may be warp-level iff that next exchange is warp-local with the
+    // same warp bits (for the tile's last exchange: exchange 0 of the next tile)
+    {
+        auto wset = [&](int fs) {
+            uint32_t m = 0;
+            for (int i = 0; i < sp.W; i++) m |= 1u << sp.lays[fs].warp[i];
+            return m;
+        };
+        auto xw = [&](int x) {  // kernel exchange x warp-local?
+            const int f = bwd ? nseg - 2 - x : x;
+            return f >= 0 && f < (int)sp.xwarp.size() && sp.xwarp[f];
+        };
+        for (int x = 0; x + 1 < nseg; x++) {
+            uint8_t v = xw(x) ? 1 : 0;
+            bool tail;
+            if (x + 2 < nseg) tail = xw(x + 1);
+            else tail = xw(0) && wset(0) == wset(nseg - 1);
+            if (tail) v |= 2;
+            if (ds.flags & 1) v = 0;  // experiment: CTA barriers everywhere
+            ds.xsync[x] = v;
+        }
+    }
     // layout changes: forward exchange s applies the map of forward segment s on
     // the write side; the adjoint (exchange from forward layout f+1 to f) applies
     // it on the read side (amp_pre[x] = amp_post[A x + b])
@@ -1235,6 +1321,8 @@ std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg
             for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.st_phys[t];
             os << "],\"swz\":[";
             for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.swz[t];
+            os << "],\"xwarp\":[";
+            for (size_t s = 0; s < sp.xwarp.size(); s++) os << (s ? "," : "") << (int)sp.xwarp[s];
             os << "],\"layouts\":[";
             for (size_t s = 0; s < sp.lays.size(); s++) {
                 const Layout &L = sp.lays[s];

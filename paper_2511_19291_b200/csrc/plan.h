@@ -88,6 +88,7 @@ struct SweepPlan {
     std::vector<POp> ops;               // in execution order, seg ascending
     std::vector<uint32_t> swz;
     std::vector<TileMap> maps;          // per segment: permutation gates applied after its ops
+    std::vector<uint8_t> xwarp;         // per exchange s -> s+1: 1 = warp-local (same warp bits, map keeps them)
     int n_gates = 0;                    // gates applied (incl. relabels / identities)
     int n_arith = 0;                    // ops needing arithmetic (kernel launch needed if > 0 or maps)
 };

@@ -28,7 +28,8 @@
 
 namespace tqd {
 
-constexpr int SWEEP_R = 4;  // register bits: 16 amplitudes (x2 states in the adjoint) per thread
+constexpr int SWEEP_R = TQD_SWEEP_R;  // register bits: 2^R amplitudes (x2 states in the adjoint) per thread
+constexpr int SWEEP_THREADS = 32 << (12 - 5 - SWEEP_R);  // threads per CTA at k = 12
 constexpr int NR = 1 << SWEEP_R;
 constexpr int MAX_WARPS = 1 << WMAX;
 
@@ -131,6 +132,7 @@ __device__ __forceinline__ void layer_diag(C *t, const Real *m) {
 // controlled general 2x2 (rare: controlled MAT2), in place; runtime control
 template <int T, typename C, typename Real>
 __device__ __forceinline__ void op_cu(C *a, const Real *m, int cm, bool on) {
+    if constexpr (T >= SWEEP_R) return;
 #pragma unroll
     for (int r = 0; r < NR; r++) {
         if (r & (1 << T)) continue;
@@ -145,6 +147,7 @@ __device__ __forceinline__ void op_cu(C *a, const Real *m, int cm, bool on) {
 
 template <int T0, int T1, typename C, typename Real>
 __device__ __forceinline__ void op_u2(C *a, const Real *m) {
+    if constexpr (T0 >= SWEEP_R || T1 >= SWEEP_R) return;
 #pragma unroll
     for (int r = 0; r < NR; r++) {
         if (r & ((1 << T0) | (1 << T1))) continue;
@@ -182,6 +185,7 @@ __device__ __forceinline__ double2 cfma_elem(double2 x, double2 y, double2 z) {
 template <int T, typename C, typename Real>
 __device__ __forceinline__ Real grad_bit(const C *a, const C *l, int gk, const Real *g) {
     Real acc = 0;
+    if constexpr (T >= SWEEP_R) return acc;
     if (gk == GEN_Y) {  // G = -(i/2) Y = [[0, -1/2], [1/2, 0]]: Re(conj l1 a0) - Re(conj l0 a1)
         C pos = mk<C>(0, 0), neg = mk<C>(0, 0);
 #pragma unroll
@@ -243,6 +247,7 @@ __device__ __forceinline__ double2 pmul(double2 x, double2 y) { return make_doub
 // two packed accumulators (independent FFMA2 chains), one final add
 template <int T, typename C, typename Real>
 __device__ __forceinline__ Real grad_y(const C *a, const C *l) {
+    if constexpr (T >= SWEEP_R) return (Real)0;
     C acc[2] = {mk<C>(0, 0), mk<C>(0, 0)};
     int i = 0;
 #pragma unroll
@@ -262,7 +267,7 @@ __device__ __forceinline__ void grad_y_layer(const C *a, const C *l, uint32_t gm
     if constexpr ((MASK & 1) != 0) if (gm & 1) tt[soff[0]] += grad_y<0, C, Real>(a, l);
     if constexpr ((MASK & 2) != 0) if (gm & 2) tt[soff[1]] += grad_y<1, C, Real>(a, l);
     if constexpr ((MASK & 4) != 0) if (gm & 4) tt[soff[2]] += grad_y<2, C, Real>(a, l);
-    if constexpr ((MASK & 8) != 0) if (gm & 8) tt[soff[3]] += grad_y<3, C, Real>(a, l);
+    if constexpr ((MASK & 8) != 0 && SWEEP_R > 3) if (gm & 8) tt[soff[3]] += grad_y<3, C, Real>(a, l);
 }
 
 // RZ generators G = -(i/2) Z on the register bits of a diagonal layer:
@@ -271,23 +276,22 @@ __device__ __forceinline__ void grad_y_layer(const C *a, const C *l, uint32_t gm
 // butterfly (differences at each level, sums carried up)
 template <typename C, typename Real>
 __device__ __forceinline__ void grad_z_layer(const C *a, const C *l, uint32_t gm, const uint16_t *soff, Real *tt) {
-    C p[NR];
+    C cur[NR];
 #pragma unroll
-    for (int r = 0; r < NR; r++) p[r] = pmul(l[r], pswap(a[r]));
-    C P[NR / 2], m[NR / 2];
+    for (int r = 0; r < NR; r++) cur[r] = pmul(l[r], pswap(a[r]));
 #pragma unroll
-    for (int j = 0; j < NR / 2; j++) { P[j] = padd(p[2 * j], p[2 * j + 1]); m[j] = psub(p[2 * j], p[2 * j + 1]); }
-    const C d0 = padd(padd(padd(m[0], m[1]), padd(m[2], m[3])), padd(padd(m[4], m[5]), padd(m[6], m[7])));
-    C Q[NR / 4], n[NR / 4];
+    for (int b = 0; b < SWEEP_R; b++) {
+        // level b: pairs differ in original bit b; differences summed, sums carried up
+        const int half = NR >> (b + 1);
+        C d = psub(cur[0], cur[1]);
+        cur[0] = padd(cur[0], cur[1]);
 #pragma unroll
-    for (int j = 0; j < NR / 4; j++) { Q[j] = padd(P[2 * j], P[2 * j + 1]); n[j] = psub(P[2 * j], P[2 * j + 1]); }
-    const C d1 = padd(padd(n[0], n[1]), padd(n[2], n[3]));
-    const C d2 = padd(psub(Q[0], Q[1]), psub(Q[2], Q[3]));
-    const C d3 = psub(padd(Q[0], Q[1]), padd(Q[2], Q[3]));
-    if (gm & 1) tt[soff[0]] += d0.x - d0.y;
-    if (gm & 2) tt[soff[1]] += d1.x - d1.y;
-    if (gm & 4) tt[soff[2]] += d2.x - d2.y;
-    if (gm & 8) tt[soff[3]] += d3.x - d3.y;
+        for (int j = 1; j < half; j++) {
+            d = padd(d, psub(cur[2 * j], cur[2 * j + 1]));
+            cur[j] = padd(cur[2 * j], cur[2 * j + 1]);
+        }
+        if ((gm >> b) & 1) tt[soff[b]] += d.x - d.y;
+    }
 }
 
 // ---- one op, in place on psi (and lambda in the adjoint) ----------------------
@@ -400,7 +404,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
 
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
 template <typename Real, bool BWD>
-__global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
+__global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (SWEEP_R == 3 ? 2 : (BWD ? 2 : 3)) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
@@ -583,7 +587,8 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
                         if (BWD) *reinterpret_cast<C *>(reinterpret_cast<char *>(sm_l) + o[r]) = l[r];
                     }
                 }
-                __syncthreads();
+                if (S.xsync[x] & 1) __syncwarp();  // warp-local layout change
+                else __syncthreads();
                 {
                     uint32_t c[SWEEP_R], o[NR];
 #pragma unroll
@@ -597,7 +602,8 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 ? (BWD ? 2 : 3) : 1) sw
                         if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_l) + o[r]);
                     }
                 }
-                __syncthreads();
+                if (S.xsync[x] & 2) __syncwarp();  // the next exchange only touches this warp's region
+                else __syncthreads();
             }
             const uint32_t tix = s_tix[s * blockDim.x + threadIdx.x];
             const int e = S.seg_begin[s + 1];

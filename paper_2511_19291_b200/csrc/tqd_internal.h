@@ -25,7 +25,10 @@ namespace tqd {
 
 constexpr int KMAX = 16;    // max tile bits
 constexpr int RMAX = 5;     // max register bits
-constexpr int WMAX = 3;     // max warp bits (8 warps = 256 threads)
+constexpr int WMAX = 4;     // max warp bits (16 warps = 512 threads)
+#ifndef TQD_SWEEP_R
+#define TQD_SWEEP_R 4  // register bits per thread in the sweep kernels (experiment knob)
+#endif
 constexpr int LANE_BITS = 5;
 constexpr int MAXSEG = 8;   // layouts per sweep stage
 constexpr int NAFF = 8;     // base-controlled affine terms per exchange
@@ -138,7 +141,7 @@ struct DevLayout {
     uint8_t reg[RMAX];
     uint8_t lane[LANE_BITS];
     uint8_t warp[WMAX];
-    uint8_t pad[2];
+    uint8_t pad[1];
 };
 
 struct DevStage {
@@ -158,13 +161,18 @@ struct DevStage {
     uint8_t aff_read[MAXSEG];   // 1: affine terms apply to the read side
     uint8_t aff_pos[MAXSEG][NAFF];
     uint32_t aff_vec[MAXSEG][NAFF];
+    uint8_t xsync[MAXSEG];      // exchange x: bit 0 = warp-local (__syncwarp between write and read),
+                                // bit 1 = the sync after its reads may be __syncwarp (next exchange warp-local)
     int32_t seg_begin[MAXSEG + 1];
     DevLayout lay[MAXSEG];
     int32_t op_base, n_ops;     // into the launch's DevOp array
     int32_t slot_base, n_slots; // into the launch's slot -> parameter table
     int32_t lam_init;           // backward only: 1 = build lambda = H psi on load
-    int32_t pad;
+    int32_t flags;              // kernel variant bits (SWF_*)
 };
+
+// sweep-kernel variant bits (DevStage::flags)
+enum : int32_t { SWF_NONE = 0 };  // 4: timing only (wrong results)
 
 // Z-string observable in PHYSICAL masks (full index incl. rank bits)
 // lambda-init form: h(b) = cst - 2 sum_p w[p] bit_p(b) + sum_t c_t (-1)^{popc(b & z_t)}

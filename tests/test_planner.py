@@ -94,6 +94,14 @@ def check_invariants(plan):
         assert [stp[t] for t in last[:C]] == list(range(C))
         segs = [op["seg"] for op in st["ops"]]
         assert segs == sorted(segs)
+        # warp-local exchanges: same warp bits on both sides and no
+        # permutation gate of the segment targets a warp bit
+        for s, xw in enumerate(st["xwarp"][: len(lays) - 1]):
+            if xw:
+                assert lays[s]["warp"] == lays[s + 1]["warp"]
+                for op in st["ops"]:
+                    if op["perm"] and op["seg"] == s:
+                        assert ld.index(op["tp0"]) not in lays[s]["warp"]
         for op in st["ops"]:
             if op["perm"]:  # CNOT / X folded into a layout-change map: target only needs to be in the tile
                 assert op["tp0"] in ld
