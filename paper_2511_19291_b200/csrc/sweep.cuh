@@ -29,7 +29,16 @@
 namespace tqd {
 
 constexpr int SWEEP_R = TQD_SWEEP_R;  // register bits: 2^R amplitudes (x2 states in the adjoint) per thread
-constexpr int SWEEP_THREADS = 32 << (12 - 5 - SWEEP_R);  // threads per CTA at k = 12
+#ifndef TQD_LB_THREADS
+#define TQD_LB_THREADS (32 << (12 - 5 - SWEEP_R))  // threads per CTA at k = 12
+#endif
+#ifndef TQD_LB_MINB_F32_BWD
+#define TQD_LB_MINB_F32_BWD 2
+#endif
+#ifndef TQD_LB_MINB_F32_FWD
+#define TQD_LB_MINB_F32_FWD (SWEEP_R == 3 ? 2 : 3)
+#endif
+constexpr int SWEEP_THREADS = TQD_LB_THREADS;
 constexpr int NR = 1 << SWEEP_R;
 constexpr int MAX_WARPS = 1 << WMAX;
 
@@ -404,7 +413,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
 
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
 template <typename Real, bool BWD>
-__global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (SWEEP_R == 3 ? 2 : (BWD ? 2 : 3)) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
+__global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_LB_MINB_F32_BWD : TQD_LB_MINB_F32_FWD) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
