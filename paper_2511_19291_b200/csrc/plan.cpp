@@ -681,8 +681,10 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         for (size_t b = 0; b < wc[s].size(); b++) {
             int bc = 1 << 30, bf = 0;
             for (size_t a = 0; a < wc[s - 1].size(); a++) {
-                const bool local = wc[s - 1][a] == wc[s][b] && !(perm_tgt[s - 1] & wc[s][b]);
-                const int c = cost[s - 1][a] + (local ? 0 : 1);
+                // warp bits kept by the layout change (and by its permutation map):
+                // the exchange then splits into independent groups of 2^(W - kept) warps
+                const int kept = __builtin_popcount(wc[s - 1][a] & wc[s][b] & ~perm_tgt[s - 1]);
+                const int c = cost[s - 1][a] + (W - kept);
                 if (c < bc) { bc = c; bf = (int)a; }
             }
             cost[s][b] = bc;
@@ -699,10 +701,23 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
             b = from[s][b];
         }
     }
+    std::vector<int> prev_warps;
     for (int s = 0; s < nseg; s++) {
         const std::vector<int> &regs = regs_of[s];
         std::vector<int> warps, lanes;
-        for (int t = 0; t < k; t++) if ((wsel[s] >> t) & 1) warps.push_back(t);
+        // warp order: bits shared with the previous layout keep their warp-index position
+        if (s == 0) {
+            for (int t = 0; t < k; t++) if ((wsel[s] >> t) & 1) warps.push_back(t);
+        } else {
+            warps.assign(W, -1);
+            for (int i = 0; i < W; i++)
+                if ((wsel[s] >> prev_warps[i]) & 1) warps[i] = prev_warps[i];
+            for (int t = 0; t < k; t++) {
+                if (!((wsel[s] >> t) & 1) || std::count(warps.begin(), warps.end(), t)) continue;
+                for (int i = 0; i < W; i++) if (warps[i] < 0) { warps[i] = t; break; }
+            }
+        }
+        prev_warps = warps;
         if (s == 0) for (int t = 0; t < C; t++) lanes.push_back(t);
         if (s == nseg - 1 && s != 0) lanes = last_pin;
         if (s == nseg - 1 && s != 0)
@@ -716,9 +731,18 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         for (int i = 0; i < LANE_BITS; i++) L.lane[i] = lanes[i];
         for (int i = 0; i < WMAX; i++) L.warp[i] = i < W ? warps[i] : 0;
     }
+    // per exchange: warp-index bits kept (same tile bit at the same warp position,
+    // not a permutation target of the segment) -> independent warp groups
+    sp.perm_tgt = perm_tgt;
+    sp.xumask.assign(nseg, 0);
     sp.xwarp.assign(nseg, 0);
-    for (int s = 0; s + 1 < nseg; s++)
-        sp.xwarp[s] = (wsel[s] == wsel[s + 1] && !(perm_tgt[s] & wsel[s])) ? 1 : 0;
+    for (int s = 0; s + 1 < nseg; s++) {
+        uint8_t um = 0;
+        for (int i = 0; i < W; i++)
+            if (sp.lays[s].warp[i] == sp.lays[s + 1].warp[i] && !((perm_tgt[s] >> sp.lays[s].warp[i]) & 1)) um |= 1 << i;
+        sp.xumask[s] = um;
+        sp.xwarp[s] = um == (1 << W) - 1 ? 1 : 0;
+    }
     // output permutation sigma: last layout's lanes land on physical 0..4
     sp.st_phys.assign(k, -1);
     {
@@ -1211,28 +1235,36 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
     ds.n_ops = (int)ops.size() - ds.op_base;
     ds.n_slots = nslots;
-    // exchange synchronisation (kernel order): warp-local exchanges need only
-    // __syncwarp; the sync after an exchange's reads protects the next exchange's
-    // writes, so it may be warp-level iff that next exchange is warp-local with the
-    // same warp bits (for the tile's last exchange: exchange 0 of the next tile)
+    // exchange synchronisation (kernel order x; fwd segment f = x, adjoint f = nseg-2-x).
+    // Write -> read: warps that keep their warp-index bits U_x only exchange among the
+    // group of warps sharing those bits (named barrier per group; U = all -> __syncwarp).
+    // Read -> next write: a warp's next writes land in the region it just read iff the
+    // map that relates them keeps the warp bits of the layout in between (forward: the
+    // next exchange's map, applied on its write side; adjoint: this exchange's map,
+    // applied on its read side); then __syncwarp suffices.  The tile's last exchange
+    // always ends with a CTA barrier (the next tile restarts at layout 0).
     {
         auto wset = [&](int fs) {
             uint32_t m = 0;
             for (int i = 0; i < sp.W; i++) m |= 1u << sp.lays[fs].warp[i];
             return m;
         };
-        auto xw = [&](int x) {  // kernel exchange x warp-local?
-            const int f = bwd ? nseg - 2 - x : x;
-            return f >= 0 && f < (int)sp.xwarp.size() && sp.xwarp[f];
-        };
         for (int x = 0; x + 1 < nseg; x++) {
-            uint8_t v = xw(x) ? 1 : 0;
-            bool tail;
-            if (x + 2 < nseg) tail = xw(x + 1);
-            else tail = xw(0) && wset(0) == wset(nseg - 1);
-            if (tail) v |= 2;
-            if (ds.flags & 1) v = 0;  // experiment: CTA barriers everywhere
-            ds.xsync[x] = v;
+            const int f = bwd ? nseg - 2 - x : x;
+            uint8_t v = (uint8_t)(sp.xumask[f] & 0x0f);
+            bool tail = false;
+            if (x + 2 < nseg) {
+                if (!bwd) tail = !(sp.perm_tgt[x + 1] & wset(x + 1));
+                else tail = !(sp.perm_tgt[f] & wset(f));  // kernel layout x+1 = fwd layout f
+                // a group barrier (named barrier per warp group) must not be entered
+                // while other warps still wait in this exchange's group barriers: keep
+                // the CTA barrier before a partially-kept exchange
+                const int fn = bwd ? f - 1 : x + 1;
+                const uint8_t un = sp.xumask[fn];
+                if (un != 0 && un != (1 << sp.W) - 1) tail = false;
+            }
+            if (ds.flags & 1) { v = 0; tail = false; }  // experiment: CTA barriers everywhere
+            ds.xsync[x] = v | (tail ? 0x80 : 0);
         }
     }
     // layout changes: forward exchange s applies the map of forward segment s on
@@ -1323,6 +1355,8 @@ std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg
             for (int t = 0; t < sp.k; t++) os << (t ? "," : "") << sp.swz[t];
             os << "],\"xwarp\":[";
             for (size_t s = 0; s < sp.xwarp.size(); s++) os << (s ? "," : "") << (int)sp.xwarp[s];
+            os << "],\"xumask\":[";
+            for (size_t s = 0; s < sp.xumask.size(); s++) os << (s ? "," : "") << (int)sp.xumask[s];
             os << "],\"layouts\":[";
             for (size_t s = 0; s < sp.lays.size(); s++) {
                 const Layout &L = sp.lays[s];

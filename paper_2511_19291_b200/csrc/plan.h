@@ -89,6 +89,8 @@ struct SweepPlan {
     std::vector<uint32_t> swz;
     std::vector<TileMap> maps;          // per segment: permutation gates applied after its ops
     std::vector<uint8_t> xwarp;         // per exchange s -> s+1: 1 = warp-local (same warp bits, map keeps them)
+    std::vector<uint8_t> xumask;        // per exchange: warp-index bits kept (groups of 2^(W - popc) warps)
+    std::vector<uint32_t> perm_tgt;     // per segment: tile bits targeted by its permutation gates
     int n_gates = 0;                    // gates applied (incl. relabels / identities)
     int n_arith = 0;                    // ops needing arithmetic (kernel launch needed if > 0 or maps)
 };

@@ -596,8 +596,18 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                         if (BWD) *reinterpret_cast<C *>(reinterpret_cast<char *>(sm_l) + o[r]) = l[r];
                     }
                 }
-                if (S.xsync[x] & 1) __syncwarp();  // warp-local layout change
-                else __syncthreads();
+                {
+                    // write -> read: only the warps sharing the kept warp-index bits exchange data
+                    const uint32_t um = S.xsync[x] & 0x0fu, full = (1u << W) - 1u;
+                    if (um == full) {
+                        __syncwarp();
+                    } else if (um == 0) {
+                        __syncthreads();
+                    } else {
+                        const uint32_t nthr = 32u << (W - __popc(um));
+                        asm volatile("bar.sync %0, %1;" ::"r"(1u + ((uint32_t)warp & um)), "r"(nthr) : "memory");
+                    }
+                }
                 {
                     uint32_t c[SWEEP_R], o[NR];
 #pragma unroll
@@ -611,7 +621,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                         if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_l) + o[r]);
                     }
                 }
-                if (S.xsync[x] & 2) __syncwarp();  // the next exchange only touches this warp's region
+                if (S.xsync[x] & 0x80) __syncwarp();  // the next writes stay in this warp's region
                 else __syncthreads();
             }
             const uint32_t tix = s_tix[s * blockDim.x + threadIdx.x];

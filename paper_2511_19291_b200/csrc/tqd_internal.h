@@ -161,8 +161,8 @@ struct DevStage {
     uint8_t aff_read[MAXSEG];   // 1: affine terms apply to the read side
     uint8_t aff_pos[MAXSEG][NAFF];
     uint32_t aff_vec[MAXSEG][NAFF];
-    uint8_t xsync[MAXSEG];      // exchange x: bit 0 = warp-local (__syncwarp between write and read),
-                                // bit 1 = the sync after its reads may be __syncwarp (next exchange warp-local)
+    uint8_t xsync[MAXSEG];      // exchange x: bits 0..3 = warp-index bits kept (write -> read sync only
+                                // among warps sharing them), bit 7 = the sync after its reads may be __syncwarp
     int32_t seg_begin[MAXSEG + 1];
     DevLayout lay[MAXSEG];
     int32_t op_base, n_ops;     // into the launch's DevOp array

@@ -96,12 +96,16 @@ def check_invariants(plan):
         assert segs == sorted(segs)
         # warp-local exchanges: same warp bits on both sides and no
         # permutation gate of the segment targets a warp bit
-        for s, xw in enumerate(st["xwarp"][: len(lays) - 1]):
-            if xw:
-                assert lays[s]["warp"] == lays[s + 1]["warp"]
-                for op in st["ops"]:
-                    if op["perm"] and op["seg"] == s:
-                        assert ld.index(op["tp0"]) not in lays[s]["warp"]
+        for s, um in enumerate(st["xumask"][: len(lays) - 1]):
+            # warp groups: a kept warp-index bit is the same tile bit on both sides and
+            # no permutation gate of the segment targets it
+            for i in range(st["W"]):
+                if (um >> i) & 1:
+                    assert lays[s]["warp"][i] == lays[s + 1]["warp"][i]
+                    for op in st["ops"]:
+                        if op["perm"] and op["seg"] == s:
+                            assert ld.index(op["tp0"]) != lays[s]["warp"][i]
+            assert st["xwarp"][s] == (1 if um == (1 << st["W"]) - 1 else 0)
         for op in st["ops"]:
             if op["perm"]:  # CNOT / X folded into a layout-change map: target only needs to be in the tile
                 assert op["tp0"] in ld
