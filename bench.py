@@ -43,7 +43,7 @@ METRIC = "circuit fwd+grad time and gate-sweep HBM GB/s at 30/33/36 qubits, 1-8 
 UNIT = "Gamp-gates/s (fwd+grad)"
 DEPTH = 20
 BASE_QUBITS = 30
-CPU_SAMPLE_QUBITS = 21   # oracle sample width for cpu_baseline (same ansatz, full circuit)
+CPU_SAMPLE_QUBITS = 22   # oracle sample width for cpu_baseline (same ansatz, full circuit; ~12 s on 16 cores)
 REF_SAMPLE_QUBITS = 19   # oracle width per --impl reference step
 
 
