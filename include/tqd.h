@@ -90,7 +90,10 @@ typedef enum {
     TQD_OPT_SMALL_MAX = 1,    /* n_loc <= this runs the single-CTA whole-state kernel (default 10) */
     TQD_OPT_PROFILE = 2,      /* 1: time every kernel with CUDA events (see tqd_metrics) */
     TQD_OPT_GRID_CTAS = 3,    /* persistent CTAs per launch (0 = auto: SMs x resident CTAs) */
-    TQD_OPT_USE_GRAPH = 4     /* 1: replay cached plans as CUDA graphs (default 0)      */
+    TQD_OPT_USE_GRAPH = 4,    /* 1: replay cached plans as CUDA graphs (default 0)      */
+    TQD_OPT_FUSED_REMAP = 5   /* 1: a remap right after a sweep is fused into it: the sweep
+                               * stores straight into the owners' peer memory (default 1);
+                               * 0: pack -> all-to-all -> unpack                          */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.
@@ -114,6 +117,7 @@ typedef struct tqd_metrics {
     uint64_t kernel_launches;   /* library kernels launched                          */
     uint64_t h2d_bytes;         /* host->device bytes (plan descriptors, masks)      */
     uint64_t d2h_bytes;         /* device->host bytes (values, gradients, amplitudes) */
+    uint64_t fused_remaps;      /* remaps done by the preceding sweep's peer-memory stores */
 } tqd_metrics;
 
 /* --- context ------------------------------------------------------------- */

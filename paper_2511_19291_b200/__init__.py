@@ -28,7 +28,7 @@ GATES = {
     "RX": 14, "RY": 15, "RZ": 16, "U3": 17,
 }
 C64, C128 = 0, 1
-OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH = 0, 1, 2, 3, 4
+OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP = 0, 1, 2, 3, 4, 5
 ERRORS = {0: "TQD_OK", -1: "TQD_ERR_ARG", -2: "TQD_ERR_QUBITS", -3: "TQD_ERR_WORLD",
           -4: "TQD_ERR_NOT_UNITARY", -5: "TQD_ERR_OOM", -6: "TQD_ERR_CUDA", -7: "TQD_ERR_NCCL",
           -8: "TQD_ERR_UNSUPPORTED", -9: "TQD_ERR_STATE"}
@@ -49,7 +49,7 @@ class Metrics(ctypes.Structure):
         ("other_ms", ctypes.c_double), ("a2a_ms", ctypes.c_double),
         ("fwd_sweep_bytes", ctypes.c_uint64), ("bwd_sweep_bytes", ctypes.c_uint64),
         ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-        ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64),
+        ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("fused_remaps", ctypes.c_uint64),
     ]
 
     def as_dict(self):

@@ -19,8 +19,8 @@
 namespace tqd {
 // kernels.cu
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
-                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots,
-                         int nseg, int grid, cudaStream_t s);
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W,
+                         int n_ops, int n_slots, int nseg, int grid, cudaStream_t s);
 int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
                          uint64_t rank_hi, cudaStream_t s);
@@ -76,7 +76,11 @@ struct tqd_state {
     std::vector<int> pos;
     bool consumed = false;
     // options
-    int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0;
+    int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1;
+    // fused sweep -> remap (peer memory): every rank's psi / recv and lambda / send
+    // allocations, shared once; the current roles are looked up by pointer identity
+    std::vector<void *> peer_psi, peer_lam;  // [rank * 2 + i], i = 0: first psi / lam, 1: recv / send
+    void *psi_first = nullptr, *recv_first = nullptr, *lam_first = nullptr, *send_first = nullptr;
     tqd_metrics met;
     double *d_red = nullptr;  // reductions: values / grads
     uint64_t *d_xy = nullptr;  // X/Y adjoint-seed term scratch: z masks, coefficients, #Y
@@ -222,6 +226,8 @@ static int ensure_xchg(tqd_state *st) {
         return fail(TQD_ERR_OOM, "cannot allocate remap staging buffers");
     }
     st->own_xchg = true;
+    st->send_first = st->sendb;
+    st->recv_first = st->recvb;
     st->met.peak_device_bytes += 2 * b;
     return TQD_OK;
 }
@@ -243,6 +249,7 @@ static int ensure_lambda(tqd_state *st) {
         return fail(TQD_ERR_OOM, "cannot allocate the adjoint state lambda");
     }
     st->own_lam = true;
+    st->lam_first = st->lam;
     st->met.peak_device_bytes += b;
     return TQD_OK;
 }
@@ -336,6 +343,27 @@ struct Encoded {
 static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E);
 
 // Launch an encoded stage list (forward or backward) on the context stream.
+// The remap right after a sweep is fused into it: the sweep stores every amplitude
+// straight into its post-remap owner's receive buffer (peer memory over NVLink; the
+// loopback world: the same device), then one barrier and a pointer swap replace the
+// pack -> all-to-all -> unpack of exec_remap.
+static bool fusable_remap(const tqd_state *st, bool bwd) {
+    return st->opt_fused && st->ctx->world > 1 && st->ctx->world <= SCATTER_MAX_RANKS && st->own_psi &&
+           (!bwd || st->own_lam);
+}
+
+static int share_pair(tqd_state *st, void *a, void *b, std::vector<void *> &table) {
+    if (!table.empty()) return TQD_OK;
+    void *loc[2] = {a, b};
+    COMM_TRY(st, st->ctx->comm->share_buffers(loc, 2, table, st->ctx->stream));
+    return TQD_OK;
+}
+
+static uint64_t peer_of(const tqd_state *st, const std::vector<void *> &table, void *first, void *cur, int r) {
+    // the role of a buffer is symmetric over the ranks: same slot on every rank
+    return (uint64_t)table[r * 2 + (cur == first ? 0 : 1)];
+}
+
 static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool bwd, const Encoded &E, double *d_grad) {
     tqd_ctx *c = st->ctx;
     const DevStage *d_st = (const DevStage *)E.dev;
@@ -343,14 +371,47 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
     const char *d_kops = (const char *)E.dev + E.off_kops;
     const int32_t *d_sl = (const int32_t *)((char *)E.dev + E.off_sl);
     const uint64_t sb = shard_bytes(st);
-    for (const Encoded::L &l : E.launches) {
+    for (size_t li = 0; li < E.launches.size(); li++) {
+        const Encoded::L &l = E.launches[li];
         const Stage &s = stages[l.stage];
         if (l.type == ST_SWEEP) {
             const SweepPlan &sp = s.sw;
+            ScatterInfo sc;
+            memset(&sc, 0, sizeof(sc));
+            const bool fuse = li + 1 < E.launches.size() && E.launches[li + 1].type == ST_REMAP && fusable_remap(st, bwd);
+            if (fuse) {
+                int rc = ensure_xchg(st);
+                if (rc) return rc;
+                rc = share_pair(st, st->psi_first, st->recv_first, st->peer_psi);
+                if (rc) return rc;
+                if (bwd) {
+                    rc = share_pair(st, st->lam_first, st->send_first, st->peer_lam);
+                    if (rc) return rc;
+                }
+                const RemapPlan &rp = stages[E.launches[li + 1].stage].rm;
+                sc.m = rp.m;
+                sc.n_loc = st->n_loc;
+                for (int i = 0; i < rp.m && i < 8; i++) { sc.gbit[i] = (uint8_t)rp.gpos[i]; sc.lbit[i] = (uint8_t)rp.lpos[i]; }
+                for (int r = 0; r < c->world; r++) {
+                    sc.dst_psi[r] = peer_of(st, st->peer_psi, st->psi_first, st->recvb, r);
+                    if (bwd) sc.dst_lam[r] = peer_of(st, st->peer_lam, st->lam_first, st->sendb, r);
+                }
+            }
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
-                                      sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(), l.grid, c->stream));
+                                      sc, sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(), l.grid, c->stream));
             ev_end(st, ev);
+            if (fuse) {
+                // every rank's stores into its peers' receive buffers are complete
+                COMM_TRY(st, c->comm->barrier(c->stream));
+                std::swap(st->psi, st->recvb);
+                if (bwd) std::swap(st->lam, st->sendb);
+                const uint64_t moved = sb - (sb >> sc.m);
+                st->met.a2a_bytes += bwd ? 2 * moved : moved;
+                st->met.remaps++;
+                st->met.fused_remaps++;
+                li++;  // the remap is done
+            }
             if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += sp.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
             st->met.kernel_launches++;
@@ -630,6 +691,7 @@ int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_by
             return fail(TQD_ERR_OOM, "cannot allocate the state shard");
         }
         st->own_psi = true;
+        st->psi_first = st->psi;
         st->met.peak_device_bytes = sb;
     }
     int rc = tqd_state_reset(st);
@@ -680,6 +742,10 @@ int tqd_state_rewind(tqd_state *st) {
 int tqd_state_free(tqd_state *st) {
     if (!st) return fail(TQD_ERR_ARG, "state is NULL");
     if (st->ctx && st->ctx->stream) cudaStreamSynchronize(st->ctx->stream);
+    if (st->ctx && st->ctx->comm) {
+        st->ctx->comm->release_buffers(st->peer_psi, 2);
+        st->ctx->comm->release_buffers(st->peer_lam, 2);
+    }
     if (st->own_psi) cudaFree(st->psi);
     if (st->own_lam) cudaFree(st->lam);
     if (st->own_xchg) { cudaFree(st->sendb); cudaFree(st->recvb); }
@@ -708,6 +774,7 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
         if (v < 0) return fail(TQD_ERR_ARG, "grid must be >= 0");
         st->opt_grid = (int)v; return TQD_OK;
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     default: return fail(TQD_ERR_ARG, "unknown option");
     }
 }

@@ -32,6 +32,7 @@ class NcclComm : public Comm {
   public:
     ncclComm_t c = nullptr;
     ~NcclComm() override {
+        if (flag) cudaFree(flag);
         if (c) ncclCommDestroy(c);
     }
     int check(ncclResult_t r, const char *what) {
@@ -51,6 +52,49 @@ class NcclComm : public Comm {
         return check(ncclAllReduce(buf, buf, count, t == CE_F64 ? ncclDouble : ncclFloat, ncclSum, c, s),
                      "ncclAllReduce");
     }
+    int cuda(cudaError_t e, const char *what) {
+        if (e == cudaSuccess) return 0;
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        return 1;
+    }
+    int share_buffers(void *const *local, int nbuf, std::vector<void *> &table, cudaStream_t s) override {
+        const size_t hs = sizeof(cudaIpcMemHandle_t);
+        std::vector<char> mine(nbuf * hs), all((size_t)world * nbuf * hs);
+        for (int i = 0; i < nbuf; i++)
+            if (cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + i * hs), local[i]), "cudaIpcGetMemHandle"))
+                return 1;
+        char *d = nullptr;
+        if (cuda(cudaMalloc(&d, all.size() + mine.size()), "cudaMalloc")) return 1;
+        int rc = cuda(cudaMemcpyAsync(d, mine.data(), mine.size(), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+        if (!rc) rc = check(ncclAllGather(d, d + mine.size(), mine.size(), ncclUint8, c, s), "ncclAllGather");
+        if (!rc) rc = cuda(cudaMemcpyAsync(all.data(), d + mine.size(), all.size(), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+        if (!rc) rc = cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        cudaFree(d);
+        if (rc) return rc;
+        table.assign((size_t)world * nbuf, nullptr);
+        for (int r = 0; r < world; r++)
+            for (int i = 0; i < nbuf; i++) {
+                if (r == rank) { table[r * nbuf + i] = local[i]; continue; }
+                cudaIpcMemHandle_t hdl;
+                memcpy(&hdl, all.data() + ((size_t)r * nbuf + i) * hs, hs);
+                if (cuda(cudaIpcOpenMemHandle(&table[r * nbuf + i], hdl, cudaIpcMemLazyEnablePeerAccess),
+                         "cudaIpcOpenMemHandle"))
+                    return 1;
+            }
+        return 0;
+    }
+    void release_buffers(std::vector<void *> &table, int nbuf) override {
+        for (int r = 0; r < world; r++)
+            for (int i = 0; i < nbuf && (size_t)(r * nbuf + i) < table.size(); i++)
+                if (r != rank && table[r * nbuf + i]) cudaIpcCloseMemHandle(table[r * nbuf + i]);
+        table.clear();
+    }
+    int barrier(cudaStream_t s) override {
+        if (!flag && cuda(cudaMalloc(&flag, sizeof(int)), "cudaMalloc")) return 1;
+        if (check(ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, c, s), "ncclAllReduce")) return 1;
+        return cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+    }
+    int *flag = nullptr;
 };
 
 // ---------------------------------------------------------------- loopback
@@ -67,6 +111,7 @@ struct Hub {
     };
     std::vector<std::vector<Post>> sends;  // per source rank, current group
     std::vector<void *> bufs;              // per rank, current reduction
+    std::vector<std::vector<void *>> shared;  // per rank, share_buffers
     // all ranks arrive; false on timeout (a rank died or diverged)
     bool barrier() {
         std::unique_lock<std::mutex> lk(mu);
@@ -88,7 +133,6 @@ class LoopComm : public Comm {
   public:
     Hub *hub = nullptr;
     uint64_t key = 0;
-    int world = 1, rank = 0;
     struct Req {
         void *ptr;
         size_t bytes;
@@ -158,6 +202,21 @@ class LoopComm : public Comm {
         // every rank finished reading its peers' send buffers
         return sync_all("group_end (copies)");
     }
+    int share_buffers(void *const *local, int nbuf, std::vector<void *> &table, cudaStream_t) override {
+        {
+            std::lock_guard<std::mutex> g(hub->mu);
+            hub->shared[rank].assign(local, local + nbuf);
+        }
+        if (sync_all("share_buffers (post)")) return 1;
+        table.assign((size_t)world * nbuf, nullptr);
+        for (int r = 0; r < world; r++)
+            for (int i = 0; i < nbuf; i++) table[r * nbuf + i] = hub->shared[r][i];
+        return sync_all("share_buffers (read)");
+    }
+    int barrier(cudaStream_t s) override {
+        if (cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize")) return 1;
+        return sync_all("barrier");
+    }
     int allreduce_sum(void *buf, size_t count, CommElem t, cudaStream_t s) override {
         if (cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize")) return 1;
         {
@@ -200,6 +259,7 @@ Comm *comm_create(const void *id128, int world, int rank, std::string &err) {
             h->world = world;
             h->sends.resize(world);
             h->bufs.resize(world, nullptr);
+            h->shared.resize(world);
         }
         if (h->world != world) {
             err = "loopback id reused with another world size";
@@ -211,6 +271,8 @@ Comm *comm_create(const void *id128, int world, int rank, std::string &err) {
         return c;
     }
     NcclComm *c = new NcclComm();
+    c->world = world;
+    c->rank = rank;
     ncclUniqueId id;
     memcpy(&id, id128, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->c, world, id, rank);

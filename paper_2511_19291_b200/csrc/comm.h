@@ -16,6 +16,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 namespace tqd {
 
@@ -32,6 +33,15 @@ class Comm {
     virtual int group_end(cudaStream_t s) = 0;
     // in-place elementwise sum over all ranks of a device buffer
     virtual int allreduce_sum(void *buf, size_t count, CommElem t, cudaStream_t s) = 0;
+    // make nbuf local device allocations addressable by every rank (peer memory):
+    // table[r * nbuf + i] = rank r's buffer i, usable in this process's kernels.
+    // NCCL: CUDA IPC handles exchanged with an all-gather (NVLink P2P); loopback:
+    // plain pointers (same device).  Collective.
+    virtual int share_buffers(void *const *local, int nbuf, std::vector<void *> &table, cudaStream_t s) = 0;
+    virtual void release_buffers(std::vector<void *> &table, int nbuf) {}
+    // returns once the work every rank queued before it has completed (host-blocking)
+    virtual int barrier(cudaStream_t s) = 0;
+    int rank = 0, world = 1;
     std::string err;
 };
 

@@ -353,7 +353,7 @@ __global__ void remap_unpack_kernel(const typename CT<Real>::C *__restrict__ src
 // Launchers (host side, called from engine.cpp)
 #define TQD_DECL(NAME)                                                                                          \
     cudaError_t launch_sweep_##NAME(const DevStage *, const void *, const int32_t *, void *, void *, double *,       \
-                                    uint64_t, int, int, int, int, int, int, cudaStream_t);                          \
+                                    uint64_t, const ScatterInfo &, int, int, int, int, int, int, cudaStream_t);     \
     int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg);
 TQD_DECL(f32_fwd)
 TQD_DECL(f32_bwd)
@@ -362,13 +362,13 @@ TQD_DECL(f64_bwd)
 #undef TQD_DECL
 
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
-                         void *psi, void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots,
-                         int nseg, int grid, cudaStream_t s) {
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W,
+                         int n_ops, int n_slots, int nseg, int grid, cudaStream_t s) {
     if (dbl)
-        return bwd ? launch_sweep_f64_bwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, nseg, grid, s)
-                   : launch_sweep_f64_fwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, nseg, grid, s);
-    return bwd ? launch_sweep_f32_bwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, nseg, grid, s)
-               : launch_sweep_f32_fwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, nseg, grid, s);
+        return bwd ? launch_sweep_f64_bwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, grid, s)
+                   : launch_sweep_f64_fwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, grid, s);
+    return bwd ? launch_sweep_f32_bwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, grid, s)
+               : launch_sweep_f32_fwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, grid, s);
 }
 
 int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg) {

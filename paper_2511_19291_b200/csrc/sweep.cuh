@@ -417,7 +417,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
-                                                    double *__restrict__ grad, uint64_t rank_hi) {
+                                                    double *__restrict__ grad, uint64_t rank_hi,
+                                                    const __grid_constant__ ScatterInfo sc) {
     typedef typename CT<Real>::C C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevStage S;
@@ -644,10 +645,26 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             o[0] = b0;
 #pragma unroll
             for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] + c[ctz4(r)];
+            if (sc.m == 0) {
 #pragma unroll
-            for (int r = 0; r < NR; r++) {
-                psi[o[r]] = a[r];
-                if (BWD) lam[o[r]] = l[r];
+                for (int r = 0; r < NR; r++) {
+                    psi[o[r]] = a[r];
+                    if (BWD) lam[o[r]] = l[r];
+                }
+            } else {
+                // fused remap: store to the post-remap owner (peer memory) and position
+                const uint64_t lmask = (1ull << sc.n_loc) - 1;
+#pragma unroll
+                for (int r = 0; r < NR; r++) {
+                    const uint64_t P = o[r] | rank_hi;
+                    uint64_t flip = 0;
+                    for (int i = 0; i < sc.m; i++)
+                        if (((P >> sc.gbit[i]) ^ (P >> sc.lbit[i])) & 1ull) flip |= (1ull << sc.gbit[i]) | (1ull << sc.lbit[i]);
+                    const uint64_t Q = P ^ flip;
+                    const int rr = (int)(Q >> sc.n_loc);
+                    reinterpret_cast<C *>(sc.dst_psi[rr])[Q & lmask] = a[r];
+                    if (BWD) reinterpret_cast<C *>(sc.dst_lam[rr])[Q & lmask] = l[r];
+                }
             }
         }
     }
@@ -699,14 +716,14 @@ template <typename Real, bool BWD> static std::atomic<uint64_t> &sweep_cap_flag(
 
 template <typename Real, bool BWD>
 cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                              double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, int nseg,
-                              int grid, cudaStream_t s) {
+                              double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops,
+                              int n_slots, int nseg, int grid, cudaStream_t s) {
     typedef typename CT<Real>::C C;
     auto fn = sweep_kernel<Real, BWD>;
     const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
     cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>());
     if (e != cudaSuccess) return e;
-    fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi);
+    fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi, sc);
     return cudaGetLastError();
 }
 
@@ -731,10 +748,10 @@ int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg) {
 #define TQD_INSTANTIATE_SWEEP(REAL, BWD, NAME)                                                                    \
     namespace tqd {                                                                                             \
     cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi,  \
-                                    void *lam, double *grad, uint64_t rank_hi, int k, int W, int n_ops, int n_slots, \
-                                    int nseg, int grid, cudaStream_t s) {                                         \
-        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, k, W, n_ops, n_slots, \
-                                            nseg, grid, s);                                                     \
+                                    void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, \
+                                    int n_ops, int n_slots, int nseg, int grid, cudaStream_t s) {                 \
+        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops,     \
+                                            n_slots, nseg, grid, s);                                            \
     }                                                                                                           \
     int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg) {                                 \
         return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots, nseg);                                      \

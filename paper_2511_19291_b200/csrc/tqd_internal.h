@@ -174,6 +174,21 @@ struct DevStage {
 // sweep-kernel variant bits (DevStage::flags)
 enum : int32_t { SWF_NONE = 0 };  // 4: timing only (wrong results)
 
+// Fused sweep -> remap (PAPER.md:164 redistribution fused into the preceding sweep):
+// the sweep's store writes every amplitude straight to its post-remap owner and
+// position, through peer memory (NVLink P2P / CUDA IPC; the loopback world: same
+// device).  Full index P -> P' = P with bits gbit[i] <-> lbit[i] swapped; rank
+// P' >> n_loc, offset P' & lmask.  m = 0: plain in-place store.
+constexpr int SCATTER_MAX_RANKS = 64;
+struct ScatterInfo {
+    int32_t m;
+    int32_t n_loc;
+    uint8_t gbit[8];  // full-index positions (>= n_loc) of the swapped rank bits
+    uint8_t lbit[8];  // local positions they swap with
+    uint64_t dst_psi[SCATTER_MAX_RANKS];  // destination shard of psi on every rank
+    uint64_t dst_lam[SCATTER_MAX_RANKS];  // (adjoint) destination shard of lambda
+};
+
 // Z-string observable in PHYSICAL masks (full index incl. rank bits)
 // lambda-init form: h(b) = cst - 2 sum_p w[p] bit_p(b) + sum_t c_t (-1)^{popc(b & z_t)}
 // (single-qubit Z terms folded into per-position weights, the rest listed)

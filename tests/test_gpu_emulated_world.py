@@ -61,15 +61,19 @@ def mixed_circuit(n, seed):
     return W.random_circuit(n, 120, seed) + W.hea(n, 2, seed) + W.qft(n)[:30]
 
 
+@pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("world,n,k", [(2, 12, 9), (4, 13, 9), (8, 14, 9), (2, 16, 12), (4, 17, 12)])
-def test_world_amplitudes(tqd, orc, world, n, k, dtype):
+def test_world_amplitudes(tqd, orc, world, n, k, dtype, fused):
+    """fused = 1: remaps fused into the preceding sweep (stores into the owners'
+    peer memory); fused = 0: pack -> all-to-all -> unpack."""
     gates = mixed_circuit(n, world + n)
 
     def fn(r, ctx):
         st = tqd.State(ctx, n, dtype)
         st.set_option(tqd.OPT_TILE_QUBITS, k)
         st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.set_option(tqd.OPT_FUSED_REMAP, fused)
         st.apply_circuit(gates)
         amp = st.amplitudes()
         m = st.metrics()
@@ -80,6 +84,7 @@ def test_world_amplitudes(tqd, orc, world, n, k, dtype):
     for amp, m in out:
         assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"]
         assert m["remaps"] > 0 and m["a2a_bytes"] > 0  # the exchange really ran
+        assert (m["fused_remaps"] > 0) == bool(fused)
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
@@ -105,9 +110,10 @@ def test_world_expval_pauli(tqd, orc, world, n, dtype):
         assert np.max(np.abs(v - ref)) < TOL[dtype]["val"]
 
 
+@pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("world,n,k,small", [(2, 12, 9, False), (4, 14, 10, True), (8, 15, 9, True), (2, 17, 12, True)])
-def test_world_adjoint(tqd, orc, world, n, k, small, dtype):
+def test_world_adjoint(tqd, orc, world, n, k, small, dtype, fused):
     """Adjoint gradients with remaps replayed on psi and lambda."""
     gates = W.random_circuit(n, 80, 5 + world, small=small) + W.hea(n, 3, world, small=small)
     terms = W.random_z_terms(n, 5, world) + W.sum_z(n)
@@ -116,6 +122,7 @@ def test_world_adjoint(tqd, orc, world, n, k, small, dtype):
         st = tqd.State(ctx, n, dtype)
         st.set_option(tqd.OPT_TILE_QUBITS, k)
         st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.set_option(tqd.OPT_FUSED_REMAP, fused)
         st.apply_circuit(gates)
         val, grad = st.adjoint_grad(terms)
         st.free()
@@ -191,3 +198,33 @@ def test_world_matches_single_rank(tqd, orc):
     for world in (2, 4, 8):
         assert abs(vals[world][0] - vals[1][0]) < 1e-11
         assert np.max(np.abs(vals[world][1] - vals[1][1])) < 1e-11
+
+
+def test_world_fused_remap_repeat(tqd, orc):
+    """Fused remaps swap the roles of the shard buffers; rewinding and re-running the
+    cached plan (twice), then reading amplitudes, must still match the oracle."""
+    n, world = 14, 4
+    gates = W.hea(n, 3, 9, small=True)
+    terms = W.sum_z(n)
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, "c128")
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.apply_circuit(gates)
+        out = [st.adjoint_grad(terms)]
+        for _ in range(2):
+            st.rewind()
+            out.append(st.adjoint_grad(terms))
+        st.reset()
+        st.apply_circuit(gates)
+        amp = st.amplitudes()
+        m = st.metrics()
+        st.free()
+        return out, amp, m
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ref = orc.run(n, gates)
+    for out, amp, m in run_world(tqd, world, fn):
+        for val, grad in out:
+            assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
+        assert np.max(np.abs(amp - ref)) < 1e-12
+        assert m["remaps"] > 0
