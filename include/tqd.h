@@ -162,6 +162,18 @@ int tqd_state_bytes(int n_qubits, tqd_dtype dt, int world, int with_adjoint, siz
  * "at least two unsharded dimensions"); TQD_ERR_OOM.  Collective. */
 int tqd_state_init(tqd_ctx *ctx, int n_qubits, tqd_dtype dt, void *dev_buf, size_t buf_bytes,
                    tqd_state **out);
+/* A BATCH of `batch` states of n qubits that share one gate tape (PAPER.md:157:
+ * the first tensor dimension is the batch; the paper's profiled workload is a
+ * batch of 16 states whose encoder angles differ).  Every state
+ * starts in |0...0>.  Gates recorded with tqd_apply_gate act identically on all
+ * states (one gradient slot per parameter: the gradient is the sum over the
+ * batch); tqd_apply_gate_batch records per-state parameters.  Outputs index the
+ * batch first: tqd_expval writes out[b * n_terms + t]; tqd_get_amplitudes reads
+ * the index space [0, batch * 2^n) as b * 2^n + i; tqd_adjoint_grad takes
+ * coeff[b * n_terms + t] (NULL = all 1) and returns E = sum_b sum_t c_bt <P_t>_b.
+ * Memory: batch x the single-state buffers.  Collective. */
+int tqd_state_init_batch(tqd_ctx *ctx, int n_qubits, tqd_dtype dt, int batch, tqd_state **out);
+
 /* Back to |0...0>, empty tape, pi = identity.  Collective (device memset). */
 int tqd_state_reset(tqd_state *st);
 /* Back to |0...0> and pi = identity but KEEP the recorded tape: the next
@@ -180,6 +192,15 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t value);
  * TQD_ERR_NOT_UNITARY, TQD_ERR_STATE (state consumed by tqd_adjoint_grad). */
 int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires,
                    const double *params, const double *matrix, int trainable);
+
+/* Record a parameterised 1-qubit gate (RX, RY, RZ or U3) with PER-STATE
+ * parameters: params[b * np + i] for batch element b (np = 1, or 3 for U3), e.g.
+ * the encoder rotation carrying each state's input.  trainable != 0 gives the
+ * gate batch * np gradient slots, element b's at slot0 + b * np + i (the input
+ * gradients of Adam-on-inputs).  Errors: TQD_ERR_ARG for another
+ * kind, n_wires != 1, NULL params. */
+int tqd_apply_gate_batch(tqd_state *st, tqd_gate g, const int *wires, int n_wires, const double *params,
+                         int trainable);
 
 /* Number of gradient slots recorded so far. */
 int tqd_num_params(const tqd_state *st, int *out);

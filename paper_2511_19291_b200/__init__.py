@@ -67,6 +67,8 @@ _SIG = {
     "tqd_ctx_destroy": [_P],
     "tqd_state_bytes": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)],
     "tqd_state_init": [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, ctypes.POINTER(_P)],
+    "tqd_state_init_batch": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
+    "tqd_apply_gate_batch": [_P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int],
     "tqd_state_reset": [_P],
     "tqd_state_rewind": [_P],
     "tqd_state_free": [_P],
@@ -191,6 +193,20 @@ def tqd_apply_gate(st, gate, wires, params=(), matrix=None, trainable=True):
     _call("tqd_apply_gate", st, g, _ptr(w), int(w.size), _ptr(p), _ptr(m), 1 if trainable else 0)
 
 
+def tqd_state_init_batch(ctx, n: int, dtype: int, batch: int):
+    out = _P()
+    _call("tqd_state_init_batch", ctx, n, dtype, batch, ctypes.byref(out))
+    return out
+
+
+def tqd_apply_gate_batch(st, gate, wires, params, trainable=True):
+    """params: (batch, n_params_of_gate) per-state parameters."""
+    g = GATES[gate] if isinstance(gate, str) else int(gate)
+    w = _arr(wires, np.int32)
+    p = _arr(np.asarray(params, dtype=np.float64).reshape(-1), np.float64)
+    _call("tqd_apply_gate_batch", st, g, _ptr(w), int(w.size), _ptr(p), 1 if trainable else 0)
+
+
 def tqd_num_params(st) -> int:
     out = ctypes.c_int()
     _call("tqd_num_params", st, ctypes.byref(out))
@@ -204,15 +220,18 @@ def _terms(terms):
     return len(terms), x, z, c
 
 
-def tqd_expval(st, terms) -> np.ndarray:
+def tqd_expval(st, terms, batch: int = 1) -> np.ndarray:
     T, x, z, c = _terms(terms)
-    out = np.zeros(max(T, 1), dtype=np.float64)
+    out = np.zeros(max(T * batch, 1), dtype=np.float64)
     _call("tqd_expval", st, T, _ptr(x), _ptr(z), _ptr(c), _ptr(out))
-    return out[:T]
+    return out[:T * batch] if batch == 1 else out[:T * batch].reshape(batch, T)
 
 
-def tqd_adjoint_grad(st, terms, n_grad: int | None = None):
+def tqd_adjoint_grad(st, terms, n_grad: int | None = None, coeff=None):
+    """coeff: optional (batch, n_terms) VJP weights for a batch (default: the terms' own)."""
     T, x, z, c = _terms(terms)
+    if coeff is not None:
+        c = _arr(np.asarray(coeff, dtype=np.float64).reshape(-1), np.float64)
     if n_grad is None:
         n_grad = tqd_num_params(st)
     g = np.zeros(max(n_grad, 1), dtype=np.float64)
@@ -317,10 +336,14 @@ class Context:
 
 
 class State:
-    def __init__(self, ctx: Context, n: int, dtype: str = "c64", dev_buf: int | None = None, buf_bytes: int = 0):
-        self.ctx, self.n = ctx, n
+    def __init__(self, ctx: Context, n: int, dtype: str = "c64", dev_buf: int | None = None, buf_bytes: int = 0,
+                 batch: int = 1):
+        self.ctx, self.n, self.batch = ctx, n, batch
         self.dtype = C128 if dtype in ("c128", C128) else C64
-        self.handle = tqd_state_init(ctx.handle, n, self.dtype, dev_buf, buf_bytes)
+        if batch == 1:
+            self.handle = tqd_state_init(ctx.handle, n, self.dtype, dev_buf, buf_bytes)
+        else:
+            self.handle = tqd_state_init_batch(ctx.handle, n, self.dtype, batch)
 
     def set_option(self, opt: int, value: int):
         tqd_state_set_option(self.handle, opt, value)
@@ -342,15 +365,22 @@ class State:
     def n_params(self) -> int:
         return tqd_num_params(self.handle)
 
-    def expval(self, terms) -> np.ndarray:
-        return tqd_expval(self.handle, terms)
+    def apply_batch(self, gate, wires, params, trainable=True):
+        """Per-state parameters: params has shape (batch, n_params_of_gate)."""
+        tqd_apply_gate_batch(self.handle, gate, wires, params, trainable)
 
-    def adjoint_grad(self, terms):
-        return tqd_adjoint_grad(self.handle, terms)
+    def expval(self, terms) -> np.ndarray:
+        return tqd_expval(self.handle, terms, self.batch)
+
+    def adjoint_grad(self, terms, coeff=None):
+        """coeff: (batch, n_terms) VJP weights; default: every element uses the terms' own."""
+        if coeff is None and self.batch > 1:
+            coeff = np.tile([t[2] if len(t) > 2 else 1.0 for t in terms], (self.batch, 1))
+        return tqd_adjoint_grad(self.handle, terms, coeff=coeff)
 
     def amplitudes(self, first: int = 0, count: int | None = None) -> np.ndarray:
         if count is None:
-            count = (1 << self.n) - first
+            count = (self.batch << self.n) - first
         return tqd_get_amplitudes(self.handle, first, count, self.dtype)
 
     def metrics(self) -> dict:

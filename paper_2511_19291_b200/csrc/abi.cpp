@@ -23,7 +23,7 @@ cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void
                          int n_ops, int n_slots, int nseg, int grid, cudaStream_t s);
 int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
-                         uint64_t rank_hi, cudaStream_t s);
+                         uint64_t rank_hi, int batch, cudaStream_t s);
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
                                double *eout, cudaStream_t s);
 cudaError_t launch_expval_z(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const uint64_t *d_z, int T,
@@ -70,6 +70,8 @@ struct tqd_state {
     void *user_buf = nullptr;
     size_t user_bytes = 0;
     std::vector<GateRec> gates;
+    int batch = 1;                              // states in the batch (one tape, B shards)
+    std::vector<std::vector<GateRec>> brec;     // per gate: B per-state records (batched gates) or empty
     int n_params = 0;
     size_t executed = 0;
     std::vector<Stage> history;
@@ -217,10 +219,12 @@ static int ensure_red(tqd_state *st, size_t count) {
 }
 
 static uint64_t shard_bytes(const tqd_state *st) { return ((uint64_t)1 << st->n_loc) * st->esz; }
+// every buffer holds the shards of all batch elements back to back
+static uint64_t all_bytes(const tqd_state *st) { return shard_bytes(st) * (uint64_t)st->batch; }
 
 static int ensure_xchg(tqd_state *st) {
     if (st->sendb) return TQD_OK;
-    const size_t b = shard_bytes(st);
+    const size_t b = all_bytes(st);
     if (cudaMalloc(&st->sendb, b) != cudaSuccess || cudaMalloc(&st->recvb, b) != cudaSuccess) {
         cudaGetLastError();
         return fail(TQD_ERR_OOM, "cannot allocate remap staging buffers");
@@ -243,7 +247,7 @@ static int ensure_xy_scratch(tqd_state *st) {
 
 static int ensure_lambda(tqd_state *st) {
     if (st->lam) return TQD_OK;
-    const size_t b = shard_bytes(st);
+    const size_t b = all_bytes(st);
     if (cudaMalloc(&st->lam, b) != cudaSuccess) {
         cudaGetLastError();
         return fail(TQD_ERR_OOM, "cannot allocate the adjoint state lambda");
@@ -279,7 +283,7 @@ static void remap_schedule(int rank, int n_loc, const RemapPlan &rp, std::vector
     }
 }
 
-static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
+static int exec_remap_one(tqd_state *st, const RemapPlan &rp, void *buf) {
     int rc = ensure_xchg(st);
     if (rc) return rc;
     tqd_ctx *c = st->ctx;
@@ -318,15 +322,37 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
     return TQD_OK;
 }
 
+// a remap of every batch element's shard (staging: the first shard of send / recv)
+static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
+    for (int b = 0; b < st->batch; b++) {
+        const int rc = exec_remap_one(st, rp, (char *)buf + (size_t)b * shard_bytes(st));
+        if (rc) return rc;
+    }
+    return TQD_OK;
+}
+
 // ---- forward execution ------------------------------------------------------
 static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops, int n_slots) {
-    if (st->opt_grid > 0) return st->opt_grid;
+    if (st->opt_grid > 0) return std::max(1, st->opt_grid / st->batch) * st->batch;
     int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots, (int)sp.lays.size());
     if (per < 1) per = 1;
     int64_t g = (int64_t)per * st->ctx->sms;
     const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
-    if (g > tiles) g = tiles;
-    return (int)g;
+    // a batch of B states: the grid is a multiple of B (CTA i serves state i % B)
+    int64_t per_state = std::max<int64_t>(1, g / st->batch);
+    if (per_state > tiles) per_state = tiles;
+    return (int)(per_state * st->batch);
+}
+
+// the tape as seen by batch element b (batched gates replaced by element b's record)
+static const std::vector<GateRec> &gates_for(tqd_state *st, int b, std::vector<GateRec> &tmp) {
+    bool any = false;
+    for (const auto &v : st->brec) if (!v.empty()) { any = true; break; }
+    if (!any || b == 0) return st->gates;
+    tmp = st->gates;
+    for (size_t i = 0; i < tmp.size() && i < st->brec.size(); i++)
+        if (!st->brec[i].empty()) tmp[i] = st->brec[i][b];
+    return tmp;
 }
 
 // Encoded launch list: descriptors of a stage list, uploaded once to the device.
@@ -370,7 +396,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
     const DevOp *d_ops = (const DevOp *)((char *)E.dev + E.off_ops);
     const char *d_kops = (const char *)E.dev + E.off_kops;
     const int32_t *d_sl = (const int32_t *)((char *)E.dev + E.off_sl);
-    const uint64_t sb = shard_bytes(st);
+    const uint64_t sb = all_bytes(st);
     for (size_t li = 0; li < E.launches.size(); li++) {
         const Encoded::L &l = E.launches[li];
         const Stage &s = stages[l.stage];
@@ -418,7 +444,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
         } else if (l.type == ST_SMALL) {
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_small(st->dbl, bwd, d_ops + l.op_base, l.n_ops, st->psi, st->lam, d_grad, st->n_loc,
-                                      rank_hi(st), c->stream));
+                                      rank_hi(st), st->batch, c->stream));
             ev_end(st, ev);
             if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += s.sm.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += s.sm.n_gates; }
@@ -437,20 +463,27 @@ template <typename Real>
 static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E,
                        std::vector<DevStage> &dstages, std::vector<DevOp> &ops, std::vector<KOp<Real>> &kops,
                        std::vector<int32_t> &slots) {
+    std::vector<GateRec> tmp;
     for (size_t ii = 0; ii < stages.size(); ii++) {
         const Stage &s = stages[ii];
         if (s.type == ST_SWEEP) {
             if (s.sw.ops.empty()) continue;
+            // one copy of the op stream / slot table per batch element (same structure)
             DevStage ds;
-            encode_sweep_k<Real>(s.sw, st->gates, bwd, st->n_loc, ds, kops, slots);
+            encode_sweep_k<Real>(s.sw, gates_for(st, 0, tmp), bwd, st->n_loc, ds, kops, slots);
+            for (int b = 1; b < st->batch; b++) {
+                DevStage dsb;
+                encode_sweep_k<Real>(s.sw, gates_for(st, b, tmp), bwd, st->n_loc, dsb, kops, slots);
+            }
+            ds.batch = st->batch;
             E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
                                   sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots), ds.n_slots});
             dstages.push_back(ds);
         } else if (s.type == ST_SMALL) {
             if (s.sm.ops.empty()) continue;
             const int b = (int)ops.size();
-            encode_small(s.sm, st->gates, bwd, ops);
-            E.launches.push_back({ST_SMALL, -1, b, (int)ops.size() - b, (int)ii, 1, 0});
+            for (int bb = 0; bb < st->batch; bb++) encode_small(s.sm, gates_for(st, bb, tmp), bwd, ops);
+            E.launches.push_back({ST_SMALL, -1, b, ((int)ops.size() - b) / st->batch, (int)ii, 1, 0});
         } else {
             E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii, 0, 0});
         }
@@ -654,7 +687,18 @@ int tqd_state_bytes(int n, tqd_dtype dt, int world, int with_adjoint, size_t *ou
     return TQD_OK;
 }
 
+static int state_init(tqd_ctx *c, int n, tqd_dtype dt, int batch, void *dev_buf, size_t buf_bytes, tqd_state **out);
+
 int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_bytes, tqd_state **out) {
+    return state_init(c, n, dt, 1, dev_buf, buf_bytes, out);
+}
+
+int tqd_state_init_batch(tqd_ctx *c, int n, tqd_dtype dt, int batch, tqd_state **out) {
+    if (batch < 1 || batch > (1 << 20)) return fail(TQD_ERR_ARG, "batch must be in [1, 2^20]");
+    return state_init(c, n, dt, batch, nullptr, 0, out);
+}
+
+static int state_init(tqd_ctx *c, int n, tqd_dtype dt, int batch, void *dev_buf, size_t buf_bytes, tqd_state **out) {
     if (!c || !out) return fail(TQD_ERR_ARG, "ctx/out is NULL");
     *out = nullptr;
     if (c->poisoned) return fail(TQD_ERR_STATE, "context poisoned");
@@ -670,6 +714,7 @@ int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_by
     st->n_loc = n - g;
     st->dbl = dt == TQD_C128;
     st->esz = st->dbl ? 16 : 8;
+    st->batch = batch;
     memset(&st->met, 0, sizeof(st->met));
     st->enc_fwd = new Encoded();
     st->enc_bwd = new Encoded();
@@ -685,14 +730,14 @@ int tqd_state_init(tqd_ctx *c, int n, tqd_dtype dt, void *dev_buf, size_t buf_by
         }
         st->met.peak_device_bytes = buf_bytes;
     } else {
-        if (cudaMalloc(&st->psi, sb) != cudaSuccess) {
+        if (cudaMalloc(&st->psi, sb * batch) != cudaSuccess) {
             cudaGetLastError();
             delete st;
             return fail(TQD_ERR_OOM, "cannot allocate the state shard");
         }
         st->own_psi = true;
         st->psi_first = st->psi;
-        st->met.peak_device_bytes = sb;
+        st->met.peak_device_bytes = sb * batch;
     }
     int rc = tqd_state_reset(st);
     if (rc) { tqd_state_free(st); return rc; }
@@ -704,6 +749,7 @@ int tqd_state_reset(tqd_state *st) {
     int rc = check_live(st);
     if (rc) return rc;
     st->gates.clear();
+    st->brec.clear();
     st->history.clear();
     st->tape_version++;
     st->history_cached = false;
@@ -713,10 +759,12 @@ int tqd_state_reset(tqd_state *st) {
     st->pos.assign(st->n, 0);
     for (int q = 0; q < st->n; q++) st->pos[q] = st->n - 1 - q;  // MSB-first identity (R1)
     const int ev = ev_begin(st, CAT_OTHER);
-    CUDA_TRY(st, cudaMemsetAsync(st->psi, 0, shard_bytes(st), st->ctx->stream));
-    if (st->ctx->rank == 0) CUDA_TRY(st, launch_set_one(st->dbl, st->psi, st->ctx->stream));
+    CUDA_TRY(st, cudaMemsetAsync(st->psi, 0, all_bytes(st), st->ctx->stream));
+    if (st->ctx->rank == 0)
+        for (int b = 0; b < st->batch; b++)
+            CUDA_TRY(st, launch_set_one(st->dbl, (char *)st->psi + (size_t)b * shard_bytes(st), st->ctx->stream));
     ev_end(st, ev);
-    st->met.hbm_bytes += shard_bytes(st);
+    st->met.hbm_bytes += all_bytes(st);
     st->met.kernel_launches += 1;
     return ev_collect(st);
 }
@@ -731,10 +779,12 @@ int tqd_state_rewind(tqd_state *st) {
     st->pos.assign(st->n, 0);
     for (int q = 0; q < st->n; q++) st->pos[q] = st->n - 1 - q;
     const int ev = ev_begin(st, CAT_OTHER);
-    CUDA_TRY(st, cudaMemsetAsync(st->psi, 0, shard_bytes(st), st->ctx->stream));
-    if (st->ctx->rank == 0) CUDA_TRY(st, launch_set_one(st->dbl, st->psi, st->ctx->stream));
+    CUDA_TRY(st, cudaMemsetAsync(st->psi, 0, all_bytes(st), st->ctx->stream));
+    if (st->ctx->rank == 0)
+        for (int b = 0; b < st->batch; b++)
+            CUDA_TRY(st, launch_set_one(st->dbl, (char *)st->psi + (size_t)b * shard_bytes(st), st->ctx->stream));
     ev_end(st, ev);
-    st->met.hbm_bytes += shard_bytes(st);
+    st->met.hbm_bytes += all_bytes(st);
     st->met.kernel_launches += 1;
     return TQD_OK;
 }
@@ -801,6 +851,32 @@ int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires, con
     return TQD_OK;
 }
 
+int tqd_apply_gate_batch(tqd_state *st, tqd_gate g, const int *wires, int n_wires, const double *params, int trainable) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (g != TQD_RX && g != TQD_RY && g != TQD_RZ && g != TQD_U3)
+        return fail(TQD_ERR_ARG, "batched parameters: RX, RY, RZ or U3 only");
+    if (!wires || n_wires != 1) return fail(TQD_ERR_ARG, "batched gates act on one wire");
+    if (wires[0] < 0 || wires[0] >= st->n) return fail(TQD_ERR_ARG, "wire out of range");
+    if (!params) return fail(TQD_ERR_ARG, "params is NULL");
+    const int np_ = gate_num_params((int)g);
+    std::vector<GateRec> recs(st->batch);
+    std::string err;
+    for (int b = 0; b < st->batch; b++) {
+        int rc = make_gate((int)g, wires, 1, params + (size_t)b * np_, nullptr, trainable, st->dbl, recs[b], err);
+        if (rc) return fail(rc, err);
+        recs[b].batched = 1;
+        recs[b].cls = g == TQD_RZ ? CL_DIAG1 : CL_U1;  // by kind: the same kernel ops for every element
+        if (recs[b].trainable) recs[b].slot0 = st->n_params + b * np_;
+    }
+    if (recs[0].trainable) st->n_params += st->batch * np_;
+    st->gates.push_back(recs[0]);
+    st->brec.resize(st->gates.size());
+    st->brec.back() = std::move(recs);
+    st->tape_version++;
+    return TQD_OK;
+}
+
 int tqd_num_params(const tqd_state *st, int *out) {
     if (!st || !out) return fail(TQD_ERR_ARG, "NULL argument");
     *out = st->n_params;
@@ -817,18 +893,22 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
     rc = execute_pending(st);
     if (rc) return rc;
     if (T == 0) return ev_collect(st);
-    rc = ensure_red(st, (size_t)T + 2 * 64 + 64);
+    const int BT = st->batch * T;  // outputs: batch element b, term t at b * T + t
+    rc = ensure_red(st, (size_t)BT + 2 * 64 + 64 + 16);
     if (rc) return rc;
     tqd_ctx *c = st->ctx;
-    double *d_out = st->d_red;
-    uint64_t *d_masks = (uint64_t *)(st->d_red + T);
-    int *d_ny = (int *)(st->d_red + T + 64);
+    double *d_all = st->d_red;
+    uint64_t *d_masks = (uint64_t *)(st->d_red + BT);
+    int *d_ny = (int *)(st->d_red + BT + 64);
     const uint64_t N = 1ull << st->n_loc;
-    CUDA_TRY(st, cudaMemsetAsync(d_out, 0, T * sizeof(double), c->stream));
+    CUDA_TRY(st, cudaMemsetAsync(d_all, 0, BT * sizeof(double), c->stream));
     const int ev = ev_begin(st, CAT_OTHER);
     // Z-only terms, 16 per launch; X/Y terms grouped by x mask
     std::vector<int> zt;
     for (int t = 0; t < T; t++) if (x[t] == 0) zt.push_back(t);
+    for (int bi = 0; bi < st->batch; bi++) {
+    void *psi_b = (char *)st->psi + (size_t)bi * shard_bytes(st);
+    double *d_out = d_all + (size_t)bi * T;
     std::vector<char> done(T, 0);
     for (size_t b = 0; b < zt.size();) {
         // terms contiguous in the output? use a staging vector + scatter by index below
@@ -837,9 +917,9 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         for (int i = 0; i < cnt; i++) hm[i] = phys_mask(st, z[zt[b + i]]);
         CUDA_TRY(st, cudaMemcpyAsync(d_masks, hm, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
         // results go to d_out[T..] scratch? simpler: accumulate into d_out at the term positions via a temp
-        double *tmp = st->d_red + T + 128;
+        double *tmp = st->d_red + BT + 128;
         CUDA_TRY(st, cudaMemsetAsync(tmp, 0, 16 * sizeof(double), c->stream));
-        CUDA_TRY(st, launch_expval_z(st->dbl, st->psi, N, rank_hi(st), d_masks, cnt, tmp, c->stream));
+        CUDA_TRY(st, launch_expval_z(st->dbl, psi_b, N, rank_hi(st), d_masks, cnt, tmp, c->stream));
         for (int i = 0; i < cnt; i++)
             CUDA_TRY(st, cudaMemcpyAsync(d_out + zt[b + i], tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // hm lives on the host stack
@@ -856,7 +936,7 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         const uint64_t xp = phys_mask(st, x[t0]);
         const uint64_t xl = xp & ((1ull << st->n_loc) - 1);
         const int gx = (int)(xp >> st->n_loc);
-        const void *peer = st->psi;
+        const void *peer = psi_b;
         if (gx) {
             // X / Y on rank bits: <psi|P|psi> pairs this shard with rank ^ gx's shard
             // (a whole-shard swap with that partner)
@@ -864,7 +944,7 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
             if (rc) return rc;
             const int partner = c->rank ^ gx;
             COMM_TRY(st, c->comm->group_start());
-            COMM_TRY(st, c->comm->send(st->psi, shard_bytes(st), partner, c->stream));
+            COMM_TRY(st, c->comm->send(psi_b, shard_bytes(st), partner, c->stream));
             COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
             COMM_TRY(st, c->comm->group_end(c->stream));
             st->met.a2a_bytes += shard_bytes(st);
@@ -878,9 +958,9 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         }
         CUDA_TRY(st, cudaMemcpyAsync(d_masks, hm, grp.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
         CUDA_TRY(st, cudaMemcpyAsync(d_ny, hn, grp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        double *tmp = st->d_red + T + 128;
+        double *tmp = st->d_red + BT + 128;
         CUDA_TRY(st, cudaMemsetAsync(tmp, 0, 16 * sizeof(double), c->stream));
-        CUDA_TRY(st, launch_expval_xy(st->dbl, st->psi, peer, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp, c->stream));
+        CUDA_TRY(st, launch_expval_xy(st->dbl, psi_b, peer, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp, c->stream));
         for (size_t i = 0; i < grp.size(); i++)
             CUDA_TRY(st, cudaMemcpyAsync(d_out + grp[i], tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         CUDA_TRY(st, cudaStreamSynchronize(c->stream));
@@ -888,14 +968,15 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         st->met.kernel_launches++;
         for (int t : grp) done[t] = 1;
     }
+    }  // batch elements
     ev_end(st, ev);
-    rc = allreduce_sum(st, d_out, T);
+    rc = allreduce_sum(st, d_all, BT);
     if (rc) return rc;
-    std::vector<double> h(T);
-    CUDA_TRY(st, cudaMemcpyAsync(h.data(), d_out, T * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> h(BT);
+    CUDA_TRY(st, cudaMemcpyAsync(h.data(), d_all, BT * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));
-    st->met.d2h_bytes += T * sizeof(double);
-    for (int t = 0; t < T; t++) out[t] = (coeff ? coeff[t] : 1.0) * h[t];
+    st->met.d2h_bytes += BT * sizeof(double);
+    for (int i = 0; i < BT; i++) out[i] = (coeff ? coeff[i % T] : 1.0) * h[i];
     return ev_collect(st);
 }
 
@@ -920,79 +1001,86 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
     double *d_val = st->d_red;
     double *d_grad = st->d_red + 1;
     CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, (n_grad + 1) * sizeof(double), c->stream));
-    ZTerms zt;
-    memset(&zt, 0, sizeof(zt));
-    for (int t = 0; t < T; t++) {
-        if (x && x[t]) continue;  // X / Y strings: lambda_add_xy below
-        const uint64_t zp = phys_mask(st, z[t]);
-        const double ct = coeff ? coeff[t] : 1.0;
-        if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
-            zt.cst += ct;
-            zt.w[__builtin_ctzll(zp)] += ct;
-        } else {
-            zt.z[zt.T] = zp;
-            zt.c[zt.T] = ct;
-            zt.T++;
+    // the seed lambda = H psi per batch element; coefficients c[b * T + t] for a batch
+    // (the VJP weights of every state), c[t] for a single state
+    for (int bi = 0; bi < st->batch; bi++) {
+        void *psi_b = (char *)st->psi + (size_t)bi * shard_bytes(st);
+        void *lam_b = (char *)st->lam + (size_t)bi * shard_bytes(st);
+        const size_t cb = (size_t)bi * T;
+        ZTerms zt;
+        memset(&zt, 0, sizeof(zt));
+        for (int t = 0; t < T; t++) {
+            if (x && x[t]) continue;  // X / Y strings: lambda_add_xy below
+            const uint64_t zp = phys_mask(st, z[t]);
+            const double ct = coeff ? coeff[cb + t] : 1.0;
+            if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
+                zt.cst += ct;
+                zt.w[__builtin_ctzll(zp)] += ct;
+            } else {
+                zt.z[zt.T] = zp;
+                zt.c[zt.T] = ct;
+                zt.T++;
+            }
         }
-    }
-    const uint64_t N = 1ull << st->n_loc;
-    {
-        const int ev = ev_begin(st, CAT_OTHER);
-        CUDA_TRY(st, launch_lambda_init(st->dbl, st->psi, st->lam, N, rank_hi(st), zt, d_val, c->stream));
-        ev_end(st, ev);
-        st->met.hbm_bytes += 2 * N * st->esz;
-        st->met.kernel_launches++;
-    }
-    // X / Y strings: lambda += c_t P_t psi, grouped by x mask (<= 16 terms per launch);
-    // x masks with rank bits pair the shard with the partner rank's (as in tqd_expval)
-    if (x) {
-        std::vector<char> done(T, 0);
-        std::vector<uint64_t> hz;
-        std::vector<int> hn;
-        std::vector<double> hc;
-        for (int t0 = 0; t0 < T; t0++) {
-            if (done[t0] || !x[t0]) continue;
-            std::vector<int> grp;
-            for (int t = t0; t < T; t++)
-                if (!done[t] && x[t] == x[t0] && grp.size() < 16) grp.push_back(t);
-            const uint64_t xp = phys_mask(st, x[t0]);
-            const uint64_t xl = xp & (N - 1);
-            const int gx = (int)(xp >> st->n_loc);
-            const void *peer = st->psi;
-            if (gx) {
-                rc = ensure_xchg(st);
-                if (rc) return rc;
-                const int partner = c->rank ^ gx;
-                COMM_TRY(st, c->comm->group_start());
-                COMM_TRY(st, c->comm->send(st->psi, shard_bytes(st), partner, c->stream));
-                COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
-                COMM_TRY(st, c->comm->group_end(c->stream));
-                st->met.a2a_bytes += shard_bytes(st);
-                peer = st->recvb;
-            }
-            hz.assign(16, 0);
-            hn.assign(16, 0);
-            hc.assign(16, 0.0);
-            for (size_t i = 0; i < grp.size(); i++) {
-                hz[i] = phys_mask(st, z[grp[i]]);
-                hn[i] = __builtin_popcountll(x[grp[i]] & z[grp[i]]) & 3;
-                hc[i] = coeff ? coeff[grp[i]] : 1.0;
-            }
-            rc = ensure_xy_scratch(st);
-            if (rc) return rc;
-            CUDA_TRY(st, cudaMemcpyAsync(st->d_xy, hz.data(), 16 * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
-            CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 16, hc.data(), 16 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-            CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 32, hn.data(), 16 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        const uint64_t N = 1ull << st->n_loc;
+        {
             const int ev = ev_begin(st, CAT_OTHER);
-            CUDA_TRY(st, launch_lambda_add_xy(st->dbl, st->psi, peer, st->lam, N, rank_hi(st), xl, xp, st->d_xy,
-                                              (const int *)(st->d_xy + 32), (const double *)(st->d_xy + 16),
-                                              (int)grp.size(), d_val, c->stream));
+            CUDA_TRY(st, launch_lambda_init(st->dbl, psi_b, lam_b, N, rank_hi(st), zt, d_val, c->stream));
             ev_end(st, ev);
-            CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host staging vectors are reused
-            st->met.h2d_bytes += 16 * (8 + 8 + 4);
-            st->met.hbm_bytes += 4 * N * st->esz;
+            st->met.hbm_bytes += 2 * N * st->esz;
             st->met.kernel_launches++;
-            for (int t : grp) done[t] = 1;
+        }
+        // X / Y strings: lambda += c_t P_t psi, grouped by x mask (<= 16 terms per launch);
+        // x masks with rank bits pair the shard with the partner rank's (as in tqd_expval)
+        if (x) {
+            std::vector<char> done(T, 0);
+            std::vector<uint64_t> hz;
+            std::vector<int> hn;
+            std::vector<double> hc;
+            for (int t0 = 0; t0 < T; t0++) {
+                if (done[t0] || !x[t0]) continue;
+                std::vector<int> grp;
+                for (int t = t0; t < T; t++)
+                    if (!done[t] && x[t] == x[t0] && grp.size() < 16) grp.push_back(t);
+                const uint64_t xp = phys_mask(st, x[t0]);
+                const uint64_t xl = xp & (N - 1);
+                const int gx = (int)(xp >> st->n_loc);
+                const void *peer = psi_b;
+                if (gx) {
+                    rc = ensure_xchg(st);
+                    if (rc) return rc;
+                    const int partner = c->rank ^ gx;
+                    COMM_TRY(st, c->comm->group_start());
+                    COMM_TRY(st, c->comm->send(psi_b, shard_bytes(st), partner, c->stream));
+                    COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
+                    COMM_TRY(st, c->comm->group_end(c->stream));
+                    st->met.a2a_bytes += shard_bytes(st);
+                    peer = st->recvb;
+                }
+                hz.assign(16, 0);
+                hn.assign(16, 0);
+                hc.assign(16, 0.0);
+                for (size_t i = 0; i < grp.size(); i++) {
+                    hz[i] = phys_mask(st, z[grp[i]]);
+                    hn[i] = __builtin_popcountll(x[grp[i]] & z[grp[i]]) & 3;
+                    hc[i] = coeff ? coeff[cb + grp[i]] : 1.0;
+                }
+                rc = ensure_xy_scratch(st);
+                if (rc) return rc;
+                CUDA_TRY(st, cudaMemcpyAsync(st->d_xy, hz.data(), 16 * sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+                CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 16, hc.data(), 16 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+                CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 32, hn.data(), 16 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+                const int ev = ev_begin(st, CAT_OTHER);
+                CUDA_TRY(st, launch_lambda_add_xy(st->dbl, psi_b, peer, lam_b, N, rank_hi(st), xl, xp, st->d_xy,
+                                                  (const int *)(st->d_xy + 32), (const double *)(st->d_xy + 16),
+                                                  (int)grp.size(), d_val, c->stream));
+                ev_end(st, ev);
+                CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host staging vectors are reused
+                st->met.h2d_bytes += 16 * (8 + 8 + 4);
+                st->met.hbm_bytes += 4 * N * st->esz;
+                st->met.kernel_launches++;
+                for (int t : grp) done[t] = 1;
+            }
         }
     }
     // reverse sweep down to (and including) the earliest stage holding a trainable gate
@@ -1038,7 +1126,8 @@ int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host
     if (rc) return rc;
     if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
     if (count && !host_out) return fail(TQD_ERR_ARG, "host_out is NULL");
-    const uint64_t total = 1ull << st->n;
+    const uint64_t per = 1ull << st->n;  // amplitudes per batch element; index b * 2^n + i
+    const uint64_t total = per * (uint64_t)st->batch;
     if (first > total || count > total - first) return fail(TQD_ERR_ARG, "amplitude range out of bounds");
     rc = execute_pending(st);
     if (rc) return rc;
@@ -1053,9 +1142,10 @@ int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host
     void *tmp = nullptr;
     if (cudaMalloc(&tmp, chunk * st->esz) != cudaSuccess) { cudaGetLastError(); return fail(TQD_ERR_OOM, "gather buffer"); }
     tqd_ctx *c = st->ctx;
-    for (uint64_t o = 0; o < count; o += chunk) {
-        const uint64_t cnt = std::min(chunk, count - o);
-        cudaError_t e = launch_gather(st->dbl, st->psi, tmp, first + o, cnt, gm, c->stream);
+    for (uint64_t o = 0; o < count;) {
+        const uint64_t idx = first + o, bi = idx / per, in = idx % per;
+        const uint64_t cnt = std::min(std::min(chunk, count - o), per - in);  // within one batch element
+        cudaError_t e = launch_gather(st->dbl, (char *)st->psi + bi * shard_bytes(st), tmp, in, cnt, gm, c->stream);
         if (e == cudaSuccess && c->world > 1) {
             if (c->comm->allreduce_sum(tmp, cnt * 2, st->dbl ? CE_F64 : CE_F32, c->stream) != 0) {
                 cudaFree(tmp);
@@ -1068,6 +1158,7 @@ int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host
         if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
         if (e != cudaSuccess) { cudaFree(tmp); c->poisoned = true; return fail(TQD_ERR_CUDA, cudaGetErrorString(e)); }
         st->met.kernel_launches++;
+        o += cnt;
     }
     cudaFree(tmp);
     return ev_collect(st);

@@ -40,6 +40,10 @@ __global__ void __launch_bounds__(512) small_kernel(const DevOp *__restrict__ op
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double red[32];
     const uint64_t N = 1ull << n_loc;
+    // batch of states: CTA b runs state b with its own op list (n_ops each)
+    ops += (size_t)blockIdx.x * n_ops;
+    psi += (size_t)blockIdx.x * N;
+    if (BWD) lam += (size_t)blockIdx.x * N;
     C *A = reinterpret_cast<C *>(smem_raw);
     C *L = A + N;
     for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
@@ -378,7 +382,7 @@ int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slo
 }
 
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad,
-                         int n_loc, uint64_t rank_hi, cudaStream_t s) {
+                         int n_loc, uint64_t rank_hi, int batch, cudaStream_t s) {
     const size_t esz = dbl ? 16 : 8;
     const size_t smem = (size_t)(bwd ? 2 : 1) * ((size_t)1 << n_loc) * esz;
     const int threads = 512;
@@ -387,7 +391,7 @@ cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void
         auto fn = small_kernel<T, BB>;                                                                  \
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
         if (e != cudaSuccess) return e;                                                                 \
-        fn<<<1, threads, smem, s>>>(d_ops, n_ops, (CT<T>::C *)psi, (CT<T>::C *)lam, grad, n_loc, rank_hi); \
+        fn<<<batch, threads, smem, s>>>(d_ops, n_ops, (CT<T>::C *)psi, (CT<T>::C *)lam, grad, n_loc, rank_hi); \
         return cudaGetLastError();                                                                      \
     }
     if (dbl) { if (bwd) TQD_S(double, true) else TQD_S(double, false) }

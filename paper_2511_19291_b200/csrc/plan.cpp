@@ -231,7 +231,7 @@ static POp make_pop(const GateRec &g, int gi, const std::vector<int> &pos) {
     switch (g.cls) {
     case CL_U1:
         o.tp0 = pos[g.w[0]];
-        set1(g.M, g.trainable ? g.kind : -1);
+        set1(g.M, (g.trainable || g.batched) ? g.kind : -1);
         break;
     case CL_CTRL1:
         o.tp0 = pos[g.w[1]];
@@ -961,6 +961,15 @@ static void fill_gens(DevOp &d, const GateRec &g) {
 }
 
 // The 2x2 an op applies to its target / diagonal bit (forward or adjoint form).
+// batched 1q gates: the op's matrix is the batch element's (same op form)
+static POp pop_for(const POp &o, const GateRec &g) {
+    if (!g.batched) return o;
+    POp r = o;
+    if (o.kind == OP_D1) { r.m[0] = g.M[0]; r.m[1] = g.M[3]; }
+    else for (int i = 0; i < 4; i++) r.m[i] = g.M[i];
+    return r;
+}
+
 static void op_matrix2(const POp &o, bool dag, cd *M) {
     cd F[4];
     switch (o.kind) {
@@ -1128,7 +1137,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
         // chosen type (gates on different bits commute, same-bit order is kept);
         // the forward also composes consecutive same-type gates on one bit.  Any
         // other op (controlled / 2q / phase on a non-register bit) drains the queues.
-        struct QG { cd M[4]; int t; int gate; };
+        struct QG { cd M[4]; int t; int gate; int batched; };
         std::vector<QG> q[RMAX];
         size_t qh[RMAX] = {0, 0, 0, 0, 0};
         auto drain = [&]() {
@@ -1153,7 +1162,9 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                         for (int i = 0; i < gg.ngen; i++) add_gen(layer, gg, i, bb);
                     qh[bb]++;
                     // forward: fold following gates on this bit while the product keeps the type
-                    while (!bwd && qh[bb] < q[bb].size()) {
+                    // (never across batched gates: their type must not depend on values)
+                    const bool took_batched = q[bb][qh[bb] - 1].batched != 0;
+                    while (!bwd && !took_batched && qh[bb] < q[bb].size() && !q[bb][qh[bb]].batched) {
                         const cd *Mn = q[bb][qh[bb]].M;
                         cd Pm[4];
                         Pm[0] = Mn[0] * LM[bb][0] + Mn[1] * LM[bb][2];
@@ -1170,9 +1181,10 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             for (int bb = 0; bb < R; bb++) { q[bb].clear(); qh[bb] = 0; }
         };
         for (int jj = 0; jj < e - b && !skip_ops; jj++) {
-            const POp &o = sp.ops[bwd ? e - 1 - jj : b + jj];
-            if (o.perm) continue;  // folded into the layout-change maps below
-            const GateRec &g = gates[o.gate];
+            const POp &o0 = sp.ops[bwd ? e - 1 - jj : b + jj];
+            if (o0.perm) continue;  // folded into the layout-change maps below
+            const GateRec &g = gates[o0.gate];
+            const POp o = pop_for(o0, g);
             const bool has_gen = bwd && g.ngen > 0;
             int bit = -1;
             if ((o.kind == OP_U1 || o.kind == OP_R1 || o.kind == OP_P1) && o.cp < 0) bit = regidx(o.tp0);
@@ -1182,6 +1194,8 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 op_matrix2(o, bwd, qg.M);
                 qg.t = mtype(qg.M);
                 if (g.trainable && g.kind == TQD_RZ) qg.t = LT_DIAG;  // RZ gradients are batched on diagonal layers
+                qg.batched = g.batched;
+                if (g.batched) qg.t = g.kind == TQD_RY ? LT_REAL : g.kind == TQD_RZ ? LT_DIAG : LT_GEN;  // by kind
                 qg.gate = o.gate;
                 q[bit].push_back(qg);
                 continue;
@@ -1299,7 +1313,7 @@ template void encode_sweep_k<double>(const SweepPlan &, const std::vector<GateRe
 void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops) {
     const int m = (int)sp.ops.size();
     for (int jj = 0; jj < m; jj++) {
-        const POp &o = sp.ops[bwd ? m - 1 - jj : jj];
+        const POp o = pop_for(sp.ops[bwd ? m - 1 - jj : jj], gates[sp.ops[bwd ? m - 1 - jj : jj].gate]);
         DevOp d;
         memset(&d, 0, sizeof(d));
         d.kind = (uint8_t)o.kind;

@@ -43,6 +43,10 @@ struct GateRec {
     int ngen = 0;
     uint8_t gkind[3] = {0, 0, 0};
     cd G[3][4];        // generators (dU/dtheta_p) U^dag
+    // batched gate (per-state parameters in a batch of states, e.g. encoder inputs):
+    // structure decided by the kind alone so that every batch element encodes to the
+    // same kernel ops; the tape holds element 0, the state keeps all B records
+    int batched = 0;
 };
 
 // build matrix, class and generators; returns 0 or a TQD_ERR_* code

@@ -434,6 +434,15 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
     const int k = S.k;
     const int W = S.W;
     const int nseg = S.nseg;
+    // batch of states: CTA blockIdx.x serves state blockIdx.x % B (grid is a multiple of
+    // B); each state has its own copy of the op stream and gradient-slot table
+    const int B = S.batch > 0 ? S.batch : 1;
+    const int bidx = (int)(blockIdx.x % (unsigned)B);
+    const int gsz = (int)(gridDim.x / (unsigned)B);  // CTAs per state
+    const int gid = (int)(blockIdx.x / (unsigned)B);
+    const uint64_t bst = (uint64_t)S.n_tiles << k;     // amplitudes per state shard
+    psi += bidx * bst;
+    if (BWD) lam += bidx * bst;
     // shared memory: [exchange psi (2^k)] [exchange lambda (2^k, adjoint)] [kernel ops]
     C *sm_a = reinterpret_cast<C *>(smem_raw);
     C *sm_l = sm_a + ((size_t)1 << k);
@@ -447,7 +456,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
     // per-thread L2-prefetch offsets (element offsets within a tile, up to 2 per thread)
     uint64_t *s_pf = reinterpret_cast<uint64_t *>(s_tr + (nseg - 1) * blockDim.x);  // 8 B aligned (threads * 4 B is)
     {
-        const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base);
+        const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base + (size_t)bidx * S.n_ops);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
         const int n16 = (int)(S.n_ops * sizeof(KOp<Real>) / 16);
         for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
@@ -541,9 +550,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
         return v;
     };
     const uint64_t tmask = deposit(~0ull) & (S.n_tiles > 1 ? ~0ull : 0ull);
-    const uint64_t step = deposit((uint64_t)gridDim.x);
-    uint64_t base = deposit((uint64_t)blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < S.n_tiles; tile += gridDim.x, base = ((base | ~tmask) + step) & tmask) {
+    const uint64_t step = deposit((uint64_t)gsz);
+    uint64_t base = deposit((uint64_t)gid);
+    for (int64_t tile = gid; tile < S.n_tiles; tile += gsz, base = ((base | ~tmask) + step) & tmask) {
         const uint64_t basefull = base | rank_hi;
 
         C a[NR];
@@ -563,7 +572,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                 if (BWD) l[r] = lam[o[r]];
             }
         }
-        if (tile + gridDim.x < S.n_tiles) {
+        if (tile + gsz < S.n_tiles) {
             const uint64_t nb = ((base | ~tmask) + step) & tmask;
             for (int i = 0; i < n_pf; i++) {
                 const uint64_t e = nb + s_pf[i * blockDim.x + threadIdx.x];
@@ -662,8 +671,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                         if (((P >> sc.gbit[i]) ^ (P >> sc.lbit[i])) & 1ull) flip |= (1ull << sc.gbit[i]) | (1ull << sc.lbit[i]);
                     const uint64_t Q = P ^ flip;
                     const int rr = (int)(Q >> sc.n_loc);
-                    reinterpret_cast<C *>(sc.dst_psi[rr])[Q & lmask] = a[r];
-                    if (BWD) reinterpret_cast<C *>(sc.dst_lam[rr])[Q & lmask] = l[r];
+                    reinterpret_cast<C *>(sc.dst_psi[rr])[bidx * bst + (Q & lmask)] = a[r];
+                    if (BWD) reinterpret_cast<C *>(sc.dst_lam[rr])[bidx * bst + (Q & lmask)] = l[r];
                 }
             }
         }
@@ -676,7 +685,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             double v = 0.0;
             for (int t = lane; t < (int)blockDim.x; t += 32) v += (double)tacc[i * blockDim.x + t];
             v = warp_sum(v);
-            if (lane == 0 && v != 0.0) atomicAdd(&grad[slot_param[S.slot_base + i]], v);
+            if (lane == 0 && v != 0.0) atomicAdd(&grad[slot_param[S.slot_base + bidx * S.n_slots + i]], v);
         }
     }
 }

@@ -169,6 +169,8 @@ struct DevStage {
     int32_t slot_base, n_slots; // into the launch's slot -> parameter table
     int32_t lam_init;           // backward only: 1 = build lambda = H psi on load
     int32_t flags;              // kernel variant bits (SWF_*)
+    int32_t batch;              // states in the batch: op / slot tables repeat per state (n_ops, n_slots each)
+    int32_t pad2;
 };
 
 // sweep-kernel variant bits (DevStage::flags)
