@@ -118,6 +118,7 @@ typedef struct tqd_metrics {
     uint64_t h2d_bytes;         /* host->device bytes (plan descriptors, masks)      */
     uint64_t d2h_bytes;         /* device->host bytes (values, gradients, amplitudes) */
     uint64_t fused_remaps;      /* remaps done by the preceding sweep's peer-memory stores */
+    uint64_t plans_reused;      /* executions that reused the plan of a structurally equal tape */
 } tqd_metrics;
 
 /* --- context ------------------------------------------------------------- */

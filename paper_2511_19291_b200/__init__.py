@@ -50,6 +50,7 @@ class Metrics(ctypes.Structure):
         ("fwd_sweep_bytes", ctypes.c_uint64), ("bwd_sweep_bytes", ctypes.c_uint64),
         ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
         ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("fused_remaps", ctypes.c_uint64),
+        ("plans_reused", ctypes.c_uint64),
     ]
 
     def as_dict(self):

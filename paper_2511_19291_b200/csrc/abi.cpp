@@ -93,6 +93,7 @@ struct tqd_state {
     bool history_cached = false;
     std::vector<Stage> cached_stages, rev_stages;
     std::vector<int> cached_pos;
+    uint64_t plan_sig = 0;  // plan_signature of cached_stages
     struct Encoded *enc_fwd = nullptr, *enc_bwd = nullptr, *enc_tmp = nullptr;
     // profiling
     std::vector<cudaEvent_t> ev_pool;
@@ -559,8 +560,18 @@ static int execute_pending(tqd_state *st) {
     std::vector<Stage> stages;
     std::string err;
     const bool from_zero = st->executed == 0;
-    int rc = plan_circuit(st->gates, pending, st->pos, plan_cfg(st), stages, err);
-    if (rc) return fail(rc, err);
+    const uint64_t sig = from_zero ? plan_signature(st->gates, plan_cfg(st)) : 0;
+    if (from_zero && !st->cached_stages.empty() && sig == st->plan_sig) {
+        // same circuit structure, new parameter values: reuse the plan
+        stages = st->cached_stages;
+        refresh_plan_values(stages, st->gates);
+        st->pos = st->cached_pos;
+        st->met.plans_reused++;
+    } else {
+        int rc = plan_circuit(st->gates, pending, st->pos, plan_cfg(st), stages, err);
+        if (rc) return fail(rc, err);
+    }
+    int rc;
     Encoded &E = from_zero ? *st->enc_fwd : *st->enc_tmp;
     rc = encode_upload(st, stages, false, E);
     if (rc) return rc;
@@ -569,6 +580,7 @@ static int execute_pending(tqd_state *st) {
     if (from_zero) {
         st->cached_stages = stages;
         st->cached_pos = st->pos;
+        st->plan_sig = sig;
         st->fwd_cache_version = st->tape_version;
         st->bwd_cache_version = ~0ull;
         st->history_cached = true;

@@ -209,6 +209,18 @@ static bool real_mat(const cd *m, int n) {
     return true;
 }
 
+// op form of a 1q matrix (trainable / batched gates: by kind, so it never depends on values)
+static int op1_form(const cd *m, int trainable_kind, int &plain) {
+    plain = 0;
+    if (trainable_kind == TQD_RX || trainable_kind == TQD_U3) return OP_U1;
+    if (trainable_kind == TQD_RY) return OP_R1;
+    if (is_zero(m[0]) && is_zero(m[3])) {
+        plain = is_one(m[1]) && is_one(m[2]);
+        return OP_P1;
+    }
+    return real_mat(m, 4) ? OP_R1 : OP_U1;
+}
+
 // Build the op (physical positions) for a placed gate.
 static POp make_pop(const GateRec &g, int gi, const std::vector<int> &pos) {
     POp o;
@@ -217,16 +229,7 @@ static POp make_pop(const GateRec &g, int gi, const std::vector<int> &pos) {
     if (g.nw == 2) o.wp1 = pos[g.ow[1]];
     auto set1 = [&](const cd *m, int trainable_kind) {
         for (int i = 0; i < 4; i++) o.m[i] = m[i];
-        if (trainable_kind == TQD_RX || trainable_kind == TQD_U3) { o.kind = OP_U1; return; }
-        if (trainable_kind == TQD_RY) { o.kind = OP_R1; return; }
-        if (is_zero(m[0]) && is_zero(m[3])) {
-            o.kind = OP_P1;
-            o.plain = is_one(m[1]) && is_one(m[2]);
-        } else if (real_mat(m, 4)) {
-            o.kind = OP_R1;
-        } else {
-            o.kind = OP_U1;
-        }
+        o.kind = op1_form(m, trainable_kind, o.plain);
     };
     switch (g.cls) {
     case CL_U1:
@@ -887,6 +890,52 @@ static void plan_remap(const std::vector<GateRec> &gates, const std::vector<int>
         lq[pos[qb]] = qb;
     }
     st.pos_after = pos;
+}
+
+// Plan reuse across parameter changes (training loops re-record the same circuit
+// with new angles): the plan depends on the gates' structure only -- kinds, wires,
+// trainability, classes and op forms -- never on parameter values beyond those.
+uint64_t plan_signature(const std::vector<GateRec> &gates, const PlanConfig &cfg) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+    const int c[] = {cfg.n, cfg.n_loc, cfg.k, cfg.R, cfg.small_max, cfg.c128 ? 1 : 0, cfg.swz_bits, cfg.c_low,
+                     cfg.max_ops, cfg.max_slots};
+    for (int v : c) mix((uint64_t)(int64_t)v);
+    for (const GateRec &g : gates) {
+        mix((uint64_t)g.kind); mix((uint64_t)g.nw); mix((uint64_t)g.ow[0]); mix((uint64_t)g.ow[1]);
+        mix((uint64_t)g.w[0]); mix((uint64_t)g.w[1]); mix((uint64_t)g.trainable); mix((uint64_t)g.batched);
+        mix((uint64_t)g.cls); mix((uint64_t)g.ngen);
+        int plain = 0;
+        if (g.cls == CL_U1) mix((uint64_t)op1_form(g.M, (g.trainable || g.batched) ? g.kind : -1, plain) * 2 + plain);
+        if (g.cls == CL_CTRL1) mix((uint64_t)op1_form(g.sub, -1, plain) * 2 + plain);
+        if (g.kind == TQD_MAT1 || g.kind == TQD_MAT2)  // constants: exact bits
+            for (int i = 0; i < (g.nw == 2 ? 16 : 4); i++) {
+                double re = g.M[i].real(), im = g.M[i].imag();
+                uint64_t a, b;
+                memcpy(&a, &re, 8); memcpy(&b, &im, 8);
+                mix(a); mix(b);
+            }
+    }
+    return h;
+}
+
+// new parameter values into a reused plan (same signature): op matrices only
+void refresh_plan_values(std::vector<Stage> &stages, const std::vector<GateRec> &gates) {
+    for (Stage &st : stages) {
+        std::vector<POp> *ops = st.type == ST_SWEEP ? &st.sw.ops : st.type == ST_SMALL ? &st.sm.ops : nullptr;
+        if (!ops) continue;
+        for (POp &o : *ops) {
+            const GateRec &g = gates[o.gate];
+            switch (g.cls) {
+            case CL_U1: for (int i = 0; i < 4; i++) o.m[i] = g.M[i]; break;
+            case CL_CTRL1: for (int i = 0; i < 4; i++) o.m[i] = g.sub[i]; break;
+            case CL_U2: for (int i = 0; i < 16; i++) o.m[i] = g.M[i]; break;
+            case CL_DIAG1: o.m[0] = g.M[0]; o.m[1] = g.M[3]; break;
+            case CL_DIAG2: for (int i = 0; i < 4; i++) o.m[i] = g.M[5 * i]; break;
+            default: break;
+            }
+        }
+    }
 }
 
 int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,

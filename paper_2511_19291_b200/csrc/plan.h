@@ -134,6 +134,8 @@ struct PlanConfig {
 
 // Plan the gates `pending` (indices into gates, in recording order) starting
 // from qubit map pos (logical -> physical).  Appends stages, updates pos.
+uint64_t plan_signature(const std::vector<GateRec> &gates, const PlanConfig &cfg);
+void refresh_plan_values(std::vector<Stage> &stages, const std::vector<GateRec> &gates);
 int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,
                  const PlanConfig &cfg, std::vector<Stage> &out, std::string &err);
 

@@ -219,3 +219,20 @@ def test_batch_emulated_world(tqd, orc, world, fused):
             assert np.max(np.abs(amp[b << n:(b + 1) << n] - psi)) < 1e-12
             assert np.max(np.abs(ev[b] - orc.expval(psi, n, terms))) < 1e-10
         assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
+
+
+def test_batch_training_loop_reuses_plan(tqd, ctx, orc):
+    """Adam-on-inputs style loop: new encoder inputs every step, same structure."""
+    n, B = 12, 4
+    ansatz = W.hea(n, 2, seed=3, small=True)
+    terms = W.sum_z(n)
+    st = make(tqd, ctx, n, "c128", B, 10, 0)
+    for step in range(3):
+        x = encoder_inputs(B, n, 50 + step)
+        st.reset()
+        record_batch(st, x, ansatz)
+        val, grad = st.adjoint_grad(terms)
+        rval, rgrad = expected(orc, n, x, ansatz, terms, np.ones((B, len(terms))))
+        assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
+    assert st.metrics()["plans_reused"] == 2
+    st.free()

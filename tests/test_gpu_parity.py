@@ -350,3 +350,31 @@ def test_metrics_account_bytes(tqd, ctx):
     assert m["bwd_sweep_bytes"] == 4 * sb * m["bwd_sweeps"]
     assert m["gates_applied"] == 3 * 3 * n
     assert m["a2a_bytes"] == 0 and m["remaps"] == 0
+
+
+def test_plan_reuse_across_parameter_changes(tqd, ctx, orc):
+    """Training loops re-record the same circuit with new angles: the plan is reused
+    (metrics.plans_reused) and the results follow the NEW values; a structural change
+    (other wires, an identity-valued fixed rotation) plans afresh."""
+    n = 14
+    st = make_state(tqd, ctx, n, "c64", k=11, small_max=0)
+    reused = 0
+    for seed in range(3):
+        gates = W.hea(n, 3, seed=100 + seed, small=True)
+        gates.append(W.Gate("RZ", (3,), (0.0 if seed == 2 else 0.4,), None, False))  # identity at seed 2
+        st.reset()
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(W.sum_z(n))
+        rval, rgrad = orc.adjoint(n, gates, W.sum_z(n))
+        assert abs(val - rval) < 1e-4 and np.max(np.abs(grad - rgrad)) < 1e-4
+        m = st.metrics()
+        reused = m["plans_reused"]
+        assert reused == (1 if seed == 1 else (0 if seed == 0 else 1))
+    st.reset()
+    gates = W.hea(n, 3, seed=7, small=True, ring=False)  # other wires: new plan
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(W.sum_z(n))
+    rval, rgrad = orc.adjoint(n, gates, W.sum_z(n))
+    assert abs(val - rval) < 1e-4 and np.max(np.abs(grad - rgrad)) < 1e-4
+    assert st.metrics()["plans_reused"] == reused
+    st.free()
