@@ -72,10 +72,16 @@ def _load():
                 "orc_gate_matrix": [i, p, p, p],
                 "orc_gate_dmatrix": [i, p, i, p],
                 "orc_num_threads": [],
+                "orc_gauss_sample": [p, i, d, ctypes.c_uint64, p],
+                "orc_gauss_z": [p, i, d, ctypes.c_uint64, p],
             }.items():
                 f = getattr(lib, name)
                 f.argtypes = args
                 f.restype = ctypes.c_int
+            for name in ("orc_uniform", "orc_normal"):
+                f = getattr(lib, name)
+                f.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+                f.restype = ctypes.c_double
             _lib = lib
     return _lib
 
@@ -197,3 +203,28 @@ def gate_matrix(name: str, params=(), matrix=None) -> np.ndarray:
     _check(_load().orc_gate_matrix(KIND[name], _ptr(p), _ptr(m), _ptr(out)), "gate_matrix")
     dim = 4 if name in ("CNOT", "CZ", "SWAP", "MAT2") else 2
     return (out[0:2 * dim * dim:2] + 1j * out[1:2 * dim * dim:2]).reshape(dim, dim)
+
+
+# ---- shot noise, approximate (Gaussian) sampler ----------
+def uniform(seed: int, k: int) -> float:
+    return _load().orc_uniform(seed, k)
+
+
+def normal(seed: int, i: int) -> float:
+    return _load().orc_normal(seed, i)
+
+
+def gauss_sample(psi: np.ndarray, n: int, shots: float, seed: int) -> np.ndarray:
+    """y = shots p + sqrt(shots) D S z over the 2^n canonical outcomes."""
+    psi = np.ascontiguousarray(psi, dtype=np.complex128)
+    y = np.zeros(1 << n, dtype=np.float64)
+    _check(_load().orc_gauss_sample(_ptr(psi), n, float(shots), seed, _ptr(y)), "gauss_sample")
+    return y
+
+
+def gauss_z(n: int, gates, shots: float, seed: int) -> np.ndarray:
+    """Per-qubit <Z_q> estimates from the approximate shot sample of the circuit's state."""
+    psi = run(n, gates)
+    out = np.zeros(n, dtype=np.float64)
+    _check(_load().orc_gauss_z(_ptr(psi), n, float(shots), seed, _ptr(out)), "gauss_z")
+    return out

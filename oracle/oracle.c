@@ -441,3 +441,68 @@ int orc_finite_diff(int n, int G, const int *kinds, const int *wires, const doub
                     const uint64_t *z, const double *c, double eps, double *grad) {
     return shifted(n, G, kinds, wires, params, mats, trainable, T, x, z, c, eps, 1, grad);
 }
+
+/* ---- shot noise: approximate (Gaussian) sampler, PAPER.md:200-218 -------- */
+static uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+double orc_uniform(uint64_t seed, uint64_t k) {
+    return (double)(splitmix64(seed ^ (k * 0xD1B54A32D192ED03ull)) >> 11) * 0x1.0p-53;
+}
+
+double orc_normal(uint64_t seed, uint64_t i) {
+    const double u1 = orc_uniform(seed, 2 * i), u2 = orc_uniform(seed, 2 * i + 1);
+    return sqrt(-2.0 * log(1.0 - u1)) * cos(2.0 * M_PI * u2);
+}
+
+int orc_gauss_sample(const double *psi_, int n, double shots, uint64_t seed, double *y) {
+    if (n < 1 || n > 30 || !(shots > 0)) return -1;
+    const cplx *psi = (const cplx *)psi_;
+    const uint64_t N = (uint64_t)1 << n, K = N - 1;
+    double *u = (double *)malloc(N * sizeof(double));
+    double *v = (double *)malloc(N * sizeof(double));
+    double *z = (double *)malloc(N * sizeof(double));
+    if (!u || !v || !z) { free(u); free(v); free(z); return -1; }
+    /* u = sqrt(p);  v~ = e_K - u;  v = v~ / ||v~|| */
+    double nv = 0.0;
+    for (uint64_t i = 0; i < N; i++) {
+        const double p = creal(psi[i]) * creal(psi[i]) + cimag(psi[i]) * cimag(psi[i]);
+        u[i] = sqrt(p);
+        v[i] = (i == K ? 1.0 : 0.0) - u[i];
+        nv += v[i] * v[i];
+        z[i] = i == K ? 0.0 : orc_normal(seed, i);
+    }
+    nv = sqrt(nv);
+    for (uint64_t i = 0; i < N; i++) v[i] = nv > 1e-300 ? v[i] / nv : 0.0;
+    /* x = S z with S the Householder reflection I - 2 v v^T (reading R21: PAPER.md:209
+     * prints I - v v^T, which is a projection and not the factorisation the text asks
+     * for; the reflection maps e_K <-> u, so Cov x = S (I - e_K e_K^T) S = I - u u^T);
+     * y = shots p + sqrt(shots) D x */
+    double vz = 0.0;
+    for (uint64_t i = 0; i < N; i++) vz += v[i] * z[i];
+    for (uint64_t i = 0; i < N; i++) {
+        const double x = z[i] - 2.0 * v[i] * vz;
+        y[i] = shots * u[i] * u[i] + sqrt(shots) * u[i] * x;
+    }
+    free(u); free(v); free(z);
+    return 0;
+}
+
+int orc_gauss_z(const double *psi, int n, double shots, uint64_t seed, double *out_z) {
+    const uint64_t N = (uint64_t)1 << n;
+    double *y = (double *)malloc(N * sizeof(double));
+    if (!y) return -1;
+    int rc = orc_gauss_sample(psi, n, shots, seed, y);
+    if (rc) { free(y); return rc; }
+    for (int q = 0; q < n; q++) {
+        double acc = 0.0;
+        for (uint64_t i = 0; i < N; i++) acc += (i & qbit(n, q)) ? -y[i] : y[i];
+        out_z[q] = acc / shots;
+    }
+    free(y);
+    return 0;
+}

@@ -90,6 +90,26 @@ int  orc_finite_diff(int n, int G, const int *kinds, const int *wires, const dou
                      const uint64_t *z_mask, const double *coeff, double eps, double *grad);
 int  orc_num_threads(void);
 
+/* ---- shot noise, approximate (Gaussian) sampler ----------
+ * Counter-based random numbers (the library implements the same DEFINITION in
+ * its own code; nothing is shared):
+ *   splitmix64(x): x += 0x9E3779B97F4A7C15; x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9;
+ *                  x = (x ^ (x >> 27)) * 0x94D049BB133111EB; return x ^ (x >> 31)
+ *   uniform(seed, k) = (splitmix64(seed ^ (k * 0xD1B54A32D192ED03)) >> 11) * 2^-53
+ *   normal(seed, i)  = sqrt(-2 ln(1 - uniform(seed, 2i))) * cos(2 pi uniform(seed, 2i + 1))
+ * orc_gauss_sample: the approximate multinomial sample of `shots` shots over the
+ * 2^n canonical outcomes, y = shots p + sqrt(shots) D S z, written out as in the
+ * paper: p_i = |psi_i|^2, D = diag(sqrt p), u = sqrt p, v~ = e_K - u with K the
+ * last outcome (2^n - 1), v = v~ / ||v~|| (v = 0 if u = e_K), S = I - 2 v v^T (the
+ * Householder reflection; reading R21, PAPER.md:209 prints I - v v^T),
+ * z_i = normal(seed, i) for i < K and z_K = 0.  out_y: 2^n values.
+ * orc_gauss_z: the per-qubit estimates Z_q = (1/shots) sum_i y_i (-1)^{bit of
+ * qubit q in i} (measure_allZ with shots). */
+double orc_uniform(uint64_t seed, uint64_t k);
+double orc_normal(uint64_t seed, uint64_t i);
+int  orc_gauss_sample(const double *psi, int n, double shots, uint64_t seed, double *out_y);
+int  orc_gauss_z(const double *psi, int n, double shots, uint64_t seed, double *out_z);
+
 #ifdef __cplusplus
 }
 #endif
