@@ -231,6 +231,25 @@ int tqd_expval(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_
 int tqd_adjoint_grad(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_t *z_mask,
                      const double *coeff, double *out_value, double *out_grad, int n_grad);
 
+/* Shot noise, approximate sampler: the multinomial sample of
+ * `shots` measurements of all qubits is replaced by its Gaussian limit
+ * y = shots p + sqrt(shots) D S z over the 2^n canonical outcomes (D = diag sqrt p,
+ * S the Householder reflection mapping e_K <-> sqrt p, K = 2^n - 1; reading R21),
+ * with z_i = normal(seed + b, i) from the counter-based generator of DESIGN.md
+ * §8c (splitmix64 + Box-Muller, indexed by the canonical outcome i, so the result
+ * does not depend on the sharding).  out[b * n + q] = (1/shots) sum_i y_i (-1)^{q
+ * bit of i}: the noisy <Z_q> estimate of measure_allZ(shots).
+ * y is never materialised: the estimates follow from O(n) global sums.
+ * Collective. */
+int tqd_sample_gaussian_z(tqd_state *st, double shots, uint64_t seed, double *out);
+
+/* The differentiable (reparameterised) counterpart: value
+ * L = sum_b sum_q coeff[b * n + q] Zhat_{b,q} (coeff NULL = all 1) with the same
+ * z as tqd_sample_gaussian_z(seed), and out_grad[p] = dL/dtheta_p by the adjoint
+ * sweep seeded with lambda = dL/dpsi*.  CONSUMES the state.  Collective. */
+int tqd_adjoint_grad_gaussian(tqd_state *st, double shots, uint64_t seed, const double *coeff, double *out_value,
+                              double *out_grad, int n_grad);
+
 /* Execute pending gates and copy amplitudes [first, first+count) in CANONICAL
  * order (MoveDim^{-1} of PAPER.md:116-119 applied through pi) to host_out
  * (count complex values of the state's dtype, interleaved re, im).  Every rank

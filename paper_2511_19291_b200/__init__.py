@@ -70,6 +70,9 @@ _SIG = {
     "tqd_state_init": [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, ctypes.POINTER(_P)],
     "tqd_state_init_batch": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
     "tqd_apply_gate_batch": [_P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int],
+    "tqd_sample_gaussian_z": [_P, ctypes.c_double, ctypes.c_uint64, _P],
+    "tqd_adjoint_grad_gaussian": [_P, ctypes.c_double, ctypes.c_uint64, _P, ctypes.POINTER(ctypes.c_double), _P,
+                                  ctypes.c_int],
     "tqd_state_reset": [_P],
     "tqd_state_rewind": [_P],
     "tqd_state_free": [_P],
@@ -241,6 +244,22 @@ def tqd_adjoint_grad(st, terms, n_grad: int | None = None, coeff=None):
     return val.value, g[:n_grad]
 
 
+def tqd_sample_gaussian_z(st, n: int, shots: float, seed: int, batch: int = 1) -> np.ndarray:
+    out = np.zeros(batch * n, dtype=np.float64)
+    _call("tqd_sample_gaussian_z", st, float(shots), int(seed), _ptr(out))
+    return out if batch == 1 else out.reshape(batch, n)
+
+
+def tqd_adjoint_grad_gaussian(st, shots: float, seed: int, coeff=None, n_grad: int | None = None):
+    if n_grad is None:
+        n_grad = tqd_num_params(st)
+    c = None if coeff is None else _arr(np.asarray(coeff, dtype=np.float64).reshape(-1), np.float64)
+    g = np.zeros(max(n_grad, 1), dtype=np.float64)
+    val = ctypes.c_double()
+    _call("tqd_adjoint_grad_gaussian", st, float(shots), int(seed), _ptr(c), ctypes.byref(val), _ptr(g), n_grad)
+    return val.value, g[:n_grad]
+
+
 def tqd_get_amplitudes(st, first: int, count: int, dtype: int) -> np.ndarray:
     out = np.zeros(count, dtype=np.complex128 if dtype == C128 else np.complex64)
     _call("tqd_get_amplitudes", st, first, count, _ptr(out))
@@ -383,6 +402,14 @@ class State:
         if count is None:
             count = (self.batch << self.n) - first
         return tqd_get_amplitudes(self.handle, first, count, self.dtype)
+
+    def sample_gaussian_z(self, shots: float, seed: int) -> np.ndarray:
+        """Noisy <Z_q> estimates from the approximate shot sample."""
+        return tqd_sample_gaussian_z(self.handle, self.n, shots, seed, self.batch)
+
+    def adjoint_grad_gaussian(self, shots: float, seed: int, coeff=None):
+        """(L, dL/dtheta) for L = sum coeff * Zhat (reparameterised, differentiable)."""
+        return tqd_adjoint_grad_gaussian(self.handle, shots, seed, coeff)
 
     def metrics(self) -> dict:
         return tqd_get_metrics(self.handle)

@@ -35,6 +35,11 @@ cudaError_t launch_lambda_add_xy(bool dbl, const void *psi, const void *peer, vo
                                  int T, double *eout, cudaStream_t s);
 cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
                           cudaStream_t s);
+cudaError_t launch_gauss_sums(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const GatherMap &gm, uint64_t seed,
+                              const int *qpos, int nq, double *out, cudaStream_t s);
+cudaError_t launch_lambda_gauss(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const GatherMap &gm,
+                                uint64_t seed, const ZTerms &t, double alpha, double fc, double k2, double kc,
+                                cudaStream_t s);
 cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
 cudaError_t launch_remap_pack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s);
 cudaError_t launch_remap_unpack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s);
@@ -992,6 +997,50 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
     return ev_collect(st);
 }
 
+// The adjoint reverse sweep (lambda already seeded) and the
+// gradient / value readback; value_host is added to the device-accumulated value.
+static int reverse_and_collect(tqd_state *st, double *d_grad, int n_grad, double value_host, double *out_value,
+                               double *out_grad) {
+    tqd_ctx *c = st->ctx;
+    int rc;
+    // reverse sweep down to (and including) the earliest stage holding a trainable gate
+    int first = -1;
+    for (size_t i = 0; i < st->history.size() && first < 0; i++) {
+        const Stage &s = st->history[i];
+        const std::vector<POp> *ops = s.type == ST_SWEEP ? &s.sw.ops : s.type == ST_SMALL ? &s.sm.ops : nullptr;
+        if (!ops) continue;
+        for (const POp &o : *ops)
+            if (st->gates[o.gate].ngen) { first = (int)i; break; }
+    }
+    if (first >= 0) {
+        // backward stage list = the forward history reversed; its descriptors are
+        // cached with the forward plan when the history is the cached one
+        const bool cacheable = st->history_cached && st->fwd_cache_version == st->tape_version;
+        if (!(cacheable && st->bwd_cache_version == st->tape_version && st->enc_bwd->valid)) {
+            st->rev_stages.clear();
+            for (int i = (int)st->history.size() - 1; i >= first; i--) st->rev_stages.push_back(st->history[i]);
+            Encoded &E = cacheable ? *st->enc_bwd : *st->enc_tmp;
+            rc = encode_upload(st, st->rev_stages, true, E);
+            if (rc) return rc;
+            st->bwd_cache_version = cacheable ? st->tape_version : ~0ull;
+            rc = launch_encoded(st, st->rev_stages, true, E, d_grad);
+        } else {
+            rc = launch_encoded(st, st->rev_stages, true, *st->enc_bwd, d_grad);
+        }
+        if (rc) return rc;
+    }
+    rc = allreduce_sum(st, st->d_red, (size_t)n_grad + 1);
+    if (rc) return rc;
+    std::vector<double> h(n_grad + 1);
+    CUDA_TRY(st, cudaMemcpyAsync(h.data(), st->d_red, (n_grad + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    st->met.d2h_bytes += (n_grad + 1) * sizeof(double);
+    *out_value = h[0] + value_host;
+    for (int p = 0; p < n_grad; p++) out_grad[p] = h[p + 1];
+    st->consumed = true;
+    return ev_collect(st);
+}
+
 int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff, double *out_value,
                      double *out_grad, int n_grad) {
     int rc = check_live(st);
@@ -1095,42 +1144,141 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
             }
         }
     }
-    // reverse sweep down to (and including) the earliest stage holding a trainable gate
-    int first = -1;
-    for (size_t i = 0; i < st->history.size() && first < 0; i++) {
-        const Stage &s = st->history[i];
-        const std::vector<POp> *ops = s.type == ST_SWEEP ? &s.sw.ops : s.type == ST_SMALL ? &s.sm.ops : nullptr;
-        if (!ops) continue;
-        for (const POp &o : *ops)
-            if (st->gates[o.gate].ngen) { first = (int)i; break; }
+    return reverse_and_collect(st, d_grad, n_grad, 0.0, out_value, out_grad);
+}
+
+// ---- shot noise: approximate (Gaussian) sampler, PAPER.md:200-218 -----------
+// For batch element b (seed + b): the global sums of the sample's closed form
+// (DESIGN.md §8c): m_q = <Z_q>, A_q = sum_i u_i z_i s_q(i), B = sum_i u_i z_i and
+// psi at the last canonical outcome K; one reduction pass per 16 qubits.
+struct GaussStats {
+    std::vector<double> m, A;
+    double B = 0, uK = 0, pKr = 0, pKi = 0;
+};
+
+static GatherMap canon_map(const tqd_state *st) {
+    GatherMap gm;
+    memset(&gm, 0, sizeof(gm));
+    gm.n = st->n;
+    gm.n_loc = st->n_loc;
+    gm.rank = (uint64_t)st->ctx->rank;
+    for (int b = 0; b < st->n; b++) gm.phys_of_canon_bit[b] = (uint8_t)st->pos[st->n - 1 - b];
+    return gm;
+}
+
+static int gauss_stats(tqd_state *st, int b, uint64_t seed, GaussStats &gs) {
+    tqd_ctx *c = st->ctx;
+    const uint64_t N = 1ull << st->n_loc;
+    const GatherMap gm = canon_map(st);
+    const void *psi_b = (char *)st->psi + (size_t)b * shard_bytes(st);
+    int rc = ensure_red(st, 40);
+    if (rc) return rc;
+    gs.m.assign(st->n, 0.0);
+    gs.A.assign(st->n, 0.0);
+    for (int q0 = 0; q0 < st->n; q0 += 16) {
+        const int nq = std::min(16, st->n - q0);
+        int qpos[16];
+        for (int i = 0; i < nq; i++) qpos[i] = st->pos[q0 + i];
+        CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, 35 * sizeof(double), c->stream));
+        const int ev = ev_begin(st, CAT_OTHER);
+        CUDA_TRY(st, launch_gauss_sums(st->dbl, psi_b, N, rank_hi(st), gm, seed, qpos, nq, st->d_red, c->stream));
+        ev_end(st, ev);
+        rc = allreduce_sum(st, st->d_red, 35);
+        if (rc) return rc;
+        double h[35];
+        CUDA_TRY(st, cudaMemcpyAsync(h, st->d_red, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+        st->met.hbm_bytes += N * st->esz;
+        st->met.kernel_launches++;
+        st->met.d2h_bytes += sizeof(h);
+        for (int i = 0; i < nq; i++) { gs.m[q0 + i] = h[i]; gs.A[q0 + i] = h[16 + i]; }
+        gs.B = h[32];
+        gs.pKr = h[33];
+        gs.pKi = h[34];
     }
-    if (first >= 0) {
-        // backward stage list = the forward history reversed; its descriptors are
-        // cached with the forward plan when the history is the cached one
-        const bool cacheable = st->history_cached && st->fwd_cache_version == st->tape_version;
-        if (!(cacheable && st->bwd_cache_version == st->tape_version && st->enc_bwd->valid)) {
-            st->rev_stages.clear();
-            for (int i = (int)st->history.size() - 1; i >= first; i--) st->rev_stages.push_back(st->history[i]);
-            Encoded &E = cacheable ? *st->enc_bwd : *st->enc_tmp;
-            rc = encode_upload(st, st->rev_stages, true, E);
-            if (rc) return rc;
-            st->bwd_cache_version = cacheable ? st->tape_version : ~0ull;
-            rc = launch_encoded(st, st->rev_stages, true, E, d_grad);
-        } else {
-            rc = launch_encoded(st, st->rev_stages, true, *st->enc_bwd, d_grad);
-        }
+    gs.uK = std::sqrt(gs.pKr * gs.pKr + gs.pKi * gs.pKi);
+    return TQD_OK;
+}
+
+// Zhat_q = m_q + (A_q + B F_q) / sqrt(shots),  F_q = (u_K s_q(K) - m_q) / (1 - u_K),
+// s_q(K) = -1 (K = 1...1); the degenerate state u_K = 1 has no noise (v = 0).
+static double gauss_F(const GaussStats &gs, int q) {
+    const double D = 1.0 - gs.uK;
+    return D > 1e-14 ? (-gs.uK - gs.m[q]) / D : 0.0;
+}
+
+int tqd_sample_gaussian_z(tqd_state *st, double shots, uint64_t seed, double *out) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (!out) return fail(TQD_ERR_ARG, "out is NULL");
+    if (!(shots > 0)) return fail(TQD_ERR_ARG, "shots must be > 0");
+    rc = execute_pending(st);
+    if (rc) return rc;
+    for (int b = 0; b < st->batch; b++) {
+        GaussStats gs;
+        rc = gauss_stats(st, b, seed + (uint64_t)b, gs);
+        if (rc) return rc;
+        for (int q = 0; q < st->n; q++)
+            out[(size_t)b * st->n + q] = gs.m[q] + (gs.A[q] + gs.B * gauss_F(gs, q)) / std::sqrt(shots);
+    }
+    return ev_collect(st);
+}
+
+int tqd_adjoint_grad_gaussian(tqd_state *st, double shots, uint64_t seed, const double *coeff, double *out_value,
+                              double *out_grad, int n_grad) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (!out_value) return fail(TQD_ERR_ARG, "out_value is NULL");
+    if (!(shots > 0)) return fail(TQD_ERR_ARG, "shots must be > 0");
+    if (n_grad != st->n_params) return fail(TQD_ERR_ARG, "n_grad != tqd_num_params");
+    if (n_grad > 0 && !out_grad) return fail(TQD_ERR_ARG, "out_grad is NULL");
+    rc = execute_pending(st);
+    if (rc) return rc;
+    rc = ensure_lambda(st);
+    if (rc) return rc;
+    // statistics of every element first (their reduction scratch is reused below)
+    std::vector<GaussStats> all(st->batch);
+    for (int b = 0; b < st->batch; b++) {
+        rc = gauss_stats(st, b, seed + (uint64_t)b, all[b]);
         if (rc) return rc;
     }
-    rc = allreduce_sum(st, st->d_red, (size_t)n_grad + 1);
+    rc = ensure_red(st, (size_t)n_grad + 1);
     if (rc) return rc;
-    std::vector<double> h(n_grad + 1);
-    CUDA_TRY(st, cudaMemcpyAsync(h.data(), st->d_red, (n_grad + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(st, cudaStreamSynchronize(c->stream));
-    st->met.d2h_bytes += (n_grad + 1) * sizeof(double);
-    *out_value = h[0];
-    for (int p = 0; p < n_grad; p++) out_grad[p] = h[p + 1];
-    st->consumed = true;
-    return ev_collect(st);
+    tqd_ctx *c = st->ctx;
+    CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, (n_grad + 1) * sizeof(double), c->stream));
+    const GatherMap gm = canon_map(st);
+    const uint64_t N = 1ull << st->n_loc;
+    const double rs = std::sqrt(shots);
+    double value = 0.0;
+    for (int b = 0; b < st->batch; b++) {
+        const GaussStats &gs = all[b];
+        const double *cb = coeff ? coeff + (size_t)b * st->n : nullptr;
+        // lambda = dL/dpsi* of L = sum_q c_q Zhat_q
+        ZTerms zt;
+        memset(&zt, 0, sizeof(zt));
+        double fc = 0.0, sK = 0.0;
+        for (int q = 0; q < st->n; q++) {
+            const double cq = cb ? cb[q] : 1.0;
+            zt.cst += cq;
+            zt.w[st->pos[q]] += cq;
+            fc += cq * gauss_F(gs, q);
+            sK -= cq;
+            value += cq * (gs.m[q] + (gs.A[q] + gs.B * gauss_F(gs, q)) / rs);
+        }
+        const double D = 1.0 - gs.uK;
+        const double alpha = D > 1e-14 ? 1.0 - gs.B / (rs * D) : 1.0;
+        const double kc = D > 1e-14 ? gs.B / (2.0 * rs * D) * (sK + fc) : 0.0;
+        const int ev = ev_begin(st, CAT_OTHER);
+        CUDA_TRY(st, launch_lambda_gauss(st->dbl, (char *)st->psi + (size_t)b * shard_bytes(st),
+                                         (char *)st->lam + (size_t)b * shard_bytes(st), N, rank_hi(st), gm,
+                                         seed + (uint64_t)b, zt, alpha, fc, 0.5 / rs, kc, c->stream));
+        ev_end(st, ev);
+        st->met.hbm_bytes += 2 * N * st->esz;
+        st->met.kernel_launches++;
+    }
+    return reverse_and_collect(st, st->d_red + 1, n_grad, value, out_value, out_grad);
 }
 
 int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host_out) {

@@ -230,6 +230,103 @@ __global__ void __launch_bounds__(256) lambda_add_xy_kernel(const typename CT<Re
     if (threadIdx.x == 0) atomicAdd(eout, tot);
 }
 
+// ---------------------------------------------------------------------------
+// Shot noise, approximate (Gaussian) sampler.  Counter-based
+// normals indexed by the CANONICAL outcome (so results do not depend on the qubit
+// map pi or the sharding): splitmix64 + Box-Muller, fp64 (R21, R22).
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ double uniform_d(uint64_t seed, uint64_t k) {
+    return (double)(splitmix64_d(seed ^ (k * 0xD1B54A32D192ED03ull)) >> 11) * 0x1.0p-53;
+}
+__device__ __forceinline__ double normal_d(uint64_t seed, uint64_t i) {
+    const double u1 = uniform_d(seed, 2 * i), u2 = uniform_d(seed, 2 * i + 1);
+    return sqrt(-2.0 * log(1.0 - u1)) * cospi(2.0 * u2);
+}
+__device__ __forceinline__ uint64_t canon_of(uint64_t P, const GatherMap &gm) {
+    uint64_t c = 0;
+    for (int b = 0; b < gm.n; b++) c |= ((P >> gm.phys_of_canon_bit[b]) & 1ull) << b;
+    return c;
+}
+
+// Global sums of the sample's per-qubit estimates for up to 16 qubits (physical
+// positions qpos): out[q] += sum p s_q, out[16 + q] += sum u z s_q, out[32] += sum u z,
+// out[33..34] = psi at the last canonical outcome K (written by its owner only).
+struct GaussQ {
+    int nq;
+    uint8_t qpos[16];
+};
+template <typename Real>
+__global__ void __launch_bounds__(256) gauss_sums_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n,
+                                                         uint64_t rank_hi, GatherMap gm, uint64_t seed, GaussQ gq,
+                                                         double *__restrict__ out) {
+    typedef typename CT<Real>::C C;
+    __shared__ double red[32];
+    double m[16], A[16], B = 0;
+#pragma unroll
+    for (int q = 0; q < 16; q++) m[q] = A[q] = 0;
+    const uint64_t K = (gm.n >= 64) ? ~0ull : ((1ull << gm.n) - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t P = i | rank_hi;
+        const C x = psi[i];
+        const double p = (double)x.x * x.x + (double)x.y * x.y;
+        const uint64_t c = canon_of(P, gm);
+        const double uz = c == K ? 0.0 : sqrt(p) * normal_d(seed, c);
+        if (c == K) { out[33] = (double)x.x; out[34] = (double)x.y; }
+        B += uz;
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+            if (q < gq.nq) {
+                const bool neg = (P >> gq.qpos[q]) & 1ull;
+                m[q] += neg ? -p : p;
+                A[q] += neg ? -uz : uz;
+            }
+        }
+    }
+    for (int q = 0; q < gq.nq; q++) {
+        double t = block_sum<double>(m[q], red);
+        if (threadIdx.x == 0) atomicAdd(&out[q], t);
+        t = block_sum<double>(A[q], red);
+        if (threadIdx.x == 0) atomicAdd(&out[16 + q], t);
+    }
+    const double tb = block_sum<double>(B, red);
+    if (threadIdx.x == 0) atomicAdd(&out[32], tb);
+}
+
+// Adjoint seed of L = sum_q c_q Zhat_q (the derivative of the closed form in DESIGN.md
+// §8c w.r.t. psi*):  lambda_j = alpha S(j) psi_j + k2 z_j (S(j) + Fc) e_j + [j = K] kc e_K,
+// S(j) = sum_q c_q s_q(j) = cst - 2 sum_p w_p bit_p(j), e_j = psi_j / |psi_j|.
+template <typename Real>
+__global__ void __launch_bounds__(256) lambda_gauss_kernel(const typename CT<Real>::C *__restrict__ psi,
+                                                           typename CT<Real>::C *__restrict__ lam, uint64_t n,
+                                                           uint64_t rank_hi, GatherMap gm, uint64_t seed, ZTerms terms,
+                                                           double alpha, double fc, double k2, double kc) {
+    typedef typename CT<Real>::C C;
+    const uint64_t K = (gm.n >= 64) ? ~0ull : ((1ull << gm.n) - 1);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t P = i | rank_hi;
+        double s = terms.cst;
+        for (int b = 0; b < 64; b++)
+            if (terms.w[b] != 0.0 && ((P >> b) & 1ull)) s -= 2.0 * terms.w[b];
+        const C x = psi[i];
+        const double xr = x.x, xi = x.y, u = sqrt(xr * xr + xi * xi);
+        const uint64_t c = canon_of(P, gm);
+        double lr = alpha * s * xr, li = alpha * s * xi;
+        if (u > 0) {
+            double f = 0.0;
+            if (c != K) f += k2 * normal_d(seed, c) * (s + fc);
+            else f += kc;
+            lr += f * xr / u;
+            li += f * xi / u;
+        }
+        lam[i] = mk<C>((Real)lr, (Real)li);
+    }
+}
+
 // out[t] += sum_b |psi_b|^2 (-1)^{popc(b & z_t)}, up to 16 terms per launch
 template <typename Real>
 __global__ void __launch_bounds__(256) expval_z_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n,
@@ -446,6 +543,30 @@ cudaError_t launch_lambda_add_xy(bool dbl, const void *psi, const void *peer, vo
         lambda_add_xy_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (const float2 *)peer,
                                                                    (float2 *)lam, n, rank_hi, xloc, xfull, d_z, d_ny,
                                                                    d_c, T, eout);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gauss_sums(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const GatherMap &gm, uint64_t seed,
+                              const int *qpos, int nq, double *out, cudaStream_t s) {
+    GaussQ gq;
+    gq.nq = nq;
+    for (int q = 0; q < 16; q++) gq.qpos[q] = (uint8_t)(q < nq ? qpos[q] : 0);
+    const int th = 256;
+    if (dbl) gauss_sums_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, n, rank_hi, gm, seed, gq, out);
+    else gauss_sums_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, n, rank_hi, gm, seed, gq, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lambda_gauss(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const GatherMap &gm,
+                                uint64_t seed, const ZTerms &t, double alpha, double fc, double k2, double kc,
+                                cudaStream_t s) {
+    const int th = 256;
+    if (dbl)
+        lambda_gauss_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, (double2 *)lam, n, rank_hi, gm,
+                                                                   seed, t, alpha, fc, k2, kc);
+    else
+        lambda_gauss_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (float2 *)lam, n, rank_hi, gm,
+                                                                  seed, t, alpha, fc, k2, kc);
     return cudaGetLastError();
 }
 
