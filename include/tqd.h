@@ -231,6 +231,17 @@ int tqd_expval(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_
 int tqd_adjoint_grad(tqd_state *st, int n_terms, const uint64_t *x_mask, const uint64_t *z_mask,
                      const double *coeff, double *out_value, double *out_grad, int n_grad);
 
+/* Shot noise, exact sampler: `shots` measurements of all
+ * qubits.  out[b * shots + k] = the canonical outcome (basis index, MSB-first) of
+ * shot k of batch element b, identical on every rank.  Hierarchical multinomial:
+ * the groups are the ranks' shards; every rank learns the groups' masses q_j (one
+ * small all-reduce), draws the same uniforms u_k = uniform(seed + b, k) (counter-
+ * based, R22), assigns shot k to group j (y ~ Multinomial(shots, q)) and
+ * samples the outcomes of its own shots conditionally from its shard (inverse CDF
+ * over chunk masses, then inside the chunk on the device).  at most 2^32 shots.
+ * Collective. */
+int tqd_sample(tqd_state *st, uint64_t shots, uint64_t seed, uint64_t *out);
+
 /* Shot noise, approximate sampler: the multinomial sample of
  * `shots` measurements of all qubits is replaced by its Gaussian limit
  * y = shots p + sqrt(shots) D S z over the 2^n canonical outcomes (D = diag sqrt p,

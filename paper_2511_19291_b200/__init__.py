@@ -70,6 +70,7 @@ _SIG = {
     "tqd_state_init": [_P, ctypes.c_int, ctypes.c_int, _P, ctypes.c_size_t, ctypes.POINTER(_P)],
     "tqd_state_init_batch": [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
     "tqd_apply_gate_batch": [_P, ctypes.c_int, _P, ctypes.c_int, _P, ctypes.c_int],
+    "tqd_sample": [_P, ctypes.c_uint64, ctypes.c_uint64, _P],
     "tqd_sample_gaussian_z": [_P, ctypes.c_double, ctypes.c_uint64, _P],
     "tqd_adjoint_grad_gaussian": [_P, ctypes.c_double, ctypes.c_uint64, _P, ctypes.POINTER(ctypes.c_double), _P,
                                   ctypes.c_int],
@@ -244,6 +245,13 @@ def tqd_adjoint_grad(st, terms, n_grad: int | None = None, coeff=None):
     return val.value, g[:n_grad]
 
 
+def tqd_sample(st, shots: int, seed: int, batch: int = 1) -> np.ndarray:
+    out = np.zeros(max(batch * shots, 1), dtype=np.uint64)
+    _call("tqd_sample", st, int(shots), int(seed), _ptr(out))
+    out = out[:batch * shots]
+    return out if batch == 1 else out.reshape(batch, shots)
+
+
 def tqd_sample_gaussian_z(st, n: int, shots: float, seed: int, batch: int = 1) -> np.ndarray:
     out = np.zeros(batch * n, dtype=np.float64)
     _call("tqd_sample_gaussian_z", st, float(shots), int(seed), _ptr(out))
@@ -402,6 +410,10 @@ class State:
         if count is None:
             count = (self.batch << self.n) - first
         return tqd_get_amplitudes(self.handle, first, count, self.dtype)
+
+    def sample(self, shots: int, seed: int) -> np.ndarray:
+        """Exact shot sample: canonical outcomes."""
+        return tqd_sample(self.handle, shots, seed, self.batch)
 
     def sample_gaussian_z(self, shots: float, seed: int) -> np.ndarray:
         """Noisy <Z_q> estimates from the approximate shot sample."""

@@ -35,6 +35,11 @@ cudaError_t launch_lambda_add_xy(bool dbl, const void *psi, const void *peer, vo
                                  int T, double *eout, cudaStream_t s);
 cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
                           cudaStream_t s);
+cudaError_t launch_chunk_mass(bool dbl, const void *psi, uint64_t n_chunks, int csz, double *out, cudaStream_t s);
+cudaError_t launch_chunk_sample(bool dbl, const void *psi, int n_active, const uint64_t *chunk_id, const uint32_t *off,
+                                const double *r, const uint64_t *shot_idx, uint64_t rank_hi, const GatherMap &gm,
+                                int csz, double *out, cudaStream_t s);
+int sample_chunk_amps();
 cudaError_t launch_gauss_sums(bool dbl, const void *psi, uint64_t n, uint64_t rank_hi, const GatherMap &gm, uint64_t seed,
                               const int *qpos, int nq, double *out, cudaStream_t s);
 cudaError_t launch_lambda_gauss(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const GatherMap &gm,
@@ -1317,6 +1322,141 @@ int tqd_adjoint_grad_gaussian(tqd_state *st, double shots, uint64_t seed, const 
         st->met.kernel_launches++;
     }
     return reverse_and_collect(st, st->d_red + 1, n_grad, value, out_value, out_grad);
+}
+
+// ---- shot noise: exact hierarchical multinomial sampler, PAPER.md:184-198 ------
+// counter-based uniforms, the library's own implementation of the definition in
+// DESIGN.md R22 (splitmix64)
+static uint64_t sm64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+static double uniform01(uint64_t seed, uint64_t k) {
+    return (double)(sm64(seed ^ (k * 0xD1B54A32D192ED03ull)) >> 11) * 0x1.0p-53;
+}
+
+static int upload_bytes(tqd_state *st, void *&buf, size_t &cap, const void *src, size_t bytes) {
+    const size_t need = std::max<size_t>(bytes, 1);
+    if (cap < need) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        cap = 0;
+        if (cudaMalloc(&buf, need) != cudaSuccess) { cudaGetLastError(); return fail(TQD_ERR_OOM, "sampler scratch"); }
+        cap = need;
+    }
+    if (bytes) CUDA_TRY(st, cudaMemcpyAsync(buf, src, bytes, cudaMemcpyHostToDevice, st->ctx->stream));
+    st->met.h2d_bytes += bytes;
+    return TQD_OK;
+}
+#define UPLOAD(st, buf, cap, vec) upload_bytes(st, buf, cap, (vec).data(), (vec).size() * sizeof((vec)[0]))
+
+int tqd_sample(tqd_state *st, uint64_t shots, uint64_t seed, uint64_t *out) {
+    int rc = check_live(st);
+    if (rc) return rc;
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (shots > 0 && !out) return fail(TQD_ERR_ARG, "out is NULL");
+    if (shots > (1ull << 32)) return fail(TQD_ERR_ARG, "at most 2^32 shots per call");
+    rc = execute_pending(st);
+    if (rc) return rc;
+    if (shots == 0) return ev_collect(st);
+    tqd_ctx *c = st->ctx;
+    const uint64_t N = 1ull << st->n_loc;
+    const int csz = (int)std::min<uint64_t>((uint64_t)sample_chunk_amps(), N);
+    const uint64_t n_chunks = N / (uint64_t)csz;
+    const GatherMap gm = canon_map(st);
+    void *d_mass = nullptr, *d_cid = nullptr, *d_off = nullptr, *d_r = nullptr, *d_idx = nullptr, *d_out = nullptr;
+    size_t c_mass = 0, c_cid = 0, c_off = 0, c_r = 0, c_idx = 0;
+    auto cleanup = [&]() {
+        for (void *p : {d_mass, d_cid, d_off, d_r, d_idx, d_out}) if (p) cudaFree(p);
+    };
+    if (cudaMalloc(&d_out, shots * sizeof(double)) != cudaSuccess || cudaMalloc(&d_mass, n_chunks * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        return fail(TQD_ERR_OOM, "sampler buffers");
+    }
+    rc = ensure_red(st, (size_t)c->world);
+    if (rc) { cleanup(); return rc; }
+    std::vector<double> host(shots);
+    for (int b = 0; b < st->batch && rc == TQD_OK; b++) {
+        const void *psi_b = (char *)st->psi + (size_t)b * shard_bytes(st);
+        const uint64_t sb = seed + (uint64_t)b;
+        // 1. probability mass of every chunk of the local shard
+        std::vector<double> mass(n_chunks);
+        if (launch_chunk_mass(st->dbl, psi_b, n_chunks, csz, (double *)d_mass, c->stream) != cudaSuccess ||
+            cudaMemcpyAsync(mass.data(), d_mass, n_chunks * sizeof(double), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+            cudaStreamSynchronize(c->stream) != cudaSuccess) {
+            cleanup();
+            c->poisoned = true;
+            return fail(TQD_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
+        }
+        st->met.hbm_bytes += N * st->esz;
+        st->met.kernel_launches++;
+        double qloc = 0;
+        for (double m : mass) qloc += m;
+        // 2. the groups' masses q_j (one per rank) on every rank
+        std::vector<double> q(c->world, 0.0);
+        q[c->rank] = qloc;
+        CUDA_TRY(st, cudaMemcpyAsync(st->d_red, q.data(), c->world * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        rc = allreduce_sum(st, st->d_red, c->world);
+        if (rc) { cleanup(); return rc; }
+        CUDA_TRY(st, cudaMemcpyAsync(q.data(), st->d_red, c->world * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+        std::vector<double> Q(c->world + 1, 0.0);
+        for (int j = 0; j < c->world; j++) Q[j + 1] = Q[j] + q[j];
+        int last_pos = 0;  // rank of the last positive mass (rounding guard)
+        for (int j = 0; j < c->world; j++) if (q[j] > 0) last_pos = j;
+        // 3. shared seed: every rank draws the same uniforms; shot k goes to group j with
+        //    Q_j <= u_k Q_W < Q_{j+1} (y ~ Multinomial(shots, q)); the residual is uniform
+        //    on the group's mass, i.e. the conditional sample of PAPER.md:194-196
+        std::vector<std::pair<double, uint64_t>> mine;
+        for (uint64_t kk = 0; kk < shots; kk++) {
+            const double u = uniform01(sb, kk) * Q[c->world];
+            int j = (int)(std::upper_bound(Q.begin() + 1, Q.end(), u) - (Q.begin() + 1));
+            if (j >= c->world || q[j] <= 0) j = std::min(j, last_pos);
+            while (q[j] <= 0 && j > 0) j--;
+            if (j == c->rank) mine.push_back({std::min(u - Q[j], q[j]), kk});
+        }
+        std::sort(mine.begin(), mine.end());
+        // 4. local: chunk of every shot from the chunks' prefix masses, residual inside it
+        std::vector<uint64_t> cid, sidx;
+        std::vector<uint32_t> off;
+        std::vector<double> rr;
+        double pre = 0;
+        uint64_t ch = 0;
+        uint64_t last_nz = 0;
+        for (uint64_t i = 0; i < n_chunks; i++) if (mass[i] > 0) last_nz = i;
+        for (size_t s = 0; s < mine.size(); s++) {
+            const double u = mine[s].first;
+            while (ch < last_nz && (pre + mass[ch] <= u || mass[ch] <= 0)) { pre += mass[ch]; ch++; }
+            if (cid.empty() || cid.back() != ch) { cid.push_back(ch); off.push_back((uint32_t)rr.size()); }
+            rr.push_back(u - pre);
+            sidx.push_back(mine[s].second);
+        }
+        off.push_back((uint32_t)rr.size());
+        CUDA_TRY(st, cudaMemsetAsync(d_out, 0, shots * sizeof(double), c->stream));
+        if ((rc = UPLOAD(st, d_cid, c_cid, cid)) || (rc = UPLOAD(st, d_off, c_off, off)) ||
+            (rc = UPLOAD(st, d_r, c_r, rr)) || (rc = UPLOAD(st, d_idx, c_idx, sidx))) {
+            cleanup();
+            return rc;
+        }
+        const int ev = ev_begin(st, CAT_OTHER);
+        CUDA_TRY(st, launch_chunk_sample(st->dbl, psi_b, (int)cid.size(), (const uint64_t *)d_cid, (const uint32_t *)d_off,
+                                         (const double *)d_r, (const uint64_t *)d_idx, rank_hi(st), gm, csz,
+                                         (double *)d_out, c->stream));
+        ev_end(st, ev);
+        st->met.kernel_launches++;
+        // 5. every rank wrote its own shots; the sum assembles all of them everywhere
+        rc = allreduce_sum(st, (double *)d_out, shots);
+        if (rc) { cleanup(); return rc; }
+        CUDA_TRY(st, cudaMemcpyAsync(host.data(), d_out, shots * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+        st->met.d2h_bytes += shots * sizeof(double);
+        for (uint64_t kk = 0; kk < shots; kk++) out[(size_t)b * shots + kk] = (uint64_t)host[kk];
+    }
+    cleanup();
+    return ev_collect(st);
 }
 
 int tqd_get_amplitudes(tqd_state *st, uint64_t first, uint64_t count, void *host_out) {

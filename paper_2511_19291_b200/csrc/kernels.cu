@@ -16,6 +16,8 @@
 // numbers (float2 for complex64, double2 for complex128), physical index =
 // local bits of the qubit map pi.  See DESIGN.md "Data layout".
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "common.cuh"
@@ -327,6 +329,89 @@ __global__ void __launch_bounds__(256) lambda_gauss_kernel(const typename CT<Rea
     }
 }
 
+// ---------------------------------------------------------------------------
+// Shot noise, exact: per-chunk probability masses, then every
+// chunk that received shots resolves them by a block prefix sum over its
+// probabilities and a search per shot (inverse CDF in the shard's physical order).
+constexpr int SAMPLE_CHUNK = 4096;
+
+template <typename Real>
+__global__ void __launch_bounds__(256) chunk_mass_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n_chunks,
+                                                         int csz, double *__restrict__ out) {
+    typedef typename CT<Real>::C C;
+    __shared__ double red[32];
+    for (uint64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        double s = 0;
+        for (int i = threadIdx.x; i < csz; i += blockDim.x) {
+            const C x = psi[c * csz + i];
+            s += (double)x.x * x.x + (double)x.y * x.y;
+        }
+        s = block_sum<double>(s, red);
+        if (threadIdx.x == 0) out[c] = s;
+        __syncthreads();
+    }
+}
+
+// one CTA per chunk with shots: shots [off[j], off[j+1]) with residual uniforms
+// r (mass units inside the chunk, sorted); writes the canonical outcome of each
+template <typename Real>
+__global__ void __launch_bounds__(256) chunk_sample_kernel(const typename CT<Real>::C *__restrict__ psi,
+                                                           const uint64_t *__restrict__ chunk_id,
+                                                           const uint32_t *__restrict__ off, const double *__restrict__ r,
+                                                           const uint64_t *__restrict__ shot_idx, uint64_t rank_hi,
+                                                           GatherMap gm, int csz, double *__restrict__ out) {
+    typedef typename CT<Real>::C C;
+    __shared__ double cdf[SAMPLE_CHUNK];  // csz <= SAMPLE_CHUNK
+    __shared__ double wsum[32];
+    const uint64_t c = chunk_id[blockIdx.x];
+    // inclusive prefix of the chunk's probabilities (16 per thread, warp / block scan)
+    const int per = max(1, csz / (int)blockDim.x);  // <= 16 (blockDim = max(32, min(256, csz)))
+    double loc[16];
+    double acc = 0;
+    for (int j = 0; j < per; j++) {
+        const int e = threadIdx.x * per + j;
+        if (e < csz) {
+            const C x = psi[c * csz + e];
+            acc += (double)x.x * x.x + (double)x.y * x.y;
+        }
+        loc[j] = acc;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double incl = acc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        double v = lane < nw ? wsum[lane] : 0.0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        if (lane < nw) wsum[lane] = v;
+    }
+    __syncthreads();
+    const double before = (incl - acc) + (warp ? wsum[warp - 1] : 0.0);
+    for (int j = 0; j < per; j++)
+        if (threadIdx.x * per + j < csz) cdf[threadIdx.x * per + j] = before + loc[j];
+    __syncthreads();
+    for (uint32_t s = off[blockIdx.x] + threadIdx.x; s < off[blockIdx.x + 1]; s += blockDim.x) {
+        const double u = r[s];
+        int lo = 0, hi = csz - 1;  // first index with cdf > u (clamped to the chunk)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cdf[mid] > u) hi = mid;
+            else lo = mid + 1;
+        }
+        while (lo > 0 && cdf[lo] == cdf[lo - 1]) lo--;  // rounding at the chunk end: never a p = 0 outcome
+        const uint64_t P = (c * csz + lo) | rank_hi;
+        out[shot_idx[s]] = (double)canon_of(P, gm);
+    }
+}
+
 // out[t] += sum_b |psi_b|^2 (-1)^{popc(b & z_t)}, up to 16 terms per launch
 template <typename Real>
 __global__ void __launch_bounds__(256) expval_z_kernel(const typename CT<Real>::C *__restrict__ psi, uint64_t n,
@@ -569,6 +654,30 @@ cudaError_t launch_lambda_gauss(bool dbl, const void *psi, void *lam, uint64_t n
                                                                   seed, t, alpha, fc, k2, kc);
     return cudaGetLastError();
 }
+
+cudaError_t launch_chunk_mass(bool dbl, const void *psi, uint64_t n_chunks, int csz, double *out, cudaStream_t s) {
+    const int th = std::max(32, std::min(256, csz));
+    const int grid = (int)std::min<uint64_t>(n_chunks, 148 * 8);
+    if (dbl) chunk_mass_kernel<double><<<grid, th, 0, s>>>((const double2 *)psi, n_chunks, csz, out);
+    else chunk_mass_kernel<float><<<grid, th, 0, s>>>((const float2 *)psi, n_chunks, csz, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_sample(bool dbl, const void *psi, int n_active, const uint64_t *chunk_id, const uint32_t *off,
+                                const double *r, const uint64_t *shot_idx, uint64_t rank_hi, const GatherMap &gm,
+                                int csz, double *out, cudaStream_t s) {
+    if (n_active == 0) return cudaSuccess;
+    const int th = std::max(32, std::min(256, csz));
+    if (dbl)
+        chunk_sample_kernel<double><<<n_active, th, 0, s>>>((const double2 *)psi, chunk_id, off, r, shot_idx, rank_hi, gm,
+                                                           csz, out);
+    else
+        chunk_sample_kernel<float><<<n_active, th, 0, s>>>((const float2 *)psi, chunk_id, off, r, shot_idx, rank_hi, gm,
+                                                          csz, out);
+    return cudaGetLastError();
+}
+
+int sample_chunk_amps() { return SAMPLE_CHUNK; }
 
 cudaError_t launch_gather(bool dbl, const void *psi, void *out, uint64_t first, uint64_t count, const GatherMap &gm,
                           cudaStream_t s) {

@@ -164,3 +164,107 @@ def test_gaussian_emulated_world(tqd, orc, world):
         assert np.max(np.abs(z - ref)) < 1e-10
         assert abs(val - float(np.dot(coeff, ref))) < 1e-10
         assert np.max(np.abs(grad - gref)) < 1e-6
+
+
+
+# ---------------------------------------------------------------- exact sampler
+def chi2_pvalue(counts, p, shots):
+    """Pearson chi-square p-value of observed counts against probabilities p (bins with
+    expected < 5 merged)."""
+    from scipy.stats import chi2
+    exp = shots * p
+    order = np.argsort(exp)
+    obs_b, exp_b, ob, eb = [], [], 0.0, 0.0
+    for i in order:
+        ob += counts[i]
+        eb += exp[i]
+        if eb >= 5:
+            obs_b.append(ob); exp_b.append(eb); ob = eb = 0.0
+    if eb > 0 and exp_b:
+        obs_b[-1] += ob; exp_b[-1] += eb
+    obs_b, exp_b = np.array(obs_b), np.array(exp_b)
+    stat = float(np.sum((obs_b - exp_b) ** 2 / exp_b))
+    return float(chi2.sf(stat, len(obs_b) - 1))
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,k,small_max", [(4, None, None), (8, None, None), (13, 10, 0)])
+def test_exact_sampler_distribution(tqd, ctx, orc, n, k, small_max, dtype):
+    gates = W.hea(n, 2, seed=n) + W.random_circuit(n, 20, n)
+    shots = 200000
+    st = make(tqd, ctx, n, dtype, k, small_max)
+    st.apply_circuit(gates)
+    a = st.sample(shots, 5)
+    b = st.sample(shots, 5)
+    c = st.sample(shots, 6)
+    st.free()
+    assert a.shape == (shots,) and np.array_equal(a, b) and not np.array_equal(a, c)
+    p = np.abs(orc.run(n, gates)) ** 2
+    assert np.all(p[a] > 0)
+    counts = np.bincount(a.astype(np.int64), minlength=1 << n)
+    assert chi2_pvalue(counts, p, shots) > 1e-6
+
+
+def test_exact_sampler_ghz_and_basis(tqd, ctx):
+    n = 12
+    st = make(tqd, ctx, n, "c64", 9, 0)
+    st.apply_circuit([W.Gate("H", (0,))] + [W.Gate("CNOT", (q, q + 1)) for q in range(n - 1)])
+    s = st.sample(10000, 1)
+    st.reset()
+    st.apply_circuit([W.Gate("X", (0,)), W.Gate("X", (5,))])
+    t = st.sample(1000, 2)
+    st.free()
+    assert set(np.unique(s)) <= {0, (1 << n) - 1} and abs(np.mean(s == 0) - 0.5) < 0.03
+    assert np.all(t == (1 << (n - 1)) | (1 << (n - 6)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_exact_sampler_emulated_world(tqd, orc, world):
+    """Hierarchical sampling over ranks: every rank returns the same shots, with the
+    circuit's distribution (groups = shards)."""
+    n, shots = 11, 100000
+    gates = W.hea(n, 2, seed=world) + [W.Gate("H", (0,)), W.Gate("RY", (1,), (0.7,))]
+    lid = tqd.tqd_loopback_id()
+    res, err = [None] * world, [None] * world
+
+    def worker(r):
+        try:
+            ctx = tqd.Context(world, r, 0, lid)
+            try:
+                st = make(tqd, ctx, n, "c128", 9, 0)
+                st.apply_circuit(gates)
+                res[r] = st.sample(shots, 3)
+                st.free()
+            finally:
+                ctx.close()
+        except Exception:
+            err[r] = traceback.format_exc()
+
+    th = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    assert not any(err), "\n".join(e for e in err if e)
+    for r in range(1, world):
+        assert np.array_equal(res[r], res[0])
+    p = np.abs(orc.run(n, gates)) ** 2
+    counts = np.bincount(res[0].astype(np.int64), minlength=1 << n)
+    assert chi2_pvalue(counts, p, shots) > 1e-6
+
+
+def test_exact_sampler_batch(tqd, ctx, orc):
+    n, B, shots = 9, 3, 50000
+    ans = W.hea(n, 2, seed=2)
+    x = np.random.default_rng(4).uniform(0, 2.0, size=(n, B))
+    st = make(tqd, ctx, n, "c128", batch=B)
+    for q in range(n):
+        st.apply_batch("RY", [q], x[q].reshape(B, 1))
+    st.apply_circuit(ans)
+    s = st.sample(shots, 9)
+    st.free()
+    assert s.shape == (B, shots)
+    for b in range(B):
+        p = np.abs(orc.run(n, [W.Gate("RY", (q,), (float(x[q, b]),)) for q in range(n)] + ans)) ** 2
+        counts = np.bincount(s[b].astype(np.int64), minlength=1 << n)
+        assert chi2_pvalue(counts, p, shots) > 1e-6
