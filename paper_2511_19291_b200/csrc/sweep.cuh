@@ -411,6 +411,12 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
     }
 }
 
+// evict-first global accesses of the streamed shards (cache-streaming hints)
+__device__ __forceinline__ float2 ldcs_c(const float2 *p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ldcs_c(const double2 *p) { return __ldcs(p); }
+__device__ __forceinline__ void stcs_c(float2 *p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void stcs_c(double2 *p, double2 v) { __stcs(p, v); }
+
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
 template <typename Real, bool BWD>
 __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_LB_MINB_F32_BWD : TQD_LB_MINB_F32_FWD) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
@@ -568,8 +574,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] + c[ctz4(r)];
 #pragma unroll
             for (int r = 0; r < NR; r++) {
-                a[r] = psi[o[r]];
-                if (BWD) l[r] = lam[o[r]];
+                // streaming: read once per sweep, do not keep in L2 (the next tiles'
+                // prefetched lines must survive there)
+                a[r] = ldcs_c(psi + o[r]);
+                if (BWD) l[r] = ldcs_c(lam + o[r]);
             }
         }
         if (tile + gsz < S.n_tiles) {
@@ -657,8 +665,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             if (sc.m == 0) {
 #pragma unroll
                 for (int r = 0; r < NR; r++) {
-                    psi[o[r]] = a[r];
-                    if (BWD) lam[o[r]] = l[r];
+                    stcs_c(psi + o[r], a[r]);
+                    if (BWD) stcs_c(lam + o[r], l[r]);
                 }
             } else {
                 // fused remap: store to the post-remap owner (peer memory) and position
