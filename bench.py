@@ -15,10 +15,12 @@ value    = gate-amplitude updates per second of the whole job:
            (gates x 2^n) / (fwd+grad step time), device-timed with CUDA events
            on the library's stream, max over ranks, circuit + plan resident
            (tqd_state_rewind re-executes the recorded tape).
-e2e      = the same metric through the public C ABI per step: tqd_state_reset,
-           tqd_apply_gate x G from host arrays, tqd_adjoint_grad (plans, uploads
-           the plan descriptors host->device, runs, copies value + gradients
-           device->host); wall clock between synchronised barriers.
+e2e      = the same metric through the public C ABI per step, as in a training
+           loop (new angles every step): tqd_state_reset, tqd_apply_gate x G from
+           host arrays, tqd_adjoint_grad (reuses the cached plan structure,
+           rebuilds the op coefficients and uploads them host->device, runs,
+           copies value + gradients device->host); wall clock between
+           synchronised barriers.
 roofline = the dominant kernel (the fused adjoint sweep) from live CUDA-event
            timings of every launch: algorithmic bytes per launch (4 x 8 B x
            2^n_loc: read + write psi and lambda) / average launch time, against
@@ -59,6 +61,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--tile", type=int, default=0)
+    p.add_argument("--no-absorb", action="store_true",
+                   help="apply every gate (TQD_OPT_ABSORB_TAIL = 0) instead of absorbing the trailing "
+                        "diagonal / permutation gates into the Z observable")
     return p.parse_args()
 
 
@@ -211,6 +216,8 @@ def main():
     if args.tile:
         st.set_option(tqd.OPT_TILE_QUBITS, args.tile)
     st.set_option(tqd.OPT_PROFILE, 1)
+    if args.no_absorb:
+        st.set_option(tqd.OPT_ABSORB_TAIL, 0)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -278,13 +285,20 @@ def main():
     # end to end through the public ABI with host buffers
     e2e = None
     if not args.no_e2e:
+        # a training step: NEW angles every step (same ansatz structure), so the
+        # cached plan is reused but its op coefficients are rebuilt on the host and
+        # uploaded host->device inside the timed region (counted in h2d_bytes)
+        step_gates = [W.hea(n, args.depth, args.seed + 1 + i) for i in range(args.steps)]
+        st.reset()
+        st.apply_circuit(W.hea(n, args.depth, args.seed + 1000))
+        st.adjoint_grad(terms)  # warm: plan structure cached, as in a training loop
         st.reset_metrics()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for i in range(args.steps):
             st.reset()
-            st.apply_circuit(gates)
+            st.apply_circuit(step_gates[i])
             val, grad = st.adjoint_grad(terms)
         torch.cuda.synchronize()
         barrier()
@@ -312,6 +326,10 @@ def main():
                            "state_dtype": "complex64 (fp32 arithmetic, fp64 reductions)",
                            "parallelism": f"state sharded over {world} rank(s) by {g} global qubit(s)",
                            "l2": f"inputs larger than L2: {shard * 2 / 2**30:.0f} GiB psi+lambda per GPU",
+                           "gates_absorbed_per_step": m["gates_absorbed"] // args.steps,
+                           "absorption": "trailing diagonal/permutation gates folded into the Z observable "
+                                         "(Heisenberg picture; same value and gradients)" if not args.no_absorb
+                                         else "off: every gate applied",
                            "seed": args.seed},
                 "gpu_launches": int(m["kernel_launches"]),
                 "roofline": roofline,

@@ -91,9 +91,16 @@ typedef enum {
     TQD_OPT_PROFILE = 2,      /* 1: time every kernel with CUDA events (see tqd_metrics) */
     TQD_OPT_GRID_CTAS = 3,    /* persistent CTAs per launch (0 = auto: SMs x resident CTAs) */
     TQD_OPT_USE_GRAPH = 4,    /* 1: replay cached plans as CUDA graphs (default 0)      */
-    TQD_OPT_FUSED_REMAP = 5   /* 1: a remap right after a sweep is fused into it: the sweep
+    TQD_OPT_FUSED_REMAP = 5,  /* 1: a remap right after a sweep is fused into it: the sweep
                                * stores straight into the owners' peer memory (default 1);
                                * 0: pack -> all-to-all -> unpack                          */
+    TQD_OPT_ABSORB_TAIL = 6   /* 1 (default): tqd_adjoint_grad with Z-string terms absorbs the
+                               * circuit's trailing diagonal / permutation gates (RZ, CZ, CP,
+                               * X, Y, CNOT, SWAP ...) into the observable by conjugation
+                               * (Heisenberg picture, E = <psi|U^dag H U|psi>) instead of
+                               * applying and un-applying them; same value and gradients
+                               * (absorbed trainable gates are diagonal: gradient 0).
+                               * 0: apply every gate.                                      */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.
@@ -119,6 +126,7 @@ typedef struct tqd_metrics {
     uint64_t d2h_bytes;         /* device->host bytes (values, gradients, amplitudes) */
     uint64_t fused_remaps;      /* remaps done by the preceding sweep's peer-memory stores */
     uint64_t plans_reused;      /* executions that reused the plan of a structurally equal tape */
+    uint64_t gates_absorbed;    /* trailing gates absorbed into Z observables (TQD_OPT_ABSORB_TAIL) */
 } tqd_metrics;
 
 /* --- context ------------------------------------------------------------- */
@@ -286,6 +294,19 @@ const char *tqd_version(void);
 int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, const int *kinds, const int *wires,
                    const double *params, const double *mats, const int *trainable, char *json_out, size_t cap,
                    size_t *needed);
+
+/* Diagnostic, host only (no GPU): the observable absorption that
+ * tqd_adjoint_grad applies with TQD_OPT_ABSORB_TAIL (Heisenberg picture,
+ * E = <psi|U^dag H U|psi>; PAPER.md:226-231 seed, PAPER.md:308 Z observables).
+ * Circuit as in tqd_debug_plan; T Z-string masks z_in[T] (bit q = logical
+ * qubit q).  Writes the first absorbed gate index to *tail_begin (G if none),
+ * the conjugated masks z_out[T] and signs sign_out[T] (+1 / -1): then
+ * sum_t c_t <Z_{z_in[t]}> after all G gates equals
+ * sum_t c_t sign_out[t] <Z_{z_out[t]}> after gates [0, *tail_begin).
+ * TQD_ERR_ARG on bad sizes or NULL pointers; caller-owned arrays. */
+int tqd_debug_absorb(int n, int G, const int *kinds, const int *wires, const double *params, const double *mats,
+                     const int *trainable, int T, const uint64_t *z_in, uint64_t *z_out, double *sign_out,
+                     int *tail_begin);
 
 /* Diagnostic, host only: one rank's remap exchange schedule (PAPER.md:164, 261:
  * interchange global qubit positions gpos[0..m) with local positions

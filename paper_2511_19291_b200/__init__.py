@@ -28,7 +28,8 @@ GATES = {
     "RX": 14, "RY": 15, "RZ": 16, "U3": 17,
 }
 C64, C128 = 0, 1
-OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP = 0, 1, 2, 3, 4, 5
+OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP, OPT_ABSORB_TAIL = \
+    0, 1, 2, 3, 4, 5, 6
 ERRORS = {0: "TQD_OK", -1: "TQD_ERR_ARG", -2: "TQD_ERR_QUBITS", -3: "TQD_ERR_WORLD",
           -4: "TQD_ERR_NOT_UNITARY", -5: "TQD_ERR_OOM", -6: "TQD_ERR_CUDA", -7: "TQD_ERR_NCCL",
           -8: "TQD_ERR_UNSUPPORTED", -9: "TQD_ERR_STATE"}
@@ -50,7 +51,7 @@ class Metrics(ctypes.Structure):
         ("fwd_sweep_bytes", ctypes.c_uint64), ("bwd_sweep_bytes", ctypes.c_uint64),
         ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
         ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("fused_remaps", ctypes.c_uint64),
-        ("plans_reused", ctypes.c_uint64),
+        ("plans_reused", ctypes.c_uint64), ("gates_absorbed", ctypes.c_uint64),
     ]
 
     def as_dict(self):
@@ -88,6 +89,7 @@ _SIG = {
     "tqd_debug_plan": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                        _P, _P, _P, _P, _P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
     "tqd_debug_remap_schedule": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P],
+    "tqd_debug_absorb": [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P, _P, _P],
 }
 EXPORTS = list(_SIG) + ["tqd_last_error", "tqd_version"]
 
@@ -288,9 +290,7 @@ def tqd_last_error() -> str:
     return lib().tqd_last_error().decode()
 
 
-def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 10, c128: bool = False) -> dict:
-    """Planner diagnostic (host only, no GPU): stages of `gates` as a dict."""
-    import json
+def _gate_arrays(gates):
     G = len(gates)
     kinds = np.zeros(max(G, 1), np.int32)
     wires = np.zeros(2 * max(G, 1), np.int32)
@@ -306,6 +306,14 @@ def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 
             mats[32 * i:32 * i + 2 * mm.size:2] = mm.real
             mats[32 * i + 1:32 * i + 2 * mm.size:2] = mm.imag
         tr[i] = 1 if g.trainable else 0
+    return kinds, wires, params, mats, tr
+
+
+def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 10, c128: bool = False) -> dict:
+    """Planner diagnostic (host only, no GPU): stages of `gates` as a dict."""
+    import json
+    G = len(gates)
+    kinds, wires, params, mats, tr = _gate_arrays(gates)
     need = ctypes.c_size_t(0)
     cap = 1 << 16
     while True:
@@ -318,6 +326,20 @@ def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 
             cap = need.value
             continue
         raise TqdError(rc, tqd_last_error())
+
+
+def tqd_debug_absorb(n: int, gates, z_masks):
+    """Observable absorption of tqd_adjoint_grad (host only, no GPU):
+    (tail_begin, z_out, sign_out) -- see include/tqd.h tqd_debug_absorb."""
+    kinds, wires, params, mats, tr = _gate_arrays(gates)
+    T = len(z_masks)
+    zin = np.array(list(z_masks) or [0], np.uint64)
+    zout = np.zeros(max(T, 1), np.uint64)
+    sg = np.zeros(max(T, 1), np.float64)
+    tb = ctypes.c_int(0)
+    _call("tqd_debug_absorb", n, len(gates), _ptr(kinds), _ptr(wires), _ptr(params), _ptr(mats), _ptr(tr), T,
+          _ptr(zin), _ptr(zout), _ptr(sg), ctypes.byref(tb))
+    return tb.value, [int(v) for v in zout[:T]], sg[:T].copy()
 
 
 def tqd_debug_remap_schedule(rank: int, n_loc: int, gpos, lpos):

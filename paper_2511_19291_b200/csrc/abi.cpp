@@ -88,7 +88,7 @@ struct tqd_state {
     std::vector<int> pos;
     bool consumed = false;
     // options
-    int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1;
+    int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1, opt_absorb = 1;
     // fused sweep -> remap (peer memory): every rank's psi / recv and lambda / send
     // allocations, shared once; the current roles are looked up by pointer identity
     std::vector<void *> peer_psi, peer_lam;  // [rank * 2 + i], i = 0: first psi / lam, 1: recv / send
@@ -105,6 +105,7 @@ struct tqd_state {
     std::vector<int> cached_pos;
     uint64_t plan_sig = 0;  // plan_signature of cached_stages
     uint64_t fwd_vhash = 0, bwd_vhash = 0;  // tape_values_hash of the resident descriptors
+    uint64_t cached_tmix = 0;  // absorbed-tail length mix of the cached plan (execute_pending)
     struct Encoded *enc_fwd = nullptr, *enc_bwd = nullptr, *enc_tmp = nullptr;
     // profiling
     std::vector<cudaEvent_t> ev_pool;
@@ -579,10 +580,18 @@ static uint64_t tape_values_hash(const tqd_state *st) {
     return h;
 }
 
-static int execute_pending(tqd_state *st) {
-    if (st->executed == st->gates.size()) return TQD_OK;
+// Execute the recorded gates [executed, end).  end < gates.size() only from
+// tqd_adjoint_grad: the gates [end, size) were absorbed into the observable
+// (absorb_tail) and are never applied; the plan caches are keyed by that split.
+static int execute_pending(tqd_state *st, size_t end = SIZE_MAX) {
+    if (end > st->gates.size()) end = st->gates.size();
+    if (st->executed >= end) {
+        st->executed = st->gates.size();
+        return TQD_OK;
+    }
+    const uint64_t tmix = (uint64_t)(st->gates.size() - end) * 0x9E3779B97F4A7C15ull;
     if (st->executed == 0 && st->fwd_cache_version != st->tape_version && st->enc_fwd->valid &&
-        !st->cached_stages.empty()) {
+        !st->cached_stages.empty() && st->cached_tmix == tmix) {
         const uint64_t vh = tape_values_hash(st);
         if (vh == st->fwd_vhash) {
             st->fwd_cache_version = st->tape_version;
@@ -590,7 +599,8 @@ static int execute_pending(tqd_state *st) {
             st->met.plans_reused++;
         }
     }
-    if (st->executed == 0 && st->fwd_cache_version == st->tape_version && st->enc_fwd->valid) {
+    if (st->executed == 0 && st->fwd_cache_version == st->tape_version && st->enc_fwd->valid &&
+        st->cached_tmix == tmix) {
         // replay of the same tape from |0..0> (tqd_state_rewind): plan + descriptors are resident
         st->history = st->cached_stages;
         int rc = launch_encoded(st, st->history, false, *st->enc_fwd, nullptr);
@@ -601,11 +611,11 @@ static int execute_pending(tqd_state *st) {
         return TQD_OK;
     }
     std::vector<int> pending;
-    for (size_t i = st->executed; i < st->gates.size(); i++) pending.push_back((int)i);
+    for (size_t i = st->executed; i < end; i++) pending.push_back((int)i);
     std::vector<Stage> stages;
     std::string err;
     const bool from_zero = st->executed == 0;
-    const uint64_t sig = from_zero ? plan_signature(st->gates, plan_cfg(st)) : 0;
+    const uint64_t sig = from_zero ? plan_signature(st->gates, plan_cfg(st)) ^ tmix : 0;
     if (from_zero && !st->cached_stages.empty() && sig == st->plan_sig) {
         // same circuit structure, new parameter values: reuse the plan
         stages = st->cached_stages;
@@ -626,6 +636,7 @@ static int execute_pending(tqd_state *st) {
         st->cached_stages = stages;
         st->cached_pos = st->pos;
         st->plan_sig = sig;
+        st->cached_tmix = tmix;
         st->fwd_cache_version = st->tape_version;
         st->fwd_vhash = tape_values_hash(st);
         st->bwd_cache_version = ~0ull;
@@ -884,6 +895,7 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
         st->opt_grid = (int)v; return TQD_OK;
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
     default: return fail(TQD_ERR_ARG, "unknown option");
     }
 }
@@ -1084,6 +1096,50 @@ static int reverse_and_collect(tqd_state *st, double *d_grad, int n_grad, double
     return ev_collect(st);
 }
 
+// Observable absorption (Heisenberg picture): E = <psi_K|H|psi_K> with
+// psi_K = U_tail psi_p equals <psi_p|U_tail^dag H U_tail|psi_p>.  For a Z-string
+// H (PAPER.md:308 measure_allZ; the adjoint seed of PAPER.md:226-231) a trailing
+// run of gates that are diagonal or permutations-with-phase maps H to Z strings
+// again, gate by gate from the last one:
+//   diagonal (RZ, Z, S, T, CZ, CP, diagonal MAT1/MAT2): commutes, dropped;
+//   anti-diagonal 1q (X, Y) on q: Z_q -> -Z_q;
+//   controlled anti-diagonal (CNOT) [c, t]: Z_t -> Z_c Z_t, Z_c unchanged;
+//   SWAP(a, b): exchanges bits a and b of the mask.
+// Those gates are never applied (the state is consumed by the adjoint anyway);
+// trainable gates in the run are diagonal (RZ) and their gradient is exactly 0
+// (d/dtheta of a diagonal commuting with H).  Returns the first absorbed gate;
+// z / sgn are updated in place.  Stops at anything else, at batched non-diagonal
+// gates and at already executed gates.
+static size_t absorb_tail(const std::vector<GateRec> &gates, size_t executed, std::vector<uint64_t> &z,
+                          std::vector<double> &sgn) {
+    auto zero = [](cd v) { return v.real() == 0.0 && v.imag() == 0.0; };
+    size_t i = gates.size();
+    while (i > executed) {
+        const GateRec &g = gates[i - 1];
+        const bool diag = g.cls == CL_IDENT || g.cls == CL_DIAG1 || g.cls == CL_DIAG2;
+        if (!diag && (g.batched || g.trainable)) break;
+        if (diag) {
+            // commutes with every Z string
+        } else if (g.cls == CL_SWAP) {
+            const int a = g.w[0], b = g.w[1];
+            for (auto &m : z) {
+                const uint64_t ba = (m >> a) & 1ull, bb = (m >> b) & 1ull;
+                if (ba != bb) m ^= (1ull << a) | (1ull << b);
+            }
+        } else if (g.cls == CL_U1 && zero(g.M[0]) && zero(g.M[3])) {
+            for (size_t t = 0; t < z.size(); t++)
+                if ((z[t] >> g.w[0]) & 1ull) sgn[t] = -sgn[t];
+        } else if (g.cls == CL_CTRL1 && zero(g.sub[0]) && zero(g.sub[3])) {
+            for (auto &m : z)
+                if ((m >> g.w[1]) & 1ull) m ^= 1ull << g.w[0];
+        } else {
+            break;
+        }
+        i--;
+    }
+    return i;
+}
+
 int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff, double *out_value,
                      double *out_grad, int n_grad) {
     int rc = check_live(st);
@@ -1095,7 +1151,19 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
     rc = check_terms(st, T, x, z);
     if (rc) return rc;
     if (T > 64) return fail(TQD_ERR_UNSUPPORTED, "at most 64 observable terms in tqd_adjoint_grad");
-    rc = execute_pending(st);
+    // Z-only observables absorb the circuit's trailing diagonal / permutation gates
+    std::vector<uint64_t> zabs(z, z + T);
+    std::vector<double> sabs(T, 1.0);
+    size_t end = st->gates.size();
+    bool z_only = true;
+    for (int t = 0; t < T && x; t++)
+        if (x[t]) z_only = false;
+    if (st->opt_absorb && z_only) {
+        end = absorb_tail(st->gates, st->executed, zabs, sabs);
+        z = zabs.data();
+    }
+    st->met.gates_absorbed += st->gates.size() - end;
+    rc = execute_pending(st, end);
     if (rc) return rc;
     rc = ensure_lambda(st);
     if (rc) return rc;
@@ -1116,8 +1184,10 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
         for (int t = 0; t < T; t++) {
             if (x && x[t]) continue;  // X / Y strings: lambda_add_xy below
             const uint64_t zp = phys_mask(st, z[t]);
-            const double ct = coeff ? coeff[cb + t] : 1.0;
-            if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
+            const double ct = (coeff ? coeff[cb + t] : 1.0) * sabs[t];
+            if (zp == 0) {  // identity (e.g. Z_q Z_q after absorption)
+                zt.cst += ct;
+            } else if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
                 zt.cst += ct;
                 zt.w[__builtin_ctzll(zp)] += ct;
             } else {
@@ -1519,14 +1589,9 @@ int tqd_reset_metrics(tqd_state *st) {
 // Diagnostic (no GPU needed): plan a circuit and return the stages as JSON.
 // gates: parallel arrays as in tqd_apply_gate (kinds[G], wires[2G], params[3G],
 // mats[32G], trainable[G]).  Returns the needed size if cap is too small.
-int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, const int *kinds, const int *wires,
-                   const double *params, const double *mats, const int *trainable, char *json_out, size_t cap,
-                   size_t *needed) {
-    if (world < 1 || (world & (world - 1))) return fail(TQD_ERR_WORLD, "world size must be a power of two");
-    int g = 0;
-    while ((1 << g) < world) g++;
-    if (n < g + 2 || n > 62) return fail(TQD_ERR_QUBITS, "bad n");
-    std::vector<GateRec> gates;
+// circuit as parallel arrays (tqd_debug_plan / tqd_debug_absorb) -> gate records
+static int parse_debug_gates(int n, int c128, int G, const int *kinds, const int *wires, const double *params,
+                             const double *mats, const int *trainable, std::vector<GateRec> &gates) {
     int np = 0;
     for (int i = 0; i < G; i++) {
         GateRec r;
@@ -1539,6 +1604,38 @@ int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, cons
         if (rc) return fail(rc, err);
         if (r.trainable) { r.slot0 = np; np += gate_num_params(kinds[i]); }
         gates.push_back(r);
+    }
+    return TQD_OK;
+}
+
+int tqd_debug_absorb(int n, int G, const int *kinds, const int *wires, const double *params, const double *mats,
+                     const int *trainable, int T, const uint64_t *z_in, uint64_t *z_out, double *sign_out,
+                     int *tail_begin) {
+    if (n < 1 || n > 63 || G < 0 || T < 0 || T > 64) return fail(TQD_ERR_ARG, "bad n, G or T");
+    if ((G && (!kinds || !wires || !params || !mats || !trainable)) || (T && (!z_in || !z_out || !sign_out)) ||
+        !tail_begin)
+        return fail(TQD_ERR_ARG, "NULL argument");
+    std::vector<GateRec> gates;
+    int rc = parse_debug_gates(n, 1, G, kinds, wires, params, mats, trainable, gates);
+    if (rc) return rc;
+    std::vector<uint64_t> z(z_in, z_in + T);
+    std::vector<double> sg(T, 1.0);
+    *tail_begin = (int)absorb_tail(gates, 0, z, sg);
+    for (int t = 0; t < T; t++) { z_out[t] = z[t]; sign_out[t] = sg[t]; }
+    return TQD_OK;
+}
+
+int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, const int *kinds, const int *wires,
+                   const double *params, const double *mats, const int *trainable, char *json_out, size_t cap,
+                   size_t *needed) {
+    if (world < 1 || (world & (world - 1))) return fail(TQD_ERR_WORLD, "world size must be a power of two");
+    int g = 0;
+    while ((1 << g) < world) g++;
+    if (n < g + 2 || n > 62) return fail(TQD_ERR_QUBITS, "bad n");
+    std::vector<GateRec> gates;
+    {
+        int rc = parse_debug_gates(n, c128, G, kinds, wires, params, mats, trainable, gates);
+        if (rc) return rc;
     }
     PlanConfig cfg = make_plan_cfg(n, n - g, k, small_max, c128 != 0);
     std::vector<int> pos(n);

@@ -149,44 +149,84 @@ __global__ void __launch_bounds__(512) small_kernel(const DevOp *__restrict__ op
 
 // lambda = H psi with H = sum_t c_t Z_t (diagonal): h(b) = sum_t c_t (-1)^{popc(b & z_t)};
 // E partial = sum_b h(b) |psi_b|^2   (the seed dy of the reverse pass)
+//
+// Single-bit terms: h = cst - 2 sum_p w_p b_p (byte tables over b).  Multi-bit
+// terms (e.g. the strings of an absorbed CNOT ladder): the parity of b & z_t is
+// the XOR of three parity MASKS over the terms (bit t = parity of z_t with part
+// of b): the thread's low 8 index bits (per kernel), the amplitude's slot u in
+// a 4096-amplitude chunk (per kernel, smem) and the chunk base incl. rank bits
+// (per chunk), so each amplitude costs one XOR and ceil(T/8) byte-table lookups
+// of sum_{t in S} c_t, independent of the strings' lengths.
+constexpr int LI_U = 16;  // amplitudes per thread per 4096-amplitude chunk
 template <typename Real>
 __global__ void __launch_bounds__(256) lambda_init_kernel(const typename CT<Real>::C *__restrict__ psi,
                                                           typename CT<Real>::C *__restrict__ lam, uint64_t n,
-                                                          uint64_t rank_hi, ZTerms terms, double *__restrict__ eout) {
+                                                          uint64_t rank_hi, const __grid_constant__ ZTerms terms,
+                                                          double *__restrict__ eout) {
     typedef typename CT<Real>::C C;
     __shared__ double red[32];
-    // byte tables: tab[j][v] = sum_{i<8} w[8j + i] * bit_i(v)
-    __shared__ Real tab[8][256];
-    __shared__ int nbytes;
-    if (threadIdx.x == 0) {
-        int nb = 0;
-        for (int p = 0; p < 64; p++)
-            if (terms.w[p] != 0.0) nb = p / 8 + 1;
-        nbytes = nb;
-    }
+    // byte tables: tab[j][v] = sum_{i<8} w[8j + i] bit_i(v);  tabt[j][v] = sum_{i<8} c[8j + i] bit_i(v)
+    __shared__ Real tab[8][256], tabt[8][256];
+    __shared__ uint64_t zs[64], pu[LI_U];
+    __shared__ Real linu[LI_U];
+    const int T = terms.T;
+    int nb = 0;
+    for (int p = 0; p < 64; p++)
+        if (terms.w[p] != 0.0) nb = p / 8 + 1;
+    const int ntb = (T + 7) / 8;
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
         const int j = i >> 8, v = i & 255;
-        double s = 0;
+        double s = 0, st = 0;
         for (int q = 0; q < 8; q++)
-            if ((v >> q) & 1) s += terms.w[8 * j + q];
+            if ((v >> q) & 1) {
+                s += terms.w[8 * j + q];
+                if (8 * j + q < T) st += terms.c[8 * j + q];
+            }
         tab[j][v] = (Real)s;
+        tabt[j][v] = (Real)st;
     }
+    if (threadIdx.x < 64) zs[threadIdx.x] = threadIdx.x < T ? terms.z[threadIdx.x] : 0ull;
+    double ctot = terms.cst;
+    for (int t = 0; t < T; t++) ctot += terms.c[t];
     __syncthreads();
-    const int nb = nbytes;
-    const Real cst = (Real)terms.cst;
-    double acc = 0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t b = i | rank_hi;
+    auto pmask = [&](uint64_t b) {  // bit t = parity(b & z_t)
+        uint64_t m = 0;
+        for (int t = 0; t < T; t++) m |= (uint64_t)(__popcll(b & zs[t]) & 1) << t;
+        return m;
+    };
+    auto lin = [&](uint64_t b) {
         Real s = 0;
         for (int j = 0; j < nb; j++) s += tab[j][(b >> (8 * j)) & 255];
-        Real h = cst - 2 * s;
-        for (int t = 0; t < terms.T; t++) {
-            const Real c = (Real)terms.c[t];
-            h += (__popcll(b & terms.z[t]) & 1) ? -c : c;
+        return s;
+    };
+    if (threadIdx.x < LI_U) {
+        pu[threadIdx.x] = pmask((uint64_t)threadIdx.x << 8);
+        linu[threadIdx.x] = lin((uint64_t)threadIdx.x << 8);
+    }
+    const uint64_t pj = pmask((uint64_t)threadIdx.x);
+    const Real linj = lin((uint64_t)threadIdx.x);
+    __syncthreads();
+    const Real K = (Real)ctot;
+    double acc = 0;
+    const uint64_t chunks = (n + 4095) >> 12;
+    for (uint64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+        const uint64_t base = ch << 12;
+        const uint64_t pb = T ? pmask(base | rank_hi) : 0;
+        const Real linb = lin(base | rank_hi);
+        double cacc = 0;
+#pragma unroll 4
+        for (int u = 0; u < LI_U; u++) {
+            const uint64_t i = base + ((uint64_t)u << 8) + threadIdx.x;
+            if (i >= n) break;
+            const uint64_t S = pj ^ pu[u] ^ pb;
+            Real s = linj + linu[u] + linb;
+            for (int j = 0; j < ntb; j++) s += tabt[j][(S >> (8 * j)) & 255];
+            const Real h = K - 2 * s;
+            const C x = psi[i];
+            lam[i] = mk<C>(h * x.x, h * x.y);
+            cacc += (double)(h * (x.x * x.x + x.y * x.y));
         }
-        const C x = psi[i];
-        lam[i] = mk<C>(h * x.x, h * x.y);
-        acc += (double)(h * (x.x * x.x + x.y * x.y));
+        acc += cacc;
     }
     double tot = block_sum<double>(acc, red);
     if (threadIdx.x == 0) atomicAdd(eout, tot);
@@ -591,8 +631,9 @@ static int grid_for(uint64_t n, int threads) {
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
                                double *eout, cudaStream_t s) {
     const int th = 256;
-    if (dbl) lambda_init_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)psi, (double2 *)lam, n, rank_hi, t, eout);
-    else lambda_init_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)psi, (float2 *)lam, n, rank_hi, t, eout);
+    const int g = grid_for((n + 15) / 16, th);  // one 4096-amplitude chunk per CTA iteration
+    if (dbl) lambda_init_kernel<double><<<g, th, 0, s>>>((const double2 *)psi, (double2 *)lam, n, rank_hi, t, eout);
+    else lambda_init_kernel<float><<<g, th, 0, s>>>((const float2 *)psi, (float2 *)lam, n, rank_hi, t, eout);
     return cudaGetLastError();
 }
 

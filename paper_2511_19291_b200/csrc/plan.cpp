@@ -421,6 +421,12 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     std::vector<int> rest;
     int n_nondiag = 0, n_slots = 0;
     const int cap_nondiag = R * (MAXSEG - 2);
+    // kernel-op budget of the stage (cfg.max_ops, shared memory): every op-emitting
+    // item costs <= 1 kop plus <= 1 for the diagonal-block run it may split; merged
+    // diagonal gates (no targets, no gradient) cost <= 3 terms of DBLK_TERMS per
+    // K_DBLK; + one run per segment
+    int n_kop_items = 0, n_diag_merge = 0;
+    auto kop_estimate = [&](int items_, int diag_) { return 2 * items_ + MAXSEG + (3 * diag_ + DBLK_TERMS - 1) / DBLK_TERMS; };
     std::vector<int> aff_pos;  // distinct control positions outside the tile of folded CNOTs
 
     for (size_t ii = 0; ii < pending.size(); ii++) {
@@ -429,9 +435,13 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         bool blk = false;
         for (int j = 0; j < g.nw; j++)
             if (blocked[g.w[j]]) blk = true;
-        if (!blk && ((int)items.size() >= cfg.max_ops - 1 || n_slots + g.ngen > cfg.max_slots)) blk = true;
         int tq[2], dq[2], nt, nd;
         roles(g, tq, nt, dq, nd);
+        const bool merge_diag = g.cls != CL_SWAP && nt == 0 && g.ngen == 0;
+        if (!blk && g.cls != CL_SWAP &&
+            kop_estimate(n_kop_items + (merge_diag ? 0 : 1), n_diag_merge + (merge_diag ? 1 : 0)) > cfg.max_ops - 1)
+            blk = true;
+        if (!blk && n_slots + g.ngen > cfg.max_slots) blk = true;
         std::vector<int> newbits;
         if (!blk && g.cls != CL_SWAP && nt > 0) {
             if (n_nondiag >= cap_nondiag) blk = true;
@@ -473,6 +483,8 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
                     if (!std::count(aff_pos.begin(), aff_pos.end(), cpos)) aff_pos.push_back(cpos);
                 }
             }
+            if (merge_diag) n_diag_merge++;
+            else if (!it.op.perm) n_kop_items++;
             if (!it.op.perm)
                 for (int j = 0; j < nt; j++) it.need.push_back(tile_of[wpos[tq[j]]]);
             if (nt && !it.op.perm) n_nondiag++;
@@ -1073,6 +1085,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
         case K_CU: k.code = (uint8_t)(KC_CU + k.t0); break;
         case K_PHASE: k.code = KC_PHASE; break;
         case K_D2: k.code = KC_D2; break;
+        case K_DBLK: k.code = KC_DBLK; break;
         case K_U2: k.code = (uint8_t)(KC_U2 + u2_index(k.t0, k.t1)); break;
         default: k.code = KC_NOP; break;
         }
@@ -1229,6 +1242,75 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             }
             for (int bb = 0; bb < R; bb++) { q[bb].clear(); qh[bb] = 0; }
         };
+        // Diagonal block: consecutive diagonal gates off the register-bit queues
+        // (K_PHASE / K_D2 forms) merge into one phase polynomial (DTerm): the
+        // register-only part as a 16-entry table, the rest as fixed-point terms.
+        // Invariant: a pending block and non-empty queues never coexist (queueing
+        // a gate flushes the block, a diagonal gate drains the queues first).
+        struct DT { BitRef a, b; double ang; };
+        std::vector<DT> dterms;
+        std::vector<double> dtab(1 << R, 0.0);
+        bool dactive = false;
+        auto dref_less = [](BitRef x, BitRef y) { return x.kind != y.kind ? x.kind < y.kind : x.idx < y.idx; };
+        auto dadd = [&](BitRef x, BitRef y, double ang) {  // Phi += ang * x * y (y may be BK_NONE)
+            if (std::abs(std::remainder(ang, 2 * M_PI)) < 1e-15) return;
+            if (x.kind == BK_REG && y.kind == BK_REG) {
+                for (int r = 0; r < (1 << R); r++)
+                    if (((r >> x.idx) & 1) && ((r >> y.idx) & 1)) dtab[r] += ang;
+                return;
+            }
+            if (x.kind == BK_REG && y.kind == BK_NONE) {
+                for (int r = 0; r < (1 << R); r++)
+                    if ((r >> x.idx) & 1) dtab[r] += ang;
+                return;
+            }
+            if (y.kind == BK_REG || (x.kind != BK_REG && y.kind != BK_NONE && dref_less(y, x))) std::swap(x, y);
+            for (DT &t : dterms)
+                if (t.a.kind == x.kind && t.a.idx == x.idx && t.b.kind == y.kind && t.b.idx == y.idx) {
+                    t.ang += ang;
+                    return;
+                }
+            dterms.push_back({x, y, ang});
+        };
+        auto turn = [](double ang, double scale) {  // fraction of a full turn, fixed point
+            double f = ang / (2 * M_PI);
+            f -= std::floor(f);
+            const long double v = (long double)f * (long double)scale;
+            return v >= (long double)scale ? (long double)0 : v;
+        };
+        auto flush_dblk = [&]() {
+            if (!dactive) return;
+            size_t i0 = 0;
+            bool first = true;
+            while (first || i0 < dterms.size()) {
+                KOp<Real> k = newop(K_DBLK);
+                for (int r = 0; r < (1 << R); r++)
+                    pute(k, r, first ? std::polar(1.0, dtab[r]) : cd(1.0));
+                finalize(k);
+                const size_t cnt = std::min<size_t>(DBLK_TERMS, dterms.size() - i0);
+                DTerm<Real> *tm = reinterpret_cast<DTerm<Real> *>(k.g);
+                uint8_t xm = 0;
+                for (size_t j = 0; j < cnt; j++) {
+                    const DT &t = dterms[i0 + j];
+                    DTerm<Real> d;
+                    memset(&d, 0, sizeof(d));
+                    if (sizeof(Real) == 4) d.ang = (uint32_t)(uint64_t)turn(t.ang, 4294967296.0);
+                    else d.ang = (decltype(d.ang))turn(t.ang, 18446744073709551616.0);
+                    d.a = t.a;
+                    d.b = t.b;
+                    tm[j] = d;
+                    if (t.a.kind == BK_REG) xm |= (uint8_t)(1u << t.a.idx);
+                }
+                k.t0 = (uint8_t)cnt;
+                k.gbits = xm;
+                ops.push_back(k);
+                i0 += cnt;
+                first = false;
+            }
+            dterms.clear();
+            std::fill(dtab.begin(), dtab.end(), 0.0);
+            dactive = false;
+        };
         for (int jj = 0; jj < e - b && !skip_ops; jj++) {
             const POp &o0 = sp.ops[bwd ? e - 1 - jj : b + jj];
             if (o0.perm) continue;  // folded into the layout-change maps below
@@ -1246,10 +1328,33 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 qg.batched = g.batched;
                 if (g.batched) qg.t = g.kind == TQD_RY ? LT_REAL : g.kind == TQD_RZ ? LT_DIAG : LT_GEN;  // by kind
                 qg.gate = o.gate;
+                flush_dblk();
                 q[bit].push_back(qg);
                 continue;
             }
             drain();
+            if ((o.kind == OP_D1 && o.cp < 0 && !has_gen) || o.kind == OP_D2) {
+                // theta(u, v) = a + b u + c v + d u v with theta_uv = arg d[2u + v] (u = MSB bit)
+                dactive = true;
+                const BitRef none = {BK_NONE, 0};
+                if (o.kind == OP_D1) {
+                    cd M1[4];
+                    op_matrix2(o, bwd, M1);
+                    const double t0 = std::arg(M1[0]), t1 = std::arg(M1[3]);
+                    for (int r = 0; r < (1 << R); r++) dtab[r] += t0;
+                    dadd(bref(o.dp0), none, t1 - t0);
+                } else {
+                    double th[4];
+                    for (int q = 0; q < 4; q++) th[q] = std::arg(bwd ? std::conj(o.m[q]) : o.m[q]);
+                    for (int r = 0; r < (1 << R); r++) dtab[r] += th[0];
+                    const BitRef u = bref(o.dp0), v = bref(o.dp1);
+                    dadd(u, none, th[2] - th[0]);
+                    dadd(v, none, th[1] - th[0]);
+                    dadd(u, v, th[3] - th[2] - th[1] + th[0]);
+                }
+                continue;
+            }
+            flush_dblk();
             KOp<Real> k = newop(K_NOP);
             cd M[4];
             switch (o.kind) {
@@ -1294,6 +1399,7 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             ops.push_back(k);
         }
         drain();
+        flush_dblk();
     }
     ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
     ds.n_ops = (int)ops.size() - ds.op_base;

@@ -303,6 +303,66 @@ __device__ __forceinline__ void grad_z_layer(const C *a, const C *l, uint32_t gm
     }
 }
 
+// ---- diagonal block (K_DBLK, tqd_internal.h DTerm): one phase per amplitude for
+// a whole run of diagonal gates.  Per thread: fixed-point turn sums of the terms
+// whose lane / warp / base bits are set (th: constant, al[b]: per register bit),
+// phases by sincospi, then exp(i Phi(r)) = table[r] * w(r) with
+// w(r) = e^{i th} prod_{b in r} e^{i al[b]}.
+__device__ __forceinline__ float2 cis_turn(uint32_t u) {
+    float s, c;
+    sincospif((float)(int32_t)u * 4.656612873077393e-10f, &s, &c);  // pi * u / 2^31
+    return make_float2(c, s);
+}
+__device__ __forceinline__ double2 cis_turn(uint64_t u) {
+    double s, c;
+    sincospi((double)(int64_t)u * 1.0842021724855044e-19, &s, &c);  // pi * u / 2^63
+    return make_double2(c, s);
+}
+
+template <typename Real, bool BWD>
+__device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
+                                         typename CT<Real>::C *l, uint32_t tix, uint64_t basefull) {
+    typedef typename CT<Real>::C C;
+    typedef decltype(DTerm<Real>::ang) U;
+    auto bv = [&](BitRef r) -> uint32_t {
+        return r.kind == BK_TIX ? ((tix >> r.idx) & 1u) : r.kind == BK_BASE ? (uint32_t)((basefull >> r.idx) & 1ull) : 1u;
+    };
+    const int nt = (int)((h.x >> 24) & 0xffu);
+    const uint32_t xm = h.y & 0xffu;
+    const DTerm<Real> *tm = reinterpret_cast<const DTerm<Real> *>(op.g);
+    U th = 0, al[SWEEP_R];
+#pragma unroll
+    for (int b = 0; b < SWEEP_R; b++) al[b] = 0;
+    for (int i = 0; i < nt; i++) {
+        const DTerm<Real> t = tm[i];
+        const U add = bv(t.b) ? t.ang : (U)0;
+        if (t.a.kind == BK_REG) {
+#pragma unroll
+            for (int b = 0; b < SWEEP_R; b++) al[b] += (t.a.idx == b) ? add : (U)0;
+        } else {
+            th += bv(t.a) ? add : (U)0;
+        }
+    }
+    C w[NR];
+    w[0] = cis_turn(th);
+    if (xm) {
+        C u[SWEEP_R];
+#pragma unroll
+        for (int b = 0; b < SWEEP_R; b++) u[b] = cis_turn(al[b]);
+#pragma unroll
+        for (int r = 1; r < NR; r++) w[r] = cmul(w[r & (r - 1)], u[ctz4(r)]);
+    } else {
+#pragma unroll
+        for (int r = 1; r < NR; r++) w[r] = w[0];
+    }
+#pragma unroll
+    for (int r = 0; r < NR; r++) {
+        const C ph = cmul_e(op.m + 4 * r, w[r]);
+        a[r] = cmul(ph, a[r]);
+        if (BWD) l[r] = cmul(ph, l[r]);
+    }
+}
+
 // ---- one op, in place on psi (and lambda in the adjoint) ----------------------
 // h = the op's 16-byte dispatch header (already in registers: prefetched while
 // the previous op ran), op = the full op in shared memory (coefficients).
@@ -397,6 +457,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
         }
         break;
     }
+    case KC_DBLK: run_dblk<Real, BWD>(h, op, a, l, tix, basefull); break;
     case KC_D2: {
         const uint32_t k0 = h.z & 0xff, i0 = (h.z >> 8) & 0xff, k1 = (h.z >> 16) & 0xff, i1 = h.z >> 24;
         const int m0 = k0 == BK_REG ? (1 << i0) : 0;

@@ -95,6 +95,7 @@ enum KKind : uint8_t {
     K_PHASE = 4,  // diag(d0, d1) selected by a lane/warp/base bit b0 (+ RZ generator)
     K_D2 = 5,     // diag 2q on bits b0 (MSB), b1 (any kind)
     K_U2 = 6,     // 4x4 on register bits t0 (MSB), t1
+    K_DBLK = 7,   // merged run of diagonal gates: phase polynomial (see DTerm)
 };
 enum LType : uint8_t { LT_GEN = 0, LT_REAL = 1, LT_DIAG = 2 };
 constexpr int KOP_MAXGEN = 4;
@@ -109,7 +110,30 @@ enum KCode : uint8_t {
     KC_PHASE = 36,
     KC_D2 = 37,
     KC_U2 = 38,     // KC_U2 + u2_index(t0, t1) (38..49)
-    KC_COUNT = 50,
+    KC_DBLK = 50,   // diagonal block
+    KC_COUNT = 51,
+};
+
+// Diagonal block (K_DBLK): a run of diagonal gates (CP, CZ, Z / S / T / RZ on
+// non-register bits, diagonal MAT1 / MAT2) is one phase function of the index
+// bits, exp(i Phi(b)) with Phi a quadratic polynomial over GF(2) bits.  The part
+// that depends only on the register bits is a uniform 16-entry table (m[], as a
+// diagonal layer); the rest is a list of terms in g[] (t0 = count, <= DBLK_TERMS):
+//   a = REG bit r, b = lane/warp/base bit X (or none): Phi += ang * r * X
+//   a, b both lane/warp/base bits (b may be none):    Phi += ang * A * B
+// Angles are fixed-point fractions of a full turn (2^32 / 2^64 = 2 pi), so sums
+// wrap exactly mod 2 pi; the kernel turns the per-thread sums into phases with
+// sincospi.  gbits = register bits that carry cross terms.
+constexpr int DBLK_TERMS = 16;
+template <typename Real> struct DTerm;
+template <> struct DTerm<float> {
+    uint32_t ang;
+    BitRef a, b;
+};
+template <> struct DTerm<double> {
+    uint64_t ang;
+    BitRef a, b;
+    uint8_t pad[4];
 };
 inline int u2_index(int t0, int t1) { return t0 * 3 + (t1 > t0 ? t1 - 1 : t1); }
 

@@ -108,6 +108,40 @@ def random_circuit(n: int, n_gates: int, seed: int = 0, kinds: Optional[Sequence
     return gates
 
 
+def diag_perm_tail(n: int, n_gates: int, seed: int = 0) -> list:
+    """Random run of gates that are diagonal or permutations-with-phase (what
+    tqd_adjoint_grad's observable absorption takes): X, Y, Z, S, T, trainable RZ,
+    CNOT, CZ, SWAP, diagonal MAT2 (controlled phase), anti-diagonal MAT1 with
+    random phases, controlled anti-diagonal MAT2 (control on either wire)."""
+    rng = np.random.default_rng(seed)
+    kinds = ["X", "Y", "Z", "S", "T", "RZ", "MAT1"]
+    if n >= 2:
+        kinds += ["CNOT", "CZ", "SWAP", "MAT2D", "MAT2C"]
+    gates = []
+    for _ in range(n_gates):
+        k = kinds[int(rng.integers(len(kinds)))]
+        two = k in ("CNOT", "CZ", "SWAP", "MAT2D", "MAT2C")
+        wires = tuple(int(w) for w in rng.choice(n, size=2 if two else 1, replace=False))
+        ph = np.exp(1j * rng.uniform(0, 2 * math.pi, size=4))
+        if k == "RZ":
+            gates.append(Gate("RZ", wires, (float(rng.uniform(0, 2 * math.pi)),), None, True))
+        elif k == "MAT1":
+            gates.append(Gate("MAT1", wires, (), np.array([[0, ph[0]], [ph[1], 0]], np.complex128), False))
+        elif k == "MAT2D":
+            gates.append(Gate("MAT2", wires, (), np.diag(ph).astype(np.complex128), False))
+        elif k == "MAT2C":
+            m = np.eye(4, dtype=np.complex128)
+            if rng.integers(2):  # control = wires[0]: |1x> block anti-diagonal
+                m[2:, 2:] = [[0, ph[0]], [ph[1], 0]]
+            else:                # control = wires[1]: indices {1, 3} carry the anti-diagonal
+                m[1, 1] = m[3, 3] = 0
+                m[1, 3], m[3, 1] = ph[0], ph[1]
+            gates.append(Gate("MAT2", wires, (), m, False))
+        else:
+            gates.append(Gate(k, wires))
+    return gates
+
+
 def cphase_matrix(phi: float) -> np.ndarray:
     return np.diag([1, 1, 1, np.exp(1j * phi)]).astype(np.complex128)
 
