@@ -22,8 +22,9 @@ e2e      = the same metric through the public C ABI per step, as in a training
            copies value + gradients device->host); wall clock between
            synchronised barriers.
 roofline = the dominant kernel (the fused adjoint sweep) from live CUDA-event
-           timings of every launch: algorithmic bytes per launch (4 x 8 B x
-           2^n_loc: read + write psi and lambda) / average launch time, against
+           timings of every launch: algorithmic bytes (4 x 8 B x 2^n_loc per
+           launch: read + write psi and lambda; 2 x 8 B for the last reverse
+           sweep, which only reads) / summed launch time, against
            MEASURED_PEAKS.json hbm_gbs.
 """
 from __future__ import annotations
@@ -262,7 +263,8 @@ def main():
     fwd_avg = m["fwd_sweep_ms"] / max(m["fwd_sweeps"], 1)
     bwd_avg = m["bwd_sweep_ms"] / max(m["bwd_sweeps"], 1)
     shard = 8 << (n - g)
-    bwd_gbs = 4 * shard / (bwd_avg / 1e3) / 1e9 if bwd_avg > 0 else 0.0
+    # algorithmic bytes of all adjoint sweeps (the last reverse sweep stores nothing) / their time
+    bwd_gbs = m["bwd_sweep_bytes"] / (m["bwd_sweep_ms"] / 1e3) / 1e9 if m["bwd_sweep_ms"] > 0 else 0.0
     fwd_gbs = 2 * shard / (fwd_avg / 1e3) / 1e9 if fwd_avg > 0 else 0.0
     dominant = "adjoint_sweep" if m["bwd_sweep_ms"] >= m["fwd_sweep_ms"] else "forward_sweep"
     traffic, _ = ncu_traffic()
@@ -270,7 +272,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": traffic, "kernel": dominant,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, b.copy_)",
-                "algorithmic_bytes_per_launch": (4 if dominant == "adjoint_sweep" else 2) * shard,
+                "algorithmic_bytes_per_launch": (round(m["bwd_sweep_bytes"] / max(m["bwd_sweeps"], 1))
+                                                 if dominant == "adjoint_sweep" else 2 * shard),
                 "avg_launch_ms": round(bwd_avg if dominant == "adjoint_sweep" else fwd_avg, 4),
                 "forward_sweep": {"achieved": round(fwd_gbs, 1), "frac": round(fwd_gbs / peak, 4),
                                   "launches_per_step": m["fwd_sweeps"] // args.steps,

@@ -374,7 +374,7 @@ struct Encoded {
     size_t cap = 0;
     size_t off_ops = 0, off_sl = 0;
     size_t off_kops = 0;
-    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; int n_slots; };
+    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; int n_slots; int no_store = 0; };
     std::vector<L> launches;
     bool valid = false;
 };
@@ -451,7 +451,8 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
                 st->met.fused_remaps++;
                 li++;  // the remap is done
             }
-            if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += 4 * sb; st->met.hbm_bytes += 4 * sb; st->met.gates_unapplied += sp.n_gates; }
+            const uint64_t bb = (l.no_store ? 2 : 4) * sb;  // the last reverse sweep only reads
+            if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += bb; st->met.hbm_bytes += bb; st->met.gates_unapplied += sp.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
             st->met.kernel_launches++;
         } else if (l.type == ST_SMALL) {
@@ -477,25 +478,36 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
                        std::vector<DevStage> &dstages, std::vector<DevOp> &ops, std::vector<KOp<Real>> &kops,
                        std::vector<int32_t> &slots) {
     std::vector<GateRec> tmp;
+    // reverse sweep: nothing before the earliest trainable gate is un-applied, and
+    // the last reverse sweep stores neither psi nor lambda (only gradients remain)
+    int skip_below = 0, last_sweep = -1;
+    if (bwd) {
+        skip_below = (int)st->gates.size();
+        for (size_t i = 0; i < st->gates.size(); i++)
+            if (st->gates[i].ngen) { skip_below = (int)i; break; }
+        for (size_t ii = 0; ii < stages.size(); ii++)
+            if (stages[ii].type != ST_REMAP) last_sweep = (int)ii;
+    }
     for (size_t ii = 0; ii < stages.size(); ii++) {
         const Stage &s = stages[ii];
         if (s.type == ST_SWEEP) {
             if (s.sw.ops.empty()) continue;
             // one copy of the op stream / slot table per batch element (same structure)
             DevStage ds;
-            encode_sweep_k<Real>(s.sw, gates_for(st, 0, tmp), bwd, st->n_loc, ds, kops, slots);
+            encode_sweep_k<Real>(s.sw, gates_for(st, 0, tmp), bwd, st->n_loc, ds, kops, slots, skip_below);
             for (int b = 1; b < st->batch; b++) {
                 DevStage dsb;
-                encode_sweep_k<Real>(s.sw, gates_for(st, b, tmp), bwd, st->n_loc, dsb, kops, slots);
+                encode_sweep_k<Real>(s.sw, gates_for(st, b, tmp), bwd, st->n_loc, dsb, kops, slots, skip_below);
             }
             ds.batch = st->batch;
+            ds.no_store = (bwd && (int)ii == last_sweep) ? 1 : 0;
             E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
-                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots), ds.n_slots});
+                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots), ds.n_slots, ds.no_store});
             dstages.push_back(ds);
         } else if (s.type == ST_SMALL) {
             if (s.sm.ops.empty()) continue;
             const int b = (int)ops.size();
-            for (int bb = 0; bb < st->batch; bb++) encode_small(s.sm, gates_for(st, bb, tmp), bwd, ops);
+            for (int bb = 0; bb < st->batch; bb++) encode_small(s.sm, gates_for(st, bb, tmp), bwd, ops, skip_below);
             E.launches.push_back({ST_SMALL, -1, b, ((int)ops.size() - b) / st->batch, (int)ii, 1, 0});
         } else {
             E.launches.push_back({ST_REMAP, -1, 0, 0, (int)ii, 0, 0});
@@ -882,9 +894,13 @@ int tqd_state_free(tqd_state *st) {
 int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     if (!st) return fail(TQD_ERR_ARG, "state is NULL");
     switch (option) {
-    case TQD_OPT_TILE_QUBITS:
-        if (v < 9 || v > 14) return fail(TQD_ERR_ARG, "tile qubits must be in [9, 14]");
+    case TQD_OPT_TILE_QUBITS: {
+        // the sweep kernels are built for <= 256 threads per CTA (launch bounds):
+        // 2^k = 32 lanes x 2^R registers x <= 8 warps
+        const int kmax = LANE_BITS + TQD_SWEEP_R + 3;
+        if (v < 9 || v > kmax) return fail(TQD_ERR_ARG, "tile qubits must be in [9, " + std::to_string(kmax) + "]");
         st->opt_k = (int)v; return TQD_OK;
+    }
     case TQD_OPT_SMALL_MAX:
         if (v < 0 || v > 12) return fail(TQD_ERR_ARG, "small_max must be in [0, 12]");
         if (st->dbl && v > 11) return fail(TQD_ERR_ARG, "small_max must be <= 11 for complex128");

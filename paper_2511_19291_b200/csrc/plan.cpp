@@ -1045,7 +1045,7 @@ static void op_matrix2(const POp &o, bool dag, cd *M) {
 
 template <typename Real>
 void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
-                    std::vector<KOp<Real>> &ops, std::vector<int32_t> &slot_param) {
+                    std::vector<KOp<Real>> &ops, std::vector<int32_t> &slot_param, int skip_below) {
     memset(&ds, 0, sizeof(ds));
     const int nseg = (int)sp.lays.size();
     const int R = sp.R;
@@ -1314,6 +1314,10 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
         for (int jj = 0; jj < e - b && !skip_ops; jj++) {
             const POp &o0 = sp.ops[bwd ? e - 1 - jj : b + jj];
             if (o0.perm) continue;  // folded into the layout-change maps below
+            // reverse sweep: gates before the earliest trainable gate (tape order) are
+            // never needed -- every later gate sharing a qubit with one of them is
+            // placed after it, so the skipped ones commute with all that remain
+            if (bwd && o0.gate < skip_below) continue;
             const GateRec &g = gates[o0.gate];
             const POp o = pop_for(o0, g);
             const bool has_gen = bwd && g.ngen > 0;
@@ -1461,13 +1465,15 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
 }
 
 template void encode_sweep_k<float>(const SweepPlan &, const std::vector<GateRec> &, bool, int, DevStage &,
-                                    std::vector<KOp<float>> &, std::vector<int32_t> &);
+                                    std::vector<KOp<float>> &, std::vector<int32_t> &, int);
 template void encode_sweep_k<double>(const SweepPlan &, const std::vector<GateRec> &, bool, int, DevStage &,
-                                     std::vector<KOp<double>> &, std::vector<int32_t> &);
+                                     std::vector<KOp<double>> &, std::vector<int32_t> &, int);
 
-void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops) {
+void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops,
+                  int skip_below) {
     const int m = (int)sp.ops.size();
     for (int jj = 0; jj < m; jj++) {
+        if (bwd && sp.ops[m - 1 - jj].gate < skip_below) continue;  // as in encode_sweep_k
         const POp o = pop_for(sp.ops[bwd ? m - 1 - jj : jj], gates[sp.ops[bwd ? m - 1 - jj : jj].gate]);
         DevOp d;
         memset(&d, 0, sizeof(d));

@@ -141,9 +141,12 @@ int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, st
 
 // Encode a sweep stage into device descriptors (forward or backward order).
 template <typename Real>
+// skip_below (backward only): gates with a smaller tape index precede every
+// trainable gate; their (non-permutation) ops are left out of the reverse sweep
 void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool bwd, int n_loc, DevStage &ds,
-                    std::vector<KOp<Real>> &ops, std::vector<int32_t> &slot_param);
-void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops);
+                    std::vector<KOp<Real>> &ops, std::vector<int32_t> &slot_param, int skip_below = 0);
+void encode_small(const SmallPlan &sp, const std::vector<GateRec> &gates, bool bwd, std::vector<DevOp> &ops,
+                  int skip_below = 0);
 
 std::string plan_to_json(const std::vector<Stage> &stages, const PlanConfig &cfg);
 

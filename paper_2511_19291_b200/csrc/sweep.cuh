@@ -723,7 +723,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             o[0] = b0;
 #pragma unroll
             for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] + c[ctz4(r)];
-            if (sc.m == 0) {
+            if (BWD && S.no_store) {
+                // last reverse sweep: psi / lambda are not needed any more
+            } else if (sc.m == 0) {
 #pragma unroll
                 for (int r = 0; r < NR; r++) {
                     stcs_c(psi + o[r], a[r]);

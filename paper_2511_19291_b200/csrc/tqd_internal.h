@@ -194,7 +194,7 @@ struct DevStage {
     int32_t lam_init;           // backward only: 1 = build lambda = H psi on load
     int32_t flags;              // kernel variant bits (SWF_*)
     int32_t batch;              // states in the batch: op / slot tables repeat per state (n_ops, n_slots each)
-    int32_t pad2;
+    int32_t no_store;           // backward only: last reverse stage, psi / lambda are not needed afterwards
 };
 
 // sweep-kernel variant bits (DevStage::flags)

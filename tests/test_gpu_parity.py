@@ -307,6 +307,9 @@ def test_cfg3_parameter_shift_spot(tqd, ctx):
 def test_abi_errors(tqd, ctx):
     st = tqd.State(ctx, 5, "c64")
     with pytest.raises(tqd.TqdError) as e:
+        st.set_option(tqd.OPT_TILE_QUBITS, 13)  # > 256 threads per CTA: rejected up front
+    assert e.value.code == -1
+    with pytest.raises(tqd.TqdError) as e:
         st.apply("CNOT", [1, 1])
     assert e.value.code == -1
     with pytest.raises(tqd.TqdError) as e:
@@ -347,7 +350,8 @@ def test_metrics_account_bytes(tqd, ctx):
     sb = 8 << n
     assert m["fwd_sweeps"] > 0 and m["bwd_sweeps"] == m["fwd_sweeps"]
     assert m["fwd_sweep_bytes"] == 2 * sb * m["fwd_sweeps"]
-    assert m["bwd_sweep_bytes"] == 4 * sb * m["bwd_sweeps"]
+    # the last reverse sweep reads psi and lambda but stores neither
+    assert m["bwd_sweep_bytes"] == 4 * sb * (m["bwd_sweeps"] - 1) + 2 * sb
     # the last layer's RZs and ring CNOTs are absorbed into the Z observable
     assert m["gates_absorbed"] == 2 * n
     assert m["gates_applied"] + m["gates_absorbed"] == 3 * 3 * n

@@ -94,7 +94,7 @@ def run_case(ctx, name, wl, steps, warmup, tile=0, note=""):
         if m["bwd_sweeps"]:
             a = m["bwd_sweep_ms"] / m["bwd_sweeps"]
             out["bwd_sweep_avg_ms"] = round(a, 4)
-            out["bwd_sweep_gbs"] = round(4 * shard / (a / 1e3) / 1e9, 1)
+            out["bwd_sweep_gbs"] = round(m["bwd_sweep_bytes"] / (m["bwd_sweep_ms"] / 1e3) / 1e9, 1)
             out["bwd_sweep_frac"] = round(out["bwd_sweep_gbs"] / pk, 4)
         out["other_ms"] = round(m["other_ms"], 3)
         out["gamp_gates_per_s_fwd_grad"] = round(len(gates) * (1 << n) / (out["fwd_grad_ms"] / 1e3) / 1e9, 2)
@@ -114,7 +114,7 @@ def main():
     ap.add_argument("--cases", default="cfg1,cfg2,cfg3,cfg4,cfg5_8")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--ksweep", default="", help="tile sizes k for a 30q cfg3 sweep, e.g. 9,10,11,12,13")
+    ap.add_argument("--ksweep", default="", help="tile sizes k for a 30q cfg3 sweep, e.g. 9,10,11,12")
     ap.add_argument("--ksweep-qubits", type=int, default=30)
     args = ap.parse_args()
     torch.cuda.set_device(0)
