@@ -20,8 +20,8 @@ namespace tqd {
 // kernels.cu
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
                          void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W,
-                         int n_ops, int n_slots, int nseg, int grid, cudaStream_t s);
-int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg);
+                         int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s);
+int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg, int n_cvals);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
                          uint64_t rank_hi, int batch, cudaStream_t s);
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
@@ -197,7 +197,9 @@ static PlanConfig make_plan_cfg(int n, int n_loc, int k, int small_max, bool dbl
     if (c.k - LANE_BITS - c.R > WMAX) c.k = LANE_BITS + c.R + WMAX;
     const size_t threads = (size_t)32 << std::max(0, c.k - LANE_BITS - c.R);
     const size_t exch = ((size_t)2 << c.k) * esz;
-    const size_t tables = (size_t)3 * MAXSEG * threads * 4 + (size_t)3 * threads * 8;  // layout constants + prefetch offsets
+    // layout constants + prefetch offsets; the diagonal-block C rows / U values
+    // (<= 16.5 KB) live in the headroom between this 200 KB budget and the 227 KB opt-in
+    const size_t tables = (size_t)3 * MAXSEG * threads * 4 + (size_t)3 * threads * 8;
     const size_t kop = dbl ? sizeof(KOp<double>) : sizeof(KOp<float>);
     const size_t real = esz / 2;
     static const char *bkb = getenv("TQD_EXPERIMENT_SMEM_KB");  // timing experiments only
@@ -345,9 +347,9 @@ static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
 }
 
 // ---- forward execution ------------------------------------------------------
-static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops, int n_slots) {
+static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops, int n_slots, int n_cvals) {
     if (st->opt_grid > 0) return std::max(1, st->opt_grid / st->batch) * st->batch;
-    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots, (int)sp.lays.size());
+    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots, (int)sp.lays.size(), n_cvals);
     if (per < 1) per = 1;
     int64_t g = (int64_t)per * st->ctx->sms;
     const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
@@ -374,7 +376,7 @@ struct Encoded {
     size_t cap = 0;
     size_t off_ops = 0, off_sl = 0;
     size_t off_kops = 0;
-    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; int n_slots; int no_store = 0; };
+    struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; int n_slots; int no_store = 0; int n_cvals = 0; };
     std::vector<L> launches;
     bool valid = false;
 };
@@ -438,7 +440,8 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
             }
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
-                                      sc, sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(), l.grid, c->stream));
+                                      sc, sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(), l.n_cvals, l.grid,
+                                      c->stream));
             ev_end(st, ev);
             if (fuse) {
                 // every rank's stores into its peers' receive buffers are complete
@@ -502,7 +505,8 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
             ds.batch = st->batch;
             ds.no_store = (bwd && (int)ii == last_sweep) ? 1 : 0;
             E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
-                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots), ds.n_slots, ds.no_store});
+                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots, ds.n_cvals), ds.n_slots, ds.no_store,
+                                  ds.n_cvals});
             dstages.push_back(ds);
         } else if (s.type == ST_SMALL) {
             if (s.sm.ops.empty()) continue;

@@ -1077,6 +1077,8 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
         k.m[4 * i + 3] = (Real)v.imag();
     };
     const int threads = 32 << sp.W;
+    int n_cvals = 0, n_uvals = 0;  // diagonal-block C rows / U values of this stage
+    const int ccap = sizeof(Real) == 4 ? DBLK_CCAP_F32 : DBLK_CCAP_F64;
     auto finalize = [threads](KOp<Real> &k) {
         switch (k.kind) {
         case K_LAYER:
@@ -1242,35 +1244,36 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             }
             for (int bb = 0; bb < R; bb++) { q[bb].clear(); qh[bb] = 0; }
         };
-        // Diagonal block: consecutive diagonal gates off the register-bit queues
-        // (K_PHASE / K_D2 forms) merge into one phase polynomial (DTerm): the
-        // register-only part as a 16-entry table, the rest as fixed-point terms.
-        // Invariant: a pending block and non-empty queues never coexist (queueing
-        // a gate flushes the block, a diagonal gate drains the queues first).
+        // Diagonal blocks: diagonal gates off the register-bit queues (K_PHASE /
+        // K_D2 forms) are kept as pending phase-polynomial terms Phi += ang * x * y
+        // (x, y: register / lane-warp / base bits or none) and emitted as K_DBLK
+        // runs (DTerm): lane / warp / base terms accumulate in per-thread fixed-point
+        // registers over chained kops, the last kop of a run converts them and
+        // applies exp(i Phi) with the register-only part as a 16-entry table.
+        // Pending terms commute with every queued gate: queueing a gate on register
+        // bit b first emits the pending terms that involve b (the others stay
+        // pending), and a diagonal gate involving a register bit with queued gates
+        // drains the queues first.
         struct DT { BitRef a, b; double ang; };
-        std::vector<DT> dterms;
-        std::vector<double> dtab(1 << R, 0.0);
-        bool dactive = false;
+        std::vector<DT> dpend;
+        double dconst = 0;  // global phase of the pending terms
         auto dref_less = [](BitRef x, BitRef y) { return x.kind != y.kind ? x.kind < y.kind : x.idx < y.idx; };
+        const BitRef none = {BK_NONE, 0};
         auto dadd = [&](BitRef x, BitRef y, double ang) {  // Phi += ang * x * y (y may be BK_NONE)
             if (std::abs(std::remainder(ang, 2 * M_PI)) < 1e-15) return;
-            if (x.kind == BK_REG && y.kind == BK_REG) {
-                for (int r = 0; r < (1 << R); r++)
-                    if (((r >> x.idx) & 1) && ((r >> y.idx) & 1)) dtab[r] += ang;
-                return;
-            }
-            if (x.kind == BK_REG && y.kind == BK_NONE) {
-                for (int r = 0; r < (1 << R); r++)
-                    if ((r >> x.idx) & 1) dtab[r] += ang;
-                return;
-            }
-            if (y.kind == BK_REG || (x.kind != BK_REG && y.kind != BK_NONE && dref_less(y, x))) std::swap(x, y);
-            for (DT &t : dterms)
+            // normal order: a register bit first, else the smaller reference; none last
+            if (y.kind == BK_REG && x.kind != BK_REG) std::swap(x, y);
+            else if (x.kind != BK_REG && y.kind != BK_NONE && x.kind != BK_NONE && dref_less(y, x)) std::swap(x, y);
+            else if (x.kind == BK_REG && y.kind == BK_REG && y.idx < x.idx) std::swap(x, y);
+            for (DT &t : dpend)
                 if (t.a.kind == x.kind && t.a.idx == x.idx && t.b.kind == y.kind && t.b.idx == y.idx) {
                     t.ang += ang;
                     return;
                 }
-            dterms.push_back({x, y, ang});
+            dpend.push_back({x, y, ang});
+        };
+        auto involves = [](const DT &t, int rb) {
+            return (t.a.kind == BK_REG && t.a.idx == rb) || (t.b.kind == BK_REG && t.b.idx == rb);
         };
         auto turn = [](double ang, double scale) {  // fraction of a full turn, fixed point
             double f = ang / (2 * M_PI);
@@ -1278,38 +1281,96 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             const long double v = (long double)f * (long double)scale;
             return v >= (long double)scale ? (long double)0 : v;
         };
-        auto flush_dblk = [&]() {
-            if (!dactive) return;
-            size_t i0 = 0;
-            bool first = true;
-            while (first || i0 < dterms.size()) {
+        // emit terms (and a global phase) as one K_DBLK run; per kop the terms are
+        // ordered [C | U | M] (tqd_internal.h): C and U sums are precomputed by the
+        // kernel (per thread once, per tile once) while the budgets last
+        auto cls_of = [](const DT &t) {  // 0 = C (no base bit), 1 = U (no lane/warp bit), 2 = M
+            const bool has_base = t.a.kind == BK_BASE || t.b.kind == BK_BASE;
+            const bool has_tix = t.a.kind == BK_TIX || t.b.kind == BK_TIX;
+            return has_base ? (has_tix ? 2 : 1) : 0;
+        };
+        auto emit_dblk = [&](const std::vector<DT> &terms, double cst) {
+            std::vector<double> tab(1 << R, cst);
+            std::vector<DT> other;
+            for (const DT &t : terms) {
+                if (t.a.kind == BK_REG && (t.b.kind == BK_REG || t.b.kind == BK_NONE)) {
+                    for (int r = 0; r < (1 << R); r++)
+                        if (((r >> t.a.idx) & 1) && (t.b.kind == BK_NONE || ((r >> t.b.idx) & 1))) tab[r] += t.ang;
+                } else {
+                    other.push_back(t);
+                }
+            }
+            bool ident = true;
+            for (double v : tab)
+                if (std::abs(std::remainder(v, 2 * M_PI)) > 1e-15) ident = false;
+            if (ident && other.empty()) return;
+            uint8_t xm = 0;
+            for (const DT &t : other)
+                if (t.a.kind == BK_REG) xm |= (uint8_t)(1u << t.a.idx);
+            // run-level classes; C / U sums precomputed by the kernel while the stage
+            // budgets last (rows th, al[b] for b in xm), the rest evaluated per tile (M)
+            std::vector<DT> cl[3];
+            for (const DT &t : other) cl[cls_of(t)].push_back(t);
+            const int rows = 1 + __builtin_popcount(xm);
+            uint8_t coff = 0xff, uoff = 0xff;
+            if (!cl[0].empty() && n_cvals + rows <= ccap) { coff = (uint8_t)n_cvals; n_cvals += rows; }
+            else { cl[2].insert(cl[2].end(), cl[0].begin(), cl[0].end()); cl[0].clear(); }
+            if (!cl[1].empty() && n_uvals + rows <= DBLK_UCAP) { uoff = (uint8_t)n_uvals; n_uvals += rows; }
+            else { cl[2].insert(cl[2].end(), cl[1].begin(), cl[1].end()); cl[1].clear(); }
+            std::vector<std::pair<int, DT>> seq;  // (class, term) in [C | U | M] order
+            for (int c = 0; c < 3; c++)
+                for (const DT &t : cl[c]) seq.push_back({c, t});
+            // chunks of DBLK_TERMS: data kops (KC_DDATA, never dispatched to work) and the
+            // applying kop last (KC_DBLK), which reads the whole run's C / U / M sums
+            const int nk = std::max<int>(1, (int)((seq.size() + DBLK_TERMS - 1) / DBLK_TERMS));
+            for (int kk = 0; kk < nk; kk++) {
+                const size_t i0 = (size_t)kk * DBLK_TERMS;
+                const size_t cnt = std::min<size_t>(DBLK_TERMS, seq.size() - std::min(seq.size(), i0));
+                const bool last = kk == nk - 1;
                 KOp<Real> k = newop(K_DBLK);
-                for (int r = 0; r < (1 << R); r++)
-                    pute(k, r, first ? std::polar(1.0, dtab[r]) : cd(1.0));
+                for (int r = 0; r < (1 << R); r++) pute(k, r, last ? std::polar(1.0, tab[r]) : cd(1.0));
                 finalize(k);
-                const size_t cnt = std::min<size_t>(DBLK_TERMS, dterms.size() - i0);
+                if (!last) k.code = KC_DDATA;
+                int ncls[3] = {0, 0, 0};
                 DTerm<Real> *tm = reinterpret_cast<DTerm<Real> *>(k.g);
-                uint8_t xm = 0;
-                for (size_t j = 0; j < cnt; j++) {
-                    const DT &t = dterms[i0 + j];
+                for (size_t jx = 0; jx < cnt; jx++) {
+                    const DT &t = seq[i0 + jx].second;
+                    ncls[seq[i0 + jx].first]++;
                     DTerm<Real> d;
                     memset(&d, 0, sizeof(d));
                     if (sizeof(Real) == 4) d.ang = (uint32_t)(uint64_t)turn(t.ang, 4294967296.0);
                     else d.ang = (decltype(d.ang))turn(t.ang, 18446744073709551616.0);
                     d.a = t.a;
                     d.b = t.b;
-                    tm[j] = d;
-                    if (t.a.kind == BK_REG) xm |= (uint8_t)(1u << t.a.idx);
+                    tm[jx] = d;
                 }
-                k.t0 = (uint8_t)cnt;
+                // header bytes (unused by this kind): 2 flags (2: identity table), 3 data kops
+                // before the applying one, 4 xm, 5 c_off, 6 u_off, 8..10 nC nU nM
+                k.creg = (uint8_t)(last && ident ? 2 : 0);
+                k.t0 = (uint8_t)(last ? nk - 1 : 0);
                 k.gbits = xm;
+                k.gmask = coff;
+                k.ctrl.kind = uoff;
+                k.ctrl.idx = 0;
+                k.b0.kind = (uint8_t)ncls[0];
+                k.b0.idx = (uint8_t)ncls[1];
+                k.b1.kind = (uint8_t)ncls[2];
+                k.b1.idx = 0;
                 ops.push_back(k);
-                i0 += cnt;
-                first = false;
             }
-            dterms.clear();
-            std::fill(dtab.begin(), dtab.end(), 0.0);
-            dactive = false;
+        };
+        auto flush_dblk = [&]() {  // all pending terms
+            if (dpend.empty() && std::abs(std::remainder(dconst, 2 * M_PI)) < 1e-15) { dpend.clear(); dconst = 0; return; }
+            emit_dblk(dpend, dconst);
+            dpend.clear();
+            dconst = 0;
+        };
+        auto flush_bit = [&](int rb) {  // the pending terms that involve register bit rb
+            std::vector<DT> sel, keep;
+            for (const DT &t : dpend) (involves(t, rb) ? sel : keep).push_back(t);
+            if (sel.empty()) return;
+            emit_dblk(sel, 0.0);
+            dpend.swap(keep);
         };
         for (int jj = 0; jj < e - b && !skip_ops; jj++) {
             const POp &o0 = sp.ops[bwd ? e - 1 - jj : b + jj];
@@ -1332,32 +1393,34 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 qg.batched = g.batched;
                 if (g.batched) qg.t = g.kind == TQD_RY ? LT_REAL : g.kind == TQD_RZ ? LT_DIAG : LT_GEN;  // by kind
                 qg.gate = o.gate;
-                flush_dblk();
+                flush_bit(bit);
                 q[bit].push_back(qg);
                 continue;
             }
-            drain();
             if ((o.kind == OP_D1 && o.cp < 0 && !has_gen) || o.kind == OP_D2) {
                 // theta(u, v) = a + b u + c v + d u v with theta_uv = arg d[2u + v] (u = MSB bit)
-                dactive = true;
-                const BitRef none = {BK_NONE, 0};
+                const BitRef u = bref(o.dp0), v = o.kind == OP_D2 ? bref(o.dp1) : none;
+                bool busy = false;  // a register bit of this gate has queued gates: they go first
+                for (BitRef x : {u, v})
+                    if (x.kind == BK_REG && qh[x.idx] < q[x.idx].size()) busy = true;
+                if (busy) drain();
                 if (o.kind == OP_D1) {
                     cd M1[4];
                     op_matrix2(o, bwd, M1);
                     const double t0 = std::arg(M1[0]), t1 = std::arg(M1[3]);
-                    for (int r = 0; r < (1 << R); r++) dtab[r] += t0;
-                    dadd(bref(o.dp0), none, t1 - t0);
+                    dconst += t0;
+                    dadd(u, none, t1 - t0);
                 } else {
                     double th[4];
-                    for (int q = 0; q < 4; q++) th[q] = std::arg(bwd ? std::conj(o.m[q]) : o.m[q]);
-                    for (int r = 0; r < (1 << R); r++) dtab[r] += th[0];
-                    const BitRef u = bref(o.dp0), v = bref(o.dp1);
+                    for (int qq = 0; qq < 4; qq++) th[qq] = std::arg(bwd ? std::conj(o.m[qq]) : o.m[qq]);
+                    dconst += th[0];
                     dadd(u, none, th[2] - th[0]);
                     dadd(v, none, th[1] - th[0]);
                     dadd(u, v, th[3] - th[2] - th[1] + th[0]);
                 }
                 continue;
             }
+            drain();
             flush_dblk();
             KOp<Real> k = newop(K_NOP);
             cd M[4];
@@ -1407,6 +1470,8 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     }
     ds.seg_begin[nseg] = (int)ops.size() - ds.op_base;
     ds.n_ops = (int)ops.size() - ds.op_base;
+    ds.n_cvals = n_cvals;
+    ds.n_uvals = n_uvals;
     ds.n_slots = nslots;
     // exchange synchronisation (kernel order x; fwd segment f = x, adjoint f = nseg-2-x).
     // Write -> read: warps that keep their warp-index bits U_x only exchange among the

@@ -319,47 +319,97 @@ __device__ __forceinline__ double2 cis_turn(uint64_t u) {
     return make_double2(c, s);
 }
 
+template <typename Real> struct DAcc {
+    typedef decltype(DTerm<Real>::ang) U;
+};
+
+// sum of a kop's terms [i0, i1) with the given target (0xff = th, else register bit)
+template <typename Real>
+__device__ __forceinline__ typename DAcc<Real>::U dblk_sum(const DTerm<Real> *tm, int i0, int i1, uint32_t target,
+                                                           uint32_t tix, uint64_t basefull) {
+    typedef typename DAcc<Real>::U U;
+    U acc = 0;
+    for (int i = i0; i < i1; i++) {
+        const DTerm<Real> t = tm[i];
+        const uint32_t va = t.a.kind == BK_TIX ? ((tix >> t.a.idx) & 1u)
+                            : t.a.kind == BK_BASE ? (uint32_t)((basefull >> t.a.idx) & 1ull) : 1u;
+        const uint32_t vb = t.b.kind == BK_TIX ? ((tix >> t.b.idx) & 1u)
+                            : t.b.kind == BK_BASE ? (uint32_t)((basefull >> t.b.idx) & 1ull) : 1u;
+        const bool hit = t.a.kind == BK_REG ? (t.a.idx == target && vb) : (target == 0xffu && va && vb);
+        acc += hit ? t.ang : (U)0;
+    }
+    return acc;
+}
+
+// The applying kop of a diagonal-block run (tqd_internal.h DTerm): th / al[b] =
+// precomputed C rows (per thread) + U values (per tile) + the M terms of the run's
+// kops; then exp(i Phi(r)) = table[r] e^{i th} prod_{b in r} e^{i al_b}.
 template <typename Real, bool BWD>
 __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
-                                         typename CT<Real>::C *l, uint32_t tix, uint64_t basefull) {
+                                         typename CT<Real>::C *l, uint32_t tix, uint64_t basefull,
+                                         const typename DAcc<Real>::U *ctab, const typename DAcc<Real>::U *uacc) {
     typedef typename CT<Real>::C C;
-    typedef decltype(DTerm<Real>::ang) U;
-    auto bv = [&](BitRef r) -> uint32_t {
-        return r.kind == BK_TIX ? ((tix >> r.idx) & 1u) : r.kind == BK_BASE ? (uint32_t)((basefull >> r.idx) & 1ull) : 1u;
-    };
-    const int nt = (int)((h.x >> 24) & 0xffu);
+    typedef typename DAcc<Real>::U U;
+    const int first = (int)((h.x >> 24) & 0xffu);  // data kops before this one
     const uint32_t xm = h.y & 0xffu;
-    const DTerm<Real> *tm = reinterpret_cast<const DTerm<Real> *>(op.g);
+    const uint32_t coff = (h.y >> 8) & 0xffu, uoff = (h.y >> 16) & 0xffu;
     U th = 0, al[SWEEP_R];
 #pragma unroll
     for (int b = 0; b < SWEEP_R; b++) al[b] = 0;
-    for (int i = 0; i < nt; i++) {
-        const DTerm<Real> t = tm[i];
-        const U add = bv(t.b) ? t.ang : (U)0;
-        if (t.a.kind == BK_REG) {
+    if (coff != 0xffu) {
+        int j = (int)coff;
+        th += ctab[(j++) * blockDim.x];
 #pragma unroll
-            for (int b = 0; b < SWEEP_R; b++) al[b] += (t.a.idx == b) ? add : (U)0;
-        } else {
-            th += bv(t.a) ? add : (U)0;
-        }
+        for (int b = 0; b < SWEEP_R; b++)
+            if ((xm >> b) & 1u) al[b] += ctab[(j++) * blockDim.x];
+    }
+    if (uoff != 0xffu) {
+        int j = (int)uoff;
+        th += uacc[j++];
+#pragma unroll
+        for (int b = 0; b < SWEEP_R; b++)
+            if ((xm >> b) & 1u) al[b] += uacc[j++];
+    }
+    for (int q = first; q >= 0; q--) {  // M terms (lane / warp x base) of every kop of the run
+        const KOp<Real> &kq = (&op)[-q];
+        const uint32_t hz = reinterpret_cast<const uint4 *>(&kq)->z;
+        const int i0 = (int)((hz & 0xffu) + ((hz >> 8) & 0xffu)), i1 = i0 + (int)((hz >> 16) & 0xffu);
+        if (i1 == i0) continue;
+        const DTerm<Real> *tm = reinterpret_cast<const DTerm<Real> *>(kq.g);
+        th += dblk_sum<Real>(tm, i0, i1, 0xffu, tix, basefull);
+#pragma unroll
+        for (int b = 0; b < SWEEP_R; b++)
+            if ((xm >> b) & 1u) al[b] += dblk_sum<Real>(tm, i0, i1, (uint32_t)b, tix, basefull);
     }
     C w[NR];
     w[0] = cis_turn(th);
-    if (xm) {
-        C u[SWEEP_R];
+    // w[r] = w[0] prod_{b in r} e^{i al_b}: doubling over the register bits
 #pragma unroll
-        for (int b = 0; b < SWEEP_R; b++) u[b] = cis_turn(al[b]);
+    for (int b = 0; b < SWEEP_R; b++) {
+        if ((xm >> b) & 1u) {
+            const C u = cis_turn(al[b]);
 #pragma unroll
-        for (int r = 1; r < NR; r++) w[r] = cmul(w[r & (r - 1)], u[ctz4(r)]);
+            for (int r = 0; r < (2 << b) && r < NR; r++)
+                if (r & (1 << b)) w[r] = cmul(w[r & ~(1 << b)], u);
+        } else {
+#pragma unroll
+            for (int r = 0; r < (2 << b) && r < NR; r++)
+                if (r & (1 << b)) w[r] = w[r & ~(1 << b)];
+        }
+    }
+    if ((h.x >> 16) & 2u) {  // identity table
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            a[r] = cmul(w[r], a[r]);
+            if (BWD) l[r] = cmul(w[r], l[r]);
+        }
     } else {
 #pragma unroll
-        for (int r = 1; r < NR; r++) w[r] = w[0];
-    }
-#pragma unroll
-    for (int r = 0; r < NR; r++) {
-        const C ph = cmul_e(op.m + 4 * r, w[r]);
-        a[r] = cmul(ph, a[r]);
-        if (BWD) l[r] = cmul(ph, l[r]);
+        for (int r = 0; r < NR; r++) {
+            const C ph = cmul_e(op.m + 4 * r, w[r]);
+            a[r] = cmul(ph, a[r]);
+            if (BWD) l[r] = cmul(ph, l[r]);
+        }
     }
 }
 
@@ -368,7 +418,8 @@ __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typ
 // the previous op ran), op = the full op in shared memory (coefficients).
 template <typename Real, bool BWD>
 __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
-                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, Real *tt) {
+                                        typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, Real *tt,
+                                        const typename DAcc<Real>::U *ctab, const typename DAcc<Real>::U *uacc) {
     typedef typename CT<Real>::C C;
     auto bitval = [&](uint32_t kind, uint32_t idx) -> int {
         return kind == BK_TIX ? (int)((tix >> idx) & 1u) : (int)((basefull >> idx) & 1ull);
@@ -457,7 +508,7 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
         }
         break;
     }
-    case KC_DBLK: run_dblk<Real, BWD>(h, op, a, l, tix, basefull); break;
+    case KC_DBLK: run_dblk<Real, BWD>(h, op, a, l, tix, basefull, ctab, uacc); break;
     case KC_D2: {
         const uint32_t k0 = h.z & 0xff, i0 = (h.z >> 8) & 0xff, k1 = (h.z >> 16) & 0xff, i1 = h.z >> 24;
         const int m0 = k0 == BK_REG ? (1 << i0) : 0;
@@ -522,6 +573,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
     uint32_t *s_tr = s_tw + (nseg - 1) * blockDim.x;
     // per-thread L2-prefetch offsets (element offsets within a tile, up to 2 per thread)
     uint64_t *s_pf = reinterpret_cast<uint64_t *>(s_tr + (nseg - 1) * blockDim.x);  // 8 B aligned (threads * 4 B is)
+    // diagonal blocks: per-thread C rows [row][thread], per-tile U values [2][DBLK_UCAP]
+    typedef typename DAcc<Real>::U DU;
+    DU *s_ctab = reinterpret_cast<DU *>(s_pf + 2 * blockDim.x);
+    DU *s_uacc = s_ctab + (size_t)S.n_cvals * blockDim.x;
+    __shared__ uint8_t s_uk[DBLK_UCAP], s_ut[DBLK_UCAP];  // U value -> kop index, target (0xff = th)
     {
         const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base + (size_t)bidx * S.n_ops);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
@@ -570,6 +626,36 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             if ((warp >> w) & 1) t ^= cols[L.warp[w]];
         return t;
     };
+    // diagonal blocks: C sums once per kernel (lane / warp bits are fixed per thread
+    // and segment) into this thread's rows, the per-tile U work list (value -> applying
+    // kop, target) once per kernel
+    if (S.n_cvals || S.n_uvals) {
+        for (int j = 0; j < S.n_cvals; j++) s_ctab[j * blockDim.x + threadIdx.x] = 0;
+        for (int s = 0; s < nseg; s++) {
+            const uint32_t tx = thr_tix(S.lay[s]);
+            for (int oi = S.seg_begin[s]; oi < S.seg_begin[s + 1]; oi++) {
+                const uint4 h = *reinterpret_cast<const uint4 *>(&s_ops[oi]);
+                const uint32_t code = h.x & 0xffu;
+                if (code != KC_DBLK && code != KC_DDATA) continue;
+                const int nC = (int)(h.z & 0xffu);
+                const uint32_t xm = h.y & 0xffu, coff = (h.y >> 8) & 0xffu, uoff = (h.y >> 16) & 0xffu;
+                const DTerm<Real> *tm = reinterpret_cast<const DTerm<Real> *>(s_ops[oi].g);
+                if (nC && coff != 0xffu) {
+                    int j = (int)coff;
+                    s_ctab[(j++) * blockDim.x + threadIdx.x] += dblk_sum<Real>(tm, 0, nC, 0xffu, tx, 0);
+                    for (int b = 0; b < SWEEP_R; b++)
+                        if ((xm >> b) & 1u) s_ctab[(j++) * blockDim.x + threadIdx.x] += dblk_sum<Real>(tm, 0, nC, (uint32_t)b, tx, 0);
+                }
+                if (code == KC_DBLK && uoff != 0xffu && threadIdx.x == 0) {
+                    int j = (int)uoff;
+                    s_uk[j] = (uint8_t)oi;
+                    s_ut[j++] = 0xffu;
+                    for (int b = 0; b < SWEEP_R; b++)
+                        if ((xm >> b) & 1u) { s_uk[j] = (uint8_t)oi; s_ut[j++] = (uint8_t)b; }
+                }
+            }
+        }
+    }
     const uint64_t ld_thr = thr_phys_off(S.lay[0], S.ld_phys);
     const uint64_t st_thr = thr_phys_off(S.lay[nseg - 1], S.st_phys);
     {
@@ -641,6 +727,24 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                 if (BWD) l[r] = ldcs_c(lam + o[r]);
             }
         }
+        // diagonal blocks: this tile's U sums (base bits only), one thread per value,
+        // double-buffered by tile parity (the barrier also orders the C table writes)
+        const DU *uacc = s_uacc + ((tile / gsz) & 1) * DBLK_UCAP;
+        if (S.n_uvals) {
+            if ((int)threadIdx.x < S.n_uvals) {
+                const int oi = s_uk[threadIdx.x];
+                const int first = (int)((reinterpret_cast<const uint4 *>(&s_ops[oi])->x >> 24) & 0xffu);
+                DU v = 0;
+                for (int q = oi - first; q <= oi; q++) {  // the U terms of every kop of the run
+                    const uint32_t hz = reinterpret_cast<const uint4 *>(&s_ops[q])->z;
+                    const int nC = (int)(hz & 0xffu), nU = (int)((hz >> 8) & 0xffu);
+                    v += dblk_sum<Real>(reinterpret_cast<const DTerm<Real> *>(s_ops[q].g), nC, nC + nU, s_ut[threadIdx.x],
+                                        0, basefull);
+                }
+                const_cast<DU *>(uacc)[threadIdx.x] = v;
+            }
+            __syncthreads();
+        }
         if (tile + gsz < S.n_tiles) {
             const uint64_t nb = ((base | ~tmask) + step) & tmask;
             for (int i = 0; i < n_pf; i++) {
@@ -710,7 +814,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             for (; oi < e; oi++) {
                 // header of the next op loads while this one runs
                 const uint4 hn = oi + 1 < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi + 1]) : h;
-                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, tacc + threadIdx.x);
+                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, tacc + threadIdx.x, s_ctab + threadIdx.x, uacc);
                 h = hn;
             }
         }
@@ -762,10 +866,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
 }
 
 template <typename Real, bool BWD>
-static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int nseg) {
+static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int nseg, int n_cvals) {
+    typedef typename DAcc<Real>::U DU;
     return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
            (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t) +
-           (size_t)2 * threads * sizeof(uint64_t);
+           (size_t)2 * threads * sizeof(uint64_t) + (size_t)n_cvals * threads * sizeof(DU) + 2 * DBLK_UCAP * sizeof(DU);
 }
 
 // The dynamic shared-memory cap is a per-function attribute shared by every host
@@ -797,10 +902,10 @@ template <typename Real, bool BWD> static std::atomic<uint64_t> &sweep_cap_flag(
 template <typename Real, bool BWD>
 cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
                               double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops,
-                              int n_slots, int nseg, int grid, cudaStream_t s) {
+                              int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
     typedef typename CT<Real>::C C;
     auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, n_cvals);
     cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>());
     if (e != cudaSuccess) return e;
     fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi, sc);
@@ -808,9 +913,9 @@ cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const 
 }
 
 template <typename Real, bool BWD>
-int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg) {
+int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
     auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg);
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, n_cvals);
     if (raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>()) != cudaSuccess) {
         cudaGetLastError();
         return 1;
@@ -827,13 +932,13 @@ int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg) {
 
 #define TQD_INSTANTIATE_SWEEP(REAL, BWD, NAME)                                                                    \
     namespace tqd {                                                                                             \
-    cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi,  \
+    cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_kops, const int32_t *d_slots, void *psi,  \
                                     void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, \
-                                    int n_ops, int n_slots, int nseg, int grid, cudaStream_t s) {                 \
-        return launch_sweep_impl<REAL, BWD>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops,     \
-                                            n_slots, nseg, grid, s);                                            \
+                                    int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {    \
+        return launch_sweep_impl<REAL, BWD>(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops,    \
+                                            n_slots, nseg, n_cvals, grid, s);                                   \
     }                                                                                                           \
-    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg) {                                 \
-        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots, nseg);                                      \
+    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {                    \
+        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots, nseg, n_cvals);                             \
     }                                                                                                           \
     }

@@ -110,8 +110,9 @@ enum KCode : uint8_t {
     KC_PHASE = 36,
     KC_D2 = 37,
     KC_U2 = 38,     // KC_U2 + u2_index(t0, t1) (38..49)
-    KC_DBLK = 50,   // diagonal block
-    KC_COUNT = 51,
+    KC_DBLK = 50,   // diagonal block: applies the run ending here
+    KC_DDATA = 51,  // diagonal block: more terms of the run (no work when dispatched)
+    KC_COUNT = 52,
 };
 
 // Diagonal block (K_DBLK): a run of diagonal gates (CP, CZ, Z / S / T / RZ on
@@ -125,6 +126,17 @@ enum KCode : uint8_t {
 // wrap exactly mod 2 pi; the kernel turns the per-thread sums into phases with
 // sincospi.  gbits = register bits that carry cross terms.
 constexpr int DBLK_TERMS = 16;
+// A run is zero or more KC_DDATA kops followed by the applying KC_DBLK kop; the
+// run's terms are ordered [C | U | M] across its kops (per kop: nC, nU, nM):
+//   C: lane / warp bits only (no base bit): per-thread constants, summed once per
+//      kernel into a per-thread table (rows c_off.., DevStage::n_cvals rows);
+//   U: base bits only (no lane / warp bit): uniform over the CTA per tile, summed
+//      once per tile by one thread per value into u_acc (rows u_off..);
+//   M: lane / warp x base products: summed by every thread per tile.
+// The run's C rows / U values: 1 + popc(xm): th, then al[b] for b in xm.
+constexpr int DBLK_CCAP_F32 = 16;  // per-thread C rows per stage (shared memory: rows x threads x 4 B)
+constexpr int DBLK_CCAP_F64 = 4;   // (x 8 B); both <= 16 KB at 256 threads
+constexpr int DBLK_UCAP = 64;      // per-tile U values per stage
 template <typename Real> struct DTerm;
 template <> struct DTerm<float> {
     uint32_t ang;
@@ -195,6 +207,8 @@ struct DevStage {
     int32_t flags;              // kernel variant bits (SWF_*)
     int32_t batch;              // states in the batch: op / slot tables repeat per state (n_ops, n_slots each)
     int32_t no_store;           // backward only: last reverse stage, psi / lambda are not needed afterwards
+    int32_t n_cvals, n_uvals;   // diagonal blocks: per-thread C rows, per-tile U values (see DTerm)
+    int32_t pad3;
 };
 
 // sweep-kernel variant bits (DevStage::flags)

@@ -7,6 +7,7 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')"
 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?"
 python tools/bench_brief.py gpurun_out/bench_$TAG.log
 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref_$TAG.log | cut -c1-300
+python tools/bench_configs.py --ksweep 9,10,11,12 > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err; echo "configs rc=$?"
 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_short_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
