@@ -379,6 +379,10 @@ struct Encoded {
     struct L { int type; int idx; int op_base; int n_ops; int stage; int grid; int n_slots; int no_store = 0; int n_cvals = 0; };
     std::vector<L> launches;
     bool valid = false;
+    // pinned host staging of the descriptors (async copy); the event guards its reuse
+    void *host = nullptr;
+    size_t host_cap = 0;
+    cudaEvent_t copied = nullptr;
 };
 
 static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E);
@@ -551,14 +555,29 @@ static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool b
         }
         E.cap = nb;
     }
-    std::vector<char> host(total, 0);
-    if (b_st) memcpy(host.data(), dstages.data(), b_st);
-    if (b_ops) memcpy(host.data() + E.off_ops, ops.data(), b_ops);
-    if (b_k) memcpy(host.data() + E.off_kops, st->dbl ? (const void *)kd.data() : (const void *)kf.data(), b_k);
-    if (b_sl) memcpy(host.data() + E.off_sl, slots.data(), b_sl);
-    // pageable source: the copy is staged before cudaMemcpyAsync returns and is
-    // stream-ordered after earlier launches that may still read this buffer
-    CUDA_TRY(st, cudaMemcpyAsync(E.dev, host.data(), total, cudaMemcpyHostToDevice, st->ctx->stream));
+    // pinned staging: wait until the previous upload from it has been copied
+    if (E.copied) CUDA_TRY(st, cudaEventSynchronize(E.copied));
+    else CUDA_TRY(st, cudaEventCreateWithFlags(&E.copied, cudaEventDisableTiming));
+    if (total > E.host_cap) {
+        if (E.host) cudaFreeHost(E.host);
+        E.host = nullptr;
+        const size_t nb = std::max(total, (size_t)1 << 20);
+        if (cudaMallocHost(&E.host, nb) != cudaSuccess) {
+            cudaGetLastError();
+            E.host_cap = 0;
+            return fail(TQD_ERR_OOM, "cannot allocate pinned descriptor staging");
+        }
+        E.host_cap = nb;
+    }
+    char *host = (char *)E.host;
+    memset(host, 0, total);
+    if (b_st) memcpy(host, dstages.data(), b_st);
+    if (b_ops) memcpy(host + E.off_ops, ops.data(), b_ops);
+    if (b_k) memcpy(host + E.off_kops, st->dbl ? (const void *)kd.data() : (const void *)kf.data(), b_k);
+    if (b_sl) memcpy(host + E.off_sl, slots.data(), b_sl);
+    // stream-ordered after earlier launches that may still read the device buffer
+    CUDA_TRY(st, cudaMemcpyAsync(E.dev, host, total, cudaMemcpyHostToDevice, st->ctx->stream));
+    CUDA_TRY(st, cudaEventRecord(E.copied, st->ctx->stream));
     st->met.h2d_bytes += total;
     E.valid = true;
     return TQD_OK;
@@ -566,8 +585,12 @@ static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool b
 
 static void free_encoded(Encoded &E) {
     if (E.dev) cudaFree(E.dev);
+    if (E.host) cudaFreeHost(E.host);
+    if (E.copied) cudaEventDestroy(E.copied);
     E.dev = nullptr;
-    E.cap = 0;
+    E.host = nullptr;
+    E.copied = nullptr;
+    E.cap = E.host_cap = 0;
     E.valid = false;
 }
 
