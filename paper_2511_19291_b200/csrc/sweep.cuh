@@ -254,21 +254,28 @@ __device__ __forceinline__ double2 pmul(double2 x, double2 y) { return make_doub
 // RY generator G = -(i/2) Y on register bit T:
 //   2 Re <lam|G|psi> = sum_pairs Re(conj l1 a0) - Re(conj l0 a1)
 // two packed accumulators (independent FFMA2 chains), one final add
+#ifndef TQD_GRAD_CHAINS
+#define TQD_GRAD_CHAINS 2  // independent FFMA2 accumulator chains per RY gradient (4 measured 0.4 % slower)
+#endif
 template <int T, typename C, typename Real>
 __device__ __forceinline__ Real grad_y(const C *a, const C *l) {
     if constexpr (T >= SWEEP_R) return (Real)0;
-    C acc[2] = {mk<C>(0, 0), mk<C>(0, 0)};
+    constexpr int NC = TQD_GRAD_CHAINS;
+    C acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) acc[c] = mk<C>(0, 0);
     int i = 0;
 #pragma unroll
     for (int r = 0; r < NR; r++) {
         if (r & (1 << T)) continue;
         const int s = r | (1 << T);
-        acc[i & 1] = cfma_elem(l[s], a[r], acc[i & 1]);
-        acc[i & 1] = cfma_elem(pneg(l[r]), a[s], acc[i & 1]);
-        i++;
+        acc[i % NC] = cfma_elem(l[s], a[r], acc[i % NC]);
+        acc[(i + 1) % NC] = cfma_elem(pneg(l[r]), a[s], acc[(i + 1) % NC]);
+        i += 2;
     }
-    const C t = padd(acc[0], acc[1]);
-    return t.x + t.y;
+#pragma unroll
+    for (int c = 1; c < NC; c++) acc[0] = padd(acc[0], acc[c]);
+    return acc[0].x + acc[0].y;
 }
 
 template <int MASK, typename C, typename Real>

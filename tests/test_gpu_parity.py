@@ -303,6 +303,56 @@ def test_cfg3_parameter_shift_spot(tqd, ctx):
         assert abs((es[0] - es[1]) / 2 - grad[pi]) < 1e-3
 
 
+def test_cfg5_shard_qft_closed_form(tqd, ctx):
+    """The 2^33-amplitude shard each GPU holds at cfg 5 (36q / 8 GPUs), run as one
+    33-qubit state in bench_configs' launch configuration: X-prep |x> + QFT (diagonal-
+    block runs of 528 controlled phases, SWAP relabels).  Sampled amplitudes against
+    the closed form omega^{xy} / sqrt(N) (ledger #13) and <Z_i> = 0."""
+    n = 33
+    N = 1 << n
+    x = 0x1_2345_6789 % N
+    st = make_state(tqd, ctx, n, "c64")
+    try:
+        st.apply_circuit(W.basis_prep(n, x) + W.qft(n))
+        ez = st.expval(W.sum_z(n))
+        for first in (0, (1 << 32) + 12345, N - 64):
+            got = st.amplitudes(first, 64)
+            y = np.arange(first, first + 64, dtype=np.float64)
+            # omega^{xy} with the phase reduced exactly: (x * y) mod N in integers
+            ph = np.array([(x * int(v)) % N for v in y], dtype=np.float64) / N
+            ref = np.exp(2j * np.pi * ph) / math.sqrt(N)
+            # relative to |amplitude| = N^-1/2 (an absolute 1e-5 would be vacuous at 33 qubits)
+            assert np.max(np.abs(got - ref)) < 1e-4 / math.sqrt(N), first
+    finally:
+        st.free()
+    assert np.max(np.abs(ez)) < 1e-4
+
+
+def test_cfg4_entangler_free_33q(tqd, ctx, orc):
+    """cfg-4 size at P = 1 (33 qubits, 64 GiB psi + 64 GiB lambda on one B200): RY/RZ
+    ansatz depth 10 without CNOTs; E(sum Z_i) and all 660 gradients factor into
+    1-qubit oracle runs (exact pin at full size)."""
+    n, depth = 33, 10
+    gates = [g for g in W.hea(n, depth, seed=3, small=True) if g.name != "CNOT"]
+    st = make_state(tqd, ctx, n, "c64")
+    try:
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(W.sum_z(n))
+    finally:
+        st.free()
+    ref_val, ref_grad = 0.0, np.zeros(len(grad))
+    idx = {id(g): i for i, g in enumerate(gates)}
+    for q in range(n):
+        sub = [g for g in gates if g.wires[0] == q]
+        v, g1 = orc.adjoint(1, [W.Gate(g.name, (0,), g.params) for g in sub], [(0, 1, 1.0)])
+        ref_val += v
+        for g, d in zip(sub, g1):
+            ref_grad[idx[id(g)]] = d
+    assert len(grad) == 2 * n * depth
+    assert abs(val - ref_val) < 1e-4
+    assert np.max(np.abs(grad - ref_grad)) < 1e-4
+
+
 # ---------------------------------------------------------------- ABI errors
 def test_abi_errors(tqd, ctx):
     st = tqd.State(ctx, 5, "c64")
