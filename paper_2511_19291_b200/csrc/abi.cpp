@@ -508,9 +508,9 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
             }
             ds.batch = st->batch;
             ds.no_store = (bwd && (int)ii == last_sweep) ? 1 : 0;
+            const int ncv = ds.n_dblk ? ds.n_cvals : -1;  // -1: no diagonal blocks (plain kernel)
             E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
-                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots, ds.n_cvals), ds.n_slots, ds.no_store,
-                                  ds.n_cvals});
+                                  sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots, ncv), ds.n_slots, ds.no_store, ncv});
             dstages.push_back(ds);
         } else if (s.type == ST_SMALL) {
             if (s.sm.ops.empty()) continue;

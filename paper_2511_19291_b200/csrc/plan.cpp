@@ -1472,6 +1472,9 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     ds.n_ops = (int)ops.size() - ds.op_base;
     ds.n_cvals = n_cvals;
     ds.n_uvals = n_uvals;
+    ds.n_dblk = 0;
+    for (int i = ds.op_base; i < (int)ops.size(); i++)
+        if (ops[i].code == KC_DBLK) ds.n_dblk++;
     ds.n_slots = nslots;
     // exchange synchronisation (kernel order x; fwd segment f = x, adjoint f = nseg-2-x).
     // Write -> read: warps that keep their warp-index bits U_x only exchange among the

@@ -315,16 +315,39 @@ __device__ __forceinline__ void grad_z_layer(const C *a, const C *l, uint32_t gm
 // whose lane / warp / base bits are set (th: constant, al[b]: per register bit),
 // phases by sincospi, then exp(i Phi(r)) = table[r] * w(r) with
 // w(r) = e^{i th} prod_{b in r} e^{i al[b]}.
-__device__ __forceinline__ float2 cis_turn(uint32_t u) {
+// e^{i 2 pi u / 2^32} (float) / e^{i 2 pi u / 2^64} (double) from a 256-entry
+// table of e^{i 2 pi k / 256} (shared memory, built per CTA) times a short Taylor
+// series of the remaining angle delta < 2 pi / 256 (errors < 2e-8 / 1e-20)
+__device__ __forceinline__ float2 cis_turn(uint32_t u, const float2 *tab) {
+    const float2 t = tab[u >> 24];
+    const float d = (float)(u & 0xffffffu) * 1.4629180792671596e-09f;  // 2 pi / 2^32
+    const float d2 = d * d;
+    const float c = 1.0f - 0.5f * d2, sn = d * (1.0f - d2 * (1.0f / 6.0f));
+    return make_float2(t.x * c - t.y * sn, t.x * sn + t.y * c);
+}
+__device__ __forceinline__ double2 cis_turn(uint64_t u, const double2 *tab) {
+    const double2 t = tab[u >> 56];
+    const double d = (double)(u & 0xffffffffffffffull) * 3.4061215800865545e-19;  // 2 pi / 2^64
+    const double d2 = d * d;
+    const double c = 1.0 - d2 * (0.5 - d2 * (1.0 / 24 - d2 * (1.0 / 720 - d2 * (1.0 / 40320))));
+    const double sn = d * (1.0 - d2 * (1.0 / 6 - d2 * (1.0 / 120 - d2 * (1.0 / 5040 - d2 * (1.0 / 362880)))));
+    return make_double2(t.x * c - t.y * sn, t.x * sn + t.y * c);
+}
+__device__ __forceinline__ void cis_table_entry(int k, float2 *tab) {
     float s, c;
-    sincospif((float)(int32_t)u * 4.656612873077393e-10f, &s, &c);  // pi * u / 2^31
-    return make_float2(c, s);
+    sincospif((float)k / 128.0f, &s, &c);
+    tab[k] = make_float2(c, s);
 }
-__device__ __forceinline__ double2 cis_turn(uint64_t u) {
+__device__ __forceinline__ void cis_table_entry(int k, double2 *tab) {
     double s, c;
-    sincospi((double)(int64_t)u * 1.0842021724855044e-19, &s, &c);  // pi * u / 2^63
-    return make_double2(c, s);
+    sincospi((double)k / 128.0, &s, &c);
+    tab[k] = make_double2(c, s);
 }
+// complex product on registers (packed FMUL2 + FFMA2 for float)
+__device__ __forceinline__ float2 cmulp(float2 x, float2 y) {
+    return __ffma2_rn(make_float2(-x.y, x.y), make_float2(y.y, y.x), __fmul2_rn(make_float2(x.x, x.x), y));
+}
+__device__ __forceinline__ double2 cmulp(double2 x, double2 y) { return cmul(x, y); }
 
 template <typename Real> struct DAcc {
     typedef decltype(DTerm<Real>::ang) U;
@@ -354,9 +377,22 @@ __device__ __forceinline__ typename DAcc<Real>::U dblk_sum(const DTerm<Real> *tm
 template <typename Real, bool BWD>
 __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
                                          typename CT<Real>::C *l, uint32_t tix, uint64_t basefull,
-                                         const typename DAcc<Real>::U *ctab, const typename DAcc<Real>::U *uacc) {
+                                         const DevStage &S, const typename DAcc<Real>::U *uacc,
+                                         const typename CT<Real>::C *ctb) {
     typedef typename CT<Real>::C C;
     typedef typename DAcc<Real>::U U;
+    // this thread's C rows: dynamic shared memory after the sweep kernel's other
+    // regions (sweep_smem_bytes order); recomputed here so that the op loop carries
+    // no extra pointer (S, uacc and ctb are static shared arrays)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const U *ctab;
+    {
+        const size_t T = blockDim.x;
+        const size_t off = (size_t)(BWD ? 2 : 1) * ((size_t)1 << S.k) * sizeof(C) + (size_t)S.n_ops * sizeof(KOp<Real>) +
+                           (BWD ? (size_t)S.n_slots * T * sizeof(Real) : 0) + (size_t)(3 * S.nseg - 2) * T * sizeof(uint32_t) +
+                           2 * T * sizeof(uint64_t);
+        ctab = reinterpret_cast<const U *>(smem_raw + off) + threadIdx.x;
+    }
     const int first = (int)((h.x >> 24) & 0xffu);  // data kops before this one
     const uint32_t xm = h.y & 0xffu;
     const uint32_t coff = (h.y >> 8) & 0xffu, uoff = (h.y >> 16) & 0xffu;
@@ -388,34 +424,32 @@ __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typ
         for (int b = 0; b < SWEEP_R; b++)
             if ((xm >> b) & 1u) al[b] += dblk_sum<Real>(tm, i0, i1, (uint32_t)b, tix, basefull);
     }
-    C w[NR];
-    w[0] = cis_turn(th);
-    // w[r] = w[0] prod_{b in r} e^{i al_b}: doubling over the register bits
-#pragma unroll
-    for (int b = 0; b < SWEEP_R; b++) {
-        if ((xm >> b) & 1u) {
-            const C u = cis_turn(al[b]);
-#pragma unroll
-            for (int r = 0; r < (2 << b) && r < NR; r++)
-                if (r & (1 << b)) w[r] = cmul(w[r & ~(1 << b)], u);
-        } else {
-#pragma unroll
-            for (int r = 0; r < (2 << b) && r < NR; r++)
-                if (r & (1 << b)) w[r] = w[r & ~(1 << b)];
-        }
-    }
+    // in place, no per-amplitude phase array: table[r] e^{i th} first, then
+    // e^{i al_b} on the amplitudes with register bit b set
+    const C w0 = cis_turn(th, ctb);
     if ((h.x >> 16) & 2u) {  // identity table
 #pragma unroll
         for (int r = 0; r < NR; r++) {
-            a[r] = cmul(w[r], a[r]);
-            if (BWD) l[r] = cmul(w[r], l[r]);
+            a[r] = cmulp(w0, a[r]);
+            if (BWD) l[r] = cmulp(w0, l[r]);
         }
     } else {
 #pragma unroll
         for (int r = 0; r < NR; r++) {
-            const C ph = cmul_e(op.m + 4 * r, w[r]);
-            a[r] = cmul(ph, a[r]);
-            if (BWD) l[r] = cmul(ph, l[r]);
+            const C ph = cmul_e(op.m + 4 * r, w0);
+            a[r] = cmulp(ph, a[r]);
+            if (BWD) l[r] = cmulp(ph, l[r]);
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < SWEEP_R; b++) {
+        if (!((xm >> b) & 1u)) continue;
+        const C u = cis_turn(al[b], ctb);
+#pragma unroll
+        for (int r = 0; r < NR; r++) {
+            if (!(r & (1 << b))) continue;
+            a[r] = cmulp(u, a[r]);
+            if (BWD) l[r] = cmulp(u, l[r]);
         }
     }
 }
@@ -423,10 +457,11 @@ __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typ
 // ---- one op, in place on psi (and lambda in the adjoint) ----------------------
 // h = the op's 16-byte dispatch header (already in registers: prefetched while
 // the previous op ran), op = the full op in shared memory (coefficients).
-template <typename Real, bool BWD>
+template <typename Real, bool BWD, bool DB>
 __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, typename CT<Real>::C *a,
                                         typename CT<Real>::C *l, uint32_t tix, uint64_t basefull, Real *tt,
-                                        const typename DAcc<Real>::U *ctab, const typename DAcc<Real>::U *uacc) {
+                                        const DevStage &S, const typename DAcc<Real>::U *uacc,
+                                        const typename CT<Real>::C *ctb) {
     typedef typename CT<Real>::C C;
     auto bitval = [&](uint32_t kind, uint32_t idx) -> int {
         return kind == BK_TIX ? (int)((tix >> idx) & 1u) : (int)((basefull >> idx) & 1ull);
@@ -515,7 +550,9 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
         }
         break;
     }
-    case KC_DBLK: run_dblk<Real, BWD>(h, op, a, l, tix, basefull, ctab, uacc); break;
+    case KC_DBLK:
+        if constexpr (DB) run_dblk<Real, BWD>(h, op, a, l, tix, basefull, S, uacc, ctb);
+        break;
     case KC_D2: {
         const uint32_t k0 = h.z & 0xff, i0 = (h.z >> 8) & 0xff, k1 = (h.z >> 16) & 0xff, i1 = h.z >> 24;
         const int m0 = k0 == BK_REG ? (1 << i0) : 0;
@@ -536,8 +573,10 @@ __device__ __forceinline__ double2 ldcs_c(const double2 *p) { return __ldcs(p); 
 __device__ __forceinline__ void stcs_c(float2 *p, float2 v) { __stcs(p, v); }
 __device__ __forceinline__ void stcs_c(double2 *p, double2 v) { __stcs(p, v); }
 
-// ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles
-template <typename Real, bool BWD>
+// ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles.
+// DB: the stage has diagonal-block runs (a separate instantiation keeps their
+// shared arrays, precomputation and code out of the stages that have none)
+template <typename Real, bool BWD, bool DB>
 __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_LB_MINB_F32_BWD : TQD_LB_MINB_F32_FWD) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
@@ -583,8 +622,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
     // diagonal blocks: per-thread C rows [row][thread], per-tile U values [2][DBLK_UCAP]
     typedef typename DAcc<Real>::U DU;
     DU *s_ctab = reinterpret_cast<DU *>(s_pf + 2 * blockDim.x);
-    DU *s_uacc = s_ctab + (size_t)S.n_cvals * blockDim.x;
-    __shared__ uint8_t s_uk[DBLK_UCAP], s_ut[DBLK_UCAP];  // U value -> kop index, target (0xff = th)
+    __shared__ DU s_uacc[DB ? DBLK_UCAP : 1];  // this tile's U values
+    __shared__ uint8_t s_uk[DB ? DBLK_UCAP : 1], s_ut[DB ? DBLK_UCAP : 1];  // U value -> kop index, target (0xff = th)
+    __shared__ C s_cis[DB ? 256 : 1];                                       // e^{i 2 pi k / 256} for cis_turn
     {
         const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base + (size_t)bidx * S.n_ops);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
@@ -636,7 +676,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
     // diagonal blocks: C sums once per kernel (lane / warp bits are fixed per thread
     // and segment) into this thread's rows, the per-tile U work list (value -> applying
     // kop, target) once per kernel
-    if (S.n_cvals || S.n_uvals) {
+    if constexpr (DB)
+        for (int kk = threadIdx.x; kk < 256; kk += blockDim.x) cis_table_entry(kk, s_cis);
+    if (DB && (S.n_cvals || S.n_uvals)) {
         for (int j = 0; j < S.n_cvals; j++) s_ctab[j * blockDim.x + threadIdx.x] = 0;
         for (int s = 0; s < nseg; s++) {
             const uint32_t tx = thr_tix(S.lay[s]);
@@ -734,21 +776,27 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                 if (BWD) l[r] = ldcs_c(lam + o[r]);
             }
         }
-        // diagonal blocks: this tile's U sums (base bits only), one thread per value,
-        // double-buffered by tile parity (the barrier also orders the C table writes)
-        const DU *uacc = s_uacc + ((tile / gsz) & 1) * DBLK_UCAP;
-        if (S.n_uvals) {
-            if ((int)threadIdx.x < S.n_uvals) {
-                const int oi = s_uk[threadIdx.x];
+        // diagonal blocks: this tile's U sums (base bits only), between two barriers
+        if (DB && S.n_uvals) {
+            __syncthreads();  // every thread is done with the previous tile's values
+            // one warp per value, one lane per term of each kop of the run (nU <= 16),
+            // exact wrapping integer sums by shuffle
+            const int nw = (int)(blockDim.x >> 5);
+            for (int v = warp; v < S.n_uvals; v += nw) {
+                const int oi = s_uk[v];
+                const uint32_t tgt = s_ut[v];
                 const int first = (int)((reinterpret_cast<const uint4 *>(&s_ops[oi])->x >> 24) & 0xffu);
-                DU v = 0;
-                for (int q = oi - first; q <= oi; q++) {  // the U terms of every kop of the run
+                DU sum = 0;
+                for (int q = oi - first; q <= oi; q++) {
                     const uint32_t hz = reinterpret_cast<const uint4 *>(&s_ops[q])->z;
                     const int nC = (int)(hz & 0xffu), nU = (int)((hz >> 8) & 0xffu);
-                    v += dblk_sum<Real>(reinterpret_cast<const DTerm<Real> *>(s_ops[q].g), nC, nC + nU, s_ut[threadIdx.x],
-                                        0, basefull);
+                    if (lane < nU)
+                        sum += dblk_sum<Real>(reinterpret_cast<const DTerm<Real> *>(s_ops[q].g), nC + lane, nC + lane + 1,
+                                              tgt, 0, basefull);
                 }
-                const_cast<DU *>(uacc)[threadIdx.x] = v;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+                if (lane == 0) s_uacc[v] = sum;
             }
             __syncthreads();
         }
@@ -821,7 +869,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             for (; oi < e; oi++) {
                 // header of the next op loads while this one runs
                 const uint4 hn = oi + 1 < e ? *reinterpret_cast<const uint4 *>(&s_ops[oi + 1]) : h;
-                run_kop<Real, BWD>(h, s_ops[oi], a, l, tix, basefull, tacc + threadIdx.x, s_ctab + threadIdx.x, uacc);
+                run_kop<Real, BWD, DB>(h, s_ops[oi], a, l, tix, basefull, tacc + threadIdx.x, S, s_uacc, s_cis);
                 h = hn;
             }
         }
@@ -877,7 +925,7 @@ static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int n
     typedef typename DAcc<Real>::U DU;
     return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
            (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t) +
-           (size_t)2 * threads * sizeof(uint64_t) + (size_t)n_cvals * threads * sizeof(DU) + 2 * DBLK_UCAP * sizeof(DU);
+           (size_t)2 * threads * sizeof(uint64_t) + (size_t)n_cvals * threads * sizeof(DU);
 }
 
 // The dynamic shared-memory cap is a per-function attribute shared by every host
@@ -901,29 +949,41 @@ template <typename F> static cudaError_t raise_smem_cap_once(F fn, std::atomic<u
     return e;
 }
 
-template <typename Real, bool BWD> static std::atomic<uint64_t> &sweep_cap_flag() {
+template <typename Real, bool BWD, bool DB> static std::atomic<uint64_t> &sweep_cap_flag() {
     static std::atomic<uint64_t> f{0};
     return f;
 }
 
-template <typename Real, bool BWD>
-cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                              double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops,
-                              int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
+// n_cvals < 0: the stage has no diagonal-block runs (plain instantiation)
+template <typename Real, bool BWD, bool DB>
+cudaError_t launch_sweep_t(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
+                           double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops, int n_slots,
+                           int nseg, int n_cvals, int grid, cudaStream_t s) {
     typedef typename CT<Real>::C C;
-    auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, n_cvals);
-    cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>());
+    auto fn = sweep_kernel<Real, BWD, DB>;
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, DB ? n_cvals : 0);
+    cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD, DB>());
     if (e != cudaSuccess) return e;
     fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi, sc);
     return cudaGetLastError();
 }
 
 template <typename Real, bool BWD>
-int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
-    auto fn = sweep_kernel<Real, BWD>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, n_cvals);
-    if (raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD>()) != cudaSuccess) {
+cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
+                              double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops,
+                              int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
+    if (n_cvals >= 0)
+        return launch_sweep_t<Real, BWD, true>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops,
+                                               n_slots, nseg, n_cvals, grid, s);
+    return launch_sweep_t<Real, BWD, false>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots,
+                                            nseg, 0, grid, s);
+}
+
+template <typename Real, bool BWD, bool DB>
+int sweep_occupancy_t(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
+    auto fn = sweep_kernel<Real, BWD, DB>;
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, DB ? n_cvals : 0);
+    if (raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD, DB>()) != cudaSuccess) {
         cudaGetLastError();
         return 1;
     }
@@ -933,6 +993,12 @@ int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_c
         return 1;
     }
     return nb;
+}
+
+template <typename Real, bool BWD>
+int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
+    return n_cvals >= 0 ? sweep_occupancy_t<Real, BWD, true>(k, W, n_ops, n_slots, nseg, n_cvals)
+                        : sweep_occupancy_t<Real, BWD, false>(k, W, n_ops, n_slots, nseg, 0);
 }
 
 }  // namespace tqd

@@ -208,7 +208,7 @@ struct DevStage {
     int32_t batch;              // states in the batch: op / slot tables repeat per state (n_ops, n_slots each)
     int32_t no_store;           // backward only: last reverse stage, psi / lambda are not needed afterwards
     int32_t n_cvals, n_uvals;   // diagonal blocks: per-thread C rows, per-tile U values (see DTerm)
-    int32_t pad3;
+    int32_t n_dblk;             // applying diagonal-block kops in the stage
 };
 
 // sweep-kernel variant bits (DevStage::flags)
