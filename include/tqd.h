@@ -94,12 +94,14 @@ typedef enum {
     TQD_OPT_FUSED_REMAP = 5,  /* 1: a remap right after a sweep is fused into it: the sweep
                                * stores straight into the owners' peer memory (default 1);
                                * 0: pack -> all-to-all -> unpack                          */
-    TQD_OPT_ABSORB_TAIL = 6   /* 1 (default): tqd_adjoint_grad with Z-string terms absorbs the
-                               * circuit's trailing diagonal / permutation gates (RZ, CZ, CP,
-                               * X, Y, CNOT, SWAP ...) into the observable by conjugation
-                               * (Heisenberg picture, E = <psi|U^dag H U|psi>) instead of
-                               * applying and un-applying them; same value and gradients
-                               * (absorbed trainable gates are diagonal: gradient 0).
+    TQD_OPT_ABSORB_TAIL = 6   /* 1 (default): tqd_adjoint_grad and tqd_expval with Z-string
+                               * terms absorb the circuit's trailing diagonal / permutation
+                               * gates (RZ, CZ, CP, X, Y, CNOT, SWAP ...) into the observable by
+                               * conjugation (Heisenberg picture, E = <psi|U^dag H U|psi>)
+                               * instead of applying (and un-applying) them; same values and
+                               * gradients (absorbed trainable gates are diagonal: gradient 0).
+                               * After tqd_expval the absorbed gates stay pending: a later
+                               * readback / sample / non-Z observable applies them.
                                * 0: apply every gate.                                      */
 } tqd_option;
 

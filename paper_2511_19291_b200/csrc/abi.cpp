@@ -622,10 +622,13 @@ static uint64_t tape_values_hash(const tqd_state *st) {
 // Execute the recorded gates [executed, end).  end < gates.size() only from
 // tqd_adjoint_grad: the gates [end, size) were absorbed into the observable
 // (absorb_tail) and are never applied; the plan caches are keyed by that split.
-static int execute_pending(tqd_state *st, size_t end = SIZE_MAX) {
+// keep_tail (tqd_expval): the absorbed gates stay pending (executed = end), so a
+// later readback or non-Z observable applies them; else they count as executed.
+static int execute_pending(tqd_state *st, size_t end = SIZE_MAX, bool keep_tail = false) {
     if (end > st->gates.size()) end = st->gates.size();
+    const size_t done_to = keep_tail ? end : st->gates.size();
     if (st->executed >= end) {
-        st->executed = st->gates.size();
+        if (!keep_tail) st->executed = st->gates.size();
         return TQD_OK;
     }
     const uint64_t tmix = (uint64_t)(st->gates.size() - end) * 0x9E3779B97F4A7C15ull;
@@ -645,7 +648,7 @@ static int execute_pending(tqd_state *st, size_t end = SIZE_MAX) {
         int rc = launch_encoded(st, st->history, false, *st->enc_fwd, nullptr);
         if (rc) return rc;
         st->pos = st->cached_pos;
-        st->executed = st->gates.size();
+        st->executed = done_to;
         st->history_cached = true;
         return TQD_OK;
     }
@@ -685,7 +688,7 @@ static int execute_pending(tqd_state *st, size_t end = SIZE_MAX) {
         st->history_cached = false;
     }
     for (auto &s : stages) st->history.push_back(std::move(s));
-    st->executed = st->gates.size();
+    st->executed = done_to;
     return TQD_OK;
 }
 
@@ -997,6 +1000,9 @@ int tqd_num_params(const tqd_state *st, int *out) {
     return TQD_OK;
 }
 
+static size_t absorb_tail(const std::vector<GateRec> &gates, size_t executed, std::vector<uint64_t> &z,
+                          std::vector<double> &sgn);
+
 int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff, double *out) {
     int rc = check_live(st);
     if (rc) return rc;
@@ -1004,7 +1010,20 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
     if (T > 0 && !out) return fail(TQD_ERR_ARG, "out is NULL");
     rc = check_terms(st, T, x, z);
     if (rc) return rc;
-    rc = execute_pending(st);
+    // Z-only observables: the trailing diagonal / permutation gates are folded into
+    // the terms (absorb_tail) and stay pending for later calls
+    std::vector<uint64_t> zabs(z, z + T);
+    std::vector<double> sabs(T, 1.0);
+    size_t end = st->gates.size();
+    bool z_only = T > 0;
+    for (int t = 0; t < T; t++)
+        if (x[t]) z_only = false;
+    if (st->opt_absorb && z_only) {
+        end = absorb_tail(st->gates, st->executed, zabs, sabs);
+        z = zabs.data();
+        if (end < st->gates.size()) st->met.gates_absorbed += st->gates.size() - end;
+    }
+    rc = execute_pending(st, end, true);
     if (rc) return rc;
     if (T == 0) return ev_collect(st);
     const int BT = st->batch * T;  // outputs: batch element b, term t at b * T + t
@@ -1090,7 +1109,7 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
     CUDA_TRY(st, cudaMemcpyAsync(h.data(), d_all, BT * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));
     st->met.d2h_bytes += BT * sizeof(double);
-    for (int i = 0; i < BT; i++) out[i] = (coeff ? coeff[i % T] : 1.0) * h[i];
+    for (int i = 0; i < BT; i++) out[i] = (coeff ? coeff[i % T] : 1.0) * sabs[i % T] * h[i];
     return ev_collect(st);
 }
 

@@ -1,4 +1,4 @@
-"""GPU parity of tqd_adjoint_grad with observable absorption (TQD_OPT_ABSORB_TAIL):
+"""GPU parity of tqd_adjoint_grad / tqd_expval with observable absorption (TQD_OPT_ABSORB_TAIL):
 the trailing diagonal / permutation gates are folded into the Z-string
 observable instead of being applied and un-applied.  Every value and gradient is
 compared with the float64 oracle applying EVERY gate (tolerances as in
@@ -135,3 +135,48 @@ def test_world_absorbed_tail(tqd, orc, world, n, k, dtype):
         assert abs(val - rval) < TOL[dtype]
         assert np.max(np.abs(grad - rgrad)) < TOL[dtype]
         assert m["gates_absorbed"] >= len(tail)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,small_max", [(6, 10), (14, 0)])
+def test_expval_absorbed_tail_stays_pending(tqd, ctx, orc, n, small_max, dtype):
+    """tqd_expval with Z strings absorbs the tail and leaves it pending: the next
+    X/Y expval, readback or adjoint applies it; every result against the oracle."""
+    tol = TOL[dtype]
+    gates = W.random_circuit(n, 50, 77, small=True) + W.diag_perm_tail(n, 30, 78)
+    zt = W.random_z_terms(n, 5, 1) + W.sum_z(n)
+    xt = W.random_pauli_terms(n, 6, 2)
+    psi = orc.run(n, gates)
+    r_z, r_x = orc.expval(psi, n, zt), orc.expval(psi, n, xt)
+    rval, rgrad = orc.adjoint(n, gates, zt)
+    amp_tol = 1e-5 if dtype == "c64" else 1e-12
+
+    def fresh():
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_SMALL_MAX, small_max)
+        st.apply_circuit(gates)
+        return st
+
+    st = fresh()
+    try:
+        assert np.max(np.abs(st.expval(zt) - r_z)) < tol
+        assert st.metrics()["gates_absorbed"] >= 30
+        assert np.max(np.abs(st.expval(zt) - r_z)) < tol          # again, still pending
+        assert np.max(np.abs(st.expval(xt) - r_x)) < tol          # X/Y: the tail is applied now
+        assert np.max(np.abs(st.amplitudes() - psi)) < amp_tol
+        assert np.max(np.abs(st.expval(zt) - r_z)) < tol
+    finally:
+        st.free()
+    st = fresh()
+    try:
+        assert np.max(np.abs(st.expval(zt) - r_z)) < tol
+        assert np.max(np.abs(st.amplitudes() - psi)) < amp_tol  # readback applies the tail
+    finally:
+        st.free()
+    st = fresh()
+    try:
+        assert np.max(np.abs(st.expval(zt) - r_z)) < tol
+        val, grad = st.adjoint_grad(zt)                           # adjoint after a pending tail
+        assert abs(val - rval) < tol and np.max(np.abs(grad - rgrad)) < tol
+    finally:
+        st.free()
