@@ -1078,7 +1078,8 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
     };
     const int threads = 32 << sp.W;
     int n_cvals = 0, n_uvals = 0;  // diagonal-block C rows / U values of this stage
-    const int ccap = sizeof(Real) == 4 ? DBLK_CCAP_F32 : DBLK_CCAP_F64;
+    // the forward sweep has shared memory to spare (one state tile): more C rows
+    const int ccap = (sizeof(Real) == 4 ? DBLK_CCAP_F32 : DBLK_CCAP_F64) * (bwd ? 1 : 3);
     auto finalize = [threads](KOp<Real> &k) {
         switch (k.kind) {
         case K_LAYER:
@@ -1304,6 +1305,15 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             for (double v : tab)
                 if (std::abs(std::remainder(v, 2 * M_PI)) > 1e-15) ident = false;
             if (ident && other.empty()) return;
+            if (other.empty()) {  // register bits only: a diagonal layer (one multiply per amplitude)
+                KOp<Real> k = newop(K_LAYER);
+                k.ltype = LT_DIAG;
+                k.mask = (uint8_t)((1 << R) - 1);
+                for (int r = 0; r < (1 << R); r++) pute(k, r, std::polar(1.0, tab[r]));
+                finalize(k);
+                ops.push_back(k);
+                return;
+            }
             uint8_t xm = 0;
             for (const DT &t : other)
                 if (t.a.kind == BK_REG) xm |= (uint8_t)(1u << t.a.idx);

@@ -134,8 +134,8 @@ constexpr int DBLK_TERMS = 16;
 //      once per tile by one thread per value into u_acc (rows u_off..);
 //   M: lane / warp x base products: summed by every thread per tile.
 // The run's C rows / U values: 1 + popc(xm): th, then al[b] for b in xm.
-constexpr int DBLK_CCAP_F32 = 16;  // per-thread C rows per stage (shared memory: rows x threads x 4 B)
-constexpr int DBLK_CCAP_F64 = 4;   // (x 8 B); both <= 16 KB at 256 threads
+constexpr int DBLK_CCAP_F32 = 16;  // per-thread C rows per adjoint stage (shared memory: rows x threads x 4 B)
+constexpr int DBLK_CCAP_F64 = 4;   // (x 8 B); both <= 16 KB at 256 threads; forward stages: 3x
 constexpr int DBLK_UCAP = 64;      // per-tile U values per stage
 template <typename Real> struct DTerm;
 template <> struct DTerm<float> {
