@@ -1305,13 +1305,29 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             for (double v : tab)
                 if (std::abs(std::remainder(v, 2 * M_PI)) > 1e-15) ident = false;
             if (ident && other.empty()) return;
-            if (other.empty()) {  // register bits only: a diagonal layer (one multiply per amplitude)
-                KOp<Real> k = newop(K_LAYER);
-                k.ltype = LT_DIAG;
-                k.mask = (uint8_t)((1 << R) - 1);
-                for (int r = 0; r < (1 << R); r++) pute(k, r, std::polar(1.0, tab[r]));
-                finalize(k);
-                ops.push_back(k);
+            // cheap forms first: register bits only -> a diagonal layer; plus at most two
+            // single-bit terms on lane / warp / base bits -> K_PHASE ops (one multiply per
+            // amplitude each, no per-tile work, the plain kernel instantiation)
+            bool simple = other.size() <= 2;
+            for (const DT &t : other)
+                if (t.a.kind == BK_REG || t.b.kind != BK_NONE) simple = false;
+            if (simple) {
+                if (!ident) {
+                    KOp<Real> k = newop(K_LAYER);
+                    k.ltype = LT_DIAG;
+                    k.mask = (uint8_t)((1 << R) - 1);
+                    for (int r = 0; r < (1 << R); r++) pute(k, r, std::polar(1.0, tab[r]));
+                    finalize(k);
+                    ops.push_back(k);
+                }
+                for (const DT &t : other) {
+                    KOp<Real> k = newop(K_PHASE);
+                    k.b0 = t.a;
+                    pute(k, 0, cd(1.0));
+                    pute(k, 1, std::polar(1.0, t.ang));
+                    finalize(k);
+                    ops.push_back(k);
+                }
                 return;
             }
             uint8_t xm = 0;
