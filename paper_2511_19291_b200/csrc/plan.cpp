@@ -1423,7 +1423,9 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
                 q[bit].push_back(qg);
                 continue;
             }
-            if ((o.kind == OP_D1 && o.cp < 0 && !has_gen) || o.kind == OP_D2) {
+            // (batched gates keep their own K_PHASE op: a run's kop structure depends on
+            // the values -- zero terms vanish -- and must be equal for every batch element)
+            if ((o.kind == OP_D1 && o.cp < 0 && !has_gen && !g.batched) || o.kind == OP_D2) {
                 // theta(u, v) = a + b u + c v + d u v with theta_uv = arg d[2u + v] (u = MSB bit)
                 const BitRef u = bref(o.dp0), v = o.kind == OP_D2 ? bref(o.dp1) : none;
                 bool busy = false;  // a register bit of this gate has queued gates: they go first

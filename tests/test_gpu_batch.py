@@ -236,3 +236,28 @@ def test_batch_training_loop_reuses_plan(tqd, ctx, orc):
         assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
     assert st.metrics()["plans_reused"] == 2
     st.free()
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_batch_diagonal_runs_with_zero_inputs(tqd, ctx, orc, dtype):
+    """Batched RZ encoder inputs that are exactly 0 for some elements, placed after
+    dense gates (so they land on lane / warp / base bits) and between controlled-phase
+    runs: the kernel-op structure must not depend on the per-element values."""
+    n, B = 14, 3
+    x = encoder_inputs(B, n, 5, "RZ")
+    x[:, 1, :] = 0.0
+    x[::3, 2, :] = 0.0
+    pre = [W.Gate("H", (q,)) for q in range(n)] + W.qft(n, swaps=False)[:40]
+    post = W.qft(n, swaps=False)[40:90] + W.hea(n, 1, seed=2, small=True)
+    terms = W.sum_z(n) + W.random_z_terms(n, 3, 4)
+    st = make(tqd, ctx, n, dtype, B, 12, 0)
+    st.apply_circuit(pre)
+    for q in range(n):
+        st.apply_batch("RZ", [q], x[q], trainable=True)
+    st.apply_circuit(post)
+    amp = st.amplitudes()
+    st.free()
+    for b in range(B):
+        enc = [W.Gate("RZ", (q,), (float(x[q, b, 0]),), None, True) for q in range(n)]
+        psi = orc.run(n, pre + enc + post)
+        assert np.max(np.abs(amp[b << n:(b + 1) << n] - psi)) < TOL[dtype]["amp"], b
