@@ -397,10 +397,17 @@ static bool fusable_remap(const tqd_state *st, bool bwd) {
            (!bwd || st->own_lam);
 }
 
+// 1 = peer memory unavailable on some rank (same on every rank): fusion is turned
+// off for this state and the remap runs as pack -> all-to-all -> unpack
 static int share_pair(tqd_state *st, void *a, void *b, std::vector<void *> &table) {
     if (!table.empty()) return TQD_OK;
     void *loc[2] = {a, b};
-    COMM_TRY(st, st->ctx->comm->share_buffers(loc, 2, table, st->ctx->stream));
+    const int rc = st->ctx->comm->share_buffers(loc, 2, table, st->ctx->stream);
+    if (rc == 2) {
+        st->opt_fused = 0;
+        return 1;
+    }
+    COMM_TRY(st, rc);
     return TQD_OK;
 }
 
@@ -423,16 +430,17 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
             const SweepPlan &sp = s.sw;
             ScatterInfo sc;
             memset(&sc, 0, sizeof(sc));
-            const bool fuse = li + 1 < E.launches.size() && E.launches[li + 1].type == ST_REMAP && fusable_remap(st, bwd);
+            bool fuse = li + 1 < E.launches.size() && E.launches[li + 1].type == ST_REMAP && fusable_remap(st, bwd);
             if (fuse) {
                 int rc = ensure_xchg(st);
                 if (rc) return rc;
                 rc = share_pair(st, st->psi_first, st->recv_first, st->peer_psi);
-                if (rc) return rc;
-                if (bwd) {
-                    rc = share_pair(st, st->lam_first, st->send_first, st->peer_lam);
-                    if (rc) return rc;
-                }
+                if (rc < 0) return rc;
+                if (rc == 0 && bwd) rc = share_pair(st, st->lam_first, st->send_first, st->peer_lam);
+                if (rc < 0) return rc;
+                fuse = rc == 0;  // 1: no peer memory, the remap launch below runs unfused
+            }
+            if (fuse) {
                 const RemapPlan &rp = stages[E.launches[li + 1].stage].rm;
                 sc.m = rp.m;
                 sc.n_loc = st->n_loc;

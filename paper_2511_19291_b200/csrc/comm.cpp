@@ -57,30 +57,49 @@ class NcclComm : public Comm {
         err = std::string(what) + ": " + cudaGetErrorString(e);
         return 1;
     }
+    // Collective.  Returns 0 (table filled), 1 (communication error) or 2 (CUDA IPC
+    // is unavailable on some rank: every rank gets 2 and the caller falls back to
+    // pack -> all-to-all -> unpack).  IPC failures never skip a collective.
     int share_buffers(void *const *local, int nbuf, std::vector<void *> &table, cudaStream_t s) override {
         const size_t hs = sizeof(cudaIpcMemHandle_t);
-        std::vector<char> mine(nbuf * hs), all((size_t)world * nbuf * hs);
-        for (int i = 0; i < nbuf; i++)
-            if (cuda(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + i * hs), local[i]), "cudaIpcGetMemHandle"))
-                return 1;
+        std::vector<char> mine(nbuf * hs, 0), all((size_t)world * nbuf * hs);
+        int ok = 1;
+        for (int i = 0; i < nbuf && ok; i++)
+            if (cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(mine.data() + i * hs), local[i]) != cudaSuccess) {
+                cudaGetLastError();
+                ok = 0;
+            }
         char *d = nullptr;
-        if (cuda(cudaMalloc(&d, all.size() + mine.size()), "cudaMalloc")) return 1;
+        if (cuda(cudaMalloc(&d, all.size() + mine.size() + sizeof(int)), "cudaMalloc")) return 1;
         int rc = cuda(cudaMemcpyAsync(d, mine.data(), mine.size(), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
         if (!rc) rc = check(ncclAllGather(d, d + mine.size(), mine.size(), ncclUint8, c, s), "ncclAllGather");
         if (!rc) rc = cuda(cudaMemcpyAsync(all.data(), d + mine.size(), all.size(), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
         if (!rc) rc = cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
-        cudaFree(d);
-        if (rc) return rc;
         table.assign((size_t)world * nbuf, nullptr);
-        for (int r = 0; r < world; r++)
+        for (int r = 0; r < world && !rc; r++)
             for (int i = 0; i < nbuf; i++) {
                 if (r == rank) { table[r * nbuf + i] = local[i]; continue; }
+                if (!ok) continue;
                 cudaIpcMemHandle_t hdl;
                 memcpy(&hdl, all.data() + ((size_t)r * nbuf + i) * hs, hs);
-                if (cuda(cudaIpcOpenMemHandle(&table[r * nbuf + i], hdl, cudaIpcMemLazyEnablePeerAccess),
-                         "cudaIpcOpenMemHandle"))
-                    return 1;
+                if (cudaIpcOpenMemHandle(&table[r * nbuf + i], hdl, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    table[r * nbuf + i] = nullptr;
+                    ok = 0;
+                }
             }
+        // every rank learns whether all ranks opened every peer buffer
+        int *dok = reinterpret_cast<int *>(d + all.size() + mine.size());
+        if (!rc) rc = cuda(cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s), "cudaMemcpyAsync");
+        if (!rc) rc = check(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c, s), "ncclAllReduce");
+        if (!rc) rc = cuda(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+        if (!rc) rc = cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        cudaFree(d);
+        if (rc) return rc;
+        if (!ok) {
+            release_buffers(table, nbuf);
+            return 2;
+        }
         return 0;
     }
     void release_buffers(std::vector<void *> &table, int nbuf) override {

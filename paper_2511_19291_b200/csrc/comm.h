@@ -36,7 +36,8 @@ class Comm {
     // make nbuf local device allocations addressable by every rank (peer memory):
     // table[r * nbuf + i] = rank r's buffer i, usable in this process's kernels.
     // NCCL: CUDA IPC handles exchanged with an all-gather (NVLink P2P); loopback:
-    // plain pointers (same device).  Collective.
+    // plain pointers (same device).  Collective.  Returns 0, 1 (error) or 2 (peer
+    // memory unavailable on some rank -- the same answer on every rank).
     virtual int share_buffers(void *const *local, int nbuf, std::vector<void *> &table, cudaStream_t s) = 0;
     virtual void release_buffers(std::vector<void *> &table, int nbuf) {}
     // returns once the work every rank queued before it has completed (host-blocking)
