@@ -1305,10 +1305,11 @@ void encode_sweep_k(const SweepPlan &sp, const std::vector<GateRec> &gates, bool
             for (double v : tab)
                 if (std::abs(std::remainder(v, 2 * M_PI)) > 1e-15) ident = false;
             if (ident && other.empty()) return;
-            // cheap forms first: register bits only -> a diagonal layer; plus at most two
+            // cheap forms first: register bits only -> a diagonal layer; plus at most six
             // single-bit terms on lane / warp / base bits -> K_PHASE ops (one multiply per
-            // amplitude each, no per-tile work, the plain kernel instantiation)
-            bool simple = other.size() <= 2;
+            // amplitude each, no per-tile work, the plain kernel instantiation: the
+            // diagonal-block instantiation costs ~2 ms more per 30-qubit sweep)
+            bool simple = other.size() <= 6;
             for (const DT &t : other)
                 if (t.a.kind == BK_REG || t.b.kind != BK_NONE) simple = false;
             if (simple) {
