@@ -90,7 +90,10 @@ typedef enum {
     TQD_OPT_SMALL_MAX = 1,    /* n_loc <= this runs the single-CTA whole-state kernel (default 10) */
     TQD_OPT_PROFILE = 2,      /* 1: time every kernel with CUDA events (see tqd_metrics) */
     TQD_OPT_GRID_CTAS = 3,    /* persistent CTAs per launch (0 = auto: SMs x resident CTAs) */
-    TQD_OPT_USE_GRAPH = 4,    /* 1: replay cached plans as CUDA graphs (default 0)      */
+    TQD_OPT_USE_GRAPH = 4,    /* 1: replays of a cached plan (tqd_state_rewind, or a re-recorded
+                               * tape of the same structure) launch the forward and reverse
+                               * sweep sequences as CUDA graphs (one rank, PROFILE off;
+                               * default 0)                                               */
     TQD_OPT_FUSED_REMAP = 5,  /* 1: a remap right after a sweep is fused into it: the sweep
                                * stores straight into the owners' peer memory (default 1);
                                * 0: pack -> all-to-all -> unpack                          */

@@ -107,6 +107,10 @@ struct tqd_state {
     uint64_t fwd_vhash = 0, bwd_vhash = 0;  // tape_values_hash of the resident descriptors
     uint64_t cached_tmix = 0;  // absorbed-tail length mix of the cached plan (execute_pending)
     struct Encoded *enc_fwd = nullptr, *enc_bwd = nullptr, *enc_tmp = nullptr;
+    // TQD_OPT_USE_GRAPH: the cached forward / reverse launch sequences as CUDA graphs
+    cudaGraphExec_t g_fwd = nullptr, g_bwd = nullptr;
+    uint64_t g_fwd_key = 0, g_bwd_key = 0;
+    tqd_metrics g_fwd_delta, g_bwd_delta;
     // profiling
     std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<int, int>> ev_used;  // (start index, category); stop = start+1
@@ -488,6 +492,55 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
     return TQD_OK;
 }
 
+// Replays of a cached launch sequence as one CUDA graph (TQD_OPT_USE_GRAPH; one
+// rank, no profiling events): captured on first use, relaunched while the key
+// (plan structure, descriptor / state / gradient buffers) is unchanged.  The
+// descriptors are read from device memory at run time, so new parameter values
+// uploaded into the same buffer need no re-capture.  Host-side metrics of the
+// captured launches are re-added on every replay.
+static void add_counts(tqd_metrics &m, const tqd_metrics &d, int sign) {
+    auto f = [&](uint64_t &x, uint64_t y) { x = sign > 0 ? x + y : x - y; };
+    f(m.fwd_sweeps, d.fwd_sweeps); f(m.bwd_sweeps, d.bwd_sweeps); f(m.remaps, d.remaps);
+    f(m.gates_applied, d.gates_applied); f(m.gates_unapplied, d.gates_unapplied); f(m.hbm_bytes, d.hbm_bytes);
+    f(m.a2a_bytes, d.a2a_bytes); f(m.fwd_sweep_bytes, d.fwd_sweep_bytes); f(m.bwd_sweep_bytes, d.bwd_sweep_bytes);
+    f(m.kernel_launches, d.kernel_launches); f(m.fused_remaps, d.fused_remaps);
+}
+
+static int launch_graphed(tqd_state *st, const std::vector<Stage> &stages, bool bwd, const Encoded &E, double *d_grad,
+                          cudaGraphExec_t &ge, uint64_t &gkey, tqd_metrics &delta) {
+    if (!st->opt_graph || st->ctx->world != 1 || st->opt_profile) return launch_encoded(st, stages, bwd, E, d_grad);
+    uint64_t key = st->plan_sig ^ (st->cached_tmix * 3) ^ 0x51ED27ull;
+    for (uint64_t v : {(uint64_t)E.dev, (uint64_t)st->psi, (uint64_t)st->lam, (uint64_t)d_grad, (uint64_t)E.launches.size(),
+                       (uint64_t)stages.size()})
+        key = (key ^ v) * 1099511628211ull;
+    cudaStream_t s = st->ctx->stream;
+    if (ge && gkey == key) {
+        CUDA_TRY(st, cudaGraphLaunch(ge, s));
+        add_counts(st->met, delta, +1);
+        return TQD_OK;
+    }
+    const tqd_metrics before = st->met;
+    CUDA_TRY(st, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int rc = launch_encoded(st, stages, bwd, E, d_grad);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (rc) {
+        if (e == cudaSuccess && g) cudaGraphDestroy(g);
+        return rc;
+    }
+    CUDA_TRY(st, e);
+    if (ge) cudaGraphExecDestroy(ge);
+    ge = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(st, ei);
+    delta = st->met;
+    add_counts(delta, before, -1);
+    gkey = key;
+    CUDA_TRY(st, cudaGraphLaunch(ge, s));
+    return TQD_OK;
+}
+
 template <typename Real>
 static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E,
                        std::vector<DevStage> &dstages, std::vector<DevOp> &ops, std::vector<KOp<Real>> &kops,
@@ -653,7 +706,7 @@ static int execute_pending(tqd_state *st, size_t end = SIZE_MAX, bool keep_tail 
         st->cached_tmix == tmix) {
         // replay of the same tape from |0..0> (tqd_state_rewind): plan + descriptors are resident
         st->history = st->cached_stages;
-        int rc = launch_encoded(st, st->history, false, *st->enc_fwd, nullptr);
+        int rc = launch_graphed(st, st->history, false, *st->enc_fwd, nullptr, st->g_fwd, st->g_fwd_key, st->g_fwd_delta);
         if (rc) return rc;
         st->pos = st->cached_pos;
         st->executed = done_to;
@@ -922,6 +975,8 @@ int tqd_state_free(tqd_state *st) {
     for (Encoded *E : {st->enc_fwd, st->enc_bwd, st->enc_tmp}) {
         if (E) { free_encoded(*E); delete E; }
     }
+    if (st->g_fwd) cudaGraphExecDestroy(st->g_fwd);
+    if (st->g_bwd) cudaGraphExecDestroy(st->g_bwd);
     if (st->d_red) cudaFree(st->d_red);
     if (st->d_xy) cudaFree(st->d_xy);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
@@ -1150,7 +1205,7 @@ static int reverse_and_collect(tqd_state *st, double *d_grad, int n_grad, double
             st->bwd_vhash = cacheable ? st->fwd_vhash : 0;
             rc = launch_encoded(st, st->rev_stages, true, E, d_grad);
         } else {
-            rc = launch_encoded(st, st->rev_stages, true, *st->enc_bwd, d_grad);
+            rc = launch_graphed(st, st->rev_stages, true, *st->enc_bwd, d_grad, st->g_bwd, st->g_bwd_key, st->g_bwd_delta);
         }
         if (rc) return rc;
     }

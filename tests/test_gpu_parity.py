@@ -489,3 +489,41 @@ def test_diagonal_blocks(tqd, ctx, orc, n, k, dtype):
     N = 1 << n
     ref = np.exp(2j * np.pi * x * np.arange(N) / N) / math.sqrt(N)
     assert np.max(np.abs(got - ref)) < TOL[dtype]["amp"]
+
+
+def test_cuda_graph_replay(tqd, ctx, orc):
+    """TQD_OPT_USE_GRAPH: replays of the cached plan (rewind, and a re-recorded tape
+    with new angles) run as CUDA graphs; values, gradients and metrics unchanged."""
+    n = 16
+    res = {}
+    for graph in (0, 1):
+        st = make_state(tqd, ctx, n, "c64", small_max=0)
+        st.set_option(tqd.OPT_USE_GRAPH, graph)
+        out = []
+        try:
+            for seed in (0, 1):
+                gates = W.hea(n, 5, seed=seed, small=True)
+                rval, rgrad = orc.adjoint(n, gates, W.sum_z(n))
+                st.reset()
+                st.apply_circuit(gates)
+                for it in range(3):
+                    if it:
+                        st.rewind()
+                    st.reset_metrics()
+                    val, grad = st.adjoint_grad(W.sum_z(n))
+                    m = st.metrics()
+                    assert abs(val - rval) < 1e-4 and np.max(np.abs(grad - rgrad)) < 1e-4, (graph, seed, it)
+                    out.append((m["fwd_sweeps"], m["bwd_sweeps"], m["kernel_launches"], m["hbm_bytes"]))
+            ez = None
+            st.reset()
+            st.apply_circuit(W.hea(n, 5, seed=0, small=True))
+            for it in range(2):
+                if it:
+                    st.rewind()
+                ez = st.expval(W.sum_z(n))
+            ref = orc.expval(orc.run(n, W.hea(n, 5, seed=0, small=True)), n, W.sum_z(n))
+            assert np.max(np.abs(ez - ref)) < 1e-4
+        finally:
+            st.free()
+        res[graph] = out
+    assert res[0] == res[1]

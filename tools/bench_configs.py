@@ -39,14 +39,19 @@ def peak_gbs():
         return 6650.0
 
 
+GRAPH = 0
+
+
 def run_case(ctx, name, wl, steps, warmup, tile=0, note=""):
     stream = torch.cuda.current_stream()
     n, gates, terms = wl.n, wl.gates, wl.terms
     st = tqd.State(ctx, n, wl.dtype)
     if tile:
         st.set_option(tqd.OPT_TILE_QUBITS, tile)
+    if GRAPH:
+        st.set_option(tqd.OPT_USE_GRAPH, 1)
     out = {"case": name, "workload": wl.name, "n_qubits": n, "dtype": wl.dtype, "gates": len(gates),
-           "tile_k": tile or "default", "note": note}
+           "tile_k": tile or "default", "cuda_graph": GRAPH, "note": note}
     try:
         st.apply_circuit(gates)
 
@@ -116,7 +121,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--ksweep", default="", help="tile sizes k for a 30q cfg3 sweep, e.g. 9,10,11,12")
     ap.add_argument("--ksweep-qubits", type=int, default=30)
+    ap.add_argument("--graph", action="store_true", help="TQD_OPT_USE_GRAPH = 1 (cached plans as CUDA graphs)")
     args = ap.parse_args()
+    global GRAPH
+    GRAPH = 1 if args.graph else 0
     torch.cuda.set_device(0)
     ctx = tqd.Context.from_torch()
     cases = [c for c in args.cases.split(",") if c]
