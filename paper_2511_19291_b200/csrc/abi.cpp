@@ -1771,6 +1771,21 @@ int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, cons
     std::string err;
     int rc = plan_circuit(gates, pending, pos, cfg, stages, err);
     if (rc) return fail(rc, err);
+    if (getenv("TQD_DEBUG_KOPS")) {  // diagnostic: kernel-op counts per sweep stage (forward encoding)
+        for (size_t si = 0; si < stages.size(); si++) {
+            if (stages[si].type != ST_SWEEP) continue;
+            DevStage ds;
+            std::vector<KOp<float>> kops;
+            std::vector<int32_t> slots;
+            encode_sweep_k<float>(stages[si].sw, gates, false, n - g, ds, kops, slots);
+            int cnt[KC_COUNT + 1] = {0};
+            for (const auto &k : kops) cnt[std::min<int>(k.code, KC_COUNT)]++;
+            fprintf(stderr, "stage %zu: %d kops:", si, (int)kops.size());
+            for (int c = 0; c <= KC_COUNT; c++)
+                if (cnt[c]) fprintf(stderr, " %d:%d", c, cnt[c]);
+            fprintf(stderr, "  (C rows %d, U values %d)\n", ds.n_cvals, ds.n_uvals);
+        }
+    }
     std::string js = plan_to_json(stages, cfg);
     if (needed) *needed = js.size() + 1;
     if (!json_out || cap < js.size() + 1) return fail(TQD_ERR_ARG, "json buffer too small");
