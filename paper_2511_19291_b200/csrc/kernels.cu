@@ -213,20 +213,26 @@ __global__ void __launch_bounds__(256) lambda_init_kernel(const typename CT<Real
         const uint64_t base = ch << 12;
         const uint64_t pb = T ? pmask(base | rank_hi) : 0;
         const Real linb = lin(base | rank_hi);
-        double cacc = 0;
-#pragma unroll 4
+        // all 16 loads first (memory-level parallelism), then h and the stores
+        C xs[LI_U];
+#pragma unroll
         for (int u = 0; u < LI_U; u++) {
             const uint64_t i = base + ((uint64_t)u << 8) + threadIdx.x;
-            if (i >= n) break;
-            const uint64_t S = pj ^ pu[u] ^ pb;
-            Real s = linj + linu[u] + linb;
-            for (int j = 0; j < ntb; j++) s += tabt[j][(S >> (8 * j)) & 255];
-            const Real h = K - 2 * s;
-            const C x = psi[i];
-            lam[i] = mk<C>(h * x.x, h * x.y);
-            cacc += (double)(h * (x.x * x.x + x.y * x.y));
+            xs[u] = i < n ? psi[i] : mk<C>(0, 0);
         }
-        acc += cacc;
+        Real cacc = 0;
+#pragma unroll
+        for (int u = 0; u < LI_U; u++) {
+            const uint64_t i = base + ((uint64_t)u << 8) + threadIdx.x;
+            const uint64_t S = pj ^ pu[u] ^ pb;
+            Real sv = linj + linu[u] + linb;
+            for (int j = 0; j < ntb; j++) sv += tabt[j][(S >> (8 * j)) & 255];
+            const Real h = K - 2 * sv;
+            const C x = xs[u];
+            if (i < n) lam[i] = mk<C>(h * x.x, h * x.y);
+            cacc += h * (x.x * x.x + x.y * x.y);
+        }
+        acc += (double)cacc;
     }
     double tot = block_sum<double>(acc, red);
     if (threadIdx.x == 0) atomicAdd(eout, tot);
