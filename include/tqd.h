@@ -87,7 +87,9 @@ enum {
 /* Options (tqd_state_set_option).  Defaults are tuned for B200. */
 typedef enum {
     TQD_OPT_TILE_QUBITS = 0,  /* k: amplitudes per fused-sweep tile = 2^k (9..12; default 12) */
-    TQD_OPT_SMALL_MAX = 1,    /* n_loc <= this runs the single-CTA whole-state kernel (default 10) */
+    TQD_OPT_SMALL_MAX = 1,    /* n_loc <= this runs the single-CTA whole-state kernel (default 8:
+                               * from 9 local qubits a one-tile fused sweep is faster, e.g.
+                               * cfg1 10q c128 fwd+grad 0.29 -> 0.17 ms) */
     TQD_OPT_PROFILE = 2,      /* 1: time every kernel with CUDA events (see tqd_metrics) */
     TQD_OPT_GRID_CTAS = 3,    /* persistent CTAs per launch (0 = auto: SMs x resident CTAs) */
     TQD_OPT_USE_GRAPH = 4,    /* 1: replays of a cached plan (tqd_state_rewind, or a re-recorded

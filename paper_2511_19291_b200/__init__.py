@@ -309,7 +309,7 @@ def _gate_arrays(gates):
     return kinds, wires, params, mats, tr
 
 
-def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 10, c128: bool = False) -> dict:
+def tqd_debug_plan(n: int, gates, world: int = 1, k: int = 12, small_max: int = 8, c128: bool = False) -> dict:
     """Planner diagnostic (host only, no GPU): stages of `gates` as a dict."""
     import json
     G = len(gates)

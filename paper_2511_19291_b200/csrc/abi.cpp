@@ -88,7 +88,7 @@ struct tqd_state {
     std::vector<int> pos;
     bool consumed = false;
     // options
-    int opt_k = 12, opt_small = 10, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1, opt_absorb = 1;
+    int opt_k = 12, opt_small = 8, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1, opt_absorb = 1;
     // fused sweep -> remap (peer memory): every rank's psi / recv and lambda / send
     // allocations, shared once; the current roles are looked up by pointer identity
     std::vector<void *> peer_psi, peer_lam;  // [rank * 2 + i], i = 0: first psi / lam, 1: recv / send

@@ -8,7 +8,7 @@ after W warm-up replays; per-kernel averages from the library's PROFILE mode
 (a separate pass, so the step times above are not perturbed by per-launch
 events).  One JSON line per case on stdout.
 
-  cfg1   10q HEA d4 complex128, <Z0> + 80 gradients (latency: single-CTA kernel)
+  cfg1   10q HEA d4 complex128, <Z0> + 80 gradients (latency: one-tile sweeps, a single CTA)
   cfg2   24q HEA d20 complex64, sum Z_i
   cfg3   30q HEA d20 complex64 (= bench.py), plus a tile-size sweep (--ksweep)
   cfg4   33q HEA d10 complex64 at P = 1 (128 GiB psi + lambda on one GPU)
@@ -132,7 +132,7 @@ def main():
         for c in cases:
             if c == "cfg1":
                 run_case(ctx, c, W.config(1), max(args.steps, 20), max(args.warmup, 5),
-                         note="whole state in one CTA's shared memory: latency-bound")
+                         note="10 local qubits: one-tile fused sweeps (a single CTA), latency-bound")
             elif c == "cfg2":
                 run_case(ctx, c, W.config(2), max(args.steps, 5), args.warmup,
                          note="128 MiB psi + 128 MiB lambda: partly L2-resident (126 MB L2)")
