@@ -158,6 +158,19 @@ def cpu_baseline_line(depth, seed):
             "seconds": dt}
 
 
+def ref_config(args, world, n_sample):
+    """The ours-arm workload this arm samples (same workload string and width), plus the sample."""
+    import workloads as W
+    g = int(round(math.log2(world)))
+    n = args.qubits or (BASE_QUBITS + g)
+    G = len(W.hea(n, args.depth, args.seed))
+    return {"workload": f"cfg3-family HEA ring depth {args.depth}, {n} qubits complex64, "
+                        f"fwd + adjoint grad of sum Z_i ({G} gates)",
+            "n_qubits": n, "depth": args.depth, "gates": G, "seed": args.seed,
+            "sample": f"each step: the same ansatz at n={n_sample} qubits on the float64 oracle; "
+                      f"throughput in the same unit (gate-amplitude updates per second)"}
+
+
 def run_reference(args, world, rank):
     """--impl reference: the oracle on this box's host cores (rank 0 only)."""
     if rank != 0:
@@ -180,8 +193,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"hea{n}_d{args.depth} oracle sample of cfg3 (fwd+grad, sum Z_i)",
-                       "n_qubits": n, "depth": args.depth},
+            "config": ref_config(args, world, n),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
