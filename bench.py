@@ -175,6 +175,9 @@ def run_reference(args, world, rank):
     """--impl reference: the oracle on this box's host cores (rank 0 only)."""
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 is the only worker here, so the
+    # oracle gets the host's cores as at N=1 (libgomp reads this when liboracle.so loads).
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     import oracle
     oracle.build()
     n = REF_SAMPLE_QUBITS
