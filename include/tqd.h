@@ -209,6 +209,17 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t value);
 int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires,
                    const double *params, const double *matrix, int trainable);
 
+/* Record G gates at once, in order, exactly as G tqd_apply_gate calls would
+ * (same validation, same gradient slots), from host parallel arrays (caller
+ * owned, read during the call only): kinds[G] (tqd_gate), wires[2G] (second
+ * entry ignored for 1-qubit kinds), params[3G] (first gate_num_params used),
+ * mats[32G] (MAT1 2x2 / MAT2 4x4 row-major re,im; ignored for other kinds),
+ * trainable[G].  One call per circuit instead of one per gate (the circuit
+ * building of Listing 1, recorded lazily).  All-or-nothing: on error no
+ * gate is recorded.  G = 0 is a no-op.  Errors: as tqd_apply_gate. */
+int tqd_apply_circuit(tqd_state *st, int G, const int *kinds, const int *wires, const double *params,
+                      const double *mats, const int *trainable);
+
 /* Record a parameterised 1-qubit gate (RX, RY, RZ or U3) with PER-STATE
  * parameters: params[b * np + i] for batch element b (np = 1, or 3 for U3), e.g.
  * the encoder rotation carrying each state's input.  trainable != 0 gives the

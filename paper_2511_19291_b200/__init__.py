@@ -80,6 +80,7 @@ _SIG = {
     "tqd_state_free": [_P],
     "tqd_state_set_option": [_P, ctypes.c_int, ctypes.c_int64],
     "tqd_apply_gate": [_P, ctypes.c_int, _P, ctypes.c_int, _P, _P, ctypes.c_int],
+    "tqd_apply_circuit": [_P, ctypes.c_int, _P, _P, _P, _P, _P],
     "tqd_num_params": [_P, ctypes.POINTER(ctypes.c_int)],
     "tqd_expval": [_P, ctypes.c_int, _P, _P, _P, _P],
     "tqd_adjoint_grad": [_P, ctypes.c_int, _P, _P, _P, ctypes.POINTER(ctypes.c_double), _P, ctypes.c_int],
@@ -200,6 +201,14 @@ def tqd_apply_gate(st, gate, wires, params=(), matrix=None, trainable=True):
     _call("tqd_apply_gate", st, g, _ptr(w), int(w.size), _ptr(p), _ptr(m), 1 if trainable else 0)
 
 
+def tqd_apply_circuit(st, gates):
+    """Record a whole gate list with one C call (same result as tqd_apply_gate per gate)."""
+    if not len(gates):
+        return
+    kinds, wires, params, mats, tr = _gate_arrays(gates)
+    _call("tqd_apply_circuit", st, len(gates), _ptr(kinds), _ptr(wires), _ptr(params), _ptr(mats), _ptr(tr))
+
+
 def tqd_state_init_batch(ctx, n: int, dtype: int, batch: int):
     out = _P()
     _call("tqd_state_init_batch", ctx, n, dtype, batch, ctypes.byref(out))
@@ -290,22 +299,40 @@ def tqd_last_error() -> str:
     return lib().tqd_last_error().decode()
 
 
+_ARITY = np.array([2 if k in ("CNOT", "CZ", "SWAP", "MAT2") else 1
+                   for k in sorted(GATES, key=GATES.get)], np.int32)
+_NPARAMS = np.array([{"RX": 1, "RY": 1, "RZ": 1, "U3": 3}.get(k, 0)
+                     for k in sorted(GATES, key=GATES.get)], np.int32)
+
+
 def _gate_arrays(gates):
     G = len(gates)
-    kinds = np.zeros(max(G, 1), np.int32)
-    wires = np.zeros(2 * max(G, 1), np.int32)
-    params = np.zeros(3 * max(G, 1), np.float64)
-    mats = np.zeros(32 * max(G, 1), np.float64)
-    tr = np.zeros(max(G, 1), np.int32)
+    m = max(G, 1)
+    kinds = np.zeros(m, np.int32)
+    wires = np.zeros((m, 2), np.int32)
+    params = np.zeros((m, 3), np.float64)
+    mats = np.zeros(32 * m, np.float64)
+    tr = np.zeros(m, np.int32)
+    if G:
+        kinds[:G] = [GATES[g.name] for g in gates]
+        wires[:G] = [(tuple(g.wires) + (0, 0))[:2] for g in gates]
+        params[:G] = [(tuple(g.params) + (0.0, 0.0, 0.0))[:3] for g in gates]
+        tr[:G] = [1 if g.trainable else 0 for g in gates]
+    wires, params = wires.reshape(-1), params.reshape(-1)
+    if G:  # the packed arrays carry no counts: check them as tqd_apply_gate does (errors, not padding)
+        nw = np.fromiter((len(g.wires) for g in gates), np.int32, G)
+        npar = np.fromiter((len(g.params) for g in gates), np.int32, G)
+        kk = np.clip(kinds[:G], 0, len(_ARITY) - 1)
+        bad = np.flatnonzero((nw != _ARITY[kk]) | (npar < _NPARAMS[kk]) | (npar > 3))
+        if bad.size:
+            i = int(bad[0])
+            raise TqdError(-1, f"gate {i} ({gates[i].name}): {len(gates[i].wires)} wires / "
+                               f"{len(gates[i].params)} params do not fit the gate")
     for i, g in enumerate(gates):
-        kinds[i] = GATES[g.name]
-        wires[2 * i:2 * i + len(g.wires)] = g.wires
-        params[3 * i:3 * i + len(g.params)] = g.params
         if g.matrix is not None:
             mm = np.asarray(g.matrix, np.complex128).reshape(-1)
             mats[32 * i:32 * i + 2 * mm.size:2] = mm.real
             mats[32 * i + 1:32 * i + 2 * mm.size:2] = mm.imag
-        tr[i] = 1 if g.trainable else 0
     return kinds, wires, params, mats, tr
 
 
@@ -408,8 +435,7 @@ class State:
         tqd_apply_gate(self.handle, name, wires, params, matrix, trainable)
 
     def apply_circuit(self, gates):
-        for g in gates:
-            tqd_apply_gate(self.handle, g.name, g.wires, g.params, g.matrix, g.trainable)
+        tqd_apply_circuit(self.handle, gates)
 
     @property
     def n_params(self) -> int:

@@ -1031,6 +1031,35 @@ int tqd_apply_gate(tqd_state *st, tqd_gate g, const int *wires, int n_wires, con
     return TQD_OK;
 }
 
+int tqd_apply_circuit(tqd_state *st, int G, const int *kinds, const int *wires, const double *params,
+                      const double *mats, const int *trainable) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");
+    if (G < 0) return fail(TQD_ERR_ARG, "G < 0");
+    if (G == 0) return TQD_OK;
+    if (!kinds || !wires || !params || !mats || !trainable) return fail(TQD_ERR_ARG, "NULL argument");
+    std::vector<GateRec> recs;
+    recs.reserve(G);
+    int np_ = st->n_params;
+    for (int i = 0; i < G; i++) {
+        const int nw = gate_arity(kinds[i]);
+        if (nw < 1 || nw > 2) return fail(TQD_ERR_ARG, "unknown gate kind");
+        for (int j = 0; j < nw; j++)
+            if (wires[2 * i + j] < 0 || wires[2 * i + j] >= st->n) return fail(TQD_ERR_ARG, "wire out of range");
+        if (nw == 2 && wires[2 * i] == wires[2 * i + 1]) return fail(TQD_ERR_ARG, "duplicate wires");
+        GateRec rec;
+        std::string err;
+        int rc = make_gate(kinds[i], wires + 2 * i, nw, params + 3 * i, mats + 32 * i, trainable[i], st->dbl, rec, err);
+        if (rc) return fail(rc, err);
+        if (rec.trainable) { rec.slot0 = np_; np_ += gate_num_params(kinds[i]); }
+        recs.push_back(rec);
+    }
+    st->gates.insert(st->gates.end(), recs.begin(), recs.end());
+    st->n_params = np_;
+    st->tape_version++;
+    return TQD_OK;
+}
+
 int tqd_apply_gate_batch(tqd_state *st, tqd_gate g, const int *wires, int n_wires, const double *params, int trainable) {
     if (!st) return fail(TQD_ERR_ARG, "state is NULL");
     if (st->consumed) return fail(TQD_ERR_STATE, "state consumed by tqd_adjoint_grad; call tqd_state_reset");

@@ -65,3 +65,16 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.h" not in txt, f
+
+
+def test_gate_arrays_checks_counts():
+    """The packed gate arrays of tqd_apply_circuit carry no per-gate counts: wrong wire or
+    parameter counts are rejected in the binding (as tqd_apply_gate rejects them), never padded."""
+    import paper_2511_19291_b200 as tqd
+    k, w, p, m, tr = tqd._gate_arrays([W.Gate("RY", (3,), (0.5,)), W.Gate("CNOT", (1, 2))])
+    assert list(k) == [tqd.GATES["RY"], tqd.GATES["CNOT"]] and list(w) == [3, 0, 1, 2]
+    assert list(p) == [0.5, 0, 0, 0, 0, 0] and list(tr) == [1, 1] and m.size == 64
+    for bad in (W.Gate("CNOT", (1,)), W.Gate("RY", (1,), ()), W.Gate("U3", (0,), (0.1, 0.2)),
+                W.Gate("X", (0, 1))):
+        with pytest.raises(tqd.TqdError):
+            tqd._gate_arrays([W.Gate("H", (0,)), bad])

@@ -527,3 +527,51 @@ def test_cuda_graph_replay(tqd, ctx, orc):
             st.free()
         res[graph] = out
     assert res[0] == res[1]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_apply_circuit_matches_per_gate(tqd, ctx, orc, dtype):
+    """tqd_apply_circuit (one C call) records exactly what G tqd_apply_gate calls record:
+    bit-identical amplitudes (same tape, same kernels), value and gradients equal up to the order
+    of their fp64 atomic sums, and all-or-nothing errors."""
+    n = 13
+    gates = W.random_circuit(n, 160, seed=7)
+    out = []
+    for mode in ("circuit", "per_gate"):
+        st = make_state(tqd, ctx, n, dtype, k=10, small_max=0)
+        if mode == "circuit":
+            st.apply_circuit(gates)
+        else:
+            for g in gates:
+                st.apply(g.name, g.wires, g.params, g.matrix, g.trainable)
+        npar = st.n_params
+        amps = st.amplitudes()
+        st.reset()
+        if mode == "circuit":
+            st.apply_circuit(gates)
+        else:
+            for g in gates:
+                st.apply(g.name, g.wires, g.params, g.matrix, g.trainable)
+        val, grad = st.adjoint_grad(W.sum_z(n))
+        st.free()
+        out.append((npar, amps, val, np.asarray(grad)))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    # value / gradients are fp64 sums with atomic (order-free) accumulation across CTAs:
+    # equal up to that summation order, not bitwise
+    assert abs(out[0][2] - out[1][2]) < 1e-12
+    assert np.max(np.abs(out[0][3] - out[1][3])) < 1e-12
+    ref = orc.run(n, gates)
+    assert np.max(np.abs(out[0][1] - ref)) < TOL[dtype]["amp"]
+    # a bad gate anywhere in the list records nothing
+    st = make_state(tqd, ctx, n, dtype)
+    st.apply_circuit(gates[:5])
+    before = st.n_params
+    with pytest.raises(tqd.TqdError) as e:
+        st.apply_circuit(gates[:5] + [W.Gate("CNOT", (2, 2))])
+    assert e.value.code == -1 and st.n_params == before
+    with pytest.raises(tqd.TqdError):
+        st.apply_circuit([W.Gate("RY", (n,), (0.1,))])
+    assert st.n_params == before
+    st.apply_circuit([])
+    st.free()
