@@ -11,8 +11,12 @@ host.  At N GPUs the state has 30 + log2(N) qubits sharded over the ranks
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1)
 
+  --config 2|3|4 selects BASELINE.json configs[1..3] (24q d20 / 30q d20 / 33q d10);
+  the default (3) is the headline.
+
 value    = gate-amplitude updates per second of the whole job:
-           (gates x 2^n) / (fwd+grad step time), device-timed with CUDA events
+           (gates applied per step x 2^n) / (fwd+grad step time) -- the trailing
+           gates absorbed into the Z observable are not counted -- device-timed with CUDA events
            on the library's stream, max over ranks, circuit + plan resident
            (tqd_state_rewind re-executes the recorded tape).
 e2e      = the same metric through the public C ABI per step, as in a training
@@ -21,6 +25,8 @@ e2e      = the same metric through the public C ABI per step, as in a training
            rebuilds the op coefficients and uploads them host->device, runs,
            copies value + gradients device->host); wall clock between
            synchronised barriers.
+forward  = the same for a forward-only pass (|0..0> -> sweeps -> <Z_i>), with the
+           forward sweep's roofline fraction.
 roofline = the dominant kernel (the fused adjoint sweep) from live CUDA-event
            timings of every launch: algorithmic bytes (4 x 8 B x 2^n_loc per
            launch: read + write psi and lambda; 2 x 8 B for the last reverse
@@ -56,8 +62,11 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--qubits", type=int, default=0, help="override n (default 30 + log2 N)")
-    p.add_argument("--depth", type=int, default=DEPTH)
+    p.add_argument("--config", type=int, choices=[2, 3, 4], default=3,
+                   help="BASELINE.json configs[i-1]: 2 = 24q depth 20, 3 = 30q depth 20 (default, the "
+                        "headline), 4 = 33q depth 10 (fixed width: strong scaling over N)")
+    p.add_argument("--qubits", type=int, default=0, help="override n (default per --config)")
+    p.add_argument("--depth", type=int, default=0, help="override the depth (default per --config)")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -66,6 +75,21 @@ def parse():
                    help="apply every gate (TQD_OPT_ABSORB_TAIL = 0) instead of absorbing the trailing "
                         "diagonal / permutation gates into the Z observable")
     return p.parse_args()
+
+
+CONFIGS = {  # BASELINE.json configs: (base qubits, depth, weak scaling: + log2 N qubits)
+    2: (24, 20, True),
+    3: (30, 20, True),
+    4: (33, 10, False),
+}
+
+
+def resolve(args, world):
+    """(n, depth, scaling) of the run: the --config family, weak scaling adds log2 N qubits."""
+    g = int(round(math.log2(world)))
+    base, depth, weak = CONFIGS[args.config]
+    n = args.qubits or (base + g if weak else base)
+    return n, args.depth or depth, "weak" if (weak or args.qubits) else "strong"
 
 
 def measured_peaks():
@@ -161,12 +185,11 @@ def cpu_baseline_line(depth, seed):
 def ref_config(args, world, n_sample):
     """The ours-arm workload this arm samples (same workload string and width), plus the sample."""
     import workloads as W
-    g = int(round(math.log2(world)))
-    n = args.qubits or (BASE_QUBITS + g)
-    G = len(W.hea(n, args.depth, args.seed))
-    return {"workload": f"cfg3-family HEA ring depth {args.depth}, {n} qubits complex64, "
+    n, depth, _ = resolve(args, world)
+    G = len(W.hea(n, depth, args.seed))
+    return {"workload": f"cfg{args.config}-family HEA ring depth {depth}, {n} qubits complex64, "
                         f"fwd + adjoint grad of sum Z_i ({G} gates)",
-            "n_qubits": n, "depth": args.depth, "gates": G, "seed": args.seed,
+            "n_qubits": n, "depth": depth, "gates": G, "seed": args.seed,
             "sample": f"each step: the same ansatz at n={n_sample} qubits on the float64 oracle; "
                       f"throughput in the same unit (gate-amplitude updates per second)"}
 
@@ -181,21 +204,22 @@ def run_reference(args, world, rank):
     import oracle
     oracle.build()
     n = REF_SAMPLE_QUBITS
+    _, depth, scaling = resolve(args, world)
     for _ in range(args.warmup):
-        oracle_fwd_grad_sample(n, args.depth, args.seed)
+        oracle_fwd_grad_sample(n, depth, args.seed)
     times = []
     G = 0
     for _ in range(args.steps):
-        G, dt = oracle_fwd_grad_sample(n, args.depth, args.seed)
+        G, dt = oracle_fwd_grad_sample(n, depth, args.seed)
         times.append(dt)
     t = sum(times) / len(times)
     value = G * (1 << n) / t / 1e9
     cores = oracle.num_threads()
     sample = (f"float64 C oracle (OpenMP, {cores} threads), each step = full fwd+adjoint-grad of the "
-              f"ansatz (HEA ring depth {args.depth}, sum Z_i) at n={n} qubits, {G} gates")
+              f"ansatz (HEA ring depth {depth}, sum Z_i) at n={n} qubits, {G} gates")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": ref_config(args, world, n),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -221,11 +245,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     g = int(round(math.log2(world)))
     assert 1 << g == world, "world size must be a power of two"
-    n = args.qubits or (BASE_QUBITS + g)
+    n, depth, scaling = resolve(args, world)
+    args.depth = depth
     gates = W.hea(n, args.depth, args.seed)
     terms = W.sum_z(n)
     G = len(gates)
-    units = G * (1 << n)
 
     ctx = tqd.Context.from_torch()
     st = tqd.State(ctx, n, "c64")
@@ -271,7 +295,35 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # the unit counts the gates the step APPLIES (forward), not the recorded ones: the
+    # trailing gates absorbed into the Z observable are never applied nor un-applied
+    g_applied = m["gates_applied"] // args.steps
+    g_unapplied = m["gates_unapplied"] // args.steps
+    g_absorbed = m["gates_absorbed"] // args.steps
+    units = g_applied * (1 << n)
     value = units / (ms / 1e3) / 1e9
+
+    # forward only (|0..0> -> all fused forward sweeps -> <Z_i>): same unit, device-timed
+    st.rewind()
+    st.expval(terms)
+    st.reset_metrics()
+    barrier()
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        st.rewind()
+        st.expval(terms)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    fms = f0.elapsed_time(f1) / args.steps
+    mf = st.metrics()
+    if world > 1:
+        t = torch.tensor([fms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        fms = float(t.item())
+    f_applied = mf["gates_applied"] // args.steps
 
     # roofline of the dominant kernel (live CUDA-event timings of every launch)
     peak, peak_src = measured_peaks()
@@ -299,6 +351,13 @@ def main():
                 "bytes_per_gate_per_amp_fwd": round(m["fwd_sweep_bytes"] / (m["gates_applied"] * (1 << (n - g))), 3)
                 if m["gates_applied"] else None}
     kernel_ms = m["fwd_sweep_ms"] + m["bwd_sweep_ms"] + m["other_ms"] + m["a2a_ms"]
+    f_avg = mf["fwd_sweep_ms"] / max(mf["fwd_sweeps"], 1)
+    forward = {"ms_per_step": round(fms, 3), "value": round(f_applied * (1 << n) / (fms / 1e3) / 1e9, 3),
+               "unit": "Gamp-gates/s (forward)", "gates_applied_per_step": f_applied,
+               "sweeps_per_step": mf["fwd_sweeps"] // args.steps,
+               "forward_sweep": {"achieved": round(2 * shard / (f_avg / 1e3) / 1e9, 1) if f_avg > 0 else None,
+                                 "frac": round(2 * shard / (f_avg / 1e3) / 1e9 / peak, 4) if f_avg > 0 else None,
+                                 "avg_launch_ms": round(f_avg, 4)}}
 
     # end to end through the public ABI with host buffers
     e2e = None
@@ -336,21 +395,24 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"cfg3-family HEA ring depth {args.depth}, {n} qubits complex64, "
+                "config": {"workload": f"cfg{args.config}-family HEA ring depth {args.depth}, {n} qubits complex64, "
                                        f"fwd + adjoint grad of sum Z_i ({G} gates, {len(grad)} params)",
                            "n_qubits": n, "depth": args.depth, "gates": G, "params": len(grad),
+                           "gates_applied_per_step": g_applied, "gates_unapplied_per_step": g_unapplied,
+                           "unit_counts": "gates applied per step (recorded minus absorbed) x 2^n",
                            "state_dtype": "complex64 (fp32 arithmetic, fp64 reductions)",
                            "parallelism": f"state sharded over {world} rank(s) by {g} global qubit(s)",
                            "l2": f"inputs larger than L2: {shard * 2 / 2**30:.0f} GiB psi+lambda per GPU",
-                           "gates_absorbed_per_step": m["gates_absorbed"] // args.steps,
+                           "gates_absorbed_per_step": g_absorbed,
                            "absorption": "trailing diagonal/permutation gates folded into the Z observable "
                                          "(Heisenberg picture; same value and gradients)" if not args.no_absorb
                                          else "off: every gate applied",
                            "seed": args.seed},
                 "gpu_launches": int(m["kernel_launches"]),
                 "roofline": roofline,
+                "forward": forward,
                 "cpu_baseline": cpu,
                 "e2e": e2e,
                 "clocks": clocks,

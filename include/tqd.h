@@ -96,10 +96,14 @@ typedef enum {
                                * tape of the same structure) launch the forward and reverse
                                * sweep sequences as CUDA graphs (one rank, PROFILE off;
                                * default 0)                                               */
-    TQD_OPT_FUSED_REMAP = 5,  /* 1: a remap right after a sweep is fused into it: the sweep
-                               * stores straight into the owners' peer memory (default 1);
-                               * 0: pack -> all-to-all -> unpack                          */
-    TQD_OPT_ABSORB_TAIL = 6   /* 1 (default): tqd_adjoint_grad and tqd_expval with Z-string
+    TQD_OPT_FUSED_REMAP = 5,  /* 1: a FORWARD remap right after a sweep is fused into it: the
+                               * sweep stores straight into the owners' lambda buffers over
+                               * peer memory (idle until the adjoint seed; allocated on
+                               * first use: the with_adjoint budget of tqd_state_bytes) and
+                               * the buffers swap roles (default 1); 0: every remap runs
+                               * pack -> all-to-all -> unpack through the bounded staging
+                               * (always the case for adjoint remaps: psi and lambda live) */
+    TQD_OPT_ABSORB_TAIL = 6,  /* 1 (default): tqd_adjoint_grad and tqd_expval with Z-string
                                * terms absorb the circuit's trailing diagonal / permutation
                                * gates (RZ, CZ, CP, X, Y, CNOT, SWAP ...) into the observable by
                                * conjugation (Heisenberg picture, E = <psi|U^dag H U|psi>)
@@ -108,6 +112,10 @@ typedef enum {
                                * After tqd_expval the absorbed gates stay pending: a later
                                * readback / sample / non-Z observable applies them.
                                * 0: apply every gate.                                      */
+    TQD_OPT_STAGING_BYTES = 7  /* world > 1: bytes of the exchange staging (send + receive
+                               * halves; remap blocks and X/Y partner shards move through it
+                               * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
+                               * force a few KiB so the chunk loop iterates.               */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.
@@ -165,7 +173,11 @@ int tqd_ctx_destroy(tqd_ctx *ctx);
 
 /* Device bytes per rank for an n-qubit state of dtype dt on `world` ranks:
  * the shard psi (2^{n - log2 world} amplitudes), plus lambda for the adjoint
- * when with_adjoint != 0, plus the remap staging when world > 1. */
+ * when with_adjoint != 0, plus the bounded exchange staging when world > 1
+ * (min(1 GiB, 2 shards); e.g. 36 qubits complex64 on 8 GPUs with the adjoint:
+ * 2 x 64 GiB + 1 GiB).  Scratch of a few MiB (descriptors, reductions) is extra.
+ * The with_adjoint = 0 figure holds for forward-only work with
+ * TQD_OPT_FUSED_REMAP = 0 (fused forward remaps store into the lambda buffer). */
 int tqd_state_bytes(int n_qubits, tqd_dtype dt, int world, int with_adjoint, size_t *bytes_per_rank);
 
 /* Allocate and initialise |0...0> (reset_states):
@@ -228,6 +240,12 @@ int tqd_apply_circuit(tqd_state *st, int G, const int *kinds, const int *wires, 
  * kind, n_wires != 1, NULL params. */
 int tqd_apply_gate_batch(tqd_state *st, tqd_gate g, const int *wires, int n_wires, const double *params,
                          int trainable);
+
+/* Shape of a state: qubits, batch size (1 for tqd_state_init) and dtype
+ * (tqd_dtype); NULL outputs are skipped.  Bindings size the caller-owned arrays
+ * of tqd_expval / tqd_adjoint_grad / tqd_apply_gate_batch from it (the ABI takes
+ * no array lengths). */
+int tqd_state_info(const tqd_state *st, int *n_qubits, int *batch, int *dtype);
 
 /* Number of gradient slots recorded so far. */
 int tqd_num_params(const tqd_state *st, int *out);

@@ -28,8 +28,9 @@ GATES = {
     "RX": 14, "RY": 15, "RZ": 16, "U3": 17,
 }
 C64, C128 = 0, 1
-OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP, OPT_ABSORB_TAIL = \
-    0, 1, 2, 3, 4, 5, 6
+OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP, OPT_ABSORB_TAIL, \
+    OPT_STAGING_BYTES = \
+    0, 1, 2, 3, 4, 5, 6, 7
 ERRORS = {0: "TQD_OK", -1: "TQD_ERR_ARG", -2: "TQD_ERR_QUBITS", -3: "TQD_ERR_WORLD",
           -4: "TQD_ERR_NOT_UNITARY", -5: "TQD_ERR_OOM", -6: "TQD_ERR_CUDA", -7: "TQD_ERR_NCCL",
           -8: "TQD_ERR_UNSUPPORTED", -9: "TQD_ERR_STATE"}
@@ -82,6 +83,7 @@ _SIG = {
     "tqd_apply_gate": [_P, ctypes.c_int, _P, ctypes.c_int, _P, _P, ctypes.c_int],
     "tqd_apply_circuit": [_P, ctypes.c_int, _P, _P, _P, _P, _P],
     "tqd_num_params": [_P, ctypes.POINTER(ctypes.c_int)],
+    "tqd_state_info": [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
     "tqd_expval": [_P, ctypes.c_int, _P, _P, _P, _P],
     "tqd_adjoint_grad": [_P, ctypes.c_int, _P, _P, _P, ctypes.POINTER(ctypes.c_double), _P, ctypes.c_int],
     "tqd_get_amplitudes": [_P, ctypes.c_uint64, ctypes.c_uint64, _P],
@@ -189,13 +191,30 @@ def tqd_state_set_option(st, opt: int, value: int):
     _call("tqd_state_set_option", st, opt, int(value))
 
 
-def tqd_apply_gate(st, gate, wires, params=(), matrix=None, trainable=True):
+def _gate_code(gate) -> int:
     g = GATES[gate] if isinstance(gate, str) else int(gate)
+    if not 0 <= g < len(GATES):
+        raise TqdError(-1, f"unknown gate kind {gate!r}")
+    return g
+
+
+def tqd_apply_gate(st, gate, wires, params=(), matrix=None, trainable=True):
+    # the C call takes no array lengths: check what it will read (errors, not over-reads)
+    g = _gate_code(gate)
     w = _arr(wires, np.int32)
-    p = _arr(params, np.float64) if len(params) else None
+    if w.size != _ARITY[g]:
+        raise TqdError(-1, f"gate {gate}: {w.size} wires, needs {_ARITY[g]}")
+    pp = np.asarray(params, dtype=np.float64).reshape(-1)
+    if pp.size != _NPARAMS[g]:
+        raise TqdError(-1, f"gate {gate}: {pp.size} params, needs {_NPARAMS[g]}")
+    p = _arr(pp, np.float64) if pp.size else None
     m = None
-    if matrix is not None:
+    if g in (GATES["MAT1"], GATES["MAT2"]):
+        if matrix is None:
+            raise TqdError(-1, f"gate {gate}: matrix required")
         mm = np.asarray(matrix, dtype=np.complex128).reshape(-1)
+        if mm.size != (4 if g == GATES["MAT1"] else 16):
+            raise TqdError(-1, f"gate {gate}: matrix has {mm.size} entries")
         m = np.empty(2 * mm.size, dtype=np.float64)
         m[0::2], m[1::2] = mm.real, mm.imag
     _call("tqd_apply_gate", st, g, _ptr(w), int(w.size), _ptr(p), _ptr(m), 1 if trainable else 0)
@@ -215,11 +234,23 @@ def tqd_state_init_batch(ctx, n: int, dtype: int, batch: int):
     return out
 
 
+def tqd_state_info(st):
+    """(n_qubits, batch, dtype) of a state handle."""
+    n, b, d = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _call("tqd_state_info", st, ctypes.byref(n), ctypes.byref(b), ctypes.byref(d))
+    return n.value, b.value, d.value
+
+
 def tqd_apply_gate_batch(st, gate, wires, params, trainable=True):
     """params: (batch, n_params_of_gate) per-state parameters."""
-    g = GATES[gate] if isinstance(gate, str) else int(gate)
+    g = _gate_code(gate)
     w = _arr(wires, np.int32)
     p = _arr(np.asarray(params, dtype=np.float64).reshape(-1), np.float64)
+    batch = tqd_state_info(st)[1]
+    if w.size != 1:
+        raise TqdError(-1, "batched gates act on one wire")
+    if p.size != batch * max(int(_NPARAMS[g]), 1):
+        raise TqdError(-1, f"params: {p.size} values for batch {batch} x {_NPARAMS[g]} parameters")
     _call("tqd_apply_gate_batch", st, g, _ptr(w), int(w.size), _ptr(p), 1 if trainable else 0)
 
 
@@ -236,8 +267,12 @@ def _terms(terms):
     return len(terms), x, z, c
 
 
-def tqd_expval(st, terms, batch: int = 1) -> np.ndarray:
+def tqd_expval(st, terms, batch: int | None = None) -> np.ndarray:
     T, x, z, c = _terms(terms)
+    hb = tqd_state_info(st)[1]
+    if batch is not None and batch != hb:
+        raise TqdError(-1, f"batch {batch} != the state's batch {hb}")
+    batch = hb
     out = np.zeros(max(T * batch, 1), dtype=np.float64)
     _call("tqd_expval", st, T, _ptr(x), _ptr(z), _ptr(c), _ptr(out))
     return out[:T * batch] if batch == 1 else out[:T * batch].reshape(batch, T)
@@ -246,8 +281,13 @@ def tqd_expval(st, terms, batch: int = 1) -> np.ndarray:
 def tqd_adjoint_grad(st, terms, n_grad: int | None = None, coeff=None):
     """coeff: optional (batch, n_terms) VJP weights for a batch (default: the terms' own)."""
     T, x, z, c = _terms(terms)
+    batch = tqd_state_info(st)[1]
     if coeff is not None:
         c = _arr(np.asarray(coeff, dtype=np.float64).reshape(-1), np.float64)
+        if c.size != batch * T:
+            raise TqdError(-1, f"coeff: {c.size} values for batch {batch} x {T} terms")
+    elif batch > 1:
+        c = _arr(np.tile(c[:T], batch), np.float64)  # every element uses the terms' own coefficients
     if n_grad is None:
         n_grad = tqd_num_params(st)
     g = np.zeros(max(n_grad, 1), dtype=np.float64)
@@ -256,14 +296,16 @@ def tqd_adjoint_grad(st, terms, n_grad: int | None = None, coeff=None):
     return val.value, g[:n_grad]
 
 
-def tqd_sample(st, shots: int, seed: int, batch: int = 1) -> np.ndarray:
+def tqd_sample(st, shots: int, seed: int, batch: int | None = None) -> np.ndarray:
+    batch = tqd_state_info(st)[1]
     out = np.zeros(max(batch * shots, 1), dtype=np.uint64)
     _call("tqd_sample", st, int(shots), int(seed), _ptr(out))
     out = out[:batch * shots]
     return out if batch == 1 else out.reshape(batch, shots)
 
 
-def tqd_sample_gaussian_z(st, n: int, shots: float, seed: int, batch: int = 1) -> np.ndarray:
+def tqd_sample_gaussian_z(st, n: int | None, shots: float, seed: int, batch: int | None = None) -> np.ndarray:
+    n, batch, _ = tqd_state_info(st)
     out = np.zeros(batch * n, dtype=np.float64)
     _call("tqd_sample_gaussian_z", st, float(shots), int(seed), _ptr(out))
     return out if batch == 1 else out.reshape(batch, n)
@@ -272,14 +314,18 @@ def tqd_sample_gaussian_z(st, n: int, shots: float, seed: int, batch: int = 1) -
 def tqd_adjoint_grad_gaussian(st, shots: float, seed: int, coeff=None, n_grad: int | None = None):
     if n_grad is None:
         n_grad = tqd_num_params(st)
+    n, batch, _ = tqd_state_info(st)
     c = None if coeff is None else _arr(np.asarray(coeff, dtype=np.float64).reshape(-1), np.float64)
+    if c is not None and c.size != batch * n:
+        raise TqdError(-1, f"coeff: {c.size} values for batch {batch} x {n} qubits")
     g = np.zeros(max(n_grad, 1), dtype=np.float64)
     val = ctypes.c_double()
     _call("tqd_adjoint_grad_gaussian", st, float(shots), int(seed), _ptr(c), ctypes.byref(val), _ptr(g), n_grad)
     return val.value, g[:n_grad]
 
 
-def tqd_get_amplitudes(st, first: int, count: int, dtype: int) -> np.ndarray:
+def tqd_get_amplitudes(st, first: int, count: int, dtype: int | None = None) -> np.ndarray:
+    dtype = tqd_state_info(st)[2]
     out = np.zeros(count, dtype=np.complex128 if dtype == C128 else np.complex64)
     _call("tqd_get_amplitudes", st, first, count, _ptr(out))
     return out
@@ -450,8 +496,6 @@ class State:
 
     def adjoint_grad(self, terms, coeff=None):
         """coeff: (batch, n_terms) VJP weights; default: every element uses the terms' own."""
-        if coeff is None and self.batch > 1:
-            coeff = np.tile([t[2] if len(t) > 2 else 1.0 for t in terms], (self.batch, 1))
         return tqd_adjoint_grad(self.handle, terms, coeff=coeff)
 
     def amplitudes(self, first: int = 0, count: int | None = None) -> np.ndarray:

@@ -46,8 +46,9 @@ cudaError_t launch_lambda_gauss(bool dbl, const void *psi, void *lam, uint64_t n
                                 uint64_t seed, const ZTerms &t, double alpha, double fc, double k2, double kc,
                                 cudaStream_t s);
 cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
-cudaError_t launch_remap_pack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s);
-cudaError_t launch_remap_unpack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s);
+cudaError_t launch_remap_block(bool dbl, void *shard, void *stage, uint64_t e0, uint64_t cnt, uint64_t bdep, uint64_t rest,
+                              bool unpack, cudaStream_t s);
+cudaError_t launch_debug_delay(uint32_t us, cudaStream_t s);
 }  // namespace tqd
 
 using namespace tqd;
@@ -75,8 +76,11 @@ struct tqd_state {
     int n = 0, n_loc = 0, g = 0;
     bool dbl = false;
     size_t esz = 8;
-    void *psi = nullptr, *lam = nullptr, *sendb = nullptr, *recvb = nullptr;
-    bool own_psi = false, own_lam = false, own_xchg = false;
+    void *psi = nullptr, *lam = nullptr;
+    // bounded exchange staging (world > 1): [send half | receive half], stg_bytes in all
+    void *stg = nullptr;
+    size_t stg_bytes = 0;
+    bool own_psi = false, own_lam = false, own_stg = false;
     void *user_buf = nullptr;
     size_t user_bytes = 0;
     std::vector<GateRec> gates;
@@ -89,10 +93,13 @@ struct tqd_state {
     bool consumed = false;
     // options
     int opt_k = 12, opt_small = 8, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1, opt_absorb = 1;
-    // fused sweep -> remap (peer memory): every rank's psi / recv and lambda / send
-    // allocations, shared once; the current roles are looked up by pointer identity
-    std::vector<void *> peer_psi, peer_lam;  // [rank * 2 + i], i = 0: first psi / lam, 1: recv / send
-    void *psi_first = nullptr, *recv_first = nullptr, *lam_first = nullptr, *send_first = nullptr;
+    size_t opt_stage = 0;  // TQD_OPT_STAGING_BYTES (0 = default)
+    // fused forward sweep -> remap (peer memory): every rank's two shard allocations
+    // (first psi, first lambda), shared once; the forward stores into the owners'
+    // lambda-role buffer (idle until the adjoint seed) and the roles swap.  The
+    // current role of a buffer is looked up by pointer identity.
+    std::vector<void *> peer_pl;  // [rank * 2 + i], i = 0: first psi, 1: first lambda
+    void *psi_first = nullptr, *lam_first = nullptr;
     tqd_metrics met;
     double *d_red = nullptr;  // reductions: values / grads
     uint64_t *d_xy = nullptr;  // X/Y adjoint-seed term scratch: z masks, coefficients, #Y
@@ -241,17 +248,35 @@ static uint64_t shard_bytes(const tqd_state *st) { return ((uint64_t)1 << st->n_
 // every buffer holds the shards of all batch elements back to back
 static uint64_t all_bytes(const tqd_state *st) { return shard_bytes(st) * (uint64_t)st->batch; }
 
-static int ensure_xchg(tqd_state *st) {
-    if (st->sendb) return TQD_OK;
-    const size_t b = all_bytes(st);
-    if (cudaMalloc(&st->sendb, b) != cudaSuccess || cudaMalloc(&st->recvb, b) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(TQD_ERR_OOM, "cannot allocate remap staging buffers");
+// Exchange staging (world > 1): bounded, independent of the shard size -- the
+// remap and the partner-shard exchange of X / Y strings move their blocks through
+// it chunk by chunk (SURVEY.md §8(e) memory: at 36 qubits on 8 GPUs psi + lambda are
+// 2 x 64 GiB per GPU; two shard-sized staging buffers would not fit).
+static constexpr size_t kDefaultStagingBytes = (size_t)1 << 30;  // send half + receive half
+static size_t staging_bytes_for(size_t shard, size_t esz, size_t opt) {
+    size_t b = opt ? opt : kDefaultStagingBytes;
+    b = std::min(b, 2 * shard);
+    b = std::max(b, 2 * esz);  // at least one amplitude per half
+    return b & ~(2 * esz - 1);
+}
+
+static int ensure_staging(tqd_state *st) {
+    const size_t want = staging_bytes_for(shard_bytes(st), st->esz, st->opt_stage);
+    if (st->stg && st->stg_bytes >= want) return TQD_OK;
+    if (st->stg && st->own_stg) {
+        CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream));
+        cudaFree(st->stg);
+        st->met.peak_device_bytes -= st->stg_bytes;
     }
-    st->own_xchg = true;
-    st->send_first = st->sendb;
-    st->recv_first = st->recvb;
-    st->met.peak_device_bytes += 2 * b;
+    st->stg = nullptr;
+    if (cudaMalloc(&st->stg, want) != cudaSuccess) {
+        cudaGetLastError();
+        st->stg_bytes = 0;
+        return fail(TQD_ERR_OOM, "cannot allocate the exchange staging buffer");
+    }
+    st->own_stg = true;
+    st->stg_bytes = want;
+    st->met.peak_device_bytes += want;
     return TQD_OK;
 }
 
@@ -302,49 +327,87 @@ static void remap_schedule(int rank, int n_loc, const RemapPlan &rp, std::vector
     }
 }
 
+// One remap of one shard through the bounded staging: with every partner of the
+// rank group (XOR schedule s = 1 .. 2^m - 1; the partner's gpos-bits are
+// b = mine ^ s) this rank swaps its block b -- send block b, receive the partner's
+// block (its lpos-bits = my gpos-bits) into the same place -- chunk by chunk:
+// pack -> grouped send/recv (NCCL over NVLink) -> unpack.  Block b = mine stays.
 static int exec_remap_one(tqd_state *st, const RemapPlan &rp, void *buf) {
-    int rc = ensure_xchg(st);
+    int rc = ensure_staging(st);
     if (rc) return rc;
     tqd_ctx *c = st->ctx;
-    RemapMap rm;
-    memset(&rm, 0, sizeof(rm));
-    rm.m = rp.m;
-    rm.n_loc = st->n_loc;
-    std::vector<char> isl(st->n_loc, 0);
-    for (int i = 0; i < rp.m; i++) { rm.lpos[i] = (uint8_t)rp.lpos[i]; isl[rp.lpos[i]] = 1; }
-    int r = 0;
-    for (int p = 0; p < st->n_loc; p++) if (!isl[p]) rm.rest[r++] = (uint8_t)p;
+    uint64_t lmask = 0;
+    for (int i = 0; i < rp.m; i++) lmask |= 1ull << rp.lpos[i];
+    const uint64_t rest = ((st->n_loc >= 64 ? 0 : (1ull << st->n_loc)) - 1) & ~lmask;
     const uint64_t blk = (uint64_t)1 << (st->n_loc - rp.m);
+    const uint64_t chunk = std::min<uint64_t>(blk, (st->stg_bytes / 2) / st->esz);
+    char *sb = (char *)st->stg, *rb = (char *)st->stg + st->stg_bytes / 2;
+    int mine = 0;
+    for (int i = 0; i < rp.m; i++) mine |= ((c->rank >> (rp.gpos[i] - st->n_loc)) & 1) << i;
+    const char *dly = getenv("TQD_DEBUG_REMAP_DELAY_US");  // race tests: odd ranks lag before unpacking
+    const uint32_t delay_us = (dly && (c->rank & 1)) ? (uint32_t)atoi(dly) : 0;
     const int ev = ev_begin(st, CAT_A2A);
-    CUDA_TRY(st, launch_remap_pack(st->dbl, buf, st->sendb, rm, c->stream));
-    const size_t bb = blk * st->esz;
-    char *sb = (char *)st->sendb, *rb = (char *)st->recvb;
-    std::vector<int> peers, ublk;
-    remap_schedule(c->rank, st->n_loc, rp, peers, ublk);
-    COMM_TRY(st, c->comm->group_start());
-    for (uint64_t b = 0; b < ((uint64_t)1 << rp.m); b++) {
-        const int peer = peers[b];
-        const uint64_t u = (uint64_t)ublk[b];
-        if (peer == c->rank) {
-            CUDA_TRY(st, cudaMemcpyAsync(rb + u * bb, sb + b * bb, bb, cudaMemcpyDeviceToDevice, c->stream));
-        } else {
-            COMM_TRY(st, c->comm->send(sb + b * bb, bb, peer, c->stream));
-            COMM_TRY(st, c->comm->recv(rb + u * bb, bb, peer, c->stream));
-            st->met.a2a_bytes += bb;
+    for (int sx = 1; sx < (1 << rp.m); sx++) {
+        const int b = mine ^ sx;
+        int peer = c->rank;
+        uint64_t bdep = 0;
+        for (int i = 0; i < rp.m; i++) {
+            const int gb = rp.gpos[i] - st->n_loc;
+            peer = (peer & ~(1 << gb)) | (((b >> i) & 1) << gb);
+            if ((b >> i) & 1) bdep |= 1ull << rp.lpos[i];
+        }
+        for (uint64_t e0 = 0; e0 < blk; e0 += chunk) {
+            const uint64_t cnt = std::min(chunk, blk - e0);
+            const size_t bytes = cnt * st->esz;
+            CUDA_TRY(st, launch_remap_block(st->dbl, buf, sb, e0, cnt, bdep, rest, false, c->stream));
+            COMM_TRY(st, c->comm->group_start());
+            COMM_TRY(st, c->comm->send(sb, bytes, peer, c->stream));
+            COMM_TRY(st, c->comm->recv(rb, bytes, peer, c->stream));
+            COMM_TRY(st, c->comm->group_end(c->stream));
+            if (delay_us) CUDA_TRY(st, launch_debug_delay(delay_us, c->stream));
+            CUDA_TRY(st, launch_remap_block(st->dbl, buf, rb, e0, cnt, bdep, rest, true, c->stream));
+            st->met.a2a_bytes += bytes;
+            st->met.hbm_bytes += 4 * bytes;
+            st->met.kernel_launches += 2;
         }
     }
-    COMM_TRY(st, c->comm->group_end(c->stream));
-    CUDA_TRY(st, launch_remap_unpack(st->dbl, st->recvb, buf, rm, c->stream));
     ev_end(st, ev);
-    st->met.hbm_bytes += 4 * shard_bytes(st);
-    st->met.kernel_launches += 2;
     return TQD_OK;
 }
 
-// a remap of every batch element's shard (staging: the first shard of send / recv)
+// a remap of every batch element's shard
 static int exec_remap(tqd_state *st, const RemapPlan &rp, void *buf) {
     for (int b = 0; b < st->batch; b++) {
         const int rc = exec_remap_one(st, rp, (char *)buf + (size_t)b * shard_bytes(st));
+        if (rc) return rc;
+    }
+    return TQD_OK;
+}
+
+// X / Y strings acting on rank bits pair this shard with the partner rank's
+// (rank ^ gx): local index i meets the partner's i ^ xl.  Chunk by chunk through
+// the staging receive half: in step j both ranks send their chunk j ^ (xl's bits
+// above the chunk) and run `fn` on their own chunk j against the received one
+// (fn(psi_off, peer_chunk, count, xl within the chunk); the kernels see the chunk's
+// full index through rank_hi | psi_off).
+template <typename F>
+static int xy_partner_chunks(tqd_state *st, const void *psi_b, int gx, uint64_t xl, F &&fn) {
+    int rc = ensure_staging(st);
+    if (rc) return rc;
+    tqd_ctx *c = st->ctx;
+    const uint64_t N = 1ull << st->n_loc;
+    uint64_t C = 1;  // power of two <= the receive half
+    while (C * 2 * st->esz <= st->stg_bytes / 2 && C * 2 <= N) C *= 2;
+    const uint64_t hi = xl & ~(C - 1), lo = xl & (C - 1);
+    void *rb = (char *)st->stg + st->stg_bytes / 2;
+    const int partner = c->rank ^ gx;
+    for (uint64_t j0 = 0; j0 < N; j0 += C) {
+        COMM_TRY(st, c->comm->group_start());
+        COMM_TRY(st, c->comm->send((const char *)psi_b + (j0 ^ hi) * st->esz, C * st->esz, partner, c->stream));
+        COMM_TRY(st, c->comm->recv(rb, C * st->esz, partner, c->stream));
+        COMM_TRY(st, c->comm->group_end(c->stream));
+        st->met.a2a_bytes += C * st->esz;
+        rc = fn(j0, (const void *)rb, C, lo);
         if (rc) return rc;
     }
     return TQD_OK;
@@ -396,9 +459,12 @@ static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool b
 // straight into its post-remap owner's receive buffer (peer memory over NVLink; the
 // loopback world: the same device), then one barrier and a pointer swap replace the
 // pack -> all-to-all -> unpack of exec_remap.
+// Forward only: the stores go into the owners' lambda-role buffer, which holds
+// nothing until the adjoint seed (no extra memory).  In the adjoint psi and lambda
+// are both live, so its remaps run through the bounded staging.
 static bool fusable_remap(const tqd_state *st, bool bwd) {
-    return st->opt_fused && st->ctx->world > 1 && st->ctx->world <= SCATTER_MAX_RANKS && st->own_psi &&
-           (!bwd || st->own_lam);
+    return !bwd && st->opt_fused && st->ctx->world > 1 && st->ctx->world <= SCATTER_MAX_RANKS && st->own_psi &&
+           (!st->lam || st->own_lam);
 }
 
 // 1 = peer memory unavailable on some rank (same on every rank): fusion is turned
@@ -415,9 +481,9 @@ static int share_pair(tqd_state *st, void *a, void *b, std::vector<void *> &tabl
     return TQD_OK;
 }
 
-static uint64_t peer_of(const tqd_state *st, const std::vector<void *> &table, void *first, void *cur, int r) {
+static uint64_t peer_of(const std::vector<void *> &table, void *psi_first, void *cur, int r) {
     // the role of a buffer is symmetric over the ranks: same slot on every rank
-    return (uint64_t)table[r * 2 + (cur == first ? 0 : 1)];
+    return (uint64_t)table[r * 2 + (cur == psi_first ? 0 : 1)];
 }
 
 static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool bwd, const Encoded &E, double *d_grad) {
@@ -435,12 +501,12 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
             ScatterInfo sc;
             memset(&sc, 0, sizeof(sc));
             bool fuse = li + 1 < E.launches.size() && E.launches[li + 1].type == ST_REMAP && fusable_remap(st, bwd);
-            if (fuse) {
-                int rc = ensure_xchg(st);
+            if (fuse && !st->lam) {  // the lambda buffer (the fwd+grad budget) receives the remap
+                const int rc = ensure_lambda(st);
                 if (rc) return rc;
-                rc = share_pair(st, st->psi_first, st->recv_first, st->peer_psi);
-                if (rc < 0) return rc;
-                if (rc == 0 && bwd) rc = share_pair(st, st->lam_first, st->send_first, st->peer_lam);
+            }
+            if (fuse) {
+                const int rc = share_pair(st, st->psi_first, st->lam_first, st->peer_pl);
                 if (rc < 0) return rc;
                 fuse = rc == 0;  // 1: no peer memory, the remap launch below runs unfused
             }
@@ -449,10 +515,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
                 sc.m = rp.m;
                 sc.n_loc = st->n_loc;
                 for (int i = 0; i < rp.m && i < 8; i++) { sc.gbit[i] = (uint8_t)rp.gpos[i]; sc.lbit[i] = (uint8_t)rp.lpos[i]; }
-                for (int r = 0; r < c->world; r++) {
-                    sc.dst_psi[r] = peer_of(st, st->peer_psi, st->psi_first, st->recvb, r);
-                    if (bwd) sc.dst_lam[r] = peer_of(st, st->peer_lam, st->lam_first, st->sendb, r);
-                }
+                for (int r = 0; r < c->world; r++) sc.dst_psi[r] = peer_of(st->peer_pl, st->psi_first, st->lam, r);
             }
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
@@ -460,12 +523,12 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
                                       c->stream));
             ev_end(st, ev);
             if (fuse) {
-                // every rank's stores into its peers' receive buffers are complete
+                // every rank's stores into its peers' lambda-role buffers are complete
+                // (and every rank finished reading its psi, the next target)
                 COMM_TRY(st, c->comm->barrier(c->stream));
-                std::swap(st->psi, st->recvb);
-                if (bwd) std::swap(st->lam, st->sendb);
+                std::swap(st->psi, st->lam);
                 const uint64_t moved = sb - (sb >> sc.m);
-                st->met.a2a_bytes += bwd ? 2 * moved : moved;
+                st->met.a2a_bytes += moved;
                 st->met.remaps++;
                 st->met.fused_remaps++;
                 li++;  // the remap is done
@@ -511,8 +574,12 @@ static int launch_graphed(tqd_state *st, const std::vector<Stage> &stages, bool 
     if (!st->opt_graph || st->ctx->world != 1 || st->opt_profile) return launch_encoded(st, stages, bwd, E, d_grad);
     uint64_t key = st->plan_sig ^ (st->cached_tmix * 3) ^ 0x51ED27ull;
     for (uint64_t v : {(uint64_t)E.dev, (uint64_t)st->psi, (uint64_t)st->lam, (uint64_t)d_grad, (uint64_t)E.launches.size(),
-                       (uint64_t)stages.size()})
+                       (uint64_t)stages.size(), (uint64_t)E.off_ops, (uint64_t)E.off_kops, (uint64_t)E.off_sl})
         key = (key ^ v) * 1099511628211ull;
+    for (const Encoded::L &l : E.launches)  // every captured launch parameter
+        for (uint64_t v : {(uint64_t)l.type, (uint64_t)l.idx, (uint64_t)l.op_base, (uint64_t)l.n_ops, (uint64_t)l.stage,
+                           (uint64_t)l.grid, (uint64_t)l.n_slots, (uint64_t)l.no_store, (uint64_t)(int64_t)l.n_cvals})
+            key = (key ^ v) * 1099511628211ull;
     cudaStream_t s = st->ctx->stream;
     if (ge && gkey == key) {
         CUDA_TRY(st, cudaGraphLaunch(ge, s));
@@ -585,6 +652,12 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
 }
 
 static int encode_upload(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E) {
+    // a captured graph carries the launch parameters (op counts, shared-memory sizes,
+    // kernel instantiations, descriptor offsets) of the encoding it was captured
+    // from: re-encoding into the same buffer invalidates it (values can change the
+    // kernel-op structure, e.g. diagonal runs with zero or cancelling terms)
+    if (&E == st->enc_fwd && st->g_fwd) { cudaGraphExecDestroy(st->g_fwd); st->g_fwd = nullptr; st->g_fwd_key = 0; }
+    if (&E == st->enc_bwd && st->g_bwd) { cudaGraphExecDestroy(st->g_bwd); st->g_bwd = nullptr; st->g_bwd_key = 0; }
     std::vector<DevStage> dstages;
     std::vector<DevOp> ops;
     std::vector<KOp<float>> kf;
@@ -856,7 +929,7 @@ int tqd_state_bytes(int n, tqd_dtype dt, int world, int with_adjoint, size_t *ou
     if (n < (g ? g + 2 : 1) || n > 62) return fail(TQD_ERR_QUBITS, "need g + 2 <= n <= 62");
     const size_t esz = dt == TQD_C128 ? 16 : 8;
     const size_t shard = ((size_t)1 << (n - g)) * esz;
-    *out = shard * (with_adjoint ? 2 : 1) + (world > 1 ? 2 * shard : 0);
+    *out = shard * (with_adjoint ? 2 : 1) + (world > 1 ? staging_bytes_for(shard, esz, 0) : 0);
     return TQD_OK;
 }
 
@@ -895,12 +968,12 @@ static int state_init(tqd_ctx *c, int n, tqd_dtype dt, int batch, void *dev_buf,
     const size_t sb = shard_bytes(st);
     if (dev_buf) {
         if (buf_bytes < sb) { delete st; return fail(TQD_ERR_OOM, "dev_buf smaller than one shard"); }
+        // carve: psi, then lambda (when two shards fit), then the staging (world > 1)
         st->psi = dev_buf;
-        if (buf_bytes >= 2 * sb) st->lam = (char *)dev_buf + sb;
-        if (c->world > 1 && buf_bytes >= 4 * sb) {
-            st->sendb = (char *)dev_buf + 2 * sb;
-            st->recvb = (char *)dev_buf + 3 * sb;
-        }
+        size_t used = sb;
+        if (buf_bytes >= 2 * sb) { st->lam = (char *)dev_buf + sb; used = 2 * sb; }
+        const size_t sg = staging_bytes_for(sb, st->esz, 0);
+        if (c->world > 1 && buf_bytes >= used + sg) { st->stg = (char *)dev_buf + used; st->stg_bytes = sg; }
         st->met.peak_device_bytes = buf_bytes;
     } else {
         if (cudaMalloc(&st->psi, sb * batch) != cudaSuccess) {
@@ -966,12 +1039,11 @@ int tqd_state_free(tqd_state *st) {
     if (!st) return fail(TQD_ERR_ARG, "state is NULL");
     if (st->ctx && st->ctx->stream) cudaStreamSynchronize(st->ctx->stream);
     if (st->ctx && st->ctx->comm) {
-        st->ctx->comm->release_buffers(st->peer_psi, 2);
-        st->ctx->comm->release_buffers(st->peer_lam, 2);
+        st->ctx->comm->release_buffers(st->peer_pl, 2);
     }
     if (st->own_psi) cudaFree(st->psi);
     if (st->own_lam) cudaFree(st->lam);
-    if (st->own_xchg) { cudaFree(st->sendb); cudaFree(st->recvb); }
+    if (st->own_stg) cudaFree(st->stg);
     for (Encoded *E : {st->enc_fwd, st->enc_bwd, st->enc_tmp}) {
         if (E) { free_encoded(*E); delete E; }
     }
@@ -1005,6 +1077,9 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_STAGING_BYTES:
+        if (v < 0) return fail(TQD_ERR_ARG, "staging bytes must be >= 0");
+        st->opt_stage = (size_t)v; return TQD_OK;
     default: return fail(TQD_ERR_ARG, "unknown option");
     }
 }
@@ -1086,6 +1161,14 @@ int tqd_apply_gate_batch(tqd_state *st, tqd_gate g, const int *wires, int n_wire
     return TQD_OK;
 }
 
+int tqd_state_info(const tqd_state *st, int *n_qubits, int *batch, int *dtype) {
+    if (!st) return fail(TQD_ERR_ARG, "state is NULL");
+    if (n_qubits) *n_qubits = st->n;
+    if (batch) *batch = st->batch;
+    if (dtype) *dtype = st->dbl ? TQD_C128 : TQD_C64;
+    return TQD_OK;
+}
+
 int tqd_num_params(const tqd_state *st, int *out) {
     if (!st || !out) return fail(TQD_ERR_ARG, "NULL argument");
     *out = st->n_params;
@@ -1161,20 +1244,6 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         const uint64_t xp = phys_mask(st, x[t0]);
         const uint64_t xl = xp & ((1ull << st->n_loc) - 1);
         const int gx = (int)(xp >> st->n_loc);
-        const void *peer = psi_b;
-        if (gx) {
-            // X / Y on rank bits: <psi|P|psi> pairs this shard with rank ^ gx's shard
-            // (a whole-shard swap with that partner)
-            rc = ensure_xchg(st);
-            if (rc) return rc;
-            const int partner = c->rank ^ gx;
-            COMM_TRY(st, c->comm->group_start());
-            COMM_TRY(st, c->comm->send(psi_b, shard_bytes(st), partner, c->stream));
-            COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
-            COMM_TRY(st, c->comm->group_end(c->stream));
-            st->met.a2a_bytes += shard_bytes(st);
-            peer = st->recvb;
-        }
         uint64_t hm[16];
         int hn[16];
         for (size_t i = 0; i < grp.size(); i++) {
@@ -1185,7 +1254,19 @@ int tqd_expval(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const
         CUDA_TRY(st, cudaMemcpyAsync(d_ny, hn, grp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
         double *tmp = st->d_red + BT + 128;
         CUDA_TRY(st, cudaMemsetAsync(tmp, 0, 16 * sizeof(double), c->stream));
-        CUDA_TRY(st, launch_expval_xy(st->dbl, psi_b, peer, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp, c->stream));
+        if (gx) {
+            // X / Y on rank bits: <psi|P|psi> pairs this shard with rank ^ gx's shard
+            // (PAPER.md:164), exchanged chunk by chunk through the bounded staging
+            rc = xy_partner_chunks(st, psi_b, gx, xl, [&](uint64_t off, const void *pc, uint64_t cnt, uint64_t lo) {
+                CUDA_TRY(st, launch_expval_xy(st->dbl, (const char *)psi_b + off * st->esz, pc, cnt, rank_hi(st) | off, lo,
+                                              d_masks, d_ny, (int)grp.size(), tmp, c->stream));
+                return (int)TQD_OK;
+            });
+            if (rc) return rc;
+        } else {
+            CUDA_TRY(st, launch_expval_xy(st->dbl, psi_b, psi_b, N, rank_hi(st), xl, d_masks, d_ny, (int)grp.size(), tmp,
+                                          c->stream));
+        }
         for (size_t i = 0; i < grp.size(); i++)
             CUDA_TRY(st, cudaMemcpyAsync(d_out + grp[i], tmp + i, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         CUDA_TRY(st, cudaStreamSynchronize(c->stream));
@@ -1317,9 +1398,11 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
         z = zabs.data();
     }
     st->met.gates_absorbed += st->gates.size() - end;
-    rc = execute_pending(st, end);
-    if (rc) return rc;
+    // lambda first: the forward's remaps can then be fused into its sweeps (they
+    // store into the owners' still idle lambda buffers)
     rc = ensure_lambda(st);
+    if (rc) return rc;
+    rc = execute_pending(st, end);
     if (rc) return rc;
     rc = ensure_red(st, (size_t)n_grad + 1);
     if (rc) return rc;
@@ -1373,18 +1456,6 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
                 const uint64_t xp = phys_mask(st, x[t0]);
                 const uint64_t xl = xp & (N - 1);
                 const int gx = (int)(xp >> st->n_loc);
-                const void *peer = psi_b;
-                if (gx) {
-                    rc = ensure_xchg(st);
-                    if (rc) return rc;
-                    const int partner = c->rank ^ gx;
-                    COMM_TRY(st, c->comm->group_start());
-                    COMM_TRY(st, c->comm->send(psi_b, shard_bytes(st), partner, c->stream));
-                    COMM_TRY(st, c->comm->recv(st->recvb, shard_bytes(st), partner, c->stream));
-                    COMM_TRY(st, c->comm->group_end(c->stream));
-                    st->met.a2a_bytes += shard_bytes(st);
-                    peer = st->recvb;
-                }
                 hz.assign(16, 0);
                 hn.assign(16, 0);
                 hc.assign(16, 0.0);
@@ -1399,9 +1470,21 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
                 CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 16, hc.data(), 16 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
                 CUDA_TRY(st, cudaMemcpyAsync(st->d_xy + 32, hn.data(), 16 * sizeof(int), cudaMemcpyHostToDevice, c->stream));
                 const int ev = ev_begin(st, CAT_OTHER);
-                CUDA_TRY(st, launch_lambda_add_xy(st->dbl, psi_b, peer, lam_b, N, rank_hi(st), xl, xp, st->d_xy,
-                                                  (const int *)(st->d_xy + 32), (const double *)(st->d_xy + 16),
-                                                  (int)grp.size(), d_val, c->stream));
+                if (gx) {  // partner rank's shard, chunk by chunk (as in tqd_expval)
+                    rc = xy_partner_chunks(st, psi_b, gx, xl, [&](uint64_t off, const void *pc, uint64_t cnt, uint64_t lo) {
+                        CUDA_TRY(st, launch_lambda_add_xy(st->dbl, (const char *)psi_b + off * st->esz, pc,
+                                                          (char *)lam_b + off * st->esz, cnt, rank_hi(st) | off, lo, xp,
+                                                          st->d_xy, (const int *)(st->d_xy + 32),
+                                                          (const double *)(st->d_xy + 16), (int)grp.size(), d_val,
+                                                          c->stream));
+                        return (int)TQD_OK;
+                    });
+                    if (rc) return rc;
+                } else {
+                    CUDA_TRY(st, launch_lambda_add_xy(st->dbl, psi_b, psi_b, lam_b, N, rank_hi(st), xl, xp, st->d_xy,
+                                                      (const int *)(st->d_xy + 32), (const double *)(st->d_xy + 16),
+                                                      (int)grp.size(), d_val, c->stream));
+                }
                 ev_end(st, ev);
                 CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host staging vectors are reused
                 st->met.h2d_bytes += 16 * (8 + 8 + 4);

@@ -10,7 +10,7 @@
 //   lambda_add_xy_kernel         lambda += c P psi, E += c <psi|P|psi> (X / Y strings)
 //   expval_z_kernel / expval_xy_kernel   <psi|P_t|psi> partial sums
 //   gather_kernel                canonical-order readback through pi
-//   remap_pack / remap_unpack    qubit-remap staging for the NCCL exchange
+//   remap_block_kernel           qubit-remap chunk pack / unpack for the NCCL exchange
 //
 // Data layout in HBM: the shard is an array of interleaved (re, im) complex
 // numbers (float2 for complex64, double2 for complex128), physical index =
@@ -575,40 +575,43 @@ __global__ void set_one_kernel(typename CT<Real>::C *psi) {
     psi[0] = mk<typename CT<Real>::C>(1, 0);
 }
 
-// Remap staging.  The exchange swaps global positions gpos[i] (rank bit i of
-// the group) with local positions lpos[i], i < m.  pack: send block b (the
-// values of the local bits lpos) collects, in order of the remaining local
-// bits, every amplitude whose lpos-bits equal b.  unpack: the block received
-// from group peer s goes back with lpos-bits := s's rank bits.
-template <typename Real>
-__global__ void remap_pack_kernel(const typename CT<Real>::C *__restrict__ src, typename CT<Real>::C *__restrict__ dst,
-                                  RemapMap rm) {
-    const uint64_t blk = 1ull << (rm.n_loc - rm.m);
-    const uint64_t n = 1ull << rm.n_loc;
-    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t b = o / blk, r = o % blk;
-        uint64_t p = 0;
-        for (int i = 0; i < rm.n_loc - rm.m; i++)
-            if ((r >> i) & 1) p |= 1ull << rm.rest[i];
-        for (int i = 0; i < rm.m; i++)
-            if ((b >> i) & 1) p |= 1ull << rm.lpos[i];
-        dst[o] = src[p];
+// Remap exchange through bounded staging ("interchanging qubit
+// positions" + redistribution; SURVEY.md §8(e) chunked exchange).  The exchange
+// swaps global positions gpos[i] with local positions lpos[i]: with the partner
+// rank whose gpos-bits equal b, this rank swaps its block b (the amplitudes whose
+// lpos-bits equal b), chunk by chunk.  Element e of a block = the local index
+// with the lpos-bits = b (bdep) and the remaining local bits (ascending, the mask
+// `rest`) = e.  pack: stage[i] = shard[idx(e0 + i)]; unpack: the reverse.
+__device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
+    uint64_t r = 0;
+    for (uint64_t bb = 1; mask; bb <<= 1) {
+        const uint64_t low = mask & (~mask + 1);
+        if (v & bb) r |= low;
+        mask &= mask - 1;
     }
+    return r;
 }
 template <typename Real>
-__global__ void remap_unpack_kernel(const typename CT<Real>::C *__restrict__ src, typename CT<Real>::C *__restrict__ dst,
-                                    RemapMap rm) {
-    const uint64_t blk = 1ull << (rm.n_loc - rm.m);
-    const uint64_t n = 1ull << rm.n_loc;
-    for (uint64_t o = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = o / blk, r = o % blk;
-        uint64_t p = 0;
-        for (int i = 0; i < rm.n_loc - rm.m; i++)
-            if ((r >> i) & 1) p |= 1ull << rm.rest[i];
-        for (int i = 0; i < rm.m; i++)
-            if ((s >> i) & 1) p |= 1ull << rm.lpos[i];
-        dst[p] = src[o];
+__global__ void __launch_bounds__(256) remap_block_kernel(typename CT<Real>::C *__restrict__ shard,
+                                                          typename CT<Real>::C *__restrict__ stage, uint64_t e0,
+                                                          uint64_t cnt, uint64_t bdep, uint64_t rest, int unpack) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+    if (t >= cnt) return;
+    // deposit once, then step by a masked add (carries pass through the non-rest bits)
+    uint64_t idx = pdep64(e0 + t, rest);
+    const uint64_t sdep = pdep64(stride, rest);
+    for (uint64_t i = t; i < cnt; i += stride) {
+        const uint64_t p = idx | bdep;
+        if (unpack) shard[p] = stage[i];
+        else stage[i] = shard[p];
+        idx = ((idx | ~rest) + sdep) & rest;
     }
+}
+
+// test hook (TQD_DEBUG_REMAP_DELAY_US): hold this rank's stream for a while so a
+// peer runs ahead (exchange race tests); sleeps, waits on nothing
+__global__ void debug_delay_kernel(uint32_t us) {
+    for (uint32_t i = 0; i < us; i++) __nanosleep(1000);
 }
 
 // ---------------------------------------------------------------------------
@@ -773,18 +776,16 @@ cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_remap_pack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s) {
+cudaError_t launch_remap_block(bool dbl, void *shard, void *stage, uint64_t e0, uint64_t cnt, uint64_t bdep, uint64_t rest,
+                              bool unpack, cudaStream_t s) {
+    if (cnt == 0) return cudaSuccess;
     const int th = 256;
-    const uint64_t n = 1ull << rm.n_loc;
-    if (dbl) remap_pack_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)src, (double2 *)dst, rm);
-    else remap_pack_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)src, (float2 *)dst, rm);
+    if (dbl) remap_block_kernel<double><<<grid_for(cnt, th), th, 0, s>>>((double2 *)shard, (double2 *)stage, e0, cnt, bdep, rest, unpack);
+    else remap_block_kernel<float><<<grid_for(cnt, th), th, 0, s>>>((float2 *)shard, (float2 *)stage, e0, cnt, bdep, rest, unpack);
     return cudaGetLastError();
 }
-cudaError_t launch_remap_unpack(bool dbl, const void *src, void *dst, const RemapMap &rm, cudaStream_t s) {
-    const int th = 256;
-    const uint64_t n = 1ull << rm.n_loc;
-    if (dbl) remap_unpack_kernel<double><<<grid_for(n, th), th, 0, s>>>((const double2 *)src, (double2 *)dst, rm);
-    else remap_unpack_kernel<float><<<grid_for(n, th), th, 0, s>>>((const float2 *)src, (float2 *)dst, rm);
+cudaError_t launch_debug_delay(uint32_t us, cudaStream_t s) {
+    debug_delay_kernel<<<1, 1, 0, s>>>(us);
     return cudaGetLastError();
 }
 

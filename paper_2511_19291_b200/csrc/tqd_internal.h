@@ -247,11 +247,4 @@ struct GatherMap {
     uint8_t phys_of_canon_bit[64];  // canonical bit b -> physical position
 };
 
-// remap staging: local positions swapped with the global ones, and the rest
-struct RemapMap {
-    int m, n_loc;
-    uint8_t lpos[8];
-    uint8_t rest[64];  // remaining local positions, ascending (n_loc - m of them)
-};
-
 }  // namespace tqd

@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 import workloads as W
@@ -34,7 +35,14 @@ def test_version_string():
 
 def test_state_bytes():
     assert tqd.tqd_state_bytes(30, tqd.C64, 1, 1) == 2 * 8 * (1 << 30)
-    assert tqd.tqd_state_bytes(36, tqd.C64, 8, 0) == 8 * (1 << 33) * 3
+    # the north-star target, 36 qubits complex64 fwd+grad on 8 GPUs: psi + lambda (2 x 64 GiB)
+    # plus the bounded exchange staging (1 GiB), within a B200's ~179 GB (SURVEY.md §8(e) memory)
+    shard = 8 * (1 << 33)
+    assert tqd.tqd_state_bytes(36, tqd.C64, 8, 1) == 2 * shard + (1 << 30)
+    assert tqd.tqd_state_bytes(36, tqd.C64, 8, 1) <= 130 * 2**30 < 179e9
+    assert tqd.tqd_state_bytes(36, tqd.C64, 8, 0) == shard + (1 << 30)
+    # small shards: staging = two shards at most
+    assert tqd.tqd_state_bytes(12, tqd.C128, 2, 1) == 2 * 16 * (1 << 11) + 2 * 16 * (1 << 11)
     with pytest.raises(tqd.TqdError) as e:
         tqd.tqd_state_bytes(3, tqd.C64, 4, 0)        # n < log2(world) + 2
     assert e.value.code == -2
@@ -78,3 +86,14 @@ def test_gate_arrays_checks_counts():
                 W.Gate("X", (0, 1))):
         with pytest.raises(tqd.TqdError):
             tqd._gate_arrays([W.Gate("H", (0,)), bad])
+
+
+def test_apply_gate_binding_checks_counts():
+    """tqd_apply_gate takes no lengths: the binding rejects wrong wire / parameter /
+    matrix sizes before the C call could read past a numpy buffer."""
+    for gate, wires, params, mat in (("U3", [0], (0.1,), None), ("RY", [0], (), None), ("RY", [0, 1], (0.1,), None),
+                                     ("CNOT", [0], (), None), ("X", [0], (0.3,), None), ("MAT1", [0], (), None),
+                                     ("MAT2", [0, 1], (), np.eye(2))):
+        with pytest.raises(tqd.TqdError) as e:
+            tqd.tqd_apply_gate(None, gate, wires, params, mat)  # raised before the handle is used
+        assert e.value.code == -1

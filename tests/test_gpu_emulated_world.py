@@ -61,10 +61,11 @@ def mixed_circuit(n, seed):
     return W.random_circuit(n, 120, seed) + W.hea(n, 2, seed) + W.qft(n)[:30]
 
 
+@pytest.mark.parametrize("grid", [0, 3])
 @pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("world,n,k", [(2, 12, 9), (4, 13, 9), (8, 14, 9), (2, 16, 12), (4, 17, 12)])
-def test_world_amplitudes(tqd, orc, world, n, k, dtype, fused):
+def test_world_amplitudes(tqd, orc, world, n, k, dtype, fused, grid):
     """fused = 1: remaps fused into the preceding sweep (stores into the owners'
     peer memory); fused = 0: pack -> all-to-all -> unpack."""
     gates = mixed_circuit(n, world + n)
@@ -74,6 +75,7 @@ def test_world_amplitudes(tqd, orc, world, n, k, dtype, fused):
         st.set_option(tqd.OPT_TILE_QUBITS, k)
         st.set_option(tqd.OPT_SMALL_MAX, 0)
         st.set_option(tqd.OPT_FUSED_REMAP, fused)
+        st.set_option(tqd.OPT_GRID_CTAS, grid)
         st.apply_circuit(gates)
         amp = st.amplitudes()
         m = st.metrics()
@@ -110,10 +112,11 @@ def test_world_expval_pauli(tqd, orc, world, n, dtype):
         assert np.max(np.abs(v - ref)) < TOL[dtype]["val"]
 
 
+@pytest.mark.parametrize("grid", [0, 3])
 @pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("world,n,k,small", [(2, 12, 9, False), (4, 14, 10, True), (8, 15, 9, True), (2, 17, 12, True)])
-def test_world_adjoint(tqd, orc, world, n, k, small, dtype, fused):
+def test_world_adjoint(tqd, orc, world, n, k, small, dtype, fused, grid):
     """Adjoint gradients with remaps replayed on psi and lambda."""
     gates = W.random_circuit(n, 80, 5 + world, small=small) + W.hea(n, 3, world, small=small)
     terms = W.random_z_terms(n, 5, world) + W.sum_z(n)
@@ -123,6 +126,7 @@ def test_world_adjoint(tqd, orc, world, n, k, small, dtype, fused):
         st.set_option(tqd.OPT_TILE_QUBITS, k)
         st.set_option(tqd.OPT_SMALL_MAX, 0)
         st.set_option(tqd.OPT_FUSED_REMAP, fused)
+        st.set_option(tqd.OPT_GRID_CTAS, grid)
         st.apply_circuit(gates)
         val, grad = st.adjoint_grad(terms)
         st.free()
@@ -228,3 +232,81 @@ def test_world_fused_remap_repeat(tqd, orc):
             assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
         assert np.max(np.abs(amp - ref)) < 1e-12
         assert m["remaps"] > 0
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n", [(2, 12), (4, 13), (8, 14)])
+def test_world_bounded_staging(tqd, orc, world, n, dtype, fused):
+    """Remaps and X / Y partner exchanges through a staging buffer forced to 2 KiB
+    (TQD_OPT_STAGING_BYTES), so every block moves in many chunks: amplitudes,
+    Pauli expectation values (X / Y on rank bits) and adjoint gradients (psi and
+    lambda remapped) against the oracle (SURVEY.md §8(e) bounded exchange)."""
+    gates = mixed_circuit(n, 5 * world + n)
+    terms = W.random_z_terms(n, 4, world) + [(1, 0, 0.7), (3, 4, -1.1), (2, 1 | (1 << (n - 1)), 0.3)]
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.set_option(tqd.OPT_FUSED_REMAP, fused)
+        st.set_option(tqd.OPT_STAGING_BYTES, 2048)
+        st.apply_circuit(gates)
+        amp = st.amplitudes()
+        ev = st.expval(terms)
+        st.reset()
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(terms)
+        m = st.metrics()
+        st.free()
+        return amp, ev, val, grad, m
+    ref = orc.run(n, gates)
+    rev = orc.expval(ref, n, terms)
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    for amp, ev, val, grad, m in run_world(tqd, world, fn):
+        assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"]
+        assert np.max(np.abs(ev - rev)) < TOL[dtype]["val"]
+        assert abs(val - rval) < TOL[dtype]["val"]
+        assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]
+        assert m["remaps"] > 0 and m["a2a_bytes"] > 0
+        # no shard-sized staging: psi + lambda + 2 KiB (+ the fused-forward lambda)
+        assert m["peak_device_bytes"] <= 2 * (1 << (n - (world.bit_length() - 1))) * (16 if dtype == "c128" else 8) + 2048
+
+
+def test_world_unfused_remap_then_fused_race(tqd, orc, monkeypatch):
+    """a plan [remap (unfused: nothing before it), sweep, sweep +
+    fused remap, ...] with odd ranks held back (device sleep) between receiving and
+    unpacking each remap chunk.  Round 1 staged both through the same receive
+    buffer, so a fast rank's fused stores could overwrite a slow rank's received
+    block before it was unpacked; now unfused remaps use rank-local staging and
+    fused stores go to the owners' idle lambda buffers."""
+    n, world = 12, 4
+    gates = [W.Gate("RX", (0,), (0.3,)), W.Gate("RX", (1,), (0.4,))]
+    gates += [W.Gate("CNOT", (q, q + 1)) for q in range(n - 1)] + W.hea(n, 2, 1, small=True)
+    kinds = [s["type"] for s in tqd.tqd_debug_plan(n, gates, world=world, k=9, small_max=0)["stages"]]
+    assert kinds[0] == "remap" and any(a == "sweep" and b == "remap" for a, b in zip(kinds, kinds[1:])), kinds
+    monkeypatch.setenv("TQD_DEBUG_REMAP_DELAY_US", "20000")
+    terms = W.sum_z(n) + [(0, 3, 0.5)]
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, "c128")
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.set_option(tqd.OPT_STAGING_BYTES, 4096)
+        st.apply_circuit(gates)
+        out = [st.adjoint_grad(terms)]
+        st.rewind()  # the shared peer tables exist now: the race window is open from the first stage
+        out.append(st.adjoint_grad(terms))
+        st.reset()
+        st.apply_circuit(gates)
+        amp = st.amplitudes()
+        m = st.metrics()
+        st.free()
+        return out, amp, m
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ref = orc.run(n, gates)
+    for out, amp, m in run_world(tqd, world, fn):
+        for val, grad in out:
+            assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
+        assert np.max(np.abs(amp - ref)) < 1e-12
+        assert m["fused_remaps"] > 0 and m["remaps"] > m["fused_remaps"]

@@ -32,12 +32,16 @@ def ctx(tqd):
     c.close()
 
 
-def make_state(tqd, ctx, n, dtype, k=None, small_max=None):
+def make_state(tqd, ctx, n, dtype, k=None, small_max=None, grid=None):
     st = tqd.State(ctx, n, dtype)
     if k is not None:
         st.set_option(tqd.OPT_TILE_QUBITS, k)
     if small_max is not None:
         st.set_option(tqd.OPT_SMALL_MAX, small_max)
+    if grid:
+        # a few persistent CTAs: every CTA walks many tiles (tile stepping, next-tile
+        # prefetch, accumulators carried across tiles) as at 30 qubits
+        st.set_option(tqd.OPT_GRID_CTAS, grid)
     return st
 
 
@@ -55,13 +59,17 @@ def test_small_path_amplitudes(tqd, ctx, orc, n, dtype):
         assert np.max(np.abs(got - ref)) < TOL[dtype]["amp"], (n, seed)
 
 
+GRIDS = [0, 1, 3, 7]  # 0 = auto (SMs x resident CTAs); 1 / 3 / 7: each CTA loops over many tiles
+
+
+@pytest.mark.parametrize("grid", GRIDS)
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n,k", [(9, 9), (11, 10), (12, 12), (13, 11), (15, 12), (17, 12), (18, 9)])
-def test_sweep_path_amplitudes(tqd, ctx, orc, n, k, dtype):
+def test_sweep_path_amplitudes(tqd, ctx, orc, n, k, dtype, grid):
     """Fused tiled sweeps (forced: small path off); several tiles and k values."""
     for seed in range(2):
         gates = W.random_circuit(n, 120, seed + 10 * n)
-        st = make_state(tqd, ctx, n, dtype, k=k, small_max=0)
+        st = make_state(tqd, ctx, n, dtype, k=k, small_max=0, grid=grid)
         st.apply_circuit(gates)
         got = st.amplitudes()
         m = st.metrics()
@@ -158,14 +166,15 @@ def _grad_check(tqd, ctx, orc, n, gates, terms, dtype, **opt):
     return err
 
 
+@pytest.mark.parametrize("grid", GRIDS)
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n,small_max,k", [(4, 10, None), (9, 10, None), (11, 0, 10), (14, 0, 12), (16, 0, 12)])
-def test_adjoint_random_circuits(tqd, ctx, orc, n, small_max, k, dtype):
+def test_adjoint_random_circuits(tqd, ctx, orc, n, small_max, k, dtype, grid):
     for seed in range(2):
         for small in (False, True):
             gates = W.random_circuit(n, 80, seed + 3 * n, small=small)
             terms = W.random_z_terms(n, 5, seed) + [(0, 1 << (n - 1), 0.5)]
-            _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=small_max, k=k)
+            _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=small_max, k=k, grid=grid)
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
@@ -185,11 +194,66 @@ def test_cfg1_exact(tqd, ctx, orc):
     _grad_check(tqd, ctx, orc, wl.n, wl.gates, wl.terms, "c128")
 
 
+@pytest.mark.parametrize("grid", GRIDS)
 @pytest.mark.parametrize("small", [False, True])
-def test_hea_sweep_grads(tqd, ctx, orc, small):
+def test_hea_sweep_grads(tqd, ctx, orc, small, grid):
     n = 18
     gates = W.hea(n, 6, seed=1, small=small)
-    _grad_check(tqd, ctx, orc, n, gates, W.sum_z(n), "c64", small_max=0)
+    _grad_check(tqd, ctx, orc, n, gates, W.sum_z(n), "c64", small_max=0, grid=grid)
+
+
+# ---------------------------------------------------------------- oracle parity at larger sizes
+ALL_KINDS = ["I", "X", "Y", "Z", "H", "S", "SDG", "T", "TDG", "CNOT", "CZ", "SWAP", "MAT1", "MAT2",
+             "RX", "RY", "RZ", "U3"]
+
+
+def _rel(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+@pytest.mark.parametrize("small", [False, True])
+def test_random_22q_all_kinds_vs_oracle(tqd, ctx, orc, small):
+    """22-qubit random circuit over every gate kind (c64, bench launch configuration:
+    k = 12, auto grid = 1024 tiles over 296-444 persistent CTAs, so CTAs loop over
+    tiles): amplitudes element-wise (1e-5), Z-string values and every gradient
+    (1e-4) against the float64 oracle; both angle distributions (R10)."""
+    n = 22
+    gates = W.random_circuit(n, 300, 2200 + int(small), kinds=ALL_KINDS, small=small)
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(gates)
+    amps = st.amplitudes()
+    st.free()
+    ref = orc.run(n, gates)
+    err = float(np.max(np.abs(amps - ref)))
+    print(f"22q amplitudes: max abs {err:.2e}, rel {_rel(amps, ref):.2e}")
+    assert err < 1e-5
+    terms = W.random_z_terms(n, 6, 22) + W.sum_z(n)
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(terms)
+    st.free()
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ge = float(np.max(np.abs(grad - rgrad)))
+    print(f"22q value err {abs(val - rval):.2e}; {len(grad)} gradients: max abs {ge:.2e}, rel {_rel(grad, rgrad):.2e}")
+    assert abs(val - rval) < 1e-4 and ge < 1e-4
+
+
+@pytest.mark.parametrize("small", [False, True])
+def test_cfg2_24q_hea_vs_oracle(tqd, ctx, orc, small):
+    """BASELINE.json configs[1] (SURVEY.md:315): 24-qubit HEA depth 20, complex64,
+    forward + adjoint gradient of sum <Z_i>: the value and all 960 gradients
+    element-wise against the float64 oracle (1e-4), both angle distributions."""
+    n, depth = 24, 20
+    gates = W.hea(n, depth, seed=24, small=small)
+    st = make_state(tqd, ctx, n, "c64")
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(W.sum_z(n))
+    st.free()
+    assert len(grad) == 2 * n * depth
+    rval, rgrad = orc.adjoint(n, gates, W.sum_z(n))
+    ge = float(np.max(np.abs(grad - rgrad)))
+    print(f"cfg2 value err {abs(val - rval):.2e}; 960 gradients: max abs {ge:.2e}, rel {_rel(grad, rgrad):.2e}")
+    assert abs(val - rval) < 1e-4 and ge < 1e-4
 
 
 def test_listing2_vjp(tqd, ctx, orc):
@@ -300,7 +364,7 @@ def test_cfg3_parameter_shift_spot(tqd, ctx):
             st.apply_circuit(gg)
             es.append(st.expval(W.sum_z(n)).sum())
             st.free()
-        assert abs((es[0] - es[1]) / 2 - grad[pi]) < 1e-3
+        assert abs((es[0] - es[1]) / 2 - grad[pi]) < 1e-4
 
 
 def test_cfg5_shard_qft_closed_form(tqd, ctx):
@@ -466,23 +530,24 @@ def _diag_heavy(n, seed):
     return gates + W.random_circuit(n, 4, seed + 99, kinds=["H", "RX"])
 
 
+@pytest.mark.parametrize("grid", GRIDS)
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n,k", [(12, 9), (15, 10), (18, 12)])
-def test_diagonal_blocks(tqd, ctx, orc, n, k, dtype):
+def test_diagonal_blocks(tqd, ctx, orc, n, k, dtype, grid):
     """Merged diagonal runs (K_DBLK phase polynomials) against the oracle applying
     every diagonal gate: amplitudes, QFT = DFT, and adjoint gradients."""
     for seed in range(2):
         gates = _diag_heavy(n, seed)
-        st = make_state(tqd, ctx, n, dtype, k=k, small_max=0)
+        st = make_state(tqd, ctx, n, dtype, k=k, small_max=0, grid=grid)
         st.apply_circuit(gates)
         got = st.amplitudes()
         st.free()
         assert np.max(np.abs(got - orc.run(n, gates))) < TOL[dtype]["amp"], seed
         terms = W.random_z_terms(n, 4, seed) + [(1, 2, 0.5)]
-        _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=0, k=k)
+        _grad_check(tqd, ctx, orc, n, gates, terms, dtype, small_max=0, k=k, grid=grid)
     x = 0b1011 % (1 << n)
     gates = W.basis_prep(n, x) + W.qft(n)
-    st = make_state(tqd, ctx, n, dtype, k=k, small_max=0)
+    st = make_state(tqd, ctx, n, dtype, k=k, small_max=0, grid=grid)
     st.apply_circuit(gates)
     got = st.amplitudes()
     st.free()
@@ -527,6 +592,45 @@ def test_cuda_graph_replay(tqd, ctx, orc):
             st.free()
         res[graph] = out
     assert res[0] == res[1]
+
+
+def test_cuda_graph_value_dependent_structure(tqd, ctx, orc):
+    """CUDA-graph replays when re-recorded VALUES change the kernel-op structure
+    (ADVICE r1): non-trainable RZ / controlled phases whose angles are 0 or cancel
+    in pairs are dropped from diagonal runs, so the same plan signature encodes to
+    other kernel ops.  Every tape is checked against the oracle after rewinds."""
+    n = 14
+    base = W.hea(n, 3, seed=11, small=True)
+
+    def tape(mode):
+        a = {"on": 0.7, "zero": 0.0, "cancel": 0.45, "on2": -1.3}[mode]
+        b = -a if mode == "cancel" else 0.25 * a
+        gates = []
+        for i, g in enumerate(base):
+            gates.append(g)
+            if i % 7 == 3:
+                q = g.wires[0]
+                gates.append(W.Gate("RZ", (q,), (a,), None, False))
+                gates.append(W.Gate("RZ", (q,), (b,), None, False))
+                gates.append(W.Gate("MAT2", (q, (q + 5) % n), (), W.cphase_matrix(a), False))
+                gates.append(W.Gate("MAT2", (q, (q + 5) % n), (), W.cphase_matrix(b), False))
+        return gates
+
+    st = make_state(tqd, ctx, n, "c64", k=11, small_max=0)
+    st.set_option(tqd.OPT_USE_GRAPH, 1)
+    try:
+        for mode in ("on", "zero", "cancel", "on2", "zero"):
+            gates = tape(mode)
+            rval, rgrad = orc.adjoint(n, gates, W.sum_z(n))
+            st.reset()
+            st.apply_circuit(gates)
+            for it in range(3):
+                if it:
+                    st.rewind()
+                val, grad = st.adjoint_grad(W.sum_z(n))
+                assert abs(val - rval) < 1e-4 and np.max(np.abs(grad - rgrad)) < 1e-4, (mode, it)
+    finally:
+        st.free()
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
