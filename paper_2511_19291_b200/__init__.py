@@ -19,7 +19,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtqd.so")
+# TQD_LIB: another in-tree build of the same library (kernel experiment variants, tools/build_variant.sh)
+LIB_PATH = os.environ.get("TQD_LIB") or os.path.join(_HERE, "libtqd.so")
 
 # this binding's own copy of the tqd_gate enum (include/tqd.h)
 GATES = {
@@ -29,8 +30,7 @@ GATES = {
 }
 C64, C128 = 0, 1
 OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP, OPT_ABSORB_TAIL, \
-    OPT_STAGING_BYTES = \
-    0, 1, 2, 3, 4, 5, 6, 7
+    OPT_STAGING_BYTES, OPT_SWEEP_TMA = 0, 1, 2, 3, 4, 5, 6, 7, 8
 ERRORS = {0: "TQD_OK", -1: "TQD_ERR_ARG", -2: "TQD_ERR_QUBITS", -3: "TQD_ERR_WORLD",
           -4: "TQD_ERR_NOT_UNITARY", -5: "TQD_ERR_OOM", -6: "TQD_ERR_CUDA", -7: "TQD_ERR_NCCL",
           -8: "TQD_ERR_UNSUPPORTED", -9: "TQD_ERR_STATE"}
@@ -103,7 +103,7 @@ def lib():
     with _lock:
         if _lib is None:
             from . import build as _build
-            if not _build.up_to_date():
+            if LIB_PATH == _build.SO and not _build.up_to_date():
                 _build.build()
             L = ctypes.CDLL(LIB_PATH)
             for name, args in _SIG.items():
