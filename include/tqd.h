@@ -112,14 +112,10 @@ typedef enum {
                                * After tqd_expval the absorbed gates stay pending: a later
                                * readback / sample / non-Z observable applies them.
                                * 0: apply every gate.                                      */
-    TQD_OPT_STAGING_BYTES = 7, /* world > 1: bytes of the exchange staging (send + receive
+    TQD_OPT_STAGING_BYTES = 7  /* world > 1: bytes of the exchange staging (send + receive
                                * halves; remap blocks and X/Y partner shards move through it
                                * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
                                * force a few KiB so the chunk loop iterates.               */
-    TQD_OPT_SWEEP_TMA = 8      /* bit 0 (forward) / bit 1 (adjoint): fused sweeps fetch the next
-                               * tile of each CTA into shared memory with the tensor-memory
-                               * accelerator (cp.async.bulk.tensor) while computing the current
-                               * one; 0: per-thread loads.                                  */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.

@@ -19,9 +19,9 @@
 namespace tqd {
 // kernels.cu
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
-                         void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, const SweepTma &tma,
-                         int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s);
-int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, bool tma);
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W,
+                         int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s);
+int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg, int n_cvals);
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad, int n_loc,
                          uint64_t rank_hi, int batch, cudaStream_t s);
 cudaError_t launch_lambda_init(bool dbl, const void *psi, void *lam, uint64_t n, uint64_t rank_hi, const ZTerms &t,
@@ -94,7 +94,6 @@ struct tqd_state {
     // options
     int opt_k = 12, opt_small = 8, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1, opt_absorb = 1;
     size_t opt_stage = 0;  // TQD_OPT_STAGING_BYTES (0 = default)
-    int opt_tma = -1;      // TQD_OPT_SWEEP_TMA (-1 = default)
     // fused forward sweep -> remap (peer memory): every rank's two shard allocations
     // (first psi, first lambda), shared once; the forward stores into the owners'
     // lambda-role buffer (idle until the adjoint seed) and the roles swap.  The
@@ -415,29 +414,9 @@ static int xy_partner_chunks(tqd_state *st, const void *psi_b, int gx, uint64_t 
 }
 
 // ---- forward execution ------------------------------------------------------
-// TMA tile loads (sweep.cuh TmaArgs): the request for one stage launch
-static SweepTma sweep_tma(const tqd_state *st, const SweepPlan &sp, bool bwd) {
-    SweepTma t;
-    memset(&t, 0, sizeof(t));
-    static const char *e = getenv("TQD_SWEEP_TMA");  // bit 0: forward sweeps, bit 1: adjoint sweeps
-    const int mask = st->opt_tma >= 0 ? st->opt_tma : (e ? atoi(e) : 0);
-    t.on = (mask >> (bwd ? 1 : 0)) & 1;
-    t.C = plan_cfg(st).c_low;
-    const std::vector<int> &lp = bwd ? sp.st_phys : sp.ld_phys;
-    int nrun = 0;
-    for (int i = 0; i < sp.k && i < 16; i++) {
-        t.ld_phys[i] = (uint8_t)lp[i];
-        if (lp[i] < t.C) nrun++;
-    }
-    if (sp.k < t.C + 3 || sp.k - t.C - 3 > 5 || nrun != t.C) t.on = 0;
-    t.bytes = all_bytes(st);
-    return t;
-}
-
 static int sweep_grid(tqd_state *st, const SweepPlan &sp, bool bwd, int n_ops, int n_slots, int n_cvals) {
     if (st->opt_grid > 0) return std::max(1, st->opt_grid / st->batch) * st->batch;
-    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots, (int)sp.lays.size(), n_cvals,
-                                    sweep_tma(st, sp, bwd).on != 0);
+    int per = sweep_max_ctas_per_sm(st->dbl, bwd, sp.k, sp.W, n_ops, n_slots, (int)sp.lays.size(), n_cvals);
     if (per < 1) per = 1;
     int64_t g = (int64_t)per * st->ctx->sms;
     const int64_t tiles = (int64_t)1 << (st->n_loc - sp.k);
@@ -540,8 +519,8 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
             }
             const int ev = ev_begin(st, bwd ? CAT_BWD : CAT_FWD);
             CUDA_TRY(st, launch_sweep(st->dbl, bwd, d_st + l.idx, d_kops, d_sl, st->psi, st->lam, d_grad, rank_hi(st),
-                                      sc, sweep_tma(st, sp, bwd), sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(),
-                                      l.n_cvals, l.grid, c->stream));
+                                      sc, sp.k, sp.W, l.n_ops, l.n_slots, (int)sp.lays.size(), l.n_cvals, l.grid,
+                                      c->stream));
             ev_end(st, ev);
             if (fuse) {
                 // every rank's stores into its peers' lambda-role buffers are complete
@@ -1098,9 +1077,6 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
-    case TQD_OPT_SWEEP_TMA:
-        if (v < 0 || v > 3) return fail(TQD_ERR_ARG, "sweep TMA mask must be in [0, 3]");
-        st->opt_tma = (int)v; return TQD_OK;
     case TQD_OPT_STAGING_BYTES:
         if (v < 0) return fail(TQD_ERR_ARG, "staging bytes must be >= 0");
         st->opt_stage = (size_t)v; return TQD_OK;

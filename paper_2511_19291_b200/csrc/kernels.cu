@@ -618,9 +618,8 @@ __global__ void debug_delay_kernel(uint32_t us) {
 // Launchers (host side, called from engine.cpp)
 #define TQD_DECL(NAME)                                                                                          \
     cudaError_t launch_sweep_##NAME(const DevStage *, const void *, const int32_t *, void *, void *, double *,       \
-                                    uint64_t, const ScatterInfo &, const SweepTma &, int, int, int, int, int, int, int, \
-                                    cudaStream_t);                                                                  \
-    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, bool tma);
+                                    uint64_t, const ScatterInfo &, int, int, int, int, int, int, int, cudaStream_t); \
+    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals);
 TQD_DECL(f32_fwd)
 TQD_DECL(f32_bwd)
 TQD_DECL(f64_fwd)
@@ -628,22 +627,22 @@ TQD_DECL(f64_bwd)
 #undef TQD_DECL
 
 cudaError_t launch_sweep(bool dbl, bool bwd, const DevStage *d_stage, const void *d_kops, const int32_t *d_slots,
-                         void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, const SweepTma &tma,
-                         int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
-#define TQD_ARGS d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, tma, k, W, n_ops, n_slots, nseg, n_cvals, grid, s
-    if (dbl) return bwd ? launch_sweep_f64_bwd(TQD_ARGS) : launch_sweep_f64_fwd(TQD_ARGS);
-    return bwd ? launch_sweep_f32_bwd(TQD_ARGS) : launch_sweep_f32_fwd(TQD_ARGS);
-#undef TQD_ARGS
-}
-
-int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, bool tma) {
+                         void *psi, void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W,
+                         int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
     if (dbl)
-        return bwd ? sweep_occupancy_f64_bwd(k, W, n_ops, n_slots, nseg, n_cvals, tma)
-                   : sweep_occupancy_f64_fwd(k, W, n_ops, n_slots, nseg, n_cvals, tma);
-    return bwd ? sweep_occupancy_f32_bwd(k, W, n_ops, n_slots, nseg, n_cvals, tma)
-               : sweep_occupancy_f32_fwd(k, W, n_ops, n_slots, nseg, n_cvals, tma);
+        return bwd ? launch_sweep_f64_bwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, n_cvals, grid, s)
+                   : launch_sweep_f64_fwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, n_cvals, grid, s);
+    return bwd ? launch_sweep_f32_bwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, n_cvals, grid, s)
+               : launch_sweep_f32_fwd(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots, nseg, n_cvals, grid, s);
 }
 
+int sweep_max_ctas_per_sm(bool dbl, bool bwd, int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
+    if (dbl)
+        return bwd ? sweep_occupancy_f64_bwd(k, W, n_ops, n_slots, nseg, n_cvals)
+                   : sweep_occupancy_f64_fwd(k, W, n_ops, n_slots, nseg, n_cvals);
+    return bwd ? sweep_occupancy_f32_bwd(k, W, n_ops, n_slots, nseg, n_cvals)
+               : sweep_occupancy_f32_fwd(k, W, n_ops, n_slots, nseg, n_cvals);
+}
 
 cudaError_t launch_small(bool dbl, bool bwd, const DevOp *d_ops, int n_ops, void *psi, void *lam, double *grad,
                          int n_loc, uint64_t rank_hi, int batch, cudaStream_t s) {

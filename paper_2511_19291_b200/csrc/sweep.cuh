@@ -21,8 +21,6 @@
 //
 // Instantiated once per (precision, direction) in sweep_*.cu.
 #pragma once
-#include <cuda.h>  // CUtensorMap (the maps are encoded through cudaGetDriverEntryPoint: no libcuda link)
-
 #include <atomic>
 
 #include "common.cuh"
@@ -39,13 +37,6 @@ constexpr int SWEEP_R = TQD_SWEEP_R;  // register bits: 2^R amplitudes (x2 state
 #endif
 #ifndef TQD_LB_MINB_F32_FWD
 #define TQD_LB_MINB_F32_FWD (SWEEP_R == 3 ? 2 : 3)
-#endif
-// TMA-staged variants (TP): shared memory holds a second tile per CTA
-#ifndef TQD_LB_MINB_TP_FWD
-#define TQD_LB_MINB_TP_FWD 2
-#endif
-#ifndef TQD_LB_MINB_TP_BWD
-#define TQD_LB_MINB_TP_BWD 1
 #endif
 constexpr int SWEEP_THREADS = TQD_LB_THREADS;
 constexpr int NR = 1 << SWEEP_R;
@@ -582,70 +573,16 @@ __device__ __forceinline__ double2 ldcs_c(const double2 *p) { return __ldcs(p); 
 __device__ __forceinline__ void stcs_c(float2 *p, float2 v) { __stcs(p, v); }
 __device__ __forceinline__ void stcs_c(double2 *p, double2 v) { __stcs(p, v); }
 
-// dynamic shared memory of the sweep kernel without the TMA staging buffer
-template <typename Real, bool BWD>
-__host__ __device__ inline size_t sweep_smem_base_bytes(int k, int n_ops, int n_slots, int threads, int nseg, int n_cvals) {
-    typedef typename DAcc<Real>::U DU;
-    return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
-           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t) +
-           (size_t)2 * threads * sizeof(uint64_t) + (size_t)n_cvals * threads * sizeof(DU);
-}
-
-// ---- TMA tile loads (TP = true) ------------------------------------------------
-// The next tile of the CTA is fetched into a shared-memory staging buffer by the
-// tensor-memory accelerator while the CTA computes the current one.  One 5-D
-// tensor map per state buffer, 8-byte elements: d0 = the 2^C contiguous
-// amplitudes of a 128-byte run (16 elements), d1 = an "offset" dimension of stride
-// 128 B spanning the whole buffer (any 128-byte-aligned tile base, incl. the batch
-// element), d2..d4 = tile bits C, C+1, C+2 (size 2, stride = their physical
-// position).  Box (16, 1, 2, 2, 2) = 1 KB = tile-local indices [0, 2^(C+3)) in
-// order; the tile's remaining bits C+3..k-1 are enumerated by the producer warp's
-// lanes (one box per lane and state), landing at staging offset lane * 1 KB, so the
-// staging buffer holds the tile in tile-local index order.
-struct TmaArgs {
-    CUtensorMap mp, ml;  // psi, lambda
-    int nbox;            // boxes per state = 2^(k - C - 3) <= 32
-    uint8_t epos[8];     // physical positions of the enumerated tile bits
-    int ne;
-    uint32_t sv[KMAX];   // staging byte offset of tile-local bit t (box order: physical run bits,
-                         // then the 3 box bits, then the enumerated bits)
-};
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t tx) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n TQD_MBW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra TQD_MBW;\n}\n" ::"r"(
-            smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_box(void *dst, const CUtensorMap *tm, int c1, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
-        "[%7];" ::"r"(smem_u32(dst)),
-        "l"(tm), "r"(0), "r"(c1), "r"(0), "r"(0), "r"(0), "r"(smem_u32(bar))
-        : "memory");
-}
-
 // ---- the fused sweep kernel: one CTA = 32 * 2^W threads, persistent over tiles.
 // DB: the stage has diagonal-block runs (a separate instantiation keeps their
 // shared arrays, precomputation and code out of the stages that have none)
-template <typename Real, bool BWD, bool DB, bool TP>
-__global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (TP ? (BWD ? TQD_LB_MINB_TP_BWD : TQD_LB_MINB_TP_FWD) : (BWD ? TQD_LB_MINB_F32_BWD : TQD_LB_MINB_F32_FWD)) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
+template <typename Real, bool BWD, bool DB>
+__global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_LB_MINB_F32_BWD : TQD_LB_MINB_F32_FWD) : 1) sweep_kernel(const DevStage *__restrict__ stg, const KOp<Real> *__restrict__ ops,
                                                     const int32_t *__restrict__ slot_param,
                                                     typename CT<Real>::C *__restrict__ psi,
                                                     typename CT<Real>::C *__restrict__ lam,
                                                     double *__restrict__ grad, uint64_t rank_hi,
-                                                    const __grid_constant__ ScatterInfo sc,
-                                                    const __grid_constant__ TmaArgs ta) {
+                                                    const __grid_constant__ ScatterInfo sc) {
     typedef typename CT<Real>::C C;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ DevStage S;
@@ -688,18 +625,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (TP ? (BWD 
     __shared__ DU s_uacc[DB ? DBLK_UCAP : 1];  // this tile's U values
     __shared__ uint8_t s_uk[DB ? DBLK_UCAP : 1], s_ut[DB ? DBLK_UCAP : 1];  // U value -> kop index, target (0xff = th)
     __shared__ C s_cis[DB ? 256 : 1];                                       // e^{i 2 pi k / 256} for cis_turn
-    // TMA staging of the next tile (after every other dynamic region, 128-byte aligned)
-    __shared__ __align__(8) uint64_t s_full, s_empty;
-    __shared__ uint32_t s_lrc[SWEEP_R];  // staging byte offsets of the register bits (layout 0)
-    C *s_stage = nullptr;
-    if constexpr (TP) {
-        const size_t off = sweep_smem_base_bytes<Real, BWD>(k, S.n_ops, S.n_slots, (int)blockDim.x, nseg,
-                                                            DB ? S.n_cvals : 0);
-        // 128-byte aligned SHARED address (the TMA destination), whatever the window's
-        // alignment of the dynamic region
-        const uint32_t b0 = smem_u32(smem_raw);
-        s_stage = reinterpret_cast<C *>(smem_raw + ((((size_t)b0 + off + 127) & ~(size_t)127) - b0));
-    }
     {
         const int4 *src = reinterpret_cast<const int4 *>(ops + S.op_base + (size_t)bidx * S.n_ops);
         int4 *dst = reinterpret_cast<int4 *>(s_ops);
@@ -717,14 +642,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (TP ? (BWD 
         }
         if (BWD)
             for (int i = threadIdx.x; i < S.n_slots * (int)blockDim.x; i += blockDim.x) tacc[i] = 0;
-        if (TP) {
-            if (threadIdx.x < SWEEP_R) s_lrc[threadIdx.x] = ta.sv[S.lay[0].reg[threadIdx.x]];
-            if (threadIdx.x == 0) {
-                mbar_init(&s_full, 1);
-                mbar_init(&s_empty, blockDim.x);
-                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            }
-        }
     }
     __syncthreads();
 
@@ -802,7 +719,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (TP ? (BWD 
     // load set is 2^(5-C) x 16 lines of 128 B per warp (C = the pinned low bits that
     // fill a line); lane j of the warp covers line i*32 + j with one prefetch per i
     int n_pf = 0;
-    if (!TP) {
+    {
         const DevLayout &L = S.lay[0];
         int C = 0;
         while (C < LANE_BITS && S.ld_phys[L.lane[C]] == C) C++;
@@ -837,56 +754,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (TP ? (BWD 
     const uint64_t tmask = deposit(~0ull) & (S.n_tiles > 1 ? ~0ull : 0ull);
     const uint64_t step = deposit((uint64_t)gsz);
     uint64_t base = deposit((uint64_t)gid);
-    // TMA producer = warp 0: lane j < nbox fetches box j (enumerated tile bits = j) of
-    // psi (and lambda) of the tile at `tb` into the staging buffer
-    uint64_t e_off = 0;  // this lane's enumerated-bit offset (elements)
-    if (TP)
-        for (int b = 0; b < ta.ne; b++)
-            if ((lane >> b) & 1) e_off |= 1ull << ta.epos[b];
-    auto tma_issue = [&](uint64_t tb) {
-        if (lane == 0) mbar_expect_tx(&s_full, (uint32_t)((BWD ? 2u : 1u) * (sizeof(C) << k)));
-        __syncwarp();
-        if (lane < ta.nbox) {
-            const int c1 = (int)(((bidx * bst + tb + e_off) * sizeof(C)) >> 7);
-            tma_load_box(reinterpret_cast<char *>(s_stage) + lane * 1024, &ta.mp, c1, &s_full);
-            if (BWD) tma_load_box(reinterpret_cast<char *>(s_stage + ((size_t)1 << k)) + lane * 1024, &ta.ml, c1, &s_full);
-        }
-    };
-    if (TP && warp == 0 && gid < S.n_tiles) tma_issue(base);
-    uint32_t tphase = 0;
     for (int64_t tile = gid; tile < S.n_tiles; tile += gsz, base = ((base | ~tmask) + step) & tmask) {
         const uint64_t basefull = base | rank_hi;
 
         C a[NR];
         C l[BWD ? NR : 1];
-        if (TP) {
-            // this tile is in the staging buffer (tile-local index order): read layout 0
-            mbar_wait(&s_full, tphase);
-            uint32_t o0 = 0;  // this thread's layout-0 lane / warp bits in staging order
-#pragma unroll
-            for (int i = 0; i < LANE_BITS; i++)
-                if ((lane >> i) & 1) o0 ^= ta.sv[S.lay[0].lane[i]];
-            for (int w = 0; w < W; w++)
-                if ((warp >> w) & 1) o0 ^= ta.sv[S.lay[0].warp[w]];
-            uint32_t c[SWEEP_R], o[NR];
-#pragma unroll
-            for (int b = 0; b < SWEEP_R; b++) c[b] = s_lrc[b];
-            o[0] = o0;
-#pragma unroll
-            for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] ^ c[ctz4(r)];
-#pragma unroll
-            for (int r = 0; r < NR; r++) {
-                a[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(s_stage) + o[r]);
-                if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(s_stage + ((size_t)1 << k)) + o[r]);
-            }
-            // staging free once every thread has read it: warp 0 then fetches the next tile
-            mbar_arrive(&s_empty);
-            if (warp == 0) {
-                mbar_wait(&s_empty, tphase);
-                if (tile + gsz < S.n_tiles) tma_issue(((base | ~tmask) + step) & tmask);
-            }
-            tphase ^= 1;
-        } else {
+        {
             // Gray-code walk over the register offsets: one 64-bit add per address
             const uint64_t b0 = base | ld_thr;
             uint64_t o[NR], c[SWEEP_R];
@@ -1048,10 +921,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (TP ? (BWD 
 }
 
 template <typename Real, bool BWD>
-static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int nseg, int n_cvals, bool tp) {
-    const size_t base = sweep_smem_base_bytes<Real, BWD>(k, n_ops, n_slots, threads, nseg, n_cvals);
-    if (!tp) return base;
-    return base + 128 + (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C);
+static size_t sweep_smem_bytes(int k, int n_ops, int n_slots, int threads, int nseg, int n_cvals) {
+    typedef typename DAcc<Real>::U DU;
+    return (size_t)(BWD ? 2 : 1) * ((size_t)1 << k) * sizeof(typename CT<Real>::C) + (size_t)n_ops * sizeof(KOp<Real>) +
+           (BWD ? (size_t)n_slots * threads * sizeof(Real) : 0) + (size_t)(3 * nseg - 2) * threads * sizeof(uint32_t) +
+           (size_t)2 * threads * sizeof(uint64_t) + (size_t)n_cvals * threads * sizeof(DU);
 }
 
 // The dynamic shared-memory cap is a per-function attribute shared by every host
@@ -1075,100 +949,41 @@ template <typename F> static cudaError_t raise_smem_cap_once(F fn, std::atomic<u
     return e;
 }
 
-template <typename Real, bool BWD, bool DB, bool TP> static std::atomic<uint64_t> &sweep_cap_flag() {
+template <typename Real, bool BWD, bool DB> static std::atomic<uint64_t> &sweep_cap_flag() {
     static std::atomic<uint64_t> f{0};
     return f;
 }
 
-typedef CUresult (*TmaEncodeFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static TmaEncodeFn tma_encode_fn() {
-    static TmaEncodeFn fn = [] {
-        void *f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess) {
-            cudaGetLastError();
-            return (TmaEncodeFn) nullptr;
-        }
-        return (TmaEncodeFn)f;
-    }();
-    return fn;
-}
-// the tensor map of one state buffer (see TmaArgs); false if it cannot be encoded
-static bool tma_make_map(CUtensorMap *tm, void *buf, const SweepTma &t, const int *boxp, size_t esz) {
-    TmaEncodeFn enc = tma_encode_fn();
-    if (!enc) return false;
-    const cuuint64_t dims[5] = {16, (cuuint64_t)(t.bytes >> 7), 2, 2, 2};
-    const cuuint64_t strides[4] = {128, (cuuint64_t)esz << boxp[0], (cuuint64_t)esz << boxp[1], (cuuint64_t)esz << boxp[2]};
-    const cuuint32_t box[5] = {16, 1, 2, 2, 2};
-    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 // n_cvals < 0: the stage has no diagonal-block runs (plain instantiation)
-template <typename Real, bool BWD, bool DB, bool TP>
+template <typename Real, bool BWD, bool DB>
 cudaError_t launch_sweep_t(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                           double *grad, uint64_t rank_hi, const ScatterInfo &sc, const TmaArgs &ta, int k, int W,
-                           int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
+                           double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops, int n_slots,
+                           int nseg, int n_cvals, int grid, cudaStream_t s) {
     typedef typename CT<Real>::C C;
-    auto fn = sweep_kernel<Real, BWD, DB, TP>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, DB ? n_cvals : 0, TP);
-    cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD, DB, TP>());
+    auto fn = sweep_kernel<Real, BWD, DB>;
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, DB ? n_cvals : 0);
+    cudaError_t e = raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD, DB>());
     if (e != cudaSuccess) return e;
-    fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi, sc, ta);
+    fn<<<grid, 32 << W, smem, s>>>(d_stage, (const KOp<Real> *)d_ops, d_slots, (C *)psi, (C *)lam, grad, rank_hi, sc);
     return cudaGetLastError();
-}
-
-// TMA loads usable for this stage: physical bits 0..C-1 are tile bits (one 128-byte
-// run) and the tile has 3..8 more bits (1..32 boxes per state).  Fills the staging
-// order: run bits by physical position, then the 3 box bits and the enumerated
-// bits in tile-local order.
-static bool sweep_tma_plan(const SweepTma &t, int k, size_t esz, TmaArgs &ta, int *boxp) {
-    if (!t.on || k < t.C + 3 || k - t.C - 3 > 5) return false;
-    int nrun = 0, nb = 0;
-    ta.ne = 0;
-    for (int i = 0; i < k; i++) {
-        const int p = t.ld_phys[i];
-        if (p < t.C) {
-            ta.sv[i] = (uint32_t)(esz << p);
-            nrun++;
-        } else if (nb < 3) {
-            ta.sv[i] = 128u << nb;
-            boxp[nb++] = p;
-        } else {
-            ta.sv[i] = 1024u << ta.ne;
-            ta.epos[ta.ne++] = (uint8_t)p;
-        }
-    }
-    ta.nbox = 1 << ta.ne;
-    return nrun == t.C && nb == 3;
 }
 
 template <typename Real, bool BWD>
 cudaError_t launch_sweep_impl(const DevStage *d_stage, const void *d_ops, const int32_t *d_slots, void *psi, void *lam,
-                              double *grad, uint64_t rank_hi, const ScatterInfo &sc, const SweepTma &tma, int k, int W,
-                              int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
-    TmaArgs ta;
-    memset(&ta, 0, sizeof(ta));
-    const size_t esz = sizeof(typename CT<Real>::C);
-    int boxp[3];
-    const bool tp = sweep_tma_plan(tma, k, esz, ta, boxp) && tma_make_map(&ta.mp, psi, tma, boxp, esz) &&
-                    (!BWD || tma_make_map(&ta.ml, lam, tma, boxp, esz));
-#define TQD_L(DBV, TPV) launch_sweep_t<Real, BWD, DBV, TPV>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, ta, k, W, \
-                                                          n_ops, n_slots, nseg, DBV ? n_cvals : 0, grid, s)
-    if (n_cvals >= 0) return tp ? TQD_L(true, true) : TQD_L(true, false);
-    return tp ? TQD_L(false, true) : TQD_L(false, false);
-#undef TQD_L
+                              double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, int n_ops,
+                              int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {
+    if (n_cvals >= 0)
+        return launch_sweep_t<Real, BWD, true>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops,
+                                               n_slots, nseg, n_cvals, grid, s);
+    return launch_sweep_t<Real, BWD, false>(d_stage, d_ops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops, n_slots,
+                                            nseg, 0, grid, s);
 }
 
-template <typename Real, bool BWD, bool DB, bool TP>
+template <typename Real, bool BWD, bool DB>
 int sweep_occupancy_t(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
-    auto fn = sweep_kernel<Real, BWD, DB, TP>;
-    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, DB ? n_cvals : 0, TP);
-    if (raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD, DB, TP>()) != cudaSuccess) {
+    auto fn = sweep_kernel<Real, BWD, DB>;
+    const size_t smem = sweep_smem_bytes<Real, BWD>(k, n_ops, n_slots, 32 << W, nseg, DB ? n_cvals : 0);
+    if (raise_smem_cap_once(fn, sweep_cap_flag<Real, BWD, DB>()) != cudaSuccess) {
         cudaGetLastError();
         return 1;
     }
@@ -1181,12 +996,9 @@ int sweep_occupancy_t(int k, int W, int n_ops, int n_slots, int nseg, int n_cval
 }
 
 template <typename Real, bool BWD>
-int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, bool tma) {
-    if (n_cvals >= 0)
-        return tma ? sweep_occupancy_t<Real, BWD, true, true>(k, W, n_ops, n_slots, nseg, n_cvals)
-                   : sweep_occupancy_t<Real, BWD, true, false>(k, W, n_ops, n_slots, nseg, n_cvals);
-    return tma ? sweep_occupancy_t<Real, BWD, false, true>(k, W, n_ops, n_slots, nseg, 0)
-               : sweep_occupancy_t<Real, BWD, false, false>(k, W, n_ops, n_slots, nseg, 0);
+int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {
+    return n_cvals >= 0 ? sweep_occupancy_t<Real, BWD, true>(k, W, n_ops, n_slots, nseg, n_cvals)
+                        : sweep_occupancy_t<Real, BWD, false>(k, W, n_ops, n_slots, nseg, 0);
 }
 
 }  // namespace tqd
@@ -1194,13 +1006,12 @@ int sweep_occupancy_impl(int k, int W, int n_ops, int n_slots, int nseg, int n_c
 #define TQD_INSTANTIATE_SWEEP(REAL, BWD, NAME)                                                                    \
     namespace tqd {                                                                                             \
     cudaError_t launch_sweep_##NAME(const DevStage *d_stage, const void *d_kops, const int32_t *d_slots, void *psi,  \
-                                    void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc,             \
-                                    const SweepTma &tma, int k, int W, int n_ops, int n_slots, int nseg,          \
-                                    int n_cvals, int grid, cudaStream_t s) {                                      \
-        return launch_sweep_impl<REAL, BWD>(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, tma, k, W,      \
-                                            n_ops, n_slots, nseg, n_cvals, grid, s);                              \
+                                    void *lam, double *grad, uint64_t rank_hi, const ScatterInfo &sc, int k, int W, \
+                                    int n_ops, int n_slots, int nseg, int n_cvals, int grid, cudaStream_t s) {    \
+        return launch_sweep_impl<REAL, BWD>(d_stage, d_kops, d_slots, psi, lam, grad, rank_hi, sc, k, W, n_ops,    \
+                                            n_slots, nseg, n_cvals, grid, s);                                   \
     }                                                                                                           \
-    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals, bool tma) {          \
-        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots, nseg, n_cvals, tma);                        \
+    int sweep_occupancy_##NAME(int k, int W, int n_ops, int n_slots, int nseg, int n_cvals) {                    \
+        return sweep_occupancy_impl<REAL, BWD>(k, W, n_ops, n_slots, nseg, n_cvals);                             \
     }                                                                                                           \
     }

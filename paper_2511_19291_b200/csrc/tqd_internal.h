@@ -229,16 +229,6 @@ struct ScatterInfo {
     uint64_t dst_lam[SCATTER_MAX_RANKS];  // (adjoint) destination shard of lambda
 };
 
-// Sweep tile loads by the tensor-memory accelerator (TMA, cp.async.bulk.tensor):
-// the host asks for them per launch; the launcher builds the tensor maps of psi /
-// lambda from the stage's load positions.  on = 0: per-thread loads.
-struct SweepTma {
-    int on;
-    int C;                // pinned low tile bits (= physical bits 0..C-1): 128-byte runs
-    uint8_t ld_phys[16];  // physical position of tile-local bit t at load
-    uint64_t bytes;       // bytes of the whole buffer (all batch elements' shards)
-};
-
 // Z-string observable in PHYSICAL masks (full index incl. rank bits)
 // lambda-init form: h(b) = cst - 2 sum_p w[p] bit_p(b) + sum_t c_t (-1)^{popc(b & z_t)}
 // (single-qubit Z terms folded into per-position weights, the rest listed)
