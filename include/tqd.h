@@ -112,10 +112,14 @@ typedef enum {
                                * After tqd_expval the absorbed gates stay pending: a later
                                * readback / sample / non-Z observable applies them.
                                * 0: apply every gate.                                      */
-    TQD_OPT_STAGING_BYTES = 7  /* world > 1: bytes of the exchange staging (send + receive
+    TQD_OPT_STAGING_BYTES = 7, /* world > 1: bytes of the exchange staging (send + receive
                                * halves; remap blocks and X/Y partner shards move through it
                                * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
                                * force a few KiB so the chunk loop iterates.               */
+    TQD_OPT_CIRCUIT_MAX = 8    /* single-GPU states of <= this many qubits (0..12; default 10)
+                               * run tqd_adjoint_grad with Z-string terms as ONE kernel launch:
+                               * forward gates, lambda = H psi and the reverse sweep in one
+                               * CTA's shared memory per state (0 = staged sweeps only)     */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.

@@ -49,6 +49,9 @@ cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
 cudaError_t launch_remap_block(bool dbl, void *shard, void *stage, uint64_t e0, uint64_t cnt, uint64_t bdep, uint64_t rest,
                               bool unpack, cudaStream_t s);
 cudaError_t launch_debug_delay(uint32_t us, cudaStream_t s);
+cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
+                           const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
+                           cudaStream_t s);
 }  // namespace tqd
 
 using namespace tqd;
@@ -94,6 +97,14 @@ struct tqd_state {
     // options
     int opt_k = 12, opt_small = 8, opt_profile = 0, opt_grid = 0, opt_graph = 0, opt_fused = 1, opt_absorb = 1;
     size_t opt_stage = 0;  // TQD_OPT_STAGING_BYTES (0 = default)
+    int opt_circuit = 10;  // TQD_OPT_CIRCUIT_MAX: single-launch fwd+grad up to this many local qubits
+    // single-launch circuit path: forward + backward op lists and Z terms on the device
+    void *circ_dev = nullptr;
+    size_t circ_cap = 0;
+    uint64_t circ_key = 0;
+    int circ_nf = 0, circ_nb = 0;
+    size_t circ_off_b = 0, circ_off_z = 0;
+    std::vector<int> circ_pos;  // qubit map after the cached circuit
     // fused forward sweep -> remap (peer memory): every rank's two shard allocations
     // (first psi, first lambda), shared once; the forward stores into the owners'
     // lambda-role buffer (idle until the adjoint seed) and the roles swap.  The
@@ -1051,6 +1062,7 @@ int tqd_state_free(tqd_state *st) {
     if (st->g_bwd) cudaGraphExecDestroy(st->g_bwd);
     if (st->d_red) cudaFree(st->d_red);
     if (st->d_xy) cudaFree(st->d_xy);
+    if (st->circ_dev) cudaFree(st->circ_dev);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
     delete st;
     return TQD_OK;
@@ -1077,6 +1089,9 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_CIRCUIT_MAX:
+        if (v < 0 || v > 12) return fail(TQD_ERR_ARG, "circuit_max must be in [0, 12]");
+        st->opt_circuit = (int)v; return TQD_OK;
     case TQD_OPT_STAGING_BYTES:
         if (v < 0) return fail(TQD_ERR_ARG, "staging bytes must be >= 0");
         st->opt_stage = (size_t)v; return TQD_OK;
@@ -1375,6 +1390,121 @@ static size_t absorb_tail(const std::vector<GateRec> &gates, size_t executed, st
     return i;
 }
 
+// Z-string seed of one batch element in physical masks (lambda-init form, ZTerms)
+static void build_zterms(const tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff,
+                         const std::vector<double> &sabs, size_t cb, ZTerms &zt) {
+    memset(&zt, 0, sizeof(zt));
+    for (int t = 0; t < T; t++) {
+        if (x && x[t]) continue;  // X / Y strings: lambda_add_xy
+        const uint64_t zp = phys_mask(st, z[t]);
+        const double ct = (coeff ? coeff[cb + t] : 1.0) * sabs[t];
+        if (zp == 0) {  // identity (e.g. Z_q Z_q after absorption)
+            zt.cst += ct;
+        } else if (__builtin_popcountll(zp) == 1) {  // c (1 - 2 b_p)
+            zt.cst += ct;
+            zt.w[__builtin_ctzll(zp)] += ct;
+        } else {
+            zt.z[zt.T] = zp;
+            zt.c[zt.T] = ct;
+            zt.T++;
+        }
+    }
+}
+
+// The whole circuit in ONE launch (circuit_kernel): forward gates, lambda = H psi and
+// the reverse sweep with gradients, one CTA per batch element, for single-GPU states
+// of <= opt_circuit qubits (BASELINE.json configs[0]: 10 qubits complex128).  The op
+// lists are cached by tape version (tqd_state_rewind replays upload nothing).
+// Returns 1 when the state does not qualify (the caller runs the staged path).
+static int adjoint_circuit(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff,
+                           const std::vector<double> &sabs, size_t end, double *out_value, double *out_grad, int n_grad) {
+    tqd_ctx *c = st->ctx;
+    if (c->world != 1 || st->executed != 0 || st->n_loc > st->opt_circuit) return 1;
+    for (int t = 0; t < T && x; t++)
+        if (x[t]) return 1;
+    const size_t smem = (size_t)2 * shard_bytes(st);
+    if (smem > 200 * 1024) return 1;
+    const uint64_t key = (st->tape_version * 0x9E3779B97F4A7C15ull) ^ (uint64_t)(st->gates.size() - end) ^
+                         ((uint64_t)T << 40);
+    std::vector<ZTerms> zts(st->batch);
+    if (st->circ_key != key || !st->circ_dev) {
+        std::vector<int> pending;
+        for (size_t i = 0; i < end; i++) pending.push_back((int)i);
+        PlanConfig cfg = plan_cfg(st);
+        cfg.small_max = st->n_loc;
+        std::vector<int> pos = st->pos;
+        std::vector<Stage> stages;
+        std::string err;
+        int rc = plan_circuit(st->gates, pending, pos, cfg, stages, err);
+        if (rc) return fail(rc, err);
+        for (const Stage &s : stages)
+            if (s.type != ST_SMALL) return 1;
+        int skip_below = (int)st->gates.size();
+        for (size_t i = 0; i < st->gates.size(); i++)
+            if (st->gates[i].ngen) { skip_below = (int)i; break; }
+        std::vector<DevOp> fops, bops;
+        std::vector<GateRec> tmp;
+        for (int b = 0; b < st->batch; b++) {
+            const std::vector<GateRec> &gb = gates_for(st, b, tmp);
+            for (const Stage &s : stages) encode_small(s.sm, gb, false, fops, 0);
+            for (int i = (int)stages.size() - 1; i >= 0; i--) encode_small(stages[i].sm, gb, true, bops, skip_below);
+        }
+        st->pos = pos;  // lambda-init sees the final qubit map
+        st->circ_nf = (int)fops.size() / st->batch;
+        st->circ_nb = (int)bops.size() / st->batch;
+        st->circ_off_b = ((fops.size() * sizeof(DevOp)) + 255) & ~(size_t)255;
+        st->circ_off_z = (st->circ_off_b + bops.size() * sizeof(DevOp) + 255) & ~(size_t)255;
+        const size_t total = st->circ_off_z + zts.size() * sizeof(ZTerms);
+        if (total > st->circ_cap) {
+            if (st->circ_dev) { CUDA_TRY(st, cudaStreamSynchronize(c->stream)); cudaFree(st->circ_dev); }
+            st->circ_dev = nullptr;
+            st->circ_cap = 0;
+            if (cudaMalloc(&st->circ_dev, total) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(TQD_ERR_OOM, "cannot allocate the circuit op lists");
+            }
+            st->circ_cap = total;
+        }
+        CUDA_TRY(st, cudaMemcpyAsync(st->circ_dev, fops.data(), fops.size() * sizeof(DevOp), cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(st, cudaMemcpyAsync((char *)st->circ_dev + st->circ_off_b, bops.data(), bops.size() * sizeof(DevOp),
+                                     cudaMemcpyHostToDevice, c->stream));
+        st->met.h2d_bytes += (fops.size() + bops.size()) * sizeof(DevOp);
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+        st->circ_key = key;
+        st->circ_pos = pos;
+    } else {
+        st->pos = st->circ_pos;
+    }
+    for (int b = 0; b < st->batch; b++) build_zterms(st, T, x, z, coeff, sabs, (size_t)b * T, zts[b]);
+    ZTerms *d_z = (ZTerms *)((char *)st->circ_dev + st->circ_off_z);
+    CUDA_TRY(st, cudaMemcpyAsync(d_z, zts.data(), zts.size() * sizeof(ZTerms), cudaMemcpyHostToDevice, c->stream));
+    st->met.h2d_bytes += zts.size() * sizeof(ZTerms);
+    int rc = ensure_red(st, (size_t)n_grad + 1);
+    if (rc) return rc;
+    CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, (n_grad + 1) * sizeof(double), c->stream));
+    const DevOp *d_f = (const DevOp *)st->circ_dev;
+    const DevOp *d_b = (const DevOp *)((char *)st->circ_dev + st->circ_off_b);
+    const int ev = ev_begin(st, CAT_BWD);
+    CUDA_TRY(st, launch_circuit(st->dbl, d_f, st->circ_nf, d_b, st->circ_nb, st->psi, d_z, st->d_red, st->d_red + 1,
+                                st->n_loc, rank_hi(st), st->batch, c->stream));
+    ev_end(st, ev);
+    st->met.kernel_launches++;
+    st->met.fwd_sweeps++;
+    st->met.bwd_sweeps++;
+    st->met.gates_applied += end * st->batch;
+    st->met.gates_unapplied += end * st->batch;
+    st->met.hbm_bytes += all_bytes(st);
+    std::vector<double> h(n_grad + 1);
+    CUDA_TRY(st, cudaMemcpyAsync(h.data(), st->d_red, (n_grad + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    st->met.d2h_bytes += (n_grad + 1) * sizeof(double);
+    *out_value = h[0];
+    for (int p = 0; p < n_grad; p++) out_grad[p] = h[p + 1];
+    st->executed = st->gates.size();
+    st->consumed = true;
+    return ev_collect(st);
+}
+
 int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z, const double *coeff, double *out_value,
                      double *out_grad, int n_grad) {
     int rc = check_live(st);
@@ -1398,6 +1528,10 @@ int tqd_adjoint_grad(tqd_state *st, int T, const uint64_t *x, const uint64_t *z,
         z = zabs.data();
     }
     st->met.gates_absorbed += st->gates.size() - end;
+    {
+        const int crc = adjoint_circuit(st, T, x, z, coeff, sabs, end, out_value, out_grad, n_grad);
+        if (crc <= 0) return crc;  // 1: the staged path below
+    }
     // lambda first: the forward's remaps can then be fused into its sweeps (they
     // store into the owners' still idle lambda buffers)
     rc = ensure_lambda(st);

@@ -145,6 +145,401 @@ __global__ void __launch_bounds__(512) small_kernel(const DevOp *__restrict__ op
 }
 
 // ---------------------------------------------------------------------------
+// Whole circuit in ONE launch for small states (PAPER.md:291-309 Listing scale;
+// BASELINE.json configs[0]): one CTA per state holds psi and lambda in shared
+// memory and runs the forward gates, the adjoint seed lambda = H psi for Z strings
+// (E = <psi|H|psi>), and the reverse sweep with its gradients,
+// gate by gate with one barrier per gate.  Gradient partials: warp shuffle sums,
+// one fp64 atomic per warp and generator.  Ops as small_kernel (physical positions).
+template <typename Real>
+__device__ __forceinline__ void circ_apply(const DevOp &op, typename CT<Real>::C *A, typename CT<Real>::C *L, uint64_t N,
+                                           uint64_t rank_hi, bool two) {
+    typedef typename CT<Real>::C C;
+    auto bit = [&](BitRef b, uint64_t idx) -> int { return (int)(((idx | rank_hi) >> b.idx) & 1ull); };
+    const int kind = op.kind;
+    switch (kind) {
+    case OP_U1: case OP_R1: case OP_P1: {
+        const int p = op.t0;
+        C m00, m01, m10, m11;
+        if (kind == OP_U1) { m00 = ldc<C>(op.m, 0); m01 = ldc<C>(op.m, 1); m10 = ldc<C>(op.m, 2); m11 = ldc<C>(op.m, 3); }
+        else if (kind == OP_R1) {
+            m00 = mk<C>((Real)op.m[0], 0); m01 = mk<C>((Real)op.m[1], 0);
+            m10 = mk<C>((Real)op.m[2], 0); m11 = mk<C>((Real)op.m[3], 0);
+        } else { m00 = mk<C>(0, 0); m01 = ldc<C>(op.m, 0); m10 = ldc<C>(op.m, 1); m11 = mk<C>(0, 0); }
+        for (uint64_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+            const uint64_t i0 = ins0(i, p), i1 = i0 | (1ull << p);
+            if (op.ctrl.kind != BK_NONE && !bit(op.ctrl, i0)) continue;
+            const C x0 = A[i0], x1 = A[i1];
+            A[i0] = cmul2(m00, x0, m01, x1);
+            A[i1] = cmul2(m10, x0, m11, x1);
+            if (two) {
+                const C y0 = L[i0], y1 = L[i1];
+                L[i0] = cmul2(m00, y0, m01, y1);
+                L[i1] = cmul2(m10, y0, m11, y1);
+            }
+        }
+        break;
+    }
+    case OP_D1: {
+        const C d0 = ldc<C>(op.m, 0), d1 = ldc<C>(op.m, 1);
+        for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+            const C d = bit(op.b0, i) ? d1 : d0;
+            A[i] = cmul(d, A[i]);
+            if (two) L[i] = cmul(d, L[i]);
+        }
+        break;
+    }
+    case OP_D2: {
+        for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+            const C d = ldc<C>(op.m, 2 * bit(op.b0, i) + bit(op.b1, i));
+            A[i] = cmul(d, A[i]);
+            if (two) L[i] = cmul(d, L[i]);
+        }
+        break;
+    }
+    case OP_U2: {
+        const int p0 = op.t0, p1 = op.t1;
+        const int lo = p0 < p1 ? p0 : p1, hi = p0 < p1 ? p1 : p0;
+        for (uint64_t i = threadIdx.x; i < N / 4; i += blockDim.x) {
+            const uint64_t b = ins0(ins0(i, lo), hi);
+            const uint64_t idx[4] = {b, b | (1ull << p1), b | (1ull << p0), b | (1ull << p0) | (1ull << p1)};
+            for (int pass = 0; pass < (two ? 2 : 1); pass++) {
+                C *X = pass ? L : A;
+                C v[4];
+                for (int q = 0; q < 4; q++) v[q] = X[idx[q]];
+                for (int r = 0; r < 4; r++) {
+                    C acc = mk<C>(0, 0);
+                    for (int q = 0; q < 4; q++) {
+                        const C pr = cmul(ldc<C>(op.m, 4 * r + q), v[q]);
+                        acc.x += pr.x;
+                        acc.y += pr.y;
+                    }
+                    X[idx[r]] = acc;
+                }
+            }
+        }
+        break;
+    }
+    default: break;
+    }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(512) circuit_kernel(const DevOp *__restrict__ fops, int n_f,
+                                                      const DevOp *__restrict__ bops, int n_b,
+                                                      const typename CT<Real>::C *__restrict__ psi,
+                                                      const ZTerms *__restrict__ zts, double *__restrict__ eval,
+                                                      double *__restrict__ grad, int n_loc, uint64_t rank_hi,
+                                                      int ops_smem) {
+    typedef typename CT<Real>::C C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[32];
+    const uint64_t N = 1ull << n_loc;
+    fops += (size_t)blockIdx.x * n_f;
+    bops += (size_t)blockIdx.x * n_b;
+    psi += (size_t)blockIdx.x * N;
+    const ZTerms &zt = zts[blockIdx.x];
+    C *A = reinterpret_cast<C *>(smem_raw);
+    C *L = A + N;
+    const int lane = threadIdx.x & 31;
+    for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) A[i] = psi[i];
+    if (ops_smem) {
+        // the op lists into shared memory (a dependent global load per gate field would
+        // cost a round trip per gate): after psi and lambda, 16-byte aligned
+        DevOp *sf = reinterpret_cast<DevOp *>(L + N);
+        DevOp *sb = sf + n_f;
+        const int4 *src = reinterpret_cast<const int4 *>(fops);
+        int4 *dst = reinterpret_cast<int4 *>(sf);
+        for (int i = threadIdx.x; i < n_f * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
+        src = reinterpret_cast<const int4 *>(bops);
+        dst = reinterpret_cast<int4 *>(sb);
+        for (int i = threadIdx.x; i < n_b * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
+        fops = sf;
+        bops = sb;
+    }
+    __syncthreads();
+    // forward
+    for (int oi = 0; oi < n_f; oi++) {
+        circ_apply<Real>(fops[oi], A, L, N, rank_hi, false);
+        __syncthreads();
+    }
+    // lambda = H psi, H = cst - 2 sum_p w_p b_p + sum_t c_t (-1)^{popc(b & z_t)}; E = <psi|H|psi>
+    double e = 0.0;
+    for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const uint64_t b = i | rank_hi;
+        double h = zt.cst;
+        for (int p = 0; p < n_loc; p++)
+            if ((b >> p) & 1ull) h -= 2.0 * zt.w[p];
+        for (int t = 0; t < zt.T; t++) h += (__popcll(b & zt.z[t]) & 1) ? -zt.c[t] : zt.c[t];
+        const C a = A[i];
+        L[i] = mk<C>((Real)h * a.x, (Real)h * a.y);
+        e += h * ((double)a.x * a.x + (double)a.y * a.y);
+    }
+    e = block_sum<double>(e, red);
+    if (threadIdx.x == 0) atomicAdd(eval, e);
+    __syncthreads();
+    // reverse sweep: gradients on the post-gate states, then psi, lambda <- U^dag
+    auto bit = [&](BitRef bb, uint64_t idx) -> int { return (int)(((idx | rank_hi) >> bb.idx) & 1ull); };
+    for (int oi = 0; oi < n_b; oi++) {
+        const DevOp &op = bops[oi];
+        for (int gi = 0; gi < op.ngen; gi++) {
+            Real part = 0;
+            const int gk = op.gkind[gi];
+            if (op.kind == OP_D1) {
+                for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+                    const Real v = im_cj(L[i], A[i]);
+                    part += bit(op.b0, i) ? -v : v;
+                }
+            } else {
+                const int p = op.t0;
+                const C g00 = ldc<C>(op.g[gi], 0), g01 = ldc<C>(op.g[gi], 1), g10 = ldc<C>(op.g[gi], 2),
+                        g11 = ldc<C>(op.g[gi], 3);
+                for (uint64_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                    const uint64_t i0 = ins0(i, p), i1 = i0 | (1ull << p);
+                    const C a0 = A[i0], a1 = A[i1], l0 = L[i0], l1 = L[i1];
+                    if (gk == GEN_Y) part += re_cj(l1, a0) - re_cj(l0, a1);
+                    else if (gk == GEN_X) part += im_cj(l0, a1) + im_cj(l1, a0);
+                    else part += 2 * (re_cj(l0, cmul2(g00, a0, g01, a1)) + re_cj(l1, cmul2(g10, a0, g11, a1)));
+                }
+            }
+            const double w = warp_sum<double>((double)part);
+            if (lane == 0 && w != 0.0) atomicAdd(&grad[op.slot[gi]], w);
+        }
+        // the un-apply reads and writes only the pairs this thread just read
+        circ_apply<Real>(op, A, L, N, rank_hi, true);
+        __syncthreads();
+    }
+}
+
+// Register-resident variant for 8 <= n_loc <= 11 (the cfg-1 latency case): thread t
+// of N/8 holds the 8 amplitudes idx = r | lane << 3 | warp << 8 (r = 0..7) of psi (and
+// lambda) in registers.  A 1-qubit gate on physical bit p is register-local (p < 3),
+// a lane shuffle with lane ^ 2^(p-3) (p < 8) or a shared-memory exchange with the
+// partner warp (p >= 8; double-buffered, one barrier); diagonal gates are local.  No
+// barrier between gates that do not cross warps.  Gradients use the post-gate pair
+// values of the same exchange.  Other ops (4x4 MAT2) fall back to
+// a shared-memory pass (circ_apply).
+template <typename C> __device__ __forceinline__ C shfl_c(C v, int m) {
+    return mk<C>(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+}
+template <typename C> __device__ __forceinline__ C cfma2(C a, C x, C b, C y) { return cmul2(a, x, b, y); }
+
+template <typename Real, int RB>
+__global__ void __launch_bounds__(512) circuit_reg_kernel(const DevOp *__restrict__ fops, int n_f,
+                                                          const DevOp *__restrict__ bops, int n_b,
+                                                          const typename CT<Real>::C *__restrict__ psi,
+                                                          const ZTerms *__restrict__ zts, double *__restrict__ eval,
+                                                          double *__restrict__ grad, int n_loc) {
+    typedef typename CT<Real>::C C;
+    constexpr int NRR = 1 << RB;  // amplitudes per thread and state
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[32];
+    const uint64_t N = 1ull << n_loc;
+    fops += (size_t)blockIdx.x * n_f;
+    bops += (size_t)blockIdx.x * n_b;
+    psi += (size_t)blockIdx.x * N;
+    const ZTerms &zt = zts[blockIdx.x];
+    // shared: 2 exchange buffers of psi + lambda (4 N), then the op lists
+    C *X0 = reinterpret_cast<C *>(smem_raw);
+    DevOp *sf = reinterpret_cast<DevOp *>(X0 + 4 * N);
+    DevOp *sb = sf + n_f;
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(fops);
+        int4 *dst = reinterpret_cast<int4 *>(sf);
+        for (int i = threadIdx.x; i < n_f * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
+        src = reinterpret_cast<const int4 *>(bops);
+        dst = reinterpret_cast<int4 *>(sb);
+        for (int i = threadIdx.x; i < n_b * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t tbase = ((uint32_t)lane << RB) | ((uint32_t)warp << (RB + 5));
+    C a[NRR], l[NRR];
+#pragma unroll
+    for (int r = 0; r < NRR; r++) a[r] = psi[tbase | r];
+    __syncthreads();
+    int xb = 0;  // exchange buffer parity
+    auto cbit = [&](BitRef b, uint32_t idx) -> bool { return b.kind == BK_NONE || ((idx >> b.idx) & 1u); };
+
+    // one 1-qubit op (U1 / R1 / P1, optional control) on psi (and lambda when two);
+    // gradient partials of its generators first when grads
+    auto one_qubit = [&](const DevOp &op, bool two, bool grads) {
+        const int p = op.t0;
+        C m[4];
+        if (op.kind == OP_U1) { m[0] = ldc<C>(op.m, 0); m[1] = ldc<C>(op.m, 1); m[2] = ldc<C>(op.m, 2); m[3] = ldc<C>(op.m, 3); }
+        else if (op.kind == OP_R1) {
+            m[0] = mk<C>((Real)op.m[0], 0); m[1] = mk<C>((Real)op.m[1], 0);
+            m[2] = mk<C>((Real)op.m[2], 0); m[3] = mk<C>((Real)op.m[3], 0);
+        } else { m[0] = mk<C>(0, 0); m[1] = ldc<C>(op.m, 0); m[2] = ldc<C>(op.m, 1); m[3] = mk<C>(0, 0); }
+        // partner amplitudes: the pair member with bit p flipped
+        C ao[NRR], lo[NRR];
+        if (p < RB) {  // compile-time register indices (a runtime index would put a[] in local memory)
+#define TQD_RX(F)                                                            \
+    _Pragma("unroll") for (int r = 0; r < NRR; r++) {                         \
+        ao[r] = a[r ^ (F)];                                                   \
+        if (two) lo[r] = l[r ^ (F)];                                          \
+    }
+            if (RB == 1 || p == 0) { TQD_RX(1) } else { TQD_RX(2 % NRR) }
+#undef TQD_RX
+        } else if (p < RB + 5) {
+            const int mk_ = 1 << (p - RB);
+#pragma unroll
+            for (int r = 0; r < NRR; r++) { ao[r] = shfl_c(a[r], mk_); if (two) lo[r] = shfl_c(l[r], mk_); }
+        } else {
+            C *XA = X0 + (size_t)xb * 2 * N, *XL = XA + N;
+            xb ^= 1;
+#pragma unroll
+            for (int r = 0; r < NRR; r++) { XA[tbase | r] = a[r]; if (two) XL[tbase | r] = l[r]; }
+            __syncthreads();
+            const uint32_t f = 1u << p;
+#pragma unroll
+            for (int r = 0; r < NRR; r++) { ao[r] = XA[(tbase | r) ^ f]; if (two) lo[r] = XL[(tbase | r) ^ f]; }
+        }
+        if (grads) {
+            for (int gi = 0; gi < op.ngen; gi++) {
+                const int gk = op.gkind[gi];
+                Real part = 0;
+#pragma unroll
+                for (int r = 0; r < NRR; r++) {
+                    const uint32_t idx = tbase | r;
+                    if ((idx >> p) & 1u) continue;  // each pair once, from its bit-0 member
+                    const C a0 = a[r], a1 = ao[r], l0 = l[r], l1 = lo[r];
+                    if (gk == GEN_Y) part += re_cj(l1, a0) - re_cj(l0, a1);
+                    else if (gk == GEN_X) part += im_cj(l0, a1) + im_cj(l1, a0);
+                    else {
+                        const C g00 = ldc<C>(op.g[gi], 0), g01 = ldc<C>(op.g[gi], 1), g10 = ldc<C>(op.g[gi], 2),
+                                g11 = ldc<C>(op.g[gi], 3);
+                        part += 2 * (re_cj(l0, cmul2(g00, a0, g01, a1)) + re_cj(l1, cmul2(g10, a0, g11, a1)));
+                    }
+                }
+                const double w = warp_sum<double>((double)part);
+                if (lane == 0 && w != 0.0) atomicAdd(&grad[op.slot[gi]], w);
+            }
+        }
+        // y_bit = m[bit][bit] x_mine + m[bit][!bit] x_other
+        if (p >= RB) {  // bit p is the same for all of this thread's amplitudes
+            const bool hi = (tbase >> p) & 1u;
+            const C cm = hi ? m[3] : m[0], co = hi ? m[2] : m[1];
+#pragma unroll
+            for (int r = 0; r < NRR; r++) {
+                if (!cbit(op.ctrl, tbase | r)) continue;
+                a[r] = cfma2(cm, a[r], co, ao[r]);
+                if (two) l[r] = cfma2(cm, l[r], co, lo[r]);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < NRR; r++) {
+                if (!cbit(op.ctrl, tbase | r)) continue;
+                const bool hi = (r >> p) & 1;
+                const C cm = hi ? m[3] : m[0], co = hi ? m[2] : m[1];
+                a[r] = cfma2(cm, a[r], co, ao[r]);
+                if (two) l[r] = cfma2(cm, l[r], co, lo[r]);
+            }
+        }
+    };
+    auto diag = [&](const DevOp &op, bool two) {
+#pragma unroll
+        for (int r = 0; r < NRR; r++) {
+            const uint32_t idx = tbase | r;
+            const C d = op.kind == OP_D1 ? ldc<C>(op.m, ((idx >> op.b0.idx) & 1u))
+                                         : ldc<C>(op.m, 2 * ((idx >> op.b0.idx) & 1u) + ((idx >> op.b1.idx) & 1u));
+            a[r] = cmul(d, a[r]);
+            if (two) l[r] = cmul(d, l[r]);
+        }
+    };
+    // anything else: through shared memory with the generic small-state code
+    auto generic = [&](const DevOp &op, bool two) {
+        C *XA = X0 + (size_t)xb * 2 * N, *XL = XA + N;
+        xb ^= 1;
+#pragma unroll
+        for (int r = 0; r < NRR; r++) { XA[tbase | r] = a[r]; if (two) XL[tbase | r] = l[r]; }
+        __syncthreads();
+        circ_apply<Real>(op, XA, XL, N, 0, two);
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < NRR; r++) { a[r] = XA[tbase | r]; if (two) l[r] = XL[tbase | r]; }
+    };
+    for (int oi = 0; oi < n_f; oi++) {
+        const DevOp &op = sf[oi];
+        if (op.kind == OP_U1 || op.kind == OP_R1 || op.kind == OP_P1) one_qubit(op, false, false);
+        else if (op.kind == OP_D1 || op.kind == OP_D2) diag(op, false);
+        else generic(op, false);
+    }
+    // lambda = H psi, E = <psi|H|psi>
+    double e = 0.0;
+#pragma unroll
+    for (int r = 0; r < NRR; r++) {
+        const uint32_t b = tbase | r;
+        double h = zt.cst;
+        for (int p = 0; p < n_loc; p++)
+            if ((b >> p) & 1u) h -= 2.0 * zt.w[p];
+        for (int t = 0; t < zt.T; t++) h += (__popcll((uint64_t)b & zt.z[t]) & 1) ? -zt.c[t] : zt.c[t];
+        l[r] = mk<C>((Real)h * a[r].x, (Real)h * a[r].y);
+        e += h * ((double)a[r].x * a[r].x + (double)a[r].y * a[r].y);
+    }
+    e = block_sum<double>(e, red);
+    if (threadIdx.x == 0) atomicAdd(eval, e);
+    // reverse sweep
+    for (int oi = 0; oi < n_b; oi++) {
+        const DevOp &op = sb[oi];
+        if (op.kind == OP_U1 || op.kind == OP_R1 || op.kind == OP_P1) {
+            one_qubit(op, true, op.ngen > 0);
+        } else if (op.kind == OP_D1 || op.kind == OP_D2) {
+            for (int gi = 0; gi < op.ngen; gi++) {  // RZ-type generator on a D1 op
+                Real part = 0;
+#pragma unroll
+                for (int r = 0; r < NRR; r++) {
+                    const Real v = im_cj(l[r], a[r]);
+                    part += (((tbase | r) >> op.b0.idx) & 1u) ? -v : v;
+                }
+                const double w = warp_sum<double>((double)part);
+                if (lane == 0 && w != 0.0) atomicAdd(&grad[op.slot[gi]], w);
+            }
+            diag(op, true);
+        } else {
+            generic(op, true);
+        }
+    }
+}
+
+cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
+                           const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
+                           cudaStream_t s) {
+    const size_t ops_bytes = (size_t)(n_f + n_b) * sizeof(DevOp);
+    const size_t reg_smem = (size_t)4 * ((size_t)1 << n_loc) * (dbl ? 16 : 8) + ops_bytes;
+    if (n_loc >= 8 && n_loc <= 11 && reg_smem <= 200 * 1024) {
+        // 2 amplitudes per thread (4 at 11 qubits): up to 512 threads for latency hiding
+        const int rb = n_loc <= 10 ? 1 : 2;
+        const int threads = 1 << (n_loc - rb);
+#define TQD_R(T)                                                                                               \
+    {                                                                                                          \
+        auto fn = rb == 1 ? circuit_reg_kernel<T, 1> : circuit_reg_kernel<T, 2>;                               \
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reg_smem); \
+        if (e != cudaSuccess) return e;                                                                        \
+        fn<<<batch, threads, reg_smem, s>>>(fops, n_f, bops, n_b, (const CT<T>::C *)psi, zts, eval, grad, n_loc); \
+        return cudaGetLastError();                                                                             \
+    }
+        if (dbl) TQD_R(double)
+        TQD_R(float)
+#undef TQD_R
+    }
+    size_t smem = (size_t)2 * ((size_t)1 << n_loc) * (dbl ? 16 : 8);
+    const int ops_smem = smem + ops_bytes <= 200 * 1024;
+    if (ops_smem) smem += ops_bytes;
+    const int threads = 512;
+#define TQD_C(T)                                                                                               \
+    {                                                                                                          \
+        auto fn = circuit_kernel<T>;                                                                           \
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+        if (e != cudaSuccess) return e;                                                                        \
+        fn<<<batch, threads, smem, s>>>(fops, n_f, bops, n_b, (const CT<T>::C *)psi, zts, eval, grad, n_loc, rank_hi, ops_smem); \
+        return cudaGetLastError();                                                                             \
+    }
+    if (dbl) TQD_C(double)
+    TQD_C(float)
+#undef TQD_C
+}
+
+// ---------------------------------------------------------------------------
 // Z-string observables in physical masks.
 
 // lambda = H psi with H = sum_t c_t Z_t (diagonal): h(b) = sum_t c_t (-1)^{popc(b & z_t)};
