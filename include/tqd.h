@@ -358,6 +358,19 @@ int tqd_debug_absorb(int n, int G, const int *kinds, const int *wires, const dou
 int tqd_debug_remap_schedule(int rank, int n_loc, int m, const int *gpos, const int *lpos, int *peer_out,
                              int *recv_block_out);
 
+/* Experiment (PAPER.md:91 custom unitaries): apply a dense
+ * 2^m x 2^m complex unitary U (row-major (re, im) doubles, m = 6) to the m LOWEST
+ * bits of a 2^n-amplitude complex64 state (13 <= n <= 33) on the tensor cores:
+ * tcgen05.mma kind::tf32 with TMEM accumulators, precision = 3 (3xTF32 split,
+ * fp32-level accuracy) or 1 (plain TF32).  Canonical index i = row * 2^m + c, the
+ * block acts on c.  psi_in / psi_out: host complex64 arrays of 2^n (NULL: zeros /
+ * no readback).  Then `iters` more applications are timed with CUDA events:
+ * *ms_out = average ms per application.  Allocates its own device buffers on
+ * `device`; not part of the circuit path.  Errors: TQD_ERR_ARG, TQD_ERR_OOM,
+ * TQD_ERR_CUDA. */
+int tqd_debug_dense_block(int device, int n, int m, int precision, const double *U, const void *psi_in, void *psi_out,
+                          int iters, double *ms_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,8 @@ _SIG = {
                        _P, _P, _P, _P, _P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)],
     "tqd_debug_remap_schedule": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P],
     "tqd_debug_absorb": [ctypes.c_int, ctypes.c_int, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P, _P, _P],
+    "tqd_debug_dense_block": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P, ctypes.c_int,
+                              ctypes.POINTER(ctypes.c_double)],
 }
 EXPORTS = list(_SIG) + ["tqd_last_error", "tqd_version"]
 
@@ -413,6 +415,24 @@ def tqd_debug_absorb(n: int, gates, z_masks):
     _call("tqd_debug_absorb", n, len(gates), _ptr(kinds), _ptr(wires), _ptr(params), _ptr(mats), _ptr(tr), T,
           _ptr(zin), _ptr(zout), _ptr(sg), ctypes.byref(tb))
     return tb.value, [int(v) for v in zout[:T]], sg[:T].copy()
+
+
+def tqd_debug_dense_block(n: int, U, psi=None, precision: int = 3, iters: int = 0, device: int = 0):
+    """Tensor-core experiment: U (2^6 x 2^6 complex) on the 6 lowest bits of a 2^n complex64
+    state by tcgen05.mma (include/tqd.h).  Returns (result or None, ms per timed application)."""
+    U = np.asarray(U, np.complex128)
+    m = int(round(np.log2(U.shape[0])))
+    if U.shape != (1 << m, 1 << m):
+        raise TqdError(-1, "U must be square 2^m x 2^m")
+    uu = np.empty(2 * U.size, np.float64)
+    uu[0::2], uu[1::2] = U.real.reshape(-1), U.imag.reshape(-1)
+    pin = None if psi is None else np.ascontiguousarray(np.asarray(psi, np.complex64))
+    if pin is not None and pin.size != (1 << n):
+        raise TqdError(-1, "psi must have 2^n amplitudes")
+    out = None if psi is None else np.zeros(1 << n, np.complex64)
+    ms = ctypes.c_double(0.0)
+    _call("tqd_debug_dense_block", device, n, m, precision, _ptr(uu), _ptr(pin), _ptr(out), iters, ctypes.byref(ms))
+    return out, ms.value
 
 
 def tqd_debug_remap_schedule(rank: int, n_loc: int, gpos, lpos):

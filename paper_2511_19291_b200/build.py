@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtqd.so")
 SOURCES = ["kernels.cu", "sweep_f32_fwd.cu", "sweep_f32_bwd.cu", "sweep_f64_fwd.cu", "sweep_f64_bwd.cu",
-           "plan.cpp", "comm.cpp", "abi.cpp"]
+           "dense_tc.cu", "plan.cpp", "comm.cpp", "abi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -49,6 +49,8 @@ cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
 cudaError_t launch_remap_block(bool dbl, void *shard, void *stage, uint64_t e0, uint64_t cnt, uint64_t bdep, uint64_t rest,
                               bool unpack, cudaStream_t s);
 cudaError_t launch_debug_delay(uint32_t us, cudaStream_t s);
+cudaError_t dense_tc_upload(const double *U, int m, void **bsplit, cudaStream_t s);
+cudaError_t dense_tc_launch(float *x, uint64_t n_amps, const void *bsplit, int prec, int sms, cudaStream_t s);
 cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
                            const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
                            cudaStream_t s);
@@ -2037,6 +2039,54 @@ int tqd_debug_plan(int n, int world, int k, int small_max, int c128, int G, cons
     if (!json_out || cap < js.size() + 1) return fail(TQD_ERR_ARG, "json buffer too small");
     memcpy(json_out, js.c_str(), js.size() + 1);
     return TQD_OK;
+}
+
+// Experiment (tensor cores): a dense m-qubit block on the
+// m lowest bits of a 2^n complex64 state by tcgen05.mma (dense_tc.cu), on `device`.
+int tqd_debug_dense_block(int device, int n, int m, int precision, const double *U, const void *psi_in, void *psi_out,
+                          int iters, double *ms_out) {
+    if (m != 6 || n < 13 || n > 33 || (precision != 1 && precision != 3) || !U || iters < 0)
+        return fail(TQD_ERR_ARG, "dense block: m = 6, 13 <= n <= 33, precision 1 or 3");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(TQD_ERR_CUDA, cudaGetErrorString(e));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const uint64_t N = 1ull << n;
+    float *x = nullptr;
+    void *bs = nullptr;
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto done = [&](int rc, const char *msg) {
+        if (s) cudaStreamSynchronize(s);
+        if (x) cudaFree(x);
+        if (bs) cudaFree(bs);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (s) cudaStreamDestroy(s);
+        return rc ? fail(rc, msg) : TQD_OK;
+    };
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess || cudaMalloc(&x, N * 8) != cudaSuccess ||
+        cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        cudaGetLastError();
+        return done(TQD_ERR_OOM, "dense block buffers");
+    }
+    if ((e = dense_tc_upload(U, m, &bs, s)) != cudaSuccess) return done(TQD_ERR_CUDA, cudaGetErrorString(e));
+    if (psi_in) e = cudaMemcpyAsync(x, psi_in, N * 8, cudaMemcpyHostToDevice, s);
+    else e = cudaMemsetAsync(x, 0, N * 8, s);
+    if (e == cudaSuccess) e = dense_tc_launch(x, N, bs, precision, sms, s);
+    if (e == cudaSuccess && psi_out) e = cudaMemcpyAsync(psi_out, x, N * 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && iters > 0) {
+        e = cudaEventRecord(e0, s);
+        for (int i = 0; i < iters && e == cudaSuccess; i++) e = dense_tc_launch(x, N, bs, precision, sms, s);
+        if (e == cudaSuccess) e = cudaEventRecord(e1, s);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        float ms = 0;
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        if (ms_out) *ms_out = ms / iters;
+    }
+    if (e != cudaSuccess) return done(TQD_ERR_CUDA, cudaGetErrorString(e));
+    return done(TQD_OK, "");
 }
 
 // Diagnostic, host only: the remap exchange schedule of one rank.  For each

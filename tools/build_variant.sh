@@ -15,7 +15,7 @@ for f in sweep_f32_fwd sweep_f32_bwd; do
 done
 wait
 objs=""
-for f in kernels sweep_f64_fwd sweep_f64_bwd plan comm abi; do objs="$objs $OBJ/$f.o"; done
+for f in kernels sweep_f64_fwd sweep_f64_bwd dense_tc plan comm abi; do objs="$objs $OBJ/$f.o"; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $PKG/variants/libtqd_$NAME.so $objs $OUT/sweep_f32_fwd.o $OUT/sweep_f32_bwd.o \
   -L$NCCL/lib -l:$(basename $(ls $NCCL/lib/libnccl.so* | head -1)) -Xlinker -rpath,$NCCL/lib
 echo $PKG/variants/libtqd_$NAME.so
