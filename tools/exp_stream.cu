@@ -14,6 +14,7 @@
 //          (trivial compute) -> STS in place, producer bulk-stores the slot back
 //          (cp.async.bulk.global.shared::cta.bulk_group)
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -o exp_stream exp_stream.cu
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -23,6 +24,7 @@
 #include <vector>
 #include <string>
 #include <cstring>
+#include <algorithm>
 
 #define CK(x)                                                                                 \
     do {                                                                                      \
@@ -155,6 +157,57 @@ __global__ void __launch_bounds__(256, MINB) ldg_kernel(const __grid_constant__ 
             const uint64_t off = base + toff + roff[r];
             __stcs(psi + off, a[r]);
             __stcs(lam + off, l[r]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- DSMEM cluster tile (k = 13)
+// A 2-CTA cluster holds a 13-bit tile: tile bit 12 = the CTA rank.  Per tile: load the
+// CTA's half (ldg, as ldg_kernel), exchange register bit 3 <-> the CTA bit through
+// distributed shared memory (half of the data to the peer CTA), cluster barrier, read,
+// exchange back, cluster barrier, store.  Same bytes per amplitude as ldg_kernel's two
+// local exchanges.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) dsmem_kernel(const __grid_constant__ TileDesc T,
+                                                                                float2 *psi, float2 *lam) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) float2 dsm[];
+    float2 *sa = dsm, *sl = dsm + 4096;
+    const int tid = threadIdx.x;
+    const unsigned rank = cl.block_rank();
+    float2 *pa = cl.map_shared_rank(sa, rank ^ 1u), *pl = cl.map_shared_rank(sl, rank ^ 1u);
+    uint64_t toff = tile_off(T, tid), roff[16];
+    for (int r = 0; r < 16; r++) roff[r] = tile_off(T, (uint32_t)r << 8);
+    const uint64_t coff = rank ? (1ull << T.pos[12]) : 0ull;
+    const uint64_t n_cl = T.n_tiles;  // tiles of 13 bits
+    for (uint64_t tile = blockIdx.x / 2; tile < n_cl; tile += gridDim.x / 2) {
+        const uint64_t base = deposit_tile(T, tile) | coff;
+        float2 a[16], l[16];
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+            a[r] = __ldcs(psi + base + toff + roff[r]);
+            l[r] = __ldcs(lam + base + toff + roff[r]);
+        }
+        for (int x = 0; x < 2; x++) {
+            // element (rank c, thread t, reg r) -> (rank (r >> 3) & 1, t, (r & 7) | c << 3)
+#pragma unroll
+            for (int r = 0; r < 16; r++) {
+                const int slot = (((r & 7) | (int)(rank << 3)) << 8) | tid;
+                if (((r >> 3) & 1) == (int)rank) { sa[slot] = a[r]; sl[slot] = l[r]; }
+                else { pa[slot] = a[r]; pl[slot] = l[r]; }
+            }
+            cl.sync();
+#pragma unroll
+            for (int r = 0; r < 16; r++) {
+                a[r] = sa[(r << 8) | tid];
+                l[r] = sl[(r << 8) | tid];
+            }
+            cl.sync();
+        }
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+            __stcs(psi + base + toff + roff[r], a[r]);
+            __stcs(lam + base + toff + roff[r], l[r]);
         }
     }
 }
@@ -515,6 +568,27 @@ int main(int argc, char **argv) {
                 go(tma_kernel<12, 3, 16>, "tma k12 3slot 16cw", 3, 16);
             }
         }
+    }
+
+    if (w == "all" || w == "dsmem") {
+        TileDesc T13 = T;  // 13-bit tile: T's 12 bits + physical bit 30 -> use bit 29's neighbour
+        T13.k = 13;
+        const int p13[13] = {0, 1, 2, 3, 5, 9, 12, 15, 18, 21, 25, 28, 7};
+        for (int i = 0; i < 13; i++) T13.pos[i] = p13[i];
+        int srt[13];
+        for (int i = 0; i < 13; i++) srt[i] = p13[i];
+        std::sort(srt, srt + 13);
+        for (int i = 0; i < 13; i++) T13.sorted[i] = srt[i];
+        T13.n_tiles = N >> 13;
+        CK(cudaFuncSetAttribute(dsmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        for (int ctas : {2, 4}) {
+            char nm[64];
+            snprintf(nm, sizeof(nm), "dsmem k13 cluster2 2xch %d CTAs/SM", ctas);
+            timeit(nm, [&] { dsmem_kernel<<<sms * ctas, 256, 65536>>>(T13, psi, lam); });
+        }
+        g_work = 0;
+        CK(cudaFuncSetAttribute(ldg_kernel<true, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+        timeit("ldg k12 2xch (same bytes)", [&] { ldg_kernel<true, true, 2><<<sms * 2, 256, 65536>>>(T, psi, lam, 0); });
     }
     CK(cudaFree(psi));
     CK(cudaFree(lam));
