@@ -521,6 +521,14 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         for (int x : a) if (!std::count(b.begin(), b.end(), x)) return false;
         return true;
     };
+    // segments per stage: every layout change moves psi (and lambda) through shared
+    // memory (~1.4 ms per forward / ~3.5 ms per adjoint exchange at
+    // 30 qubits); TQD_PLAN_MAX_SEGS caps them (experiment knob, default MAXSEG)
+    static const int env_segs = [] {
+        const char *e = getenv("TQD_PLAN_MAX_SEGS");
+        return e ? std::max(2, std::min(MAXSEG, atoi(e))) : MAXSEG;
+    }();
+    const int max_segs = env_segs;
     int nseg = 1;
     while ((int)order.size() < m) {
         const int cs = nseg - 1;
@@ -545,7 +553,7 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
             }
         }
         if (pick < 0) {
-            if (nseg == MAXSEG) break;
+            if (nseg >= max_segs) break;
             segregs.push_back({});
             nseg++;
             continue;
@@ -565,6 +573,30 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
         for (int i : order) ls = std::max(ls, seg_of[i]);
         return ls;
     };
+    // a layout change costs a fixed share of the sweep (~1.4 ms per
+    // forward and ~3.5 ms per adjoint exchange at 30 qubits, a whole sweep pair
+    // ~13.7 ms for ~24 gates): a trailing segment beyond the third that carries
+    // fewer than seg_min_gates gates is cheaper as part of the next stage.  Its items
+    // are last in dependency order, so handing them back keeps the rest closed.
+    {
+        static const int seg_min_gates = [] {  // measured: 6 -> 1029 vs 1058 ms per cfg-3 step
+            const char *e = getenv("TQD_PLAN_SEG_MIN_GATES");
+            return e ? atoi(e) : 6;
+        }();
+        for (;;) {
+            const int ls = last_used();
+            if (ls < 3 || seg_min_gates <= 0) break;
+            int cnt = 0;
+            for (int i : order) if (seg_of[i] == ls) cnt++;
+            if (cnt >= seg_min_gates) break;
+            std::vector<int> keep;
+            for (int i : order) {
+                if (seg_of[i] == ls) { done[i] = 0; seg_of[i] = -1; }
+                else keep.push_back(i);
+            }
+            order = keep;
+        }
+    }
     // permutation gates left in the last segment would need a final map at the
     // store (uncoalesced): hand them back to the next stage, unless the stage
     // has nothing else (then a trailing empty segment realises them)
