@@ -319,6 +319,50 @@ __global__ void __launch_bounds__(512) circuit_kernel(const DevOp *__restrict__ 
 // barrier between gates that do not cross warps.  Gradients use the post-gate pair
 // values of the same exchange.  Other ops (4x4 MAT2) fall back to
 // a shared-memory pass (circ_apply).
+// Compact op of the register-resident circuit kernel, decoded once per launch from
+// the DevOp (so the gate loop reads one 16-byte header and its coefficients):
+// class by where the target bit lives for RB register bits, 2x2 form, control bit,
+// the first generator's kind.  Anything else (U2 / MAT2, several or general
+// generators) keeps the DevOp path (CC_GEN).
+enum : uint8_t { CC_REG = 0, CC_LANE = 1, CC_WARP = 2, CC_D1 = 3, CC_D2 = 4, CC_GEN = 5 };
+enum : uint8_t { CF_CPLX = 0, CF_REAL = 1, CF_SWAP = 2 };
+struct alignas(16) COp {
+    uint8_t cls, p, cb, b0, b1, form, ngen, gk;  // cb = 0xff: no control
+    int32_t slot;
+    int32_t pad;
+    double m[8];  // 2x2 complex row-major (re, im); real form: m[0..3]; D1: d0, d1; D2: 4 entries
+};
+template <int RB> __device__ __forceinline__ void decode_cop(const DevOp &d, COp &c) {
+    c.cls = CC_GEN;
+    c.p = d.t0;
+    c.cb = d.ctrl.kind == BK_NONE ? 0xff : d.ctrl.idx;
+    c.b0 = d.b0.idx;
+    c.b1 = d.b1.idx;
+    c.ngen = d.ngen;
+    c.gk = d.ngen ? d.gkind[0] : GEN_NONE;
+    c.slot = d.ngen ? d.slot[0] : 0;
+    c.form = CF_CPLX;
+    for (int i = 0; i < 8; i++) c.m[i] = d.m[i];
+    const bool simple_gen = d.ngen == 0 || (d.ngen == 1 && (d.gkind[0] == GEN_Y || d.gkind[0] == GEN_X || d.gkind[0] == GEN_Z));
+    if (!simple_gen) return;
+    if (d.kind == OP_U1 || d.kind == OP_R1 || d.kind == OP_P1) {
+        if (d.ngen && d.gkind[0] == GEN_Z) return;
+        c.cls = d.t0 < RB ? CC_REG : d.t0 < RB + 5 ? CC_LANE : CC_WARP;
+        if (d.kind == OP_R1) c.form = CF_REAL;
+        if (d.kind == OP_P1) {
+            // [[0, a], [b, 0]]: m = (0, a, b, 0); a = b = 1: a swap
+            const double a0 = d.m[0], a1 = d.m[1], b0 = d.m[2], b1 = d.m[3];
+            c.m[0] = 0; c.m[1] = 0; c.m[2] = a0; c.m[3] = a1; c.m[4] = b0; c.m[5] = b1; c.m[6] = 0; c.m[7] = 0;
+            if (a0 == 1.0 && a1 == 0.0 && b0 == 1.0 && b1 == 0.0) c.form = CF_SWAP;  // X / CNOT target
+        }
+    } else if (d.kind == OP_D1) {
+        if (d.ngen && d.gkind[0] != GEN_Z) return;
+        c.cls = CC_D1;
+    } else if (d.kind == OP_D2 && d.ngen == 0) {
+        c.cls = CC_D2;
+    }
+}
+
 template <typename C> __device__ __forceinline__ C shfl_c(C v, int m) {
     return mk<C>(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
 }
@@ -343,6 +387,8 @@ __global__ void __launch_bounds__(512) circuit_reg_kernel(const DevOp *__restric
     C *X0 = reinterpret_cast<C *>(smem_raw);
     DevOp *sf = reinterpret_cast<DevOp *>(X0 + 4 * N);
     DevOp *sb = sf + n_f;
+    COp *cf = reinterpret_cast<COp *>(sb + n_b);
+    COp *cbk = cf + n_f;
     {
         const int4 *src = reinterpret_cast<const int4 *>(fops);
         int4 *dst = reinterpret_cast<int4 *>(sf);
@@ -351,6 +397,8 @@ __global__ void __launch_bounds__(512) circuit_reg_kernel(const DevOp *__restric
         dst = reinterpret_cast<int4 *>(sb);
         for (int i = threadIdx.x; i < n_b * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_f + n_b; i += blockDim.x) decode_cop<RB>(i < n_f ? sf[i] : sb[i - n_f], i < n_f ? cf[i] : cbk[i - n_f]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t tbase = ((uint32_t)lane << RB) | ((uint32_t)warp << (RB + 5));
     C a[NRR], l[NRR];
@@ -458,11 +506,95 @@ __global__ void __launch_bounds__(512) circuit_reg_kernel(const DevOp *__restric
 #pragma unroll
         for (int r = 0; r < NRR; r++) { a[r] = XA[tbase | r]; if (two) l[r] = XL[tbase | r]; }
     };
+    // ---- fast paths on the compact ops --------------------------------------
+    // y_bit = m[bit][bit] x + m[bit][!bit] x_partner, per amplitude r (hi = its bit p)
+    auto apply_pair = [&](const COp &c, C &x, const C xo, bool hi) {
+        if (c.form == CF_SWAP) {
+            x = xo;
+        } else if (c.form == CF_REAL) {
+            const Real cm = (Real)(hi ? c.m[3] : c.m[0]), co = (Real)(hi ? c.m[2] : c.m[1]);
+            x = mk<C>(cm * x.x + co * xo.x, cm * x.y + co * xo.y);
+        } else {
+            const int im_ = hi ? 3 : 0, io = hi ? 2 : 1;
+            const C cm = mk<C>((Real)c.m[2 * im_], (Real)c.m[2 * im_ + 1]);
+            const C co = mk<C>((Real)c.m[2 * io], (Real)c.m[2 * io + 1]);
+            x = cmul2(cm, x, co, xo);
+        }
+    };
+    auto fast_1q = [&](const COp &c, bool two) {
+        const int p = c.p;
+        C ao[NRR], lo[NRR];
+        if (c.cls == CC_REG) {
+            if (RB == 1 || p == 0) {
+#pragma unroll
+                for (int r = 0; r < NRR; r++) { ao[r] = a[r ^ 1]; if (two) lo[r] = l[r ^ 1]; }
+            } else {
+#pragma unroll
+                for (int r = 0; r < NRR; r++) { ao[r] = a[r ^ (2 % NRR)]; if (two) lo[r] = l[r ^ (2 % NRR)]; }
+            }
+        } else if (c.cls == CC_LANE) {
+            const int mk_ = 1 << (p - RB);
+#pragma unroll
+            for (int r = 0; r < NRR; r++) { ao[r] = shfl_c(a[r], mk_); if (two) lo[r] = shfl_c(l[r], mk_); }
+        } else {
+            C *XA = X0 + (size_t)xb * 2 * N, *XL = XA + N;
+            xb ^= 1;
+#pragma unroll
+            for (int r = 0; r < NRR; r++) { XA[tbase | r] = a[r]; if (two) XL[tbase | r] = l[r]; }
+            __syncthreads();
+            const uint32_t f = 1u << p;
+#pragma unroll
+            for (int r = 0; r < NRR; r++) { ao[r] = XA[(tbase | r) ^ f]; if (two) lo[r] = XL[(tbase | r) ^ f]; }
+        }
+        if (two && c.ngen) {  // Y or X generator: 2 Re <lam|G|psi> over the pairs, counted by bit-0 members
+            Real part = 0;
+#pragma unroll
+            for (int r = 0; r < NRR; r++) {
+                if (((tbase | r) >> p) & 1u) continue;
+                part += c.gk == GEN_Y ? re_cj(lo[r], a[r]) - re_cj(l[r], ao[r]) : im_cj(l[r], ao[r]) + im_cj(lo[r], a[r]);
+            }
+            const double w = warp_sum<double>((double)part);
+            if (lane == 0 && w != 0.0) atomicAdd(&grad[c.slot], w);
+        }
+#pragma unroll
+        for (int r = 0; r < NRR; r++) {
+            const uint32_t idx = tbase | r;
+            if (c.cb != 0xff && !((idx >> c.cb) & 1u)) continue;
+            const bool hi = (idx >> p) & 1u;
+            apply_pair(c, a[r], ao[r], hi);
+            if (two) apply_pair(c, l[r], lo[r], hi);
+        }
+    };
+    auto fast_diag = [&](const COp &c, bool two) {
+        if (two && c.ngen) {  // Z generator on bit b0
+            Real part = 0;
+#pragma unroll
+            for (int r = 0; r < NRR; r++) {
+                const Real v = im_cj(l[r], a[r]);
+                part += (((tbase | r) >> c.b0) & 1u) ? -v : v;
+            }
+            const double w = warp_sum<double>((double)part);
+            if (lane == 0 && w != 0.0) atomicAdd(&grad[c.slot], w);
+        }
+#pragma unroll
+        for (int r = 0; r < NRR; r++) {
+            const uint32_t idx = tbase | r;
+            const int j = c.cls == CC_D1 ? (int)((idx >> c.b0) & 1u) : (int)(2 * ((idx >> c.b0) & 1u) + ((idx >> c.b1) & 1u));
+            const C d = mk<C>((Real)c.m[2 * j], (Real)c.m[2 * j + 1]);
+            a[r] = cmul(d, a[r]);
+            if (two) l[r] = cmul(d, l[r]);
+        }
+    };
     for (int oi = 0; oi < n_f; oi++) {
-        const DevOp &op = sf[oi];
-        if (op.kind == OP_U1 || op.kind == OP_R1 || op.kind == OP_P1) one_qubit(op, false, false);
-        else if (op.kind == OP_D1 || op.kind == OP_D2) diag(op, false);
-        else generic(op, false);
+        const COp &c = cf[oi];
+        if (c.cls <= CC_WARP) fast_1q(c, false);
+        else if (c.cls <= CC_D2) fast_diag(c, false);
+        else {
+            const DevOp &op = sf[oi];
+            if (op.kind == OP_U1 || op.kind == OP_R1 || op.kind == OP_P1) one_qubit(op, false, false);
+            else if (op.kind == OP_D1 || op.kind == OP_D2) diag(op, false);
+            else generic(op, false);
+        }
     }
     // lambda = H psi, E = <psi|H|psi>
     double e = 0.0;
@@ -480,6 +612,9 @@ __global__ void __launch_bounds__(512) circuit_reg_kernel(const DevOp *__restric
     if (threadIdx.x == 0) atomicAdd(eval, e);
     // reverse sweep
     for (int oi = 0; oi < n_b; oi++) {
+        const COp &c = cbk[oi];
+        if (c.cls <= CC_WARP) { fast_1q(c, true); continue; }
+        if (c.cls <= CC_D2) { fast_diag(c, true); continue; }
         const DevOp &op = sb[oi];
         if (op.kind == OP_U1 || op.kind == OP_R1 || op.kind == OP_P1) {
             one_qubit(op, true, op.ngen > 0);
@@ -505,7 +640,7 @@ cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bo
                            const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
                            cudaStream_t s) {
     const size_t ops_bytes = (size_t)(n_f + n_b) * sizeof(DevOp);
-    const size_t reg_smem = (size_t)4 * ((size_t)1 << n_loc) * (dbl ? 16 : 8) + ops_bytes;
+    const size_t reg_smem = (size_t)4 * ((size_t)1 << n_loc) * (dbl ? 16 : 8) + ops_bytes + (size_t)(n_f + n_b) * sizeof(COp);
     if (n_loc >= 8 && n_loc <= 11 && reg_smem <= 200 * 1024) {
         // 2 amplitudes per thread (4 at 11 qubits): up to 512 threads for latency hiding
         const int rb = n_loc <= 10 ? 1 : 2;
