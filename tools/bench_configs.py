@@ -91,7 +91,7 @@ def run_case(ctx, name, wl, steps, warmup, tile=0, note=""):
         shard = (8 if wl.dtype == "c64" else 16) << n
         pk = peak_gbs()
         out["fwd_sweeps"], out["bwd_sweeps"] = m["fwd_sweeps"], m["bwd_sweeps"]
-        if m["fwd_sweeps"]:
+        if m["fwd_sweeps"] and m["fwd_sweep_ms"] > 0:
             a = m["fwd_sweep_ms"] / m["fwd_sweeps"]
             out["fwd_sweep_avg_ms"] = round(a, 4)
             out["fwd_sweep_gbs"] = round(2 * shard / (a / 1e3) / 1e9, 1)
@@ -102,6 +102,9 @@ def run_case(ctx, name, wl, steps, warmup, tile=0, note=""):
             out["bwd_sweep_gbs"] = round(m["bwd_sweep_bytes"] / (m["bwd_sweep_ms"] / 1e3) / 1e9, 1)
             out["bwd_sweep_frac"] = round(out["bwd_sweep_gbs"] / pk, 4)
         out["other_ms"] = round(m["other_ms"], 3)
+        out["launches_per_fwd_grad"] = m["kernel_launches"]
+        out["peak_device_bytes"] = m["peak_device_bytes"]  # psi + lambda (+ staging at world > 1)
+        out["peak_device_gib"] = round(m["peak_device_bytes"] / 2**30, 3)
         out["gamp_gates_per_s_fwd_grad"] = round(len(gates) * (1 << n) / (out["fwd_grad_ms"] / 1e3) / 1e9, 2)
         out["gamp_gates_per_s_fwd"] = round(len(gates) * (1 << n) / (out["fwd_ms"] / 1e3) / 1e9, 2)
         val, g = res["vg"]
@@ -132,7 +135,8 @@ def main():
         for c in cases:
             if c == "cfg1":
                 run_case(ctx, c, W.config(1), max(args.steps, 20), max(args.warmup, 5),
-                         note="10 local qubits: one-tile fused sweeps (a single CTA), latency-bound")
+                         note="10 qubits: the whole fwd + lambda seed + reverse sweep in ONE launch "
+                              "(circuit_reg_kernel, one CTA), latency-bound")
             elif c == "cfg2":
                 run_case(ctx, c, W.config(2), max(args.steps, 5), args.warmup,
                          note="128 MiB psi + 128 MiB lambda: partly L2-resident (126 MB L2)")

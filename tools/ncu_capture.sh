@@ -6,7 +6,7 @@ set -e
 TAG=${1:-cur}
 mkdir -p gpurun_out
 python tools/prof_sweep.py > gpurun_out/prof_plain.log 2>&1
-# launches: 69 forward sweeps, then 69 adjoint sweeps (see prof_plain.log)
+# launches: 66 forward sweeps, then 66 adjoint sweeps (see prof_plain.log): adjoint #14, forward #11
 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel --launch-skip 79 -c 1 \
     -o gpurun_out/prof_bwd_$TAG -f python tools/prof_sweep.py > gpurun_out/ncu_bwd.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel --launch-skip 10 -c 1 \
