@@ -419,10 +419,22 @@ __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typ
         const int i0 = (int)((hz & 0xffu) + ((hz >> 8) & 0xffu)), i1 = i0 + (int)((hz >> 16) & 0xffu);
         if (i1 == i0) continue;
         const DTerm<Real> *tm = reinterpret_cast<const DTerm<Real> *>(kq.g);
-        th += dblk_sum<Real>(tm, i0, i1, 0xffu, tix, basefull);
+        // one pass over the terms: a term feeds th (no register bit) or al[its register
+        // bit] (terms moved here when the C / U budgets ran out)
+        for (int i = i0; i < i1; i++) {
+            const DTerm<Real> t = tm[i];
+            const uint32_t va = t.a.kind == BK_TIX ? ((tix >> t.a.idx) & 1u)
+                                : t.a.kind == BK_BASE ? (uint32_t)((basefull >> t.a.idx) & 1ull) : 1u;
+            const uint32_t vb = t.b.kind == BK_TIX ? ((tix >> t.b.idx) & 1u)
+                                : t.b.kind == BK_BASE ? (uint32_t)((basefull >> t.b.idx) & 1ull) : 1u;
+            const typename DAcc<Real>::U v = vb ? t.ang : (typename DAcc<Real>::U)0;
+            if (t.a.kind != BK_REG) {
+                th += va ? v : (typename DAcc<Real>::U)0;
+            } else {
 #pragma unroll
-        for (int b = 0; b < SWEEP_R; b++)
-            if ((xm >> b) & 1u) al[b] += dblk_sum<Real>(tm, i0, i1, (uint32_t)b, tix, basefull);
+                for (int b = 0; b < SWEEP_R; b++) al[b] += (t.a.idx == b) ? v : (typename DAcc<Real>::U)0;
+            }
+        }
     }
     // in place, no per-amplitude phase array: table[r] e^{i th} first, then
     // e^{i al_b} on the amplitudes with register bit b set
