@@ -116,7 +116,13 @@ typedef enum {
                                * halves; remap blocks and X/Y partner shards move through it
                                * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
                                * force a few KiB so the chunk loop iterates.               */
-    TQD_OPT_CIRCUIT_MAX = 8    /* single-GPU states of <= this many qubits (0..12; default 10)
+    TQD_OPT_PRODUCT_PREFIX = 9, /* 1 (default): every qubit's leading 1-qubit gates (before its
+                               * first multi-qubit gate) act on |0>: a single state on one GPU
+                               * starts from their product state (one write pass instead of
+                               * their sweeps) and the adjoint finishes their gradients from
+                               * lambda's environments at the prefix boundary (one read pass);
+                               * same values and gradients.  0: sweep every gate.          */
+    TQD_OPT_CIRCUIT_MAX = 8,   /* single-GPU states of <= this many qubits (0..12; default 10)
                                * run tqd_adjoint_grad with Z-string terms as ONE kernel launch:
                                * forward gates, lambda = H psi and the reverse sweep in one
                                * CTA's shared memory per state (0 = staged sweeps only)     */

@@ -49,6 +49,9 @@ cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
 cudaError_t launch_remap_block(bool dbl, void *shard, void *stage, uint64_t e0, uint64_t cnt, uint64_t bdep, uint64_t rest,
                               bool unpack, cudaStream_t s);
 cudaError_t launch_debug_delay(uint32_t us, cudaStream_t s);
+cudaError_t launch_prefix_init(bool dbl, void *psi, uint64_t n, int ng, const void *tab, cudaStream_t s);
+cudaError_t launch_prefix_contract(bool dbl, const void *lam, uint64_t n, int ng, const void *tab, double *M, int sms,
+                                   cudaStream_t s);
 cudaError_t dense_tc_upload(const double *U, int m, void **bsplit, cudaStream_t s);
 cudaError_t dense_tc_launch(float *x, uint64_t n_amps, const void *bsplit, int prec, int sms, cudaStream_t s);
 cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
@@ -107,6 +110,14 @@ struct tqd_state {
     int circ_nf = 0, circ_nb = 0;
     size_t circ_off_b = 0, circ_off_z = 0;
     std::vector<int> circ_pos;  // qubit map after the cached circuit
+    // product-state prefix of the current execution (prefix_build)
+    int opt_prefix = 1;            // TQD_OPT_PRODUCT_PREFIX
+    bool pf_on = false;
+    std::vector<char> pf_in;       // per gate: in the prefix
+    std::vector<cd> pf_s;          // per qubit: s_q (2 entries)
+    int pf_ng = 0;
+    void *pf_dev = nullptr;        // group tables (device, state dtype) + M environments (fp64)
+    size_t pf_cap = 0;
     // fused forward sweep -> remap (peer memory): every rank's two shard allocations
     // (first psi, first lambda), shared once; the forward stores into the owners'
     // lambda-role buffer (idle until the adjoint seed) and the roles swap.  The
@@ -546,7 +557,7 @@ static int launch_encoded(tqd_state *st, const std::vector<Stage> &stages, bool 
                 st->met.fused_remaps++;
                 li++;  // the remap is done
             }
-            const uint64_t bb = (l.no_store ? 2 : 4) * sb;  // the last reverse sweep only reads
+            const uint64_t bb = (l.no_store == 1 ? 2 : l.no_store == 2 ? 3 : 4) * sb;  // the last reverse sweep stores less
             if (bwd) { st->met.bwd_sweeps++; st->met.bwd_sweep_bytes += bb; st->met.hbm_bytes += bb; st->met.gates_unapplied += sp.n_gates; }
             else { st->met.fwd_sweeps++; st->met.fwd_sweep_bytes += 2 * sb; st->met.hbm_bytes += 2 * sb; st->met.gates_applied += sp.n_gates; }
             st->met.kernel_launches++;
@@ -621,6 +632,14 @@ static int launch_graphed(tqd_state *st, const std::vector<Stage> &stages, bool 
     return TQD_OK;
 }
 
+// the product prefix holds trainable gates (the adjoint then runs down to its boundary)
+static bool prefix_has_grads(const tqd_state *st) {
+    if (!st->pf_on) return false;
+    for (size_t i = 0; i < st->pf_in.size(); i++)
+        if (st->pf_in[i] && st->gates[i].ngen) return true;
+    return false;
+}
+
 template <typename Real>
 static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd, Encoded &E,
                        std::vector<DevStage> &dstages, std::vector<DevOp> &ops, std::vector<KOp<Real>> &kops,
@@ -648,7 +667,9 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
                 encode_sweep_k<Real>(s.sw, gates_for(st, b, tmp), bwd, st->n_loc, dsb, kops, slots, skip_below);
             }
             ds.batch = st->batch;
-            ds.no_store = (bwd && (int)ii == last_sweep) ? 1 : 0;
+            // (with a product prefix the last reverse sweep stores lambda: its environments
+            // give the prefix gates' gradients)
+            ds.no_store = (bwd && (int)ii == last_sweep) ? (prefix_has_grads(st) ? 2 : 1) : 0;
             const int ncv = ds.n_dblk ? ds.n_cvals : -1;  // -1: no diagonal blocks (plain kernel)
             E.launches.push_back({ST_SWEEP, (int)dstages.size(), 0, ds.n_ops, (int)ii,
                                   sweep_grid(st, s.sw, bwd, ds.n_ops, ds.n_slots, ncv), ds.n_slots, ds.no_store, ncv});
@@ -766,6 +787,156 @@ static uint64_t tape_values_hash(const tqd_state *st) {
     return h;
 }
 
+// ---- product-state prefix (exact) -------------------------------------------
+// Every qubit's leading run of 1-qubit gates acts on |0> before the qubit meets any
+// multi-qubit gate (the gates of other qubits commute with them), so after those
+// gates the state is the product psi_P = (x)_q s_q with s_q = (its gates) |0>
+// (e.g. the HEA's first RY + RZ layer, Listing 2's encoder).  The
+// forward writes psi_P directly (prefix_init_kernel, the same HBM pass as the |0..0>
+// reset) instead of sweeping those gates; the adjoint stops at the prefix boundary
+// and finishes their gradients from the environments of lambda (prefix_contract_kernel,
+// one read of lambda): dE/dtheta_j = 2 Re sum_v T_q(v) (d s_q / d theta_j)(v).
+// Single state on one GPU, from |0..0>, local qubits >= 11.
+constexpr int PF_BITS_H = 10;
+static bool prefix_build(tqd_state *st, size_t end) {
+    st->pf_on = false;
+    if (!st->opt_prefix || st->ctx->world != 1 || st->batch != 1 || st->executed != 0 || st->n_loc < 11 ||
+        st->n_loc > 40)
+        return false;
+    const int n = st->n;
+    st->pf_in.assign(st->gates.size(), 0);
+    st->pf_s.assign(2 * n, cd(0.0));
+    for (int q = 0; q < n; q++) st->pf_s[2 * q] = cd(1.0);
+    std::vector<char> touched(n, 0);
+    bool any = false;
+    for (size_t i = 0; i < end; i++) {
+        const GateRec &g = st->gates[i];
+        if (g.nw != 1) {
+            for (int j = 0; j < g.nw; j++) touched[g.w[j]] = 1;
+            continue;
+        }
+        if (g.batched) { touched[g.w[0]] = 1; continue; }
+        const int q = g.w[0];
+        if (touched[q]) continue;
+        st->pf_in[i] = 1;
+        any = true;
+        const cd a = st->pf_s[2 * q], b = st->pf_s[2 * q + 1];
+        st->pf_s[2 * q] = g.M[0] * a + g.M[1] * b;
+        st->pf_s[2 * q + 1] = g.M[2] * a + g.M[3] * b;
+    }
+    st->pf_on = any;
+    return any;
+}
+
+// the group tables tab_g[i] = prod over the group's physical bits of s_q(bit), q the
+// qubit at that bit (pi = identity at the start: physical bit p = qubit n-1-p)
+static int prefix_init(tqd_state *st) {
+    const int nl = st->n_loc, n = st->n;
+    const int ng = (nl + PF_BITS_H - 1) / PF_BITS_H;
+    st->pf_ng = ng;
+    const size_t tab_elems = (size_t)ng << PF_BITS_H;
+    const size_t tab_bytes = tab_elems * st->esz, m_bytes = tab_elems * 2 * sizeof(double);
+    if (tab_bytes + m_bytes > st->pf_cap) {
+        if (st->pf_dev) { CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream)); cudaFree(st->pf_dev); }
+        st->pf_dev = nullptr;
+        st->pf_cap = 0;
+        if (cudaMalloc(&st->pf_dev, tab_bytes + m_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(TQD_ERR_OOM, "cannot allocate the product-prefix tables");
+        }
+        st->pf_cap = tab_bytes + m_bytes;
+    }
+    std::vector<double> h(tab_elems * 2, 0.0);
+    for (int g = 0; g < ng; g++) {
+        const int bits = std::min(PF_BITS_H, nl - PF_BITS_H * g);
+        for (int i = 0; i < (1 << bits); i++) {
+            cd v(1.0);
+            for (int j = 0; j < bits; j++) {
+                const int q = n - 1 - (PF_BITS_H * g + j);
+                v *= st->pf_s[2 * q + ((i >> j) & 1)];
+            }
+            h[2 * (((size_t)g << PF_BITS_H) + i)] = v.real();
+            h[2 * (((size_t)g << PF_BITS_H) + i) + 1] = v.imag();
+        }
+    }
+    std::vector<float> hf;
+    const void *src = h.data();
+    if (!st->dbl) {
+        hf.assign(h.begin(), h.end());
+        src = hf.data();
+    }
+    tqd_ctx *c = st->ctx;
+    CUDA_TRY(st, cudaMemcpyAsync(st->pf_dev, src, tab_bytes, cudaMemcpyHostToDevice, c->stream));
+    st->met.h2d_bytes += tab_bytes;
+    const int ev = ev_begin(st, CAT_OTHER);
+    CUDA_TRY(st, launch_prefix_init(st->dbl, st->psi, 1ull << nl, ng, st->pf_dev, c->stream));
+    ev_end(st, ev);
+    CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host tables go out of scope
+    st->met.kernel_launches++;
+    st->met.hbm_bytes += shard_bytes(st);
+    for (char in : st->pf_in) st->met.gates_applied += in ? 1 : 0;
+    return TQD_OK;
+}
+
+// gradients of the prefix gates from lambda at the prefix boundary (st->lam)
+static int prefix_grads(tqd_state *st, std::vector<double> &grad) {
+    tqd_ctx *c = st->ctx;
+    const int nl = st->n_loc, n = st->n, ng = st->pf_ng;
+    const size_t tab_elems = (size_t)ng << PF_BITS_H;
+    double *dM = (double *)((char *)st->pf_dev + tab_elems * st->esz);
+    CUDA_TRY(st, cudaMemsetAsync(dM, 0, tab_elems * 2 * sizeof(double), c->stream));
+    const int ev = ev_begin(st, CAT_OTHER);
+    CUDA_TRY(st, launch_prefix_contract(st->dbl, st->lam, 1ull << nl, ng, st->pf_dev, dM, c->sms, c->stream));
+    ev_end(st, ev);
+    std::vector<double> M(tab_elems * 2);
+    CUDA_TRY(st, cudaMemcpyAsync(M.data(), dM, M.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+    st->met.kernel_launches++;
+    st->met.hbm_bytes += shard_bytes(st);
+    st->met.d2h_bytes += M.size() * sizeof(double);
+    // T_q(v) = sum_{i: bit j of i = v} M_g[i] prod_{j' != j in group g} s_{q'}(bit j')
+    std::vector<cd> T(2 * n, cd(0.0));
+    for (int g = 0; g < ng; g++) {
+        const int bits = std::min(PF_BITS_H, nl - PF_BITS_H * g);
+        for (int j = 0; j < bits; j++) {
+            const int q = n - 1 - (PF_BITS_H * g + j);
+            for (int i = 0; i < (1 << bits); i++) {
+                cd e(1.0);
+                for (int jj = 0; jj < bits; jj++) {
+                    if (jj == j) continue;
+                    e *= st->pf_s[2 * (n - 1 - (PF_BITS_H * g + jj)) + ((i >> jj) & 1)];
+                }
+                const cd m(M[2 * (((size_t)g << PF_BITS_H) + i)], M[2 * (((size_t)g << PF_BITS_H) + i) + 1]);
+                T[2 * q + ((i >> j) & 1)] += m * e;
+            }
+        }
+    }
+    // d s_q / d theta for every generator of every prefix gate: replay the qubit's
+    // prefix gates with dU = G U inserted at that gate
+    for (size_t i = 0; i < st->gates.size() && i < st->pf_in.size(); i++) {
+        if (!st->pf_in[i] || !st->gates[i].ngen) continue;
+        const GateRec &gi = st->gates[i];
+        const int q = gi.w[0];
+        for (int p = 0; p < gi.ngen; p++) {
+            cd a(1.0), b(0.0);
+            for (size_t k = 0; k < st->gates.size(); k++) {
+                if (!st->pf_in[k] || st->gates[k].w[0] != q) continue;
+                const GateRec &gk = st->gates[k];
+                cd na = gk.M[0] * a + gk.M[1] * b, nb = gk.M[2] * a + gk.M[3] * b;
+                if (k == i) {
+                    const cd ga = gk.G[p][0] * na + gk.G[p][1] * nb, gb = gk.G[p][2] * na + gk.G[p][3] * nb;
+                    na = ga;
+                    nb = gb;
+                }
+                a = na;
+                b = nb;
+            }
+            grad[gi.slot0 + p] += 2.0 * (T[2 * q] * a + T[2 * q + 1] * b).real();
+        }
+    }
+    return TQD_OK;
+}
+
 // Execute the recorded gates [executed, end).  end < gates.size() only from
 // tqd_adjoint_grad: the gates [end, size) were absorbed into the observable
 // (absorb_tail) and are never applied; the plan caches are keyed by that split.
@@ -778,7 +949,14 @@ static int execute_pending(tqd_state *st, size_t end = SIZE_MAX, bool keep_tail 
         if (!keep_tail) st->executed = st->gates.size();
         return TQD_OK;
     }
-    const uint64_t tmix = (uint64_t)(st->gates.size() - end) * 0x9E3779B97F4A7C15ull;
+    uint64_t tmix = (uint64_t)(st->gates.size() - end) * 0x9E3779B97F4A7C15ull;
+    if (prefix_build(st, end)) {
+        // the prefix replaces |0..0> + its gates' sweeps; it is part of the plan's structure
+        for (size_t i = 0; i < st->pf_in.size(); i++)
+            if (st->pf_in[i]) tmix = (tmix ^ (i + 1)) * 1099511628211ull;
+        int rc = prefix_init(st);
+        if (rc) return rc;
+    }
     if (st->executed == 0 && st->fwd_cache_version != st->tape_version && st->enc_fwd->valid &&
         !st->cached_stages.empty() && st->cached_tmix == tmix) {
         const uint64_t vh = tape_values_hash(st);
@@ -800,7 +978,8 @@ static int execute_pending(tqd_state *st, size_t end = SIZE_MAX, bool keep_tail 
         return TQD_OK;
     }
     std::vector<int> pending;
-    for (size_t i = st->executed; i < end; i++) pending.push_back((int)i);
+    for (size_t i = st->executed; i < end; i++)
+        if (!st->pf_on || !st->pf_in[i]) pending.push_back((int)i);
     std::vector<Stage> stages;
     std::string err;
     const bool from_zero = st->executed == 0;
@@ -1007,6 +1186,7 @@ static int state_init(tqd_ctx *c, int n, tqd_dtype dt, int batch, void *dev_buf,
 int tqd_state_reset(tqd_state *st) {
     int rc = check_live(st);
     if (rc) return rc;
+    st->pf_on = false;
     st->gates.clear();
     st->brec.clear();
     st->history.clear();
@@ -1031,6 +1211,7 @@ int tqd_state_reset(tqd_state *st) {
 int tqd_state_rewind(tqd_state *st) {
     int rc = check_live(st);
     if (rc) return rc;
+    st->pf_on = false;
     st->history.clear();
     st->history_cached = false;
     st->executed = 0;
@@ -1065,6 +1246,7 @@ int tqd_state_free(tqd_state *st) {
     if (st->d_red) cudaFree(st->d_red);
     if (st->d_xy) cudaFree(st->d_xy);
     if (st->circ_dev) cudaFree(st->circ_dev);
+    if (st->pf_dev) cudaFree(st->pf_dev);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
     delete st;
     return TQD_OK;
@@ -1091,6 +1273,7 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_PRODUCT_PREFIX: st->opt_prefix = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_CIRCUIT_MAX:
         if (v < 0 || v > 12) return fail(TQD_ERR_ARG, "circuit_max must be in [0, 12]");
         st->opt_circuit = (int)v; return TQD_OK;
@@ -1318,6 +1501,8 @@ static int reverse_and_collect(tqd_state *st, double *d_grad, int n_grad, double
         for (const POp &o : *ops)
             if (st->gates[o.gate].ngen) { first = (int)i; break; }
     }
+    const bool pf_grads = prefix_has_grads(st);  // lambda down to the prefix boundary
+    if (pf_grads && !st->history.empty()) first = 0;
     if (first >= 0) {
         // backward stage list = the forward history reversed; its descriptors are
         // cached with the forward plan when the history is the cached one
@@ -1344,6 +1529,12 @@ static int reverse_and_collect(tqd_state *st, double *d_grad, int n_grad, double
     st->met.d2h_bytes += (n_grad + 1) * sizeof(double);
     *out_value = h[0] + value_host;
     for (int p = 0; p < n_grad; p++) out_grad[p] = h[p + 1];
+    if (pf_grads) {
+        std::vector<double> pg(n_grad, 0.0);
+        rc = prefix_grads(st, pg);
+        if (rc) return rc;
+        for (int p = 0; p < n_grad; p++) out_grad[p] += pg[p];
+    }
     st->consumed = true;
     return ev_collect(st);
 }

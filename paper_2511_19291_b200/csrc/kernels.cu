@@ -674,6 +674,123 @@ cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bo
 #undef TQD_C
 }
 
+static int grid_for(uint64_t n, int threads);
+// ---------------------------------------------------------------------------
+// Product-state prefix (exact rewrite; abi.cpp prefix_build): every qubit's leading
+// 1-qubit gates act on |0> before the qubit meets a multi-qubit gate, so after them
+// the state is the product psi_P(b) = prod_q s_q(b_q).  With the local physical bits
+// cut into groups of PF_BITS (low first), psi_P(b) = prod_g tab_g[b's bits of group g]
+// (tables built on the host in fp64).  prefix_init writes psi_P (replaces |0..0>
+// and the prefix gates' sweeps); prefix_contract computes, for the adjoint state at
+// the prefix boundary, M_g[i] = sum_{b: group g of b = i} conj(lam(b)) prod_{h != g}
+// tab_h[b's bits of group h] -- the environments from which the host finishes the
+// prefix gates' gradients 2 Re <lam|d psi_P / d theta>.
+constexpr int PF_BITS = 10;
+constexpr int PF_MAXG = 4;
+template <typename Real>
+__global__ void __launch_bounds__(256) prefix_init_kernel(typename CT<Real>::C *__restrict__ psi, uint64_t n, int ng,
+                                                          const typename CT<Real>::C *__restrict__ tab) {
+    typedef typename CT<Real>::C C;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n; b += (uint64_t)gridDim.x * blockDim.x) {
+        C v = tab[b & ((1u << PF_BITS) - 1)];
+        for (int g = 1; g < ng; g++) v = cmul(v, tab[(g << PF_BITS) + ((b >> (PF_BITS * g)) & ((1u << PF_BITS) - 1))]);
+        psi[b] = v;
+    }
+}
+
+// one CTA (256 threads) per contiguous range of 1024-amplitude chunks (group 0 = the
+// chunk offset, groups >= 1 uniform per chunk); M_0 in per-thread fp64 registers, the
+// chunk sums S_c = sum conj(lam) tab_0 -> M_g[g-index] += S_c * prod_{h >= 1, h != g}
+// tab_h in shared memory; global fp64 atomics at the end
+template <typename Real>
+__global__ void __launch_bounds__(256) prefix_contract_kernel(const typename CT<Real>::C *__restrict__ lam, uint64_t n,
+                                                              int ng, const typename CT<Real>::C *__restrict__ tab,
+                                                              double *__restrict__ M) {
+    typedef typename CT<Real>::C C;
+    constexpr int CH = 1 << PF_BITS, PER = CH / 256;
+    extern __shared__ __align__(16) double sm[];  // (ng - 1) x CH complex fp64
+    __shared__ double red[2][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < (ng - 1) * CH * 2; i += 256) sm[i] = 0.0;
+    double m0r[PER], m0i[PER];
+    C t0[PER];
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
+        m0r[j] = m0i[j] = 0.0;
+        t0[j] = tab[tid + 256 * j];
+    }
+    __syncthreads();
+    const uint64_t nch = n >> PF_BITS;
+    const uint64_t per = (nch + gridDim.x - 1) / gridDim.x;
+    const uint64_t c0 = (uint64_t)blockIdx.x * per, c1 = c0 + per < nch ? c0 + per : nch;
+    for (uint64_t c = c0; c < c1; c++) {
+        // the chunk's factors of groups >= 1 (uniform): all of them and all-but-one
+        C f[PF_MAXG];
+        C P = mk<C>(1, 0);
+        for (int g = 1; g < ng; g++) {
+            f[g] = tab[(g << PF_BITS) + ((c >> (PF_BITS * (g - 1))) & (CH - 1))];
+            P = cmul(P, f[g]);
+        }
+        double sr = 0.0, si = 0.0;
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            const C l = lam[(c << PF_BITS) + tid + 256 * j];
+            const C x = mk<C>(l.x, -l.y);  // conj(lambda)
+            const C y = cmul(x, P);
+            m0r[j] += (double)y.x;
+            m0i[j] += (double)y.y;
+            const C z = cmul(x, t0[j]);
+            sr += (double)z.x;
+            si += (double)z.y;
+        }
+        sr = warp_sum(sr);
+        si = warp_sum(si);
+        if (lane == 0) { red[0][warp] = sr; red[1][warp] = si; }
+        __syncthreads();
+        if (tid < ng - 1) {  // thread g-1 adds S_c * prod_{h >= 1, h != g} f_h into M_g
+            double Sr = 0.0, Si = 0.0;
+            for (int w = 0; w < 8; w++) { Sr += red[0][w]; Si += red[1][w]; }
+            const int g = tid + 1;
+            double er = 1.0, ei = 0.0;
+            for (int h = 1; h < ng; h++) {
+                if (h == g) continue;
+                const double nr = er * (double)f[h].x - ei * (double)f[h].y, ni = er * (double)f[h].y + ei * (double)f[h].x;
+                er = nr; ei = ni;
+            }
+            const int idx = (int)((c >> (PF_BITS * (g - 1))) & (CH - 1));
+            sm[((g - 1) * CH + idx) * 2] += Sr * er - Si * ei;
+            sm[((g - 1) * CH + idx) * 2 + 1] += Sr * ei + Si * er;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
+        if (m0r[j] != 0.0) atomicAdd(&M[(tid + 256 * j) * 2], m0r[j]);
+        if (m0i[j] != 0.0) atomicAdd(&M[(tid + 256 * j) * 2 + 1], m0i[j]);
+    }
+    for (int i = tid; i < (ng - 1) * CH * 2; i += 256)
+        if (sm[i] != 0.0) atomicAdd(&M[CH * 2 + i], sm[i]);
+}
+
+cudaError_t launch_prefix_init(bool dbl, void *psi, uint64_t n, int ng, const void *tab, cudaStream_t s) {
+    const int th = 256;
+    if (dbl) prefix_init_kernel<double><<<grid_for(n, th), th, 0, s>>>((double2 *)psi, n, ng, (const double2 *)tab);
+    else prefix_init_kernel<float><<<grid_for(n, th), th, 0, s>>>((float2 *)psi, n, ng, (const float2 *)tab);
+    return cudaGetLastError();
+}
+cudaError_t launch_prefix_contract(bool dbl, const void *lam, uint64_t n, int ng, const void *tab, double *M, int sms,
+                                   cudaStream_t s) {
+    const uint64_t nch = n >> PF_BITS;
+    const int grid = (int)std::min<uint64_t>(nch, (uint64_t)sms * 4);
+    const size_t smem = (size_t)(ng - 1) * (1u << PF_BITS) * 2 * sizeof(double);
+    cudaError_t e = dbl ? cudaFuncSetAttribute(prefix_contract_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                        : cudaFuncSetAttribute(prefix_contract_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (dbl) prefix_contract_kernel<double><<<grid, 256, smem, s>>>((const double2 *)lam, n, ng, (const double2 *)tab, M);
+    else prefix_contract_kernel<float><<<grid, 256, smem, s>>>((const float2 *)lam, n, ng, (const float2 *)tab, M);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // Z-string observables in physical masks.
 

@@ -894,12 +894,13 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             o[0] = b0;
 #pragma unroll
             for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] + c[ctz4(r)];
-            if (BWD && S.no_store) {
+            if (BWD && S.no_store == 1) {
                 // last reverse sweep: psi / lambda are not needed any more
             } else if (sc.m == 0) {
+                // no_store 2: the last reverse sweep before a product prefix keeps lambda only
 #pragma unroll
                 for (int r = 0; r < NR; r++) {
-                    stcs_c(psi + o[r], a[r]);
+                    if (!(BWD && S.no_store == 2)) stcs_c(psi + o[r], a[r]);
                     if (BWD) stcs_c(lam + o[r], l[r]);
                 }
             } else {

@@ -206,7 +206,8 @@ struct DevStage {
     int32_t lam_init;           // backward only: 1 = build lambda = H psi on load
     int32_t flags;              // kernel variant bits (SWF_*)
     int32_t batch;              // states in the batch: op / slot tables repeat per state (n_ops, n_slots each)
-    int32_t no_store;           // backward only: last reverse stage, psi / lambda are not needed afterwards
+    int32_t no_store;           // backward only, last reverse stage: 1 = psi / lambda not needed afterwards,
+                                // 2 = lambda only (product prefix: its environments give gradients)
     int32_t n_cvals, n_uvals;   // diagonal blocks: per-thread C rows, per-tile U values (see DTerm)
     int32_t n_dblk;             // applying diagonal-block kops in the stage
 };

@@ -453,9 +453,11 @@ def test_abi_errors(tqd, ctx):
     assert e.value.code == -2
 
 
-def test_metrics_account_bytes(tqd, ctx):
+@pytest.mark.parametrize("prefix", [0, 1])
+def test_metrics_account_bytes(tqd, ctx, prefix):
     n = 20
     st = make_state(tqd, ctx, n, "c64")
+    st.set_option(tqd.OPT_PRODUCT_PREFIX, prefix)
     st.apply_circuit(W.hea(n, 3, 0))
     st.reset_metrics()
     st.adjoint_grad(W.sum_z(n))
@@ -464,8 +466,9 @@ def test_metrics_account_bytes(tqd, ctx):
     sb = 8 << n
     assert m["fwd_sweeps"] > 0 and m["bwd_sweeps"] == m["fwd_sweeps"]
     assert m["fwd_sweep_bytes"] == 2 * sb * m["fwd_sweeps"]
-    # the last reverse sweep reads psi and lambda but stores neither
-    assert m["bwd_sweep_bytes"] == 4 * sb * (m["bwd_sweeps"] - 1) + 2 * sb
+    # the last reverse sweep reads psi and lambda but stores neither (with the product
+    # prefix it stores lambda: the prefix gates' gradients come from its environments)
+    assert m["bwd_sweep_bytes"] == 4 * sb * (m["bwd_sweeps"] - 1) + (3 if prefix else 2) * sb
     # the last layer's RZs and ring CNOTs are absorbed into the Z observable
     assert m["gates_absorbed"] == 2 * n
     assert m["gates_applied"] + m["gates_absorbed"] == 3 * 3 * n
@@ -679,3 +682,49 @@ def test_apply_circuit_matches_per_gate(tqd, ctx, orc, dtype):
     assert st.n_params == before
     st.apply_circuit([])
     st.free()
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [11, 14, 21])
+def test_product_prefix(tqd, ctx, orc, n, dtype):
+    """TQD_OPT_PRODUCT_PREFIX: every qubit's leading 1-qubit gates (all kinds, trainable
+    and fixed, several per qubit) form a product state written directly; their gradients
+    come from lambda's environments at the prefix boundary.  Against the oracle applying
+    every gate, and prefix on == off."""
+    rng = np.random.default_rng(n)
+    gates = []
+    for _ in range(3):  # prefix: several 1-qubit gates per qubit, interleaved across qubits
+        for q in rng.permutation(n):
+            k = ["RY", "RZ", "RX", "U3", "H", "S", "MAT1"][int(rng.integers(7))]
+            if k == "MAT1":
+                gates += W.random_circuit(n, 1, int(rng.integers(1 << 30)), kinds=["MAT1"])
+                gates[-1] = W.Gate("MAT1", (int(q),), (), gates[-1].matrix, False)
+            elif k in ("RY", "RZ", "RX"):
+                gates.append(W.Gate(k, (int(q),), (float(rng.uniform(0, 6.3)),)))
+            elif k == "U3":
+                gates.append(W.Gate(k, (int(q),), tuple(float(v) for v in rng.uniform(0, 6.3, 3))))
+            else:
+                gates.append(W.Gate(k, (int(q),)))
+    gates += [W.Gate("CNOT", (q, (q + 1) % n)) for q in range(0, n, 2)]
+    gates += [W.Gate("RY", (q,), (float(rng.uniform(0, 6.3)),)) for q in range(n)]  # q odd: still prefix
+    gates += W.hea(n, 2, seed=n, small=True) + W.random_circuit(n, 30, n + 1)
+    terms = W.random_z_terms(n, 4, n) + W.sum_z(n) + [(1, 2, 0.4)]
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ref = orc.run(n, gates)
+    out = {}
+    for pf in (1, 0):
+        st = make_state(tqd, ctx, n, dtype, small_max=0)
+        st.set_option(tqd.OPT_PRODUCT_PREFIX, pf)
+        st.apply_circuit(gates)
+        amps = st.amplitudes()
+        st.reset()
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(terms)
+        st.rewind()  # the cached plan + prefix replayed
+        val2, grad2 = st.adjoint_grad(terms)
+        st.free()
+        assert np.max(np.abs(amps - ref)) < TOL[dtype]["amp"], pf
+        for v, g in ((val, grad), (val2, grad2)):
+            assert abs(v - rval) < TOL[dtype]["val"] and np.max(np.abs(g - rgrad)) < TOL[dtype]["val"], pf
+        out[pf] = grad
+    assert np.max(np.abs(out[1] - out[0])) < TOL[dtype]["val"]
