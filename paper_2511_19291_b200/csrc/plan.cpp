@@ -583,9 +583,13 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
             const char *e = getenv("TQD_PLAN_SEG_MIN_GATES");
             return e ? atoi(e) : 6;
         }();
+        static const int seg_keep = [] {  // segments always kept (experiment knob)
+            const char *e = getenv("TQD_PLAN_SEG_KEEP");
+            return e ? std::max(1, atoi(e)) : 3;
+        }();
         for (;;) {
             const int ls = last_used();
-            if (ls < 3 || seg_min_gates <= 0) break;
+            if (ls < seg_keep || seg_min_gates <= 0) break;
             int cnt = 0;
             for (int i : order) if (seg_of[i] == ls) cnt++;
             if (cnt >= seg_min_gates) break;
