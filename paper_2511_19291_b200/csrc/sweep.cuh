@@ -440,10 +440,12 @@ __device__ __forceinline__ void run_dblk(const uint4 h, const KOp<Real> &op, typ
     // e^{i al_b} on the amplitudes with register bit b set
     const C w0 = cis_turn(th, ctb);
     if ((h.x >> 16) & 2u) {  // identity table
+        if (th != 0) {  // (a run flushed for one register bit has no th terms: th == 0 exactly)
 #pragma unroll
-        for (int r = 0; r < NR; r++) {
-            a[r] = cmulp(w0, a[r]);
-            if (BWD) l[r] = cmulp(w0, l[r]);
+            for (int r = 0; r < NR; r++) {
+                a[r] = cmulp(w0, a[r]);
+                if (BWD) l[r] = cmulp(w0, l[r]);
+            }
         }
     } else {
 #pragma unroll
