@@ -636,6 +636,213 @@ __global__ void __launch_bounds__(512) circuit_reg_kernel(const DevOp *__restric
     }
 }
 
+// Two amplitudes per thread (idx = tid << 1 | r, r = 0, 1): the cfg-1 kernel.  Same
+// op semantics as circuit_reg_kernel<Real, 1> but the gate loop is straight code on
+// scalar registers (no arrays / lambdas that the compiler shuffles through moves),
+// the partner / coefficient choice hoisted per thread.
+template <typename C>
+__device__ __forceinline__ C c_apply(uint8_t form, const double *m, bool hi, C x, C xo) {
+    typedef decltype(C::x) Real;
+    if (form == CF_SWAP) return xo;
+    if (form == CF_REAL) {
+        const Real cm = (Real)(hi ? m[3] : m[0]), co = (Real)(hi ? m[2] : m[1]);
+        return mk<C>(cm * x.x + co * xo.x, cm * x.y + co * xo.y);
+    }
+    const int im_ = hi ? 6 : 0, io = hi ? 4 : 2;
+    const C cm = mk<C>((Real)m[im_], (Real)m[im_ + 1]), co = mk<C>((Real)m[io], (Real)m[io + 1]);
+    return cmul2(cm, x, co, xo);
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(512) circuit_r1_kernel(const DevOp *__restrict__ fops, int n_f,
+                                                         const DevOp *__restrict__ bops, int n_b,
+                                                         const typename CT<Real>::C *__restrict__ psi,
+                                                         const ZTerms *__restrict__ zts, double *__restrict__ eval,
+                                                         double *__restrict__ grad, int n_loc) {
+    typedef typename CT<Real>::C C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[32];
+    const uint64_t N = 1ull << n_loc;
+    fops += (size_t)blockIdx.x * n_f;
+    bops += (size_t)blockIdx.x * n_b;
+    psi += (size_t)blockIdx.x * N;
+    const ZTerms &zt = zts[blockIdx.x];
+    C *X0 = reinterpret_cast<C *>(smem_raw);
+    DevOp *sf = reinterpret_cast<DevOp *>(X0 + 4 * N);
+    DevOp *sb = sf + n_f;
+    COp *cf = reinterpret_cast<COp *>(sb + n_b);
+    COp *cbk = cf + n_f;
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(fops);
+        int4 *dst = reinterpret_cast<int4 *>(sf);
+        for (int i = threadIdx.x; i < n_f * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
+        src = reinterpret_cast<const int4 *>(bops);
+        dst = reinterpret_cast<int4 *>(sb);
+        for (int i = threadIdx.x; i < n_b * (int)(sizeof(DevOp) / 16); i += blockDim.x) dst[i] = src[i];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_f + n_b; i += blockDim.x) decode_cop<1>(i < n_f ? sf[i] : sb[i - n_f], i < n_f ? cf[i] : cbk[i - n_f]);
+    const int lane = threadIdx.x & 31;
+    const uint32_t t0 = (uint32_t)threadIdx.x << 1, t1 = t0 | 1u;
+    C a0 = psi[t0], a1 = psi[t1], l0 = mk<C>(0, 0), l1 = mk<C>(0, 0);
+    __syncthreads();
+    int xb = 0;
+    auto grad_add = [&](int slot, Real part) {
+        const double w = warp_sum<double>((double)part);
+        if (lane == 0 && w != 0.0) atomicAdd(&grad[slot], w);
+    };
+    auto generic = [&](const DevOp &op, bool two) {
+        C *XA = X0 + (size_t)xb * 2 * N, *XL = XA + N;
+        xb ^= 1;
+        XA[t0] = a0; XA[t1] = a1;
+        if (two) { XL[t0] = l0; XL[t1] = l1; }
+        __syncthreads();
+        circ_apply<Real>(op, XA, XL, N, 0, two);
+        __syncthreads();
+        a0 = XA[t0]; a1 = XA[t1];
+        if (two) { l0 = XL[t0]; l1 = XL[t1]; }
+    };
+    for (int pass = 0; pass < 2; pass++) {
+        const bool two = pass == 1;
+        const int nops = two ? n_b : n_f;
+        const COp *cc = two ? cbk : cf;
+        const DevOp *dd = two ? sb : sf;
+        if (two) {  // lambda = H psi, E = <psi|H|psi>
+            double e = 0.0;
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const uint32_t b = r ? t1 : t0;
+                double h = zt.cst;
+                for (int p = 0; p < n_loc; p++)
+                    if ((b >> p) & 1u) h -= 2.0 * zt.w[p];
+                for (int t = 0; t < zt.T; t++) h += (__popcll((uint64_t)b & zt.z[t]) & 1) ? -zt.c[t] : zt.c[t];
+                const C a = r ? a1 : a0;
+                const C lv = mk<C>((Real)h * a.x, (Real)h * a.y);
+                if (r) l1 = lv; else l0 = lv;
+                e += h * ((double)a.x * a.x + (double)a.y * a.y);
+            }
+            e = block_sum<double>(e, red);
+            if (threadIdx.x == 0) atomicAdd(eval, e);
+        }
+        for (int oi = 0; oi < nops; oi++) {
+            const COp &c = cc[oi];
+            const uint8_t cls = c.cls;
+            if (cls == CC_REG || cls == CC_LANE || cls == CC_WARP) {
+                const int p = c.p;
+                C ao0, ao1, lo0 = mk<C>(0, 0), lo1 = mk<C>(0, 0);
+                if (cls == CC_REG) {  // p == 0: the pair is this thread's (a0, a1)
+                    ao0 = a1; ao1 = a0;
+                    if (two) { lo0 = l1; lo1 = l0; }
+                } else if (cls == CC_LANE) {
+                    const int mk_ = 1 << (p - 1);
+                    ao0 = shfl_c(a0, mk_); ao1 = shfl_c(a1, mk_);
+                    if (two) { lo0 = shfl_c(l0, mk_); lo1 = shfl_c(l1, mk_); }
+                } else {
+                    C *XA = X0 + (size_t)xb * 2 * N, *XL = XA + N;
+                    xb ^= 1;
+                    XA[t0] = a0; XA[t1] = a1;
+                    if (two) { XL[t0] = l0; XL[t1] = l1; }
+                    __syncthreads();
+                    const uint32_t f = 1u << p;
+                    ao0 = XA[t0 ^ f]; ao1 = XA[t1 ^ f];
+                    if (two) { lo0 = XL[t0 ^ f]; lo1 = XL[t1 ^ f]; }
+                }
+                if (two && c.ngen) {  // Y / X generator, each pair from its bit-0 member
+                    Real part = 0;
+                    const bool h0 = (t0 >> p) & 1u, h1 = (t1 >> p) & 1u;
+                    if (c.gk == GEN_Y) {
+                        if (!h0) part += re_cj(lo0, a0) - re_cj(l0, ao0);
+                        if (!h1) part += re_cj(lo1, a1) - re_cj(l1, ao1);
+                    } else {
+                        if (!h0) part += im_cj(l0, ao0) + im_cj(lo0, a0);
+                        if (!h1) part += im_cj(l1, ao1) + im_cj(lo1, a1);
+                    }
+                    grad_add(c.slot, part);
+                }
+                const bool on0 = c.cb == 0xff || ((t0 >> c.cb) & 1u), on1 = c.cb == 0xff || ((t1 >> c.cb) & 1u);
+                // coefficients once per op: for a lane / warp target both amplitudes share the
+                // target bit (one row of the 2x2); a register target pairs a0 (bit 0) with a1
+                if (c.form == CF_SWAP) {
+                    if (on0) { a0 = ao0; if (two) l0 = lo0; }
+                    if (on1) { a1 = ao1; if (two) l1 = lo1; }
+                } else if (c.form == CF_REAL) {
+                    if (cls == CC_REG) {
+                        const Real m00 = (Real)c.m[0], m01 = (Real)c.m[1], m10 = (Real)c.m[2], m11 = (Real)c.m[3];
+                        if (on0) {  // on0 == on1 (the control is not bit 0)
+                            const C x0 = a0, x1 = a1;
+                            a0 = mk<C>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
+                            a1 = mk<C>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
+                            if (two) {
+                                const C y0 = l0, y1 = l1;
+                                l0 = mk<C>(m00 * y0.x + m01 * y1.x, m00 * y0.y + m01 * y1.y);
+                                l1 = mk<C>(m10 * y0.x + m11 * y1.x, m10 * y0.y + m11 * y1.y);
+                            }
+                        }
+                    } else {
+                        const bool hi = (t0 >> p) & 1u;
+                        const Real cm = (Real)(hi ? c.m[3] : c.m[0]), co = (Real)(hi ? c.m[2] : c.m[1]);
+                        if (on0) {
+                            a0 = mk<C>(cm * a0.x + co * ao0.x, cm * a0.y + co * ao0.y);
+                            if (two) l0 = mk<C>(cm * l0.x + co * lo0.x, cm * l0.y + co * lo0.y);
+                        }
+                        if (on1) {
+                            a1 = mk<C>(cm * a1.x + co * ao1.x, cm * a1.y + co * ao1.y);
+                            if (two) l1 = mk<C>(cm * l1.x + co * lo1.x, cm * l1.y + co * lo1.y);
+                        }
+                    }
+                } else {
+                    const bool hi0 = (t0 >> p) & 1u, hi1 = (t1 >> p) & 1u;
+                    if (on0) { a0 = c_apply(c.form, c.m, hi0, a0, ao0); if (two) l0 = c_apply(c.form, c.m, hi0, l0, lo0); }
+                    if (on1) { a1 = c_apply(c.form, c.m, hi1, a1, ao1); if (two) l1 = c_apply(c.form, c.m, hi1, l1, lo1); }
+                }
+            } else if (cls == CC_D1 || cls == CC_D2) {
+                const int j0 = cls == CC_D1 ? (int)((t0 >> c.b0) & 1u) : (int)(2 * ((t0 >> c.b0) & 1u) + ((t0 >> c.b1) & 1u));
+                const int j1 = cls == CC_D1 ? (int)((t1 >> c.b0) & 1u) : (int)(2 * ((t1 >> c.b0) & 1u) + ((t1 >> c.b1) & 1u));
+                if (two && c.ngen) {  // Z generator on bit b0
+                    const Real v0 = im_cj(l0, a0), v1 = im_cj(l1, a1);
+                    grad_add(c.slot, (((t0 >> c.b0) & 1u) ? -v0 : v0) + (((t1 >> c.b0) & 1u) ? -v1 : v1));
+                }
+                const C d0 = mk<C>((Real)c.m[2 * j0], (Real)c.m[2 * j0 + 1]);
+                const C d1 = mk<C>((Real)c.m[2 * j1], (Real)c.m[2 * j1 + 1]);
+                a0 = cmul(d0, a0); a1 = cmul(d1, a1);
+                if (two) { l0 = cmul(d0, l0); l1 = cmul(d1, l1); }
+            } else {
+                // other ops (U2 / MAT2, general generators): shared memory, small-state code
+                const DevOp &op = dd[oi];
+                if (two && op.ngen) {
+                    C *XA = X0 + (size_t)xb * 2 * N, *XL = XA + N;
+                    XA[t0] = a0; XA[t1] = a1; XL[t0] = l0; XL[t1] = l1;
+                    __syncthreads();
+                    for (int gi = 0; gi < op.ngen; gi++) {
+                        Real part = 0;
+                        if (op.kind == OP_D1) {
+                            for (uint64_t i = threadIdx.x; i < N; i += blockDim.x) {
+                                const Real v = im_cj(XL[i], XA[i]);
+                                part += ((i >> op.b0.idx) & 1ull) ? -v : v;
+                            }
+                        } else {
+                            const int pp = op.t0;
+                            const int gk = op.gkind[gi];
+                            const C g00 = ldc<C>(op.g[gi], 0), g01 = ldc<C>(op.g[gi], 1), g10 = ldc<C>(op.g[gi], 2),
+                                    g11 = ldc<C>(op.g[gi], 3);
+                            for (uint64_t i = threadIdx.x; i < N / 2; i += blockDim.x) {
+                                const uint64_t i0 = ins0(i, pp), i1 = i0 | (1ull << pp);
+                                const C x0 = XA[i0], x1 = XA[i1], y0 = XL[i0], y1 = XL[i1];
+                                if (gk == GEN_Y) part += re_cj(y1, x0) - re_cj(y0, x1);
+                                else if (gk == GEN_X) part += im_cj(y0, x1) + im_cj(y1, x0);
+                                else part += 2 * (re_cj(y0, cmul2(g00, x0, g01, x1)) + re_cj(y1, cmul2(g10, x0, g11, x1)));
+                            }
+                        }
+                        grad_add(op.slot[gi], part);
+                    }
+                    __syncthreads();
+                }
+                generic(op, two);
+            }
+        }
+    }
+}
+
 cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
                            const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
                            cudaStream_t s) {
@@ -647,7 +854,7 @@ cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bo
         const int threads = 1 << (n_loc - rb);
 #define TQD_R(T)                                                                                               \
     {                                                                                                          \
-        auto fn = rb == 1 ? circuit_reg_kernel<T, 1> : circuit_reg_kernel<T, 2>;                               \
+        auto fn = rb == 1 ? circuit_r1_kernel<T> : circuit_reg_kernel<T, 2>;                                   \
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reg_smem); \
         if (e != cudaSuccess) return e;                                                                        \
         fn<<<batch, threads, reg_smem, s>>>(fops, n_f, bops, n_b, (const CT<T>::C *)psi, zts, eval, grad, n_loc); \
