@@ -49,7 +49,8 @@ cudaError_t launch_set_one(bool dbl, void *psi, cudaStream_t s);
 cudaError_t launch_remap_block(bool dbl, void *shard, void *stage, uint64_t e0, uint64_t cnt, uint64_t bdep, uint64_t rest,
                               bool unpack, cudaStream_t s);
 cudaError_t launch_debug_delay(uint32_t us, cudaStream_t s);
-cudaError_t launch_prefix_init(bool dbl, void *psi, uint64_t n, int ng, const void *tab, cudaStream_t s);
+cudaError_t launch_prefix_init(bool dbl, void *psi, uint64_t n, int ng, const void *tab, double cre, double cim,
+                               cudaStream_t s);
 cudaError_t launch_prefix_contract(bool dbl, const void *lam, uint64_t n, int ng, const void *tab, double *M, int sms,
                                    cudaStream_t s);
 cudaError_t dense_tc_upload(const double *U, int m, void **bsplit, cudaStream_t s);
@@ -649,8 +650,9 @@ static void encode_all(tqd_state *st, const std::vector<Stage> &stages, bool bwd
     // the last reverse sweep stores neither psi nor lambda (only gradients remain)
     int skip_below = 0, last_sweep = -1;
     if (bwd) {
-        skip_below = (int)st->gates.size();
-        for (size_t i = 0; i < st->gates.size(); i++)
+        // (prefix gradients need lambda at the prefix boundary: every gate un-applied)
+        skip_below = prefix_has_grads(st) ? 0 : (int)st->gates.size();
+        for (size_t i = 0; i < (size_t)skip_below; i++)
             if (st->gates[i].ngen) { skip_below = (int)i; break; }
         for (size_t ii = 0; ii < stages.size(); ii++)
             if (stages[ii].type != ST_REMAP) last_sweep = (int)ii;
@@ -796,13 +798,13 @@ static uint64_t tape_values_hash(const tqd_state *st) {
 // reset) instead of sweeping those gates; the adjoint stops at the prefix boundary
 // and finishes their gradients from the environments of lambda (prefix_contract_kernel,
 // one read of lambda): dE/dtheta_j = 2 Re sum_v T_q(v) (d s_q / d theta_j)(v).
-// Single state on one GPU, from |0..0>, local qubits >= 11.
+// Single state, from |0..0>, local qubits >= 11; with world > 1 the sharded qubits'
+// factors are one scalar per rank (c_r), their gradients come from every rank's total
+// contraction Z_r (one small all-reduce).
 constexpr int PF_BITS_H = 10;
 static bool prefix_build(tqd_state *st, size_t end) {
     st->pf_on = false;
-    if (!st->opt_prefix || st->ctx->world != 1 || st->batch != 1 || st->executed != 0 || st->n_loc < 11 ||
-        st->n_loc > 40)
-        return false;
+    if (!st->opt_prefix || st->batch != 1 || st->executed != 0 || st->n_loc < 11 || st->n_loc > 40) return false;
     const int n = st->n;
     st->pf_in.assign(st->gates.size(), 0);
     st->pf_s.assign(2 * n, cd(0.0));
@@ -826,6 +828,18 @@ static bool prefix_build(tqd_state *st, size_t end) {
     }
     st->pf_on = any;
     return any;
+}
+
+// the global (sharded) qubits' factor of rank r: prod over the rank bits of s_q(bit)
+// (physical position n_loc + i = qubit n-1-n_loc-i at the start), skipping qubit `skip`
+static cd prefix_rank_factor(const tqd_state *st, int r, int skip) {
+    cd v(1.0);
+    for (int i = 0; i < st->g; i++) {
+        const int q = st->n - 1 - (st->n_loc + i);
+        if (q == skip) continue;
+        v *= st->pf_s[2 * q + ((r >> i) & 1)];
+    }
+    return v;
 }
 
 // the group tables tab_g[i] = prod over the group's physical bits of s_q(bit), q the
@@ -868,8 +882,9 @@ static int prefix_init(tqd_state *st) {
     tqd_ctx *c = st->ctx;
     CUDA_TRY(st, cudaMemcpyAsync(st->pf_dev, src, tab_bytes, cudaMemcpyHostToDevice, c->stream));
     st->met.h2d_bytes += tab_bytes;
+    const cd cr = prefix_rank_factor(st, c->rank, -1);
     const int ev = ev_begin(st, CAT_OTHER);
-    CUDA_TRY(st, launch_prefix_init(st->dbl, st->psi, 1ull << nl, ng, st->pf_dev, c->stream));
+    CUDA_TRY(st, launch_prefix_init(st->dbl, st->psi, 1ull << nl, ng, st->pf_dev, cr.real(), cr.imag(), c->stream));
     ev_end(st, ev);
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host tables go out of scope
     st->met.kernel_launches++;
@@ -879,6 +894,8 @@ static int prefix_init(tqd_state *st) {
 }
 
 // gradients of the prefix gates from lambda at the prefix boundary (st->lam)
+static int allreduce_sum(tqd_state *st, double *d, size_t count);
+
 static int prefix_grads(tqd_state *st, std::vector<double> &grad) {
     tqd_ctx *c = st->ctx;
     const int nl = st->n_loc, n = st->n, ng = st->pf_ng;
@@ -894,6 +911,43 @@ static int prefix_grads(tqd_state *st, std::vector<double> &grad) {
     st->met.kernel_launches++;
     st->met.hbm_bytes += shard_bytes(st);
     st->met.d2h_bytes += M.size() * sizeof(double);
+    // world > 1: this rank's total contraction Z_r (M_0 . tab_0), then M scaled by the
+    // rank factor c_r and summed over the ranks together with every rank's Z_r
+    std::vector<cd> Zr(c->world, cd(0.0));
+    if (c->world > 1) {
+        std::vector<cd> t0(1 << PF_BITS_H, cd(0.0));
+        {
+            const int bits = std::min(PF_BITS_H, nl);
+            for (int i = 0; i < (1 << bits); i++) {
+                cd v(1.0);
+                for (int j = 0; j < bits; j++) v *= st->pf_s[2 * (n - 1 - j) + ((i >> j) & 1)];
+                t0[i] = v;
+            }
+        }
+        cd z(0.0);
+        for (int i = 0; i < (1 << PF_BITS_H); i++) z += cd(M[2 * i], M[2 * i + 1]) * t0[i];
+        const cd cr = prefix_rank_factor(st, c->rank, -1);
+        for (size_t i = 0; i < tab_elems; i++) {
+            const cd v = cd(M[2 * i], M[2 * i + 1]) * cr;
+            M[2 * i] = v.real();
+            M[2 * i + 1] = v.imag();
+        }
+        std::vector<double> buf(M);
+        buf.resize(M.size() + 2 * c->world, 0.0);
+        buf[M.size() + 2 * c->rank] = z.real();
+        buf[M.size() + 2 * c->rank + 1] = z.imag();
+        const size_t bytes = buf.size() * sizeof(double);
+        int rc = ensure_red(st, buf.size());  // (the gradients are already on the host)
+        if (rc) return rc;
+        dM = st->d_red;
+        CUDA_TRY(st, cudaMemcpyAsync(dM, buf.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+        rc = allreduce_sum(st, dM, buf.size());
+        if (rc) return rc;
+        CUDA_TRY(st, cudaMemcpyAsync(buf.data(), dM, bytes, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < M.size(); i++) M[i] = buf[i];
+        for (int r = 0; r < c->world; r++) Zr[r] = cd(buf[M.size() + 2 * r], buf[M.size() + 2 * r + 1]);
+    }
     // T_q(v) = sum_{i: bit j of i = v} M_g[i] prod_{j' != j in group g} s_{q'}(bit j')
     std::vector<cd> T(2 * n, cd(0.0));
     for (int g = 0; g < ng; g++) {
@@ -910,6 +964,12 @@ static int prefix_grads(tqd_state *st, std::vector<double> &grad) {
                 T[2 * q + ((i >> j) & 1)] += m * e;
             }
         }
+    }
+    // sharded qubits: T_q(v) = sum over the ranks whose bit of q is v of Z_r times the
+    // other sharded qubits' factors
+    for (int i = 0; i < st->g && c->world > 1; i++) {
+        const int q = n - 1 - (nl + i);
+        for (int r = 0; r < c->world; r++) T[2 * q + ((r >> i) & 1)] += Zr[r] * prefix_rank_factor(st, r, q);
     }
     // d s_q / d theta for every generator of every prefix gate: replay the qubit's
     // prefix gates with dU = G U inserted at that gate

@@ -896,10 +896,12 @@ constexpr int PF_BITS = 10;
 constexpr int PF_MAXG = 4;
 template <typename Real>
 __global__ void __launch_bounds__(256) prefix_init_kernel(typename CT<Real>::C *__restrict__ psi, uint64_t n, int ng,
-                                                          const typename CT<Real>::C *__restrict__ tab) {
+                                                          const typename CT<Real>::C *__restrict__ tab, Real cre,
+                                                          Real cim) {
     typedef typename CT<Real>::C C;
+    const C cr = mk<C>(cre, cim);  // this rank's factor of the global (sharded) qubits
     for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n; b += (uint64_t)gridDim.x * blockDim.x) {
-        C v = tab[b & ((1u << PF_BITS) - 1)];
+        C v = cmul(cr, tab[b & ((1u << PF_BITS) - 1)]);
         for (int g = 1; g < ng; g++) v = cmul(v, tab[(g << PF_BITS) + ((b >> (PF_BITS * g)) & ((1u << PF_BITS) - 1))]);
         psi[b] = v;
     }
@@ -979,10 +981,11 @@ __global__ void __launch_bounds__(256) prefix_contract_kernel(const typename CT<
         if (sm[i] != 0.0) atomicAdd(&M[CH * 2 + i], sm[i]);
 }
 
-cudaError_t launch_prefix_init(bool dbl, void *psi, uint64_t n, int ng, const void *tab, cudaStream_t s) {
+cudaError_t launch_prefix_init(bool dbl, void *psi, uint64_t n, int ng, const void *tab, double cre, double cim,
+                               cudaStream_t s) {
     const int th = 256;
-    if (dbl) prefix_init_kernel<double><<<grid_for(n, th), th, 0, s>>>((double2 *)psi, n, ng, (const double2 *)tab);
-    else prefix_init_kernel<float><<<grid_for(n, th), th, 0, s>>>((float2 *)psi, n, ng, (const float2 *)tab);
+    if (dbl) prefix_init_kernel<double><<<grid_for(n, th), th, 0, s>>>((double2 *)psi, n, ng, (const double2 *)tab, cre, cim);
+    else prefix_init_kernel<float><<<grid_for(n, th), th, 0, s>>>((float2 *)psi, n, ng, (const float2 *)tab, (float)cre, (float)cim);
     return cudaGetLastError();
 }
 cudaError_t launch_prefix_contract(bool dbl, const void *lam, uint64_t n, int ng, const void *tab, double *M, int sms,

@@ -310,3 +310,51 @@ def test_world_unfused_remap_then_fused_race(tqd, orc, monkeypatch):
             assert abs(val - rval) < 1e-10 and np.max(np.abs(grad - rgrad)) < 1e-10
         assert np.max(np.abs(amp - ref)) < 1e-12
         assert m["fused_remaps"] > 0 and m["remaps"] > m["fused_remaps"]
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n", [(2, 12), (4, 13), (8, 14)])
+def test_world_product_prefix(tqd, orc, world, n, dtype, fused):
+    """Product-state prefix with sharded qubits: each rank writes its shard of the
+    product (the rank bits' factor c_r), the prefix gradients of local qubits come from
+    the rank-summed environments, those of the sharded qubits from every rank's total
+    contraction (small all-reduce).  Against the oracle, prefix on == off."""
+    rng = np.random.default_rng(world + n)
+    gates = []
+    for _ in range(2):
+        for q in rng.permutation(n):
+            k = ["RY", "RZ", "RX", "U3", "H"][int(rng.integers(5))]
+            if k == "U3":
+                gates.append(W.Gate(k, (int(q),), tuple(float(v) for v in rng.uniform(0, 6.3, 3))))
+            elif k == "H":
+                gates.append(W.Gate(k, (int(q),)))
+            else:
+                gates.append(W.Gate(k, (int(q),), (float(rng.uniform(0, 6.3)),)))
+    gates += W.hea(n, 2, world, small=True) + W.random_circuit(n, 40, 7 * world)
+    terms = W.random_z_terms(n, 4, world) + W.sum_z(n) + [(1, 0, 0.7)]
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ref = orc.run(n, gates)
+
+    def fn(r, ctx):
+        out = {}
+        for pf in (1, 0):
+            st = tqd.State(ctx, n, dtype)
+            st.set_option(tqd.OPT_TILE_QUBITS, 9)
+            st.set_option(tqd.OPT_SMALL_MAX, 0)
+            st.set_option(tqd.OPT_FUSED_REMAP, fused)
+            st.set_option(tqd.OPT_PRODUCT_PREFIX, pf)
+            st.apply_circuit(gates)
+            amp = st.amplitudes()
+            st.reset()
+            st.apply_circuit(gates)
+            val, grad = st.adjoint_grad(terms)
+            st.free()
+            out[pf] = (amp, val, grad)
+        return out
+    for out in run_world(tqd, world, fn):
+        for pf in (1, 0):
+            amp, val, grad = out[pf]
+            assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"], pf
+            assert abs(val - rval) < TOL[dtype]["val"], pf
+            assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"], pf

@@ -692,7 +692,9 @@ def test_product_prefix(tqd, ctx, orc, n, dtype):
     come from lambda's environments at the prefix boundary.  Against the oracle applying
     every gate, and prefix on == off."""
     rng = np.random.default_rng(n)
-    gates = []
+    # fixed 2-qubit gates before the first trainable (prefix) gate: lambda must still be
+    # un-applied through them down to the prefix boundary
+    gates = [W.Gate("CZ", (n - 1, 0)), W.Gate("CNOT", (1, 2))]
     for _ in range(3):  # prefix: several 1-qubit gates per qubit, interleaved across qubits
         for q in rng.permutation(n):
             k = ["RY", "RZ", "RX", "U3", "H", "S", "MAT1"][int(rng.integers(7))]
