@@ -300,6 +300,7 @@ def main():
     g_applied = m["gates_applied"] // args.steps
     g_unapplied = m["gates_unapplied"] // args.steps
     g_absorbed = m["gates_absorbed"] // args.steps
+    g_prefix = m["gates_prefix"] // args.steps
     units = g_applied * (1 << n)
     value = units / (ms / 1e3) / 1e9
 
@@ -406,6 +407,9 @@ def main():
                            "parallelism": f"state sharded over {world} rank(s) by {g} global qubit(s)",
                            "l2": f"inputs larger than L2: {shard * 2 / 2**30:.0f} GiB psi+lambda per GPU",
                            "gates_absorbed_per_step": g_absorbed,
+                           "gates_in_product_prefix_per_step": g_prefix,
+                           "product_prefix": "leading product-preserving gates written as one product state "
+                                             "(counted in gates_applied; gradients from lambda's environments)",
                            "absorption": "trailing diagonal/permutation gates folded into the Z observable "
                                          "(Heisenberg picture; same value and gradients)" if not args.no_absorb
                                          else "off: every gate applied",

@@ -117,8 +117,11 @@ typedef enum {
                                * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
                                * force a few KiB so the chunk loop iterates.               */
     TQD_OPT_PRODUCT_PREFIX = 9, /* 1 (default): every qubit's leading 1-qubit gates (before its
-                               * first multi-qubit gate) act on |0>: a single state on one GPU
-                               * starts from their product state (one write pass instead of
+                               * first entangling gate) act on |0>; fixed 2-qubit gates that
+                               * keep the product (SWAP; diagonal or controlled gates with one
+                               * qubit in a parameter-independent basis state) join them.  A
+                               * single state (batch 1, >= 11 local qubits, any world size)
+                               * starts from that product state (one write pass instead of
                                * their sweeps) and the adjoint finishes their gradients from
                                * lambda's environments at the prefix boundary (one read pass);
                                * same values and gradients.  0: sweep every gate.          */
@@ -152,6 +155,8 @@ typedef struct tqd_metrics {
     uint64_t fused_remaps;      /* remaps done by the preceding sweep's peer-memory stores */
     uint64_t plans_reused;      /* executions that reused the plan of a structurally equal tape */
     uint64_t gates_absorbed;    /* trailing gates absorbed into Z observables (TQD_OPT_ABSORB_TAIL) */
+    uint64_t gates_prefix;      /* gates written as the product-state prefix (TQD_OPT_PRODUCT_PREFIX;
+                                   counted in gates_applied too)                      */
 } tqd_metrics;
 
 /* --- context ------------------------------------------------------------- */

@@ -53,6 +53,7 @@ class Metrics(ctypes.Structure):
         ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
         ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("fused_remaps", ctypes.c_uint64),
         ("plans_reused", ctypes.c_uint64), ("gates_absorbed", ctypes.c_uint64),
+        ("gates_prefix", ctypes.c_uint64),
     ]
 
     def as_dict(self):

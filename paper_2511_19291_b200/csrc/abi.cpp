@@ -80,6 +80,12 @@ struct tqd_ctx {
 
 enum Cat { CAT_FWD = 0, CAT_BWD = 1, CAT_OTHER = 2, CAT_A2A = 3 };
 
+// product-state prefix: one gate of the prefix as a 1-qubit op on product factor `slot`
+struct PfOp {
+    int gate, slot;
+    cd M[4];
+};
+
 struct tqd_state {
     tqd_ctx *ctx = nullptr;
     int n = 0, n_loc = 0, g = 0;
@@ -115,7 +121,9 @@ struct tqd_state {
     int opt_prefix = 1;            // TQD_OPT_PRODUCT_PREFIX
     bool pf_on = false;
     std::vector<char> pf_in;       // per gate: in the prefix
-    std::vector<cd> pf_s;          // per qubit: s_q (2 entries)
+    std::vector<cd> pf_s;          // per qubit: s_q (2 entries) at the prefix boundary
+    std::vector<PfOp> pf_ops;      // the prefix as 1-qubit ops on product factors, in gate order
+    std::vector<int> pf_slot_of;   // per qubit: its product factor at the boundary
     int pf_ng = 0;
     void *pf_dev = nullptr;        // group tables (device, state dtype) + M environments (fp64)
     size_t pf_cap = 0;
@@ -793,7 +801,12 @@ static uint64_t tape_values_hash(const tqd_state *st) {
 // Every qubit's leading run of 1-qubit gates acts on |0> before the qubit meets any
 // multi-qubit gate (the gates of other qubits commute with them), so after those
 // gates the state is the product psi_P = (x)_q s_q with s_q = (its gates) |0>
-// (e.g. the HEA's first RY + RZ layer, Listing 2's encoder).  The
+// (e.g. the HEA's first RY + RZ layer, Listing 2's encoder).  A
+// fixed 2-qubit gate on two such qubits keeps the product when it only relabels
+// (SWAP) or when one of its qubits is in a parameter-independent computational basis
+// state |v>: a diagonal gate then acts on the other qubit as diag(d[v,0], d[v,1]), a
+// controlled gate with that control as U (v = 1) or I (v = 0).  (A QFT of a basis
+// state is a product state this way: each CP meets a still-unrotated control.)  The
 // forward writes psi_P directly (prefix_init_kernel, the same HBM pass as the |0..0>
 // reset) instead of sweeping those gates; the adjoint stops at the prefix boundary
 // and finishes their gradients from the environments of lambda (prefix_contract_kernel,
@@ -807,24 +820,82 @@ static bool prefix_build(tqd_state *st, size_t end) {
     if (!st->opt_prefix || st->batch != 1 || st->executed != 0 || st->n_loc < 11 || st->n_loc > 40) return false;
     const int n = st->n;
     st->pf_in.assign(st->gates.size(), 0);
-    st->pf_s.assign(2 * n, cd(0.0));
-    for (int q = 0; q < n; q++) st->pf_s[2 * q] = cd(1.0);
+    st->pf_ops.clear();
+    // product factors ("slots"): slot f starts as qubit f in |0>; a SWAP of two
+    // untouched qubits exchanges their slots
+    std::vector<cd> sv(2 * n, cd(0.0));
+    std::vector<int> slot_of(n), fixed(n, 1);  // fixed: no trainable gate in the slot's chain yet
+    for (int q = 0; q < n; q++) { sv[2 * q] = cd(1.0); slot_of[q] = q; }
+    auto zero = [](cd v) { return v.real() == 0.0 && v.imag() == 0.0; };
+    // basis bit of a slot whose state is exactly |0> or |1> (up to a phase) and
+    // independent of the parameters, else -1
+    auto basis = [&](int f) -> int {
+        if (!fixed[f]) return -1;
+        if (zero(sv[2 * f + 1])) return 0;
+        if (zero(sv[2 * f])) return 1;
+        return -1;
+    };
+    auto apply = [&](size_t i, int f, const cd *M) {
+        PfOp o;
+        o.gate = (int)i;
+        o.slot = f;
+        for (int j = 0; j < 4; j++) o.M[j] = M[j];
+        st->pf_ops.push_back(o);
+        const cd a = sv[2 * f], b = sv[2 * f + 1];
+        sv[2 * f] = M[0] * a + M[1] * b;
+        sv[2 * f + 1] = M[2] * a + M[3] * b;
+    };
     std::vector<char> touched(n, 0);
     bool any = false;
     for (size_t i = 0; i < end; i++) {
         const GateRec &g = st->gates[i];
-        if (g.nw != 1) {
-            for (int j = 0; j < g.nw; j++) touched[g.w[j]] = 1;
-            continue;
+        bool free_ = !g.batched;
+        for (int j = 0; j < g.nw; j++) free_ = free_ && !touched[g.w[j]];
+        bool take = false;
+        if (free_ && g.nw == 1) {
+            const int f = slot_of[g.w[0]];
+            apply(i, f, g.M);
+            if (g.ngen) fixed[f] = 0;
+            take = true;
+        } else if (free_ && g.nw == 2) {
+            // a fixed 2-qubit gate keeps the product when it is a relabeling or one of
+            // its qubits is in a parameter-independent basis state: it then acts on
+            // the other factor as the 1-qubit gate selected by that bit (exact)
+            const int a = g.w[0], b = g.w[1], fa = slot_of[a], fb = slot_of[b];
+            const int va = basis(fa), vb = basis(fb);
+            if (g.cls == CL_IDENT) {
+                take = true;
+            } else if (g.cls == CL_SWAP) {
+                std::swap(slot_of[a], slot_of[b]);
+                take = true;
+            } else if (g.cls == CL_DIAG2 && (va >= 0 || vb >= 0)) {
+                // M index = 2 bit(w0) + bit(w1)
+                if (va >= 0) {
+                    const cd D[4] = {g.M[5 * (2 * va)], cd(0.0), cd(0.0), g.M[5 * (2 * va + 1)]};
+                    apply(i, fb, D);
+                } else {
+                    const cd D[4] = {g.M[5 * vb], cd(0.0), cd(0.0), g.M[5 * (2 + vb)]};
+                    apply(i, fa, D);
+                }
+                take = true;
+            } else if (g.cls == CL_CTRL1 && va >= 0) {  // [control, target]
+                if (va == 1) apply(i, fb, g.sub);
+                take = true;
+            }
         }
-        if (g.batched) { touched[g.w[0]] = 1; continue; }
-        const int q = g.w[0];
-        if (touched[q]) continue;
-        st->pf_in[i] = 1;
-        any = true;
-        const cd a = st->pf_s[2 * q], b = st->pf_s[2 * q + 1];
-        st->pf_s[2 * q] = g.M[0] * a + g.M[1] * b;
-        st->pf_s[2 * q + 1] = g.M[2] * a + g.M[3] * b;
+        if (take) {
+            st->pf_in[i] = 1;
+            any = true;
+        } else {
+            for (int j = 0; j < g.nw; j++) touched[g.w[j]] = 1;
+        }
+    }
+    // per qubit: its slot's factor
+    st->pf_s.assign(2 * n, cd(0.0));
+    st->pf_slot_of = slot_of;
+    for (int q = 0; q < n; q++) {
+        st->pf_s[2 * q] = sv[2 * slot_of[q]];
+        st->pf_s[2 * q + 1] = sv[2 * slot_of[q] + 1];
     }
     st->pf_on = any;
     return any;
@@ -889,7 +960,10 @@ static int prefix_init(tqd_state *st) {
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host tables go out of scope
     st->met.kernel_launches++;
     st->met.hbm_bytes += shard_bytes(st);
-    for (char in : st->pf_in) st->met.gates_applied += in ? 1 : 0;
+    for (char in : st->pf_in) {
+        st->met.gates_applied += in ? 1 : 0;
+        st->met.gates_prefix += in ? 1 : 0;
+    }
     return TQD_OK;
 }
 
@@ -971,20 +1045,24 @@ static int prefix_grads(tqd_state *st, std::vector<double> &grad) {
         const int q = n - 1 - (nl + i);
         for (int r = 0; r < c->world; r++) T[2 * q + ((r >> i) & 1)] += Zr[r] * prefix_rank_factor(st, r, q);
     }
-    // d s_q / d theta for every generator of every prefix gate: replay the qubit's
-    // prefix gates with dU = G U inserted at that gate
-    for (size_t i = 0; i < st->gates.size() && i < st->pf_in.size(); i++) {
-        if (!st->pf_in[i] || !st->gates[i].ngen) continue;
-        const GateRec &gi = st->gates[i];
-        const int q = gi.w[0];
+    // d s_f / d theta for every generator of every prefix gate: replay the gate's
+    // slot chain from |0> with dU = G U inserted at that gate; T of the qubit holding
+    // the slot at the boundary
+    std::vector<int> q_of_slot(n);
+    for (int q = 0; q < n; q++) q_of_slot[st->pf_slot_of[q]] = q;
+    for (size_t oi = 0; oi < st->pf_ops.size(); oi++) {
+        const PfOp &oi_ = st->pf_ops[oi];
+        const GateRec &gi = st->gates[oi_.gate];
+        if (!gi.ngen) continue;
+        const int f = oi_.slot, q = q_of_slot[f];
         for (int p = 0; p < gi.ngen; p++) {
             cd a(1.0), b(0.0);
-            for (size_t k = 0; k < st->gates.size(); k++) {
-                if (!st->pf_in[k] || st->gates[k].w[0] != q) continue;
-                const GateRec &gk = st->gates[k];
-                cd na = gk.M[0] * a + gk.M[1] * b, nb = gk.M[2] * a + gk.M[3] * b;
-                if (k == i) {
-                    const cd ga = gk.G[p][0] * na + gk.G[p][1] * nb, gb = gk.G[p][2] * na + gk.G[p][3] * nb;
+            for (size_t k = 0; k < st->pf_ops.size(); k++) {
+                const PfOp &o = st->pf_ops[k];
+                if (o.slot != f) continue;
+                cd na = o.M[0] * a + o.M[1] * b, nb = o.M[2] * a + o.M[3] * b;
+                if (k == oi) {
+                    const cd ga = gi.G[p][0] * na + gi.G[p][1] * nb, gb = gi.G[p][2] * na + gi.G[p][3] * nb;
                     na = ga;
                     nb = gb;
                 }

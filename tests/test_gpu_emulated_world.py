@@ -358,3 +358,31 @@ def test_world_product_prefix(tqd, orc, world, n, dtype, fused):
             assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"], pf
             assert abs(val - rval) < TOL[dtype]["val"], pf
             assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"], pf
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("world,n", [(2, 12), (4, 13), (8, 14)])
+def test_world_product_prefix_qft(tqd, orc, world, n, dtype):
+    """cfg-5 family sharded: X-prep + QFT (+ SWAPs) + HEA as the product prefix with
+    sharded qubits among its factors; amplitudes and gradients against the oracle."""
+    wl = W.config(5, seed=world, n_override=n)
+    rval, rgrad = orc.adjoint(n, wl.gates, wl.terms)
+    ref = orc.run(n, wl.gates)
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, dtype)
+        st.set_option(tqd.OPT_TILE_QUBITS, 9)
+        st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.apply_circuit(wl.gates)
+        amp = st.amplitudes()
+        npre = st.metrics()["gates_prefix"]
+        st.reset()
+        st.apply_circuit(wl.gates)
+        val, grad = st.adjoint_grad(wl.terms)
+        st.free()
+        return amp, val, grad, npre
+    for amp, val, grad, npre in run_world(tqd, world, fn):
+        assert npre == sum(1 for g in wl.gates if g.name in ("X", "H", "SWAP", "MAT2")) + 2 * n
+        assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"]
+        assert abs(val - rval) < TOL[dtype]["val"]
+        assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]

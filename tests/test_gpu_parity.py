@@ -730,3 +730,93 @@ def test_product_prefix(tqd, ctx, orc, n, dtype):
             assert abs(v - rval) < TOL[dtype]["val"] and np.max(np.abs(g - rgrad)) < TOL[dtype]["val"], pf
         out[pf] = grad
     assert np.max(np.abs(out[1] - out[0])) < TOL[dtype]["val"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [12, 15])
+def test_product_prefix_qft_of_basis_state(tqd, ctx, orc, n, dtype):
+    """cfg-5 family: X-prep + QFT + HEA.  The QFT of a basis state is a product state
+    (each controlled phase meets a still-unrotated control qubit), so the whole QFT,
+    its SWAPs and the HEA's first RY + RZ layer form the product prefix.  Against the
+    oracle applying every gate, prefix on == off, and the prefix gate count."""
+    wl = W.config(5, seed=n, n_override=n)
+    gates = wl.gates
+    rval, rgrad = orc.adjoint(n, gates, wl.terms)
+    ref = orc.run(n, gates)
+    n_pre = sum(1 for g in gates if g.name in ("X", "H", "SWAP") or g.name == "MAT2") + 2 * n  # + first RY, RZ layer
+    out = {}
+    for pf in (1, 0):
+        st = make_state(tqd, ctx, n, dtype, small_max=0)
+        st.set_option(tqd.OPT_PRODUCT_PREFIX, pf)
+        st.apply_circuit(gates)
+        amps = st.amplitudes()
+        m = st.metrics()
+        st.reset()
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(wl.terms)
+        st.free()
+        assert np.max(np.abs(amps - ref)) < TOL[dtype]["amp"], pf
+        assert abs(val - rval) < TOL[dtype]["val"] and np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"], pf
+        assert m["gates_prefix"] == (n_pre if pf else 0), (pf, m["gates_prefix"], n_pre)
+        out[pf] = grad
+    assert np.max(np.abs(out[1] - out[0])) < TOL[dtype]["val"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_product_prefix_two_qubit_rules(tqd, ctx, orc, seed, dtype):
+    """Random prefixes mixing X / H / trainable rotations with fixed CZ / CP / CNOT /
+    SWAP / diagonal and controlled MAT2 gates: the 2-qubit gates join the product only
+    when one qubit is in a parameter-independent basis state (a trainable rotation,
+    even RX(0) exactly, disqualifies its qubit), then random entangling gates.
+    Against the oracle and prefix off, including gradients of rotations at angle 0."""
+    n = 12
+    rng = np.random.default_rng(100 + seed)
+    gates = []
+    for _ in range(40):
+        r = rng.random()
+        a, b = (int(v) for v in rng.choice(n, 2, replace=False))
+        if r < 0.15:
+            gates.append(W.Gate("X", (a,)))
+        elif r < 0.25:
+            gates.append(W.Gate("H", (a,)))
+        elif r < 0.35:
+            k = ["RX", "RY", "RZ"][int(rng.integers(3))]
+            th = 0.0 if rng.random() < 0.3 else float(rng.uniform(0, 6.3))
+            gates.append(W.Gate(k, (a,), (th,)))
+        elif r < 0.5:
+            gates.append(W.Gate("CZ", (a, b)))
+        elif r < 0.6:
+            gates.append(W.Gate("MAT2", (a, b), (), W.cphase_matrix(float(rng.uniform(0, 6.3))), False))
+        elif r < 0.72:
+            gates.append(W.Gate("CNOT", (a, b)))
+        elif r < 0.8:
+            gates.append(W.Gate("SWAP", (a, b)))
+        elif r < 0.9:
+            d = np.exp(1j * rng.uniform(0, 6.3, 4))
+            gates.append(W.Gate("MAT2", (a, b), (), np.diag(d).astype(np.complex128), False))
+        else:  # controlled-U on wire a (block diag(I, U))
+            u = W.random_circuit(1, 1, int(rng.integers(1 << 30)), kinds=["MAT1"])[0].matrix
+            m = np.eye(4, dtype=np.complex128)
+            m[2:, 2:] = u
+            gates.append(W.Gate("MAT2", (a, b), (), m, False))
+    gates += W.hea(n, 2, seed=seed, small=True) + W.random_circuit(n, 30, seed + 5)
+    terms = W.random_z_terms(n, 4, seed) + W.sum_z(n) + [(1 << 3, 1 << 5, 0.3)]
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ref = orc.run(n, gates)
+    out = {}
+    for pf in (1, 0):
+        st = make_state(tqd, ctx, n, dtype, small_max=0)
+        st.set_option(tqd.OPT_PRODUCT_PREFIX, pf)
+        st.apply_circuit(gates)
+        amps = st.amplitudes()
+        st.reset()
+        st.apply_circuit(gates)
+        val, grad = st.adjoint_grad(terms)
+        st.free()
+        assert np.max(np.abs(amps - ref)) < TOL[dtype]["amp"], pf
+        assert abs(val - rval) < TOL[dtype]["val"] and np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"], pf
+        out[pf] = grad
+    assert np.max(np.abs(out[1] - out[0])) < TOL[dtype]["val"]

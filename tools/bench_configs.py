@@ -13,7 +13,8 @@ events).  One JSON line per case on stdout.
   cfg3   30q HEA d20 complex64 (= bench.py), plus a tile-size sweep (--ksweep)
   cfg4   33q HEA d10 complex64 at P = 1 (128 GiB psi + lambda on one GPU)
   cfg5/8 the 2^33-amplitude per-GPU shard of cfg5 (36q over 8 GPUs): 33q
-         X-prep + QFT + HEA d4 on one GPU (local sweeps only, no remaps)
+         X-prep + QFT + HEA d4 on one GPU (local sweeps only, no remaps);
+         cfg5_8_sweep: the same with the product prefix off (the QFT swept)
 
   python tools/bench_configs.py [--cases cfg1,cfg2,...] [--steps K] [--warmup W] [--ksweep 9,10,11,12,13]
 """
@@ -42,16 +43,17 @@ def peak_gbs():
 GRAPH = 0
 
 
-def run_case(ctx, name, wl, steps, warmup, tile=0, note=""):
+def run_case(ctx, name, wl, steps, warmup, tile=0, note="", prefix=1):
     stream = torch.cuda.current_stream()
     n, gates, terms = wl.n, wl.gates, wl.terms
     st = tqd.State(ctx, n, wl.dtype)
+    st.set_option(tqd.OPT_PRODUCT_PREFIX, prefix)
     if tile:
         st.set_option(tqd.OPT_TILE_QUBITS, tile)
     if GRAPH:
         st.set_option(tqd.OPT_USE_GRAPH, 1)
     out = {"case": name, "workload": wl.name, "n_qubits": n, "dtype": wl.dtype, "gates": len(gates),
-           "tile_k": tile or "default", "cuda_graph": GRAPH, "note": note}
+           "tile_k": tile or "default", "cuda_graph": GRAPH, "product_prefix": prefix, "note": note}
     try:
         st.apply_circuit(gates)
 
@@ -91,6 +93,8 @@ def run_case(ctx, name, wl, steps, warmup, tile=0, note=""):
         shard = (8 if wl.dtype == "c64" else 16) << n
         pk = peak_gbs()
         out["fwd_sweeps"], out["bwd_sweeps"] = m["fwd_sweeps"], m["bwd_sweeps"]
+        # gates written as the product-state prefix / absorbed into the observable (not swept)
+        out["gates_prefix"], out["gates_absorbed"] = m["gates_prefix"], m["gates_absorbed"]
         if m["fwd_sweeps"] and m["fwd_sweep_ms"] > 0:
             a = m["fwd_sweep_ms"] / m["fwd_sweeps"]
             out["fwd_sweep_avg_ms"] = round(a, 4)
@@ -148,7 +152,11 @@ def main():
             elif c == "cfg5_8":
                 run_case(ctx, c, W.config(5, n_override=33), args.steps, args.warmup,
                          note="the per-GPU shard size of cfg5 (36q over 8 GPUs = 2^33 amplitudes per GPU): "
-                              "local sweeps of the same circuit family, no remaps")
+                              "local sweeps of the same circuit family, no remaps; X-prep + QFT + first "
+                              "RY/RZ layer written as the product-state prefix")
+            elif c == "cfg5_8_sweep":
+                run_case(ctx, c, W.config(5, n_override=33), args.steps, args.warmup, prefix=0,
+                         note="cfg5_8 with TQD_OPT_PRODUCT_PREFIX = 0: the QFT swept (diagonal-block stages)")
         for k in [int(x) for x in args.ksweep.split(",") if x]:
             run_case(ctx, f"ksweep_k{k}", W.config(3, n_override=args.ksweep_qubits), args.steps, args.warmup,
                      tile=k, note="tile-size sweep (SURVEY.md §8(d) cfg 3)")
