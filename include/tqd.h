@@ -129,6 +129,13 @@ typedef enum {
                                * run tqd_adjoint_grad with Z-string terms as ONE kernel launch:
                                * forward gates, lambda = H psi and the reverse sweep in one
                                * CTA's shared memory per state (0 = staged sweeps only)     */
+    TQD_OPT_CIRCUIT_LAYOUT = 10, /* 0 (default): the single launch runs gate by gate (2 amplitudes
+                               * per thread, 16 warps); 1 (experiment): for 8..10 local qubits
+                               * and circuits of 1-qubit, diagonal, controlled-1-qubit and SWAP
+                               * gates, a register-layout kernel (8 amplitudes per thread, 4
+                               * warps, layout exchanges through swizzled shared memory;
+                               * metric circuit_layout_launches).  Same results; measured
+                               * slower (latency-bound at 4 warps). */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.
@@ -157,6 +164,7 @@ typedef struct tqd_metrics {
     uint64_t gates_absorbed;    /* trailing gates absorbed into Z observables (TQD_OPT_ABSORB_TAIL) */
     uint64_t gates_prefix;      /* gates written as the product-state prefix (TQD_OPT_PRODUCT_PREFIX;
                                    counted in gates_applied too)                      */
+    uint64_t circuit_layout_launches; /* single-launch circuits run by the register-layout kernel */
 } tqd_metrics;
 
 /* --- context ------------------------------------------------------------- */

@@ -30,7 +30,7 @@ GATES = {
 }
 C64, C128 = 0, 1
 OPT_TILE_QUBITS, OPT_SMALL_MAX, OPT_PROFILE, OPT_GRID_CTAS, OPT_USE_GRAPH, OPT_FUSED_REMAP, OPT_ABSORB_TAIL, \
-    OPT_STAGING_BYTES, OPT_CIRCUIT_MAX, OPT_PRODUCT_PREFIX = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9
+    OPT_STAGING_BYTES, OPT_CIRCUIT_MAX, OPT_PRODUCT_PREFIX, OPT_CIRCUIT_LAYOUT = 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10
 ERRORS = {0: "TQD_OK", -1: "TQD_ERR_ARG", -2: "TQD_ERR_QUBITS", -3: "TQD_ERR_WORLD",
           -4: "TQD_ERR_NOT_UNITARY", -5: "TQD_ERR_OOM", -6: "TQD_ERR_CUDA", -7: "TQD_ERR_NCCL",
           -8: "TQD_ERR_UNSUPPORTED", -9: "TQD_ERR_STATE"}
@@ -53,7 +53,7 @@ class Metrics(ctypes.Structure):
         ("peak_device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
         ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64), ("fused_remaps", ctypes.c_uint64),
         ("plans_reused", ctypes.c_uint64), ("gates_absorbed", ctypes.c_uint64),
-        ("gates_prefix", ctypes.c_uint64),
+        ("gates_prefix", ctypes.c_uint64), ("circuit_layout_launches", ctypes.c_uint64),
     ]
 
     def as_dict(self):

@@ -58,6 +58,10 @@ cudaError_t dense_tc_launch(float *x, uint64_t n_amps, const void *bsplit, int p
 cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
                            const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
                            cudaStream_t s);
+size_t circuit_l3_smem(bool dbl, int n_loc, int nops, int n_rows, int n_gt, int n_acc);
+cudaError_t launch_circuit_l3(bool dbl, const L3Op *ops, int n_f, int n_b, const uint32_t *xtab, const uint16_t *xreg,
+                              int n_rows, const uint16_t *accp, int n_acc, const double *gtab, int n_gt, const void *psi,
+                              const ZTerms *zts, double *eval, double *grad, int n_loc, int batch, cudaStream_t s);
 }  // namespace tqd
 
 using namespace tqd;
@@ -117,8 +121,13 @@ struct tqd_state {
     int circ_nf = 0, circ_nb = 0;
     size_t circ_off_b = 0, circ_off_z = 0;
     std::vector<int> circ_pos;  // qubit map after the cached circuit
+    // layout-circuit variant (circuit_l3_kernel) of the cached circuit
+    bool circ_l3 = false;
+    int l3_nf = 0, l3_nb = 0, l3_rows = 0, l3_nacc = 0, l3_ngt = 0;
+    size_t l3_off_x = 0, l3_off_r = 0, l3_off_a = 0, l3_off_g = 0;
     // product-state prefix of the current execution (prefix_build)
     int opt_prefix = 1;            // TQD_OPT_PRODUCT_PREFIX
+    int opt_layout = 0;            // TQD_OPT_CIRCUIT_LAYOUT (experiment, measured slower)
     bool pf_on = false;
     std::vector<char> pf_in;       // per gate: in the prefix
     std::vector<cd> pf_s;          // per qubit: s_q (2 entries) at the prefix boundary
@@ -1412,6 +1421,10 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_PRODUCT_PREFIX: st->opt_prefix = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_CIRCUIT_LAYOUT:
+        if (st->opt_layout != (v ? 1 : 0)) st->circ_key = 0;  // re-encode the cached circuit
+        st->opt_layout = v ? 1 : 0;
+        return TQD_OK;
     case TQD_OPT_CIRCUIT_MAX:
         if (v < 0 || v > 12) return fail(TQD_ERR_ARG, "circuit_max must be in [0, 12]");
         st->opt_circuit = (int)v; return TQD_OK;
@@ -1742,6 +1755,272 @@ static void build_zterms(const tqd_state *st, int T, const uint64_t *x, const ui
     }
 }
 
+// ---- layout-circuit encoder (circuit_l3_kernel; tqd_internal.h L3Op) -----------
+struct L3Enc {
+    std::vector<L3Op> ops;       // batch x (nf + nb)
+    std::vector<uint32_t> xtab;  // rows x threads
+    std::vector<uint16_t> xreg;  // rows x 16
+    std::vector<uint16_t> accp;  // batch x nacc: parameter index of each gradient accumulator
+    std::vector<double> gtab;    // batch x ngt x 8: general generators
+    int nf = 0, nb = 0, rows = 0, nacc = 0, ngt = 0;
+    std::vector<int> pos;        // qubit map after the forward (the seed's Z masks)
+};
+
+static int gf2_rank(std::vector<uint32_t> v, int nbits) {
+    int rank = 0;
+    for (int bit = 0; bit < nbits; bit++) {
+        int piv = -1;
+        for (int i = rank; i < (int)v.size(); i++)
+            if ((v[i] >> bit) & 1u) { piv = i; break; }
+        if (piv < 0) continue;
+        std::swap(v[rank], v[piv]);
+        for (int i = 0; i < (int)v.size(); i++)
+            if (i != rank && ((v[i] >> bit) & 1u)) v[i] ^= v[rank];
+        rank++;
+    }
+    return rank;
+}
+
+// Plan + encode the whole circuit for circuit_l3_kernel: gates [0, end) forward,
+// [skip_below, end) reversed with gradients.  Layouts: a gate whose target is not in
+// a register slot triggers an exchange that brings in the next (up to) three
+// register targets of the sequence (Belady: evict register bits not needed next);
+// SWAP is a relabeling of the qubit map.  false: a gate this kernel does not take
+// (general 2-qubit), or the state is out of range.
+static bool encode_l3(tqd_state *st, size_t end, int skip_below, L3Enc &E) {
+    const int n = st->n_loc;
+    if (n < 8 || n > 10 || st->n_params > 65535) return false;
+    const int T = 1 << (n - 3);
+    const int LB = st->dbl ? 3 : 4;  // lane bits of one bank phase (16-B / 8-B elements)
+    struct Item { int gate; bool bwd; int b0, b1, need; };
+    std::vector<Item> seq;
+    std::vector<int> pos = st->pos;
+    auto add = [&](int i, bool bwd) -> bool {
+        const GateRec &g = st->gates[i];
+        if (g.cls == CL_U2) return false;
+        if (g.cls == CL_IDENT) return true;
+        if (g.cls == CL_SWAP) {
+            std::swap(pos[g.w[0]], pos[g.w[1]]);
+            return true;
+        }
+        Item it{i, bwd, pos[g.w[0]], g.nw > 1 ? pos[g.w[1]] : -1, -1};
+        if (g.cls == CL_U1) it.need = it.b0;
+        else if (g.cls == CL_CTRL1) it.need = it.b1;
+        seq.push_back(it);
+        return true;
+    };
+    for (size_t i = 0; i < end; i++)
+        if (!add((int)i, false)) return false;
+    E.pos = pos;
+    E.nf = (int)seq.size();
+    for (int i = (int)end - 1; i >= skip_below; i--)
+        if (!add(i, true)) return false;
+    // layouts (slot -> physical bit) and the op order (exchanges before items)
+    std::vector<int> lay(n), where(n);
+    {
+        std::vector<int> first;
+        for (const Item &it : seq)
+            if (it.need >= 0 && std::find(first.begin(), first.end(), it.need) == first.end()) {
+                first.push_back(it.need);
+                if (first.size() == 3) break;
+            }
+        std::vector<char> used(n, 0);
+        for (int b : first) used[b] = 1;
+        int s = 0;
+        for (int b : first) lay[s++] = b;
+        for (int b = 0; b < n; b++)
+            if (!used[b]) lay[s++] = b;
+        for (int q = 0; q < n; q++) where[lay[q]] = q;
+    }
+    struct Ent { int item; int xrow; std::vector<int> wh; };  // item >= 0: gate item, else exchange row
+    std::vector<Ent> order;
+    std::vector<std::vector<int>> lays;  // per row: rows 0, 1 plain layouts; exchanges: old, new
+    std::vector<std::vector<int>> xnew;
+    lays.push_back(lay);                 // row 0
+    lays.push_back(lay);                 // row 1 (seed layout, set below)
+    xnew.push_back(lay);
+    xnew.push_back(lay);
+    int nf_ops = -1;
+    for (size_t k = 0; k <= seq.size(); k++) {
+        if ((int)k == E.nf) {
+            lays[1] = lay;
+            nf_ops = (int)order.size();
+        }
+        if (k == seq.size()) break;
+        const Item &it = seq[k];
+        if (it.need >= 0 && where[it.need] >= 3) {
+            std::vector<int> want;
+            for (size_t kk = k; kk < seq.size() && want.size() < 3; kk++) {
+                const int nd = seq[kk].need;
+                if (nd >= 0 && std::find(want.begin(), want.end(), nd) == want.end()) want.push_back(nd);
+            }
+            std::vector<int> nl = lay;
+            std::vector<int> evict;
+            for (int s = 0; s < 3; s++)
+                if (std::find(want.begin(), want.end(), lay[s]) == want.end()) evict.push_back(s);
+            size_t ei = 0;
+            for (int b : want) {
+                if (where[b] < 3) continue;
+                const int s = evict[ei++];
+                nl[where[b]] = lay[s];
+                nl[s] = b;
+            }
+            lays.push_back(lay);
+            xnew.push_back(nl);
+            order.push_back(Ent{-1, (int)lays.size() - 1, {}});
+            lay = nl;
+            for (int q = 0; q < n; q++) where[lay[q]] = q;
+        }
+        order.push_back(Ent{(int)k, -1, where});
+    }
+    E.rows = (int)lays.size();
+    if (E.rows > 65535) return false;
+    E.xtab.assign((size_t)E.rows * T, 0);
+    E.xreg.assign((size_t)E.rows * 16, 0);
+    auto thr = [&](const std::vector<int> &L, int t) {
+        uint32_t v = 0;
+        for (int i = 0; i < n - 3; i++) v |= (uint32_t)((t >> i) & 1) << L[3 + i];
+        return v;
+    };
+    auto roff = [&](const std::vector<int> &L, int r) {
+        uint32_t v = 0;
+        for (int j = 0; j < 3; j++) v |= (uint32_t)((r >> j) & 1) << L[j];
+        return v;
+    };
+    for (int e = 0; e < 2; e++) {
+        for (int t = 0; t < T; t++) E.xtab[(size_t)e * T + t] = thr(lays[e], t);
+        for (int r = 0; r < 8; r++) E.xreg[(size_t)e * 16 + r] = (uint16_t)roff(lays[e], r);
+    }
+    const uint32_t lowm = (1u << LB) - 1;
+    uint64_t rs = 0x2545F4914F6CDD1Dull;
+    for (int e = 2; e < E.rows; e++) {
+        const std::vector<int> &Lo = lays[e], &Ln = xnew[e];
+        // F: column per physical bit (LB bits), identity on the low bits; conflict-free
+        // when both layouts' first LB lane bits map to independent columns
+        std::vector<uint32_t> col(n);
+        for (int p = 0; p < n; p++) col[p] = p < LB ? (1u << p) : 0u;
+        auto ok = [&]() {
+            std::vector<uint32_t> a(LB), b(LB);
+            for (int i = 0; i < LB; i++) {
+                a[i] = col[Lo[3 + i]];
+                b[i] = col[Ln[3 + i]];
+            }
+            return gf2_rank(a, LB) == LB && gf2_rank(b, LB) == LB;
+        };
+        bool good = ok();
+        for (int tries = 0; tries < 4000 && !good; tries++) {
+            for (int p = LB; p < n; p++) {
+                rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17;
+                col[p] = (uint32_t)(rs & lowm);
+            }
+            good = ok();
+        }
+        if (!good)
+            for (int p = 0; p < n; p++) col[p] = p < LB ? (1u << p) : 0u;
+        auto S = [&](uint32_t x) {
+            uint32_t f = 0;
+            for (int p = 0; p < n; p++)
+                if ((x >> p) & 1u) f ^= col[p];
+            return (x & ~lowm) | f;
+        };
+        for (int t = 0; t < T; t++) E.xtab[(size_t)e * T + t] = S(thr(Lo, t)) | (S(thr(Ln, t)) << 16);
+        for (int r = 0; r < 8; r++) {
+            E.xreg[(size_t)e * 16 + r] = (uint16_t)S(roff(Lo, r));
+            E.xreg[(size_t)e * 16 + 8 + r] = (uint16_t)S(roff(Ln, r));
+        }
+    }
+    // accumulators / general generators (structure: the same for every batch element)
+    std::vector<int> acc0(seq.size(), -1), gi0(seq.size(), -1);
+    for (size_t k = E.nf; k < seq.size(); k++) {
+        const GateRec &g = st->gates[seq[k].gate];
+        if (!g.ngen) continue;
+        acc0[k] = E.nacc;
+        E.nacc += g.ngen;
+        bool full = false;
+        for (int p = 0; p < g.ngen; p++) full = full || (g.gkind[p] != GEN_X && g.gkind[p] != GEN_Y);
+        if (full && g.cls == CL_U1) {
+            gi0[k] = E.ngt;
+            E.ngt += g.ngen;
+        }
+    }
+    const int nops = (int)order.size();
+    E.nb = nops - nf_ops;
+    E.nf = nf_ops;
+    E.ops.assign((size_t)st->batch * nops, L3Op());
+    E.accp.assign((size_t)st->batch * E.nacc, 0);
+    E.gtab.assign((size_t)st->batch * E.ngt * 8, 0.0);
+    std::vector<GateRec> tmp;
+    for (int b = 0; b < st->batch; b++) {
+        const std::vector<GateRec> &gb = gates_for(st, b, tmp);
+        for (int oi = 0; oi < nops; oi++) {
+            L3Op &o = E.ops[(size_t)b * nops + oi];
+            memset(&o, 0, sizeof(o));
+            const Ent &en = order[oi];
+            if (en.item < 0) {
+                o.type = L3_X;
+                o.xi = (uint16_t)en.xrow;
+                continue;
+            }
+            const Item &it = seq[en.item];
+            const GateRec &g = gb[it.gate];
+            const bool bwd = it.bwd;
+            auto bk = [&](int bit, uint8_t &kind, uint8_t &idx) {
+                const int sl = en.wh[bit];
+                kind = sl < 3 ? 1 : 2;
+                idx = (uint8_t)(sl < 3 ? sl : sl - 3);
+            };
+            auto put = [&](int i, cd v) {
+                if (bwd) v = std::conj(v);
+                o.m[2 * i] = v.real();
+                o.m[2 * i + 1] = v.imag();
+            };
+            if (g.cls == CL_U1 || g.cls == CL_CTRL1) {
+                const cd *M = g.cls == CL_U1 ? g.M : g.sub;
+                o.type = L3_U1;
+                o.j = (uint8_t)en.wh[it.need];
+                if (g.cls == CL_CTRL1) bk(it.b0, o.ck, o.ci);
+                // forward M, adjoint M^dag (conj of the transpose)
+                put(0, M[0]);
+                put(1, bwd ? M[2] : M[1]);
+                put(2, bwd ? M[1] : M[2]);
+                put(3, M[3]);
+                bool real = true;
+                for (int i = 0; i < 4; i++) real = real && o.m[2 * i + 1] == 0.0;
+                const bool swp = o.m[0] == 0.0 && o.m[1] == 0.0 && o.m[6] == 0.0 && o.m[7] == 0.0 && o.m[2] == 1.0 &&
+                                 o.m[3] == 0.0 && o.m[4] == 1.0 && o.m[5] == 0.0;
+                o.form = swp ? L3F_SWAP : real ? L3F_REAL : L3F_GEN;
+            } else if (g.cls == CL_DIAG1) {
+                o.type = L3_D1;
+                bk(it.b0, o.d0k, o.d0i);
+                put(0, g.M[0]);
+                put(1, g.M[3]);
+            } else {  // CL_DIAG2: index 2 bit(w0) + bit(w1)
+                o.type = L3_D2;
+                bk(it.b0, o.d0k, o.d0i);
+                bk(it.b1, o.d1k, o.d1i);
+                for (int i = 0; i < 4; i++) put(i, g.M[5 * i]);
+            }
+            if (bwd && g.ngen) {
+                o.ngen = (uint8_t)g.ngen;
+                for (int p = 0; p < g.ngen; p++) {
+                    o.gk[p] = g.gkind[p];
+                    o.acc[p] = (uint16_t)(acc0[en.item] + p);
+                    E.accp[(size_t)b * E.nacc + acc0[en.item] + p] = (uint16_t)(g.slot0 + p);
+                }
+                if (gi0[en.item] >= 0) {
+                    o.gi = (uint16_t)gi0[en.item];
+                    for (int p = 0; p < g.ngen; p++)
+                        for (int i = 0; i < 4; i++) {
+                            E.gtab[((size_t)b * E.ngt + gi0[en.item] + p) * 8 + 2 * i] = g.G[p][i].real();
+                            E.gtab[((size_t)b * E.ngt + gi0[en.item] + p) * 8 + 2 * i + 1] = g.G[p][i].imag();
+                        }
+                }
+            }
+        }
+    }
+    return true;
+}
+
 // The whole circuit in ONE launch (circuit_kernel): forward gates, lambda = H psi and
 // the reverse sweep with gradients, one CTA per batch element, for single-GPU states
 // of <= opt_circuit qubits (BASELINE.json configs[0]: 10 qubits complex128).  The op
@@ -1758,7 +2037,60 @@ static int adjoint_circuit(tqd_state *st, int T, const uint64_t *x, const uint64
     const uint64_t key = (st->tape_version * 0x9E3779B97F4A7C15ull) ^ (uint64_t)(st->gates.size() - end) ^
                          ((uint64_t)T << 40);
     std::vector<ZTerms> zts(st->batch);
+    auto dev_alloc = [&](size_t total) -> int {
+        if (total > st->circ_cap) {
+            if (st->circ_dev) { CUDA_TRY(st, cudaStreamSynchronize(c->stream)); cudaFree(st->circ_dev); }
+            st->circ_dev = nullptr;
+            st->circ_cap = 0;
+            if (cudaMalloc(&st->circ_dev, total) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(TQD_ERR_OOM, "cannot allocate the circuit op lists");
+            }
+            st->circ_cap = total;
+        }
+        return TQD_OK;
+    };
     if (st->circ_key != key || !st->circ_dev) {
+        int skip_below = (int)st->gates.size();
+        for (size_t i = 0; i < st->gates.size(); i++)
+            if (st->gates[i].ngen) { skip_below = (int)i; break; }
+        L3Enc E;
+        st->circ_l3 = st->opt_layout && encode_l3(st, end, skip_below, E) &&
+                      circuit_l3_smem(st->dbl, st->n_loc, E.nf + E.nb, E.rows, E.ngt, E.nacc) <= 220 * 1024;
+        if (st->circ_l3) {
+            // device: [ops][xtab][xreg][accp][gtab][Z terms]
+            auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+            st->l3_nf = E.nf;
+            st->l3_nb = E.nb;
+            st->l3_rows = E.rows;
+            st->l3_nacc = E.nacc;
+            st->l3_ngt = E.ngt;
+            st->l3_off_x = al(E.ops.size() * sizeof(L3Op));
+            st->l3_off_r = al(st->l3_off_x + E.xtab.size() * sizeof(uint32_t));
+            st->l3_off_a = al(st->l3_off_r + E.xreg.size() * sizeof(uint16_t));
+            st->l3_off_g = al(st->l3_off_a + E.accp.size() * sizeof(uint16_t));
+            st->circ_off_z = al(st->l3_off_g + E.gtab.size() * sizeof(double));
+            int rc = dev_alloc(st->circ_off_z + zts.size() * sizeof(ZTerms));
+            if (rc) return rc;
+            char *d = (char *)st->circ_dev;
+            CUDA_TRY(st, cudaMemcpyAsync(d, E.ops.data(), E.ops.size() * sizeof(L3Op), cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(st, cudaMemcpyAsync(d + st->l3_off_x, E.xtab.data(), E.xtab.size() * sizeof(uint32_t),
+                                         cudaMemcpyHostToDevice, c->stream));
+            CUDA_TRY(st, cudaMemcpyAsync(d + st->l3_off_r, E.xreg.data(), E.xreg.size() * sizeof(uint16_t),
+                                         cudaMemcpyHostToDevice, c->stream));
+            if (!E.accp.empty())
+                CUDA_TRY(st, cudaMemcpyAsync(d + st->l3_off_a, E.accp.data(), E.accp.size() * sizeof(uint16_t),
+                                             cudaMemcpyHostToDevice, c->stream));
+            if (!E.gtab.empty())
+                CUDA_TRY(st, cudaMemcpyAsync(d + st->l3_off_g, E.gtab.data(), E.gtab.size() * sizeof(double),
+                                             cudaMemcpyHostToDevice, c->stream));
+            st->met.h2d_bytes += E.ops.size() * sizeof(L3Op) + E.xtab.size() * 4 + E.xreg.size() * 2 +
+                                 E.accp.size() * 2 + E.gtab.size() * 8;
+            CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+            st->pos = E.pos;  // lambda-init sees the final qubit map
+            st->circ_key = key;
+            st->circ_pos = E.pos;
+        } else {
         std::vector<int> pending;
         for (size_t i = 0; i < end; i++) pending.push_back((int)i);
         PlanConfig cfg = plan_cfg(st);
@@ -1770,9 +2102,6 @@ static int adjoint_circuit(tqd_state *st, int T, const uint64_t *x, const uint64
         if (rc) return fail(rc, err);
         for (const Stage &s : stages)
             if (s.type != ST_SMALL) return 1;
-        int skip_below = (int)st->gates.size();
-        for (size_t i = 0; i < st->gates.size(); i++)
-            if (st->gates[i].ngen) { skip_below = (int)i; break; }
         std::vector<DevOp> fops, bops;
         std::vector<GateRec> tmp;
         for (int b = 0; b < st->batch; b++) {
@@ -1785,17 +2114,8 @@ static int adjoint_circuit(tqd_state *st, int T, const uint64_t *x, const uint64
         st->circ_nb = (int)bops.size() / st->batch;
         st->circ_off_b = ((fops.size() * sizeof(DevOp)) + 255) & ~(size_t)255;
         st->circ_off_z = (st->circ_off_b + bops.size() * sizeof(DevOp) + 255) & ~(size_t)255;
-        const size_t total = st->circ_off_z + zts.size() * sizeof(ZTerms);
-        if (total > st->circ_cap) {
-            if (st->circ_dev) { CUDA_TRY(st, cudaStreamSynchronize(c->stream)); cudaFree(st->circ_dev); }
-            st->circ_dev = nullptr;
-            st->circ_cap = 0;
-            if (cudaMalloc(&st->circ_dev, total) != cudaSuccess) {
-                cudaGetLastError();
-                return fail(TQD_ERR_OOM, "cannot allocate the circuit op lists");
-            }
-            st->circ_cap = total;
-        }
+        rc = dev_alloc(st->circ_off_z + zts.size() * sizeof(ZTerms));
+        if (rc) return rc;
         CUDA_TRY(st, cudaMemcpyAsync(st->circ_dev, fops.data(), fops.size() * sizeof(DevOp), cudaMemcpyHostToDevice, c->stream));
         CUDA_TRY(st, cudaMemcpyAsync((char *)st->circ_dev + st->circ_off_b, bops.data(), bops.size() * sizeof(DevOp),
                                      cudaMemcpyHostToDevice, c->stream));
@@ -1803,6 +2123,7 @@ static int adjoint_circuit(tqd_state *st, int T, const uint64_t *x, const uint64
         CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host vectors go out of scope
         st->circ_key = key;
         st->circ_pos = pos;
+        }
     } else {
         st->pos = st->circ_pos;
     }
@@ -1813,11 +2134,21 @@ static int adjoint_circuit(tqd_state *st, int T, const uint64_t *x, const uint64
     int rc = ensure_red(st, (size_t)n_grad + 1);
     if (rc) return rc;
     CUDA_TRY(st, cudaMemsetAsync(st->d_red, 0, (n_grad + 1) * sizeof(double), c->stream));
-    const DevOp *d_f = (const DevOp *)st->circ_dev;
-    const DevOp *d_b = (const DevOp *)((char *)st->circ_dev + st->circ_off_b);
     const int ev = ev_begin(st, CAT_BWD);
-    CUDA_TRY(st, launch_circuit(st->dbl, d_f, st->circ_nf, d_b, st->circ_nb, st->psi, d_z, st->d_red, st->d_red + 1,
-                                st->n_loc, rank_hi(st), st->batch, c->stream));
+    if (st->circ_l3) {
+        const char *d = (const char *)st->circ_dev;
+        CUDA_TRY(st, launch_circuit_l3(st->dbl, (const L3Op *)d, st->l3_nf, st->l3_nb, (const uint32_t *)(d + st->l3_off_x),
+                                       (const uint16_t *)(d + st->l3_off_r), st->l3_rows,
+                                       (const uint16_t *)(d + st->l3_off_a), st->l3_nacc,
+                                       (const double *)(d + st->l3_off_g), st->l3_ngt, st->psi, d_z, st->d_red,
+                                       st->d_red + 1, st->n_loc, st->batch, c->stream));
+        st->met.circuit_layout_launches++;
+    } else {
+        const DevOp *d_f = (const DevOp *)st->circ_dev;
+        const DevOp *d_b = (const DevOp *)((char *)st->circ_dev + st->circ_off_b);
+        CUDA_TRY(st, launch_circuit(st->dbl, d_f, st->circ_nf, d_b, st->circ_nb, st->psi, d_z, st->d_red, st->d_red + 1,
+                                    st->n_loc, rank_hi(st), st->batch, c->stream));
+    }
     ev_end(st, ev);
     st->met.kernel_launches++;
     st->met.fwd_sweeps++;

@@ -843,6 +843,269 @@ __global__ void __launch_bounds__(512) circuit_r1_kernel(const DevOp *__restrict
     }
 }
 
+// ---- single-launch layout circuit (tqd_internal.h L3Op; abi.cpp encode_l3) -----
+// One CTA per state of 8..10 local qubits, 2^(n_loc-3) threads, 8 amplitudes per
+// thread in registers (register slots 0..2 = bits 0..2 of r).  Forward op list,
+// lambda = H psi (Z-strings, PAPER.md:226-231 seed) and E, then the reverse list
+// with gradients 2 Re <lam|G|psi> on the post-gate states before each un-apply
+// (PAPER.md:220-236); per-thread gradient accumulators in shared memory, summed
+// once at the end.
+template <int V> struct L3C { static constexpr int value = V; };
+template <typename F> __device__ __forceinline__ void l3_dispatch(int j, F &&f) {
+    if (j == 0) f(L3C<0>{});
+    else if (j == 1) f(L3C<1>{});
+    else f(L3C<2>{});
+}
+
+template <int J, typename Real>
+__device__ __forceinline__ void l3_u1(typename CT<Real>::C *x, const L3Op &op, const Real *mr) {
+    typedef typename CT<Real>::C C;
+    const int ck = op.ck, ci = op.ci;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        if (r & (1 << J)) continue;
+        const int s = r | (1 << J);
+        const bool on = ck != 1 || ((r >> ci) & 1);
+        const C x0 = x[r], x1 = x[s];
+        C y0, y1;
+        if (op.form == L3F_SWAP) {
+            y0 = x1;
+            y1 = x0;
+        } else if (op.form == L3F_REAL) {
+            y0 = mk<C>(mr[0] * x0.x + mr[2] * x1.x, mr[0] * x0.y + mr[2] * x1.y);
+            y1 = mk<C>(mr[4] * x0.x + mr[6] * x1.x, mr[4] * x0.y + mr[6] * x1.y);
+        } else {
+            y0 = cmul2(mk<C>(mr[0], mr[1]), x0, mk<C>(mr[2], mr[3]), x1);
+            y1 = cmul2(mk<C>(mr[4], mr[5]), x0, mk<C>(mr[6], mr[7]), x1);
+        }
+        x[r] = on ? y0 : x0;
+        x[s] = on ? y1 : x1;
+    }
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(128) circuit_l3_kernel(const L3Op *__restrict__ ops_g, int n_f, int n_b,
+                                                         const uint32_t *__restrict__ xtab,
+                                                         const uint16_t *__restrict__ xreg_g, int n_rows,
+                                                         const uint16_t *__restrict__ accp, int n_acc,
+                                                         const double *__restrict__ gtab_g, int n_gt,
+                                                         const typename CT<Real>::C *__restrict__ psi,
+                                                         const ZTerms *__restrict__ zts, double *__restrict__ eval,
+                                                         double *__restrict__ grad, int n_loc) {
+    typedef typename CT<Real>::C C;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ double red[32];
+    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t N = 1u << n_loc;
+    const int nops = n_f + n_b;
+    ops_g += (size_t)blockIdx.x * nops;
+    accp += (size_t)blockIdx.x * n_acc;
+    gtab_g += (size_t)blockIdx.x * n_gt * 8;
+    psi += (size_t)blockIdx.x * N;
+    const ZTerms &zt = zts[blockIdx.x];
+    // shared memory: [2 buffers x (psi, lambda) x N][ops][xreg rows][generators][accumulators n_acc x T]
+    C *buf = reinterpret_cast<C *>(smem_raw);
+    L3Op *sops = reinterpret_cast<L3Op *>(buf + 4 * N);
+    uint16_t *sxr = reinterpret_cast<uint16_t *>(sops + nops);
+    double *sg = reinterpret_cast<double *>(sxr + 16 * n_rows);
+    Real *tacc = reinterpret_cast<Real *>(sg + 8 * n_gt);
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(ops_g);
+        int4 *dst = reinterpret_cast<int4 *>(sops);
+        for (int i = tid; i < nops * (int)(sizeof(L3Op) / 16); i += T) dst[i] = src[i];
+        const int4 *xs = reinterpret_cast<const int4 *>(xreg_g);
+        int4 *xd = reinterpret_cast<int4 *>(sxr);
+        for (int i = tid; i < n_rows * 2; i += T) xd[i] = xs[i];
+        for (int i = tid; i < n_gt * 8; i += T) sg[i] = gtab_g[i];
+        for (int i = tid; i < n_acc * T; i += T) tacc[i] = 0;
+    }
+    C a[8], l[8];
+    {
+        const uint32_t b0 = __ldg(xtab + tid) & 0xffffu;
+        const uint16_t *xr = xreg_g;  // row 0 (global: shared memory not ready yet)
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            a[r] = psi[b0 | xr[r]];
+            l[r] = mk<C>(0, 0);
+        }
+    }
+    uint32_t xrow = n_rows > 2 ? __ldg(xtab + 2 * T + tid) : 0u;  // the next exchange's row (prefetched)
+    __syncthreads();
+    int xb = 0;
+    auto tbit = [&](int i) -> int { return (tid >> i) & 1; };
+    auto exch = [&](const L3Op &op, bool two) {
+        const uint32_t row = xrow;
+        const int e = op.xi;
+        if (e + 1 < n_rows) xrow = __ldg(xtab + (size_t)(e + 1) * T + tid);
+        C *B = buf + (size_t)xb * 2 * N;
+        xb ^= 1;
+        const uint16_t *xr = sxr + 16 * e;
+        const uint32_t wb = row & 0xffffu, rb = row >> 16;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const uint32_t o = wb ^ xr[r];
+            B[o] = a[r];
+            if (two) B[N + o] = l[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const uint32_t o = rb ^ xr[8 + r];
+            a[r] = B[o];
+            if (two) l[r] = B[N + o];
+        }
+    };
+    auto run = [&](const L3Op &op, bool two) {
+        Real mr[8];
+        const int type = op.type;
+        if (type == L3_X) {
+            exch(op, two);
+            return;
+        }
+        if (type == L3_U1) {
+#pragma unroll
+            for (int i = 0; i < 8; i++) mr[i] = (Real)op.m[i];
+            const bool ton = op.ck != 2 || tbit(op.ci);
+            l3_dispatch(op.j, [&](auto JJ) {
+                constexpr int J = decltype(JJ)::value;
+                if (two) {
+                    for (int p = 0; p < op.ngen; p++) {
+                        Real part = 0;
+                        const int gk = op.gk[p];
+#pragma unroll
+                        for (int r = 0; r < 8; r++) {
+                            if (r & (1 << J)) continue;
+                            const int s = r | (1 << J);
+                            if (gk == GEN_Y) {
+                                part += re_cj(l[s], a[r]) - re_cj(l[r], a[s]);
+                            } else if (gk == GEN_X) {
+                                part += im_cj(l[r], a[s]) + im_cj(l[s], a[r]);
+                            } else {
+                                const double *g = sg + 8 * (op.gi + p);
+                                const C g00 = mk<C>((Real)g[0], (Real)g[1]), g01 = mk<C>((Real)g[2], (Real)g[3]);
+                                const C g10 = mk<C>((Real)g[4], (Real)g[5]), g11 = mk<C>((Real)g[6], (Real)g[7]);
+                                part += 2 * (re_cj(l[r], cmul2(g00, a[r], g01, a[s])) + re_cj(l[s], cmul2(g10, a[r], g11, a[s])));
+                            }
+                        }
+                        tacc[op.acc[p] * T + tid] += part;
+                    }
+                }
+                if (ton) {
+                    l3_u1<J, Real>(a, op, mr);
+                    if (two) l3_u1<J, Real>(l, op, mr);
+                }
+            });
+            return;
+        }
+        if (type == L3_D1) {
+            const C d0 = mk<C>((Real)op.m[0], (Real)op.m[1]), d1 = mk<C>((Real)op.m[2], (Real)op.m[3]);
+            if (op.d0k == 1) {
+                l3_dispatch(op.d0i, [&](auto JJ) {
+                    constexpr int J = decltype(JJ)::value;
+                    if (two && op.ngen) {  // GEN_Z on this bit
+                        Real part = 0;
+#pragma unroll
+                        for (int r = 0; r < 8; r++) {
+                            const Real v = im_cj(l[r], a[r]);
+                            part += ((r >> J) & 1) ? -v : v;
+                        }
+                        tacc[op.acc[0] * T + tid] += part;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 8; r++) {
+                        const C d = ((r >> J) & 1) ? d1 : d0;
+                        a[r] = cmul(d, a[r]);
+                        if (two) l[r] = cmul(d, l[r]);
+                    }
+                });
+            } else {
+                const int b = tbit(op.d0i);
+                if (two && op.ngen) {
+                    Real part = 0;
+#pragma unroll
+                    for (int r = 0; r < 8; r++) part += im_cj(l[r], a[r]);
+                    tacc[op.acc[0] * T + tid] += b ? -part : part;
+                }
+                const C d = b ? d1 : d0;
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    a[r] = cmul(d, a[r]);
+                    if (two) l[r] = cmul(d, l[r]);
+                }
+            }
+            return;
+        }
+        if (type == L3_D2) {
+            C d[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) d[i] = mk<C>((Real)op.m[2 * i], (Real)op.m[2 * i + 1]);
+            const int t0 = op.d0k == 2 ? tbit(op.d0i) : 0, t1 = op.d1k == 2 ? tbit(op.d1i) : 0;
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+                const int v0 = op.d0k == 1 ? ((r >> op.d0i) & 1) : t0;
+                const int v1 = op.d1k == 1 ? ((r >> op.d1i) & 1) : t1;
+                const int v = 2 * v0 + v1;
+                const C dv = v == 0 ? d[0] : v == 1 ? d[1] : v == 2 ? d[2] : d[3];
+                a[r] = cmul(dv, a[r]);
+                if (two) l[r] = cmul(dv, l[r]);
+            }
+        }
+    };
+    for (int oi = 0; oi < n_f; oi++) run(sops[oi], false);
+    {
+        // lambda = H psi, E = <psi|H|psi> at the forward's final layout (row 1)
+        const uint32_t b1 = __ldg(xtab + T + tid) & 0xffffu;
+        const uint16_t *xr = sxr + 16;
+        double e = 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const uint32_t b = b1 | xr[r];
+            double h = zt.cst;
+            for (int p = 0; p < n_loc; p++)
+                if ((b >> p) & 1u) h -= 2.0 * zt.w[p];
+            for (int t = 0; t < zt.T; t++) h += (__popcll((uint64_t)b & zt.z[t]) & 1) ? -zt.c[t] : zt.c[t];
+            l[r] = mk<C>((Real)h * a[r].x, (Real)h * a[r].y);
+            e += h * ((double)a[r].x * a[r].x + (double)a[r].y * a[r].y);
+        }
+        e = block_sum<double>(e, red);
+        if (tid == 0) atomicAdd(eval, e);
+    }
+    for (int oi = n_f; oi < nops; oi++) run(sops[oi], true);
+    __syncthreads();
+    const int nw = T >> 5;
+    for (int k = warp; k < n_acc; k += nw) {
+        double v = 0.0;
+        for (int t = lane; t < T; t += 32) v += (double)tacc[k * T + t];
+        v = warp_sum<double>(v);
+        if (lane == 0 && v != 0.0) atomicAdd(&grad[accp[k]], v);
+    }
+}
+
+size_t circuit_l3_smem(bool dbl, int n_loc, int nops, int n_rows, int n_gt, int n_acc) {
+    const size_t esz = dbl ? 16 : 8;
+    return (size_t)4 * ((size_t)1 << n_loc) * esz + (size_t)nops * sizeof(L3Op) + (size_t)32 * n_rows +
+           (size_t)64 * n_gt + (size_t)n_acc * ((size_t)1 << (n_loc - 3)) * (dbl ? 8 : 4);
+}
+
+cudaError_t launch_circuit_l3(bool dbl, const L3Op *ops, int n_f, int n_b, const uint32_t *xtab, const uint16_t *xreg,
+                              int n_rows, const uint16_t *accp, int n_acc, const double *gtab, int n_gt, const void *psi,
+                              const ZTerms *zts, double *eval, double *grad, int n_loc, int batch, cudaStream_t s) {
+    const size_t smem = circuit_l3_smem(dbl, n_loc, n_f + n_b, n_rows, n_gt, n_acc);
+    const int threads = 1 << (n_loc - 3);
+#define TQD_L3(T)                                                                                               \
+    {                                                                                                           \
+        cudaError_t e = cudaFuncSetAttribute(circuit_l3_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                             (int)smem);                                                        \
+        if (e != cudaSuccess) return e;                                                                         \
+        circuit_l3_kernel<T><<<batch, threads, smem, s>>>(ops, n_f, n_b, xtab, xreg, n_rows, accp, n_acc, gtab, \
+                                                          n_gt, (const CT<T>::C *)psi, zts, eval, grad, n_loc);  \
+        return cudaGetLastError();                                                                              \
+    }
+    if (dbl) TQD_L3(double)
+    TQD_L3(float)
+#undef TQD_L3
+}
+
 cudaError_t launch_circuit(bool dbl, const DevOp *fops, int n_f, const DevOp *bops, int n_b, const void *psi,
                            const ZTerms *zts, double *eval, double *grad, int n_loc, uint64_t rank_hi, int batch,
                            cudaStream_t s) {

@@ -233,6 +233,31 @@ struct ScatterInfo {
 // Z-string observable in PHYSICAL masks (full index incl. rank bits)
 // lambda-init form: h(b) = cst - 2 sum_p w[p] bit_p(b) + sum_t c_t (-1)^{popc(b & z_t)}
 // (single-qubit Z terms folded into per-position weights, the rest listed)
+// ---- single-launch layout circuit (circuit_l3_kernel, 8..10 local qubits) --------
+// The whole state in registers: 8 amplitudes per thread (3 register bits, then 5
+// lane bits and n_loc - 8 warp bits = the thread index bits).  A LAYOUT assigns a
+// physical bit to every slot (0..2 register, 3.. thread bit slot-3).  Gates run on
+// register slots (diagonal gates and controls on any slot); an exchange (L3_X)
+// moves to a new layout through XOR-swizzled shared memory: amplitude with physical
+// index x is stored at S(x) = (x & ~low) | F(x), F linear with F|low invertible,
+// chosen per exchange so that both layouts' lane bits hit distinct banks
+// (abi.cpp encode_l3).  Exchange row e: per thread xtab[e][tid] = S(thread part of
+// the old layout) | S(thread part of the new layout) << 16, uniform
+// xreg[e][0..7] = S(register part r, old), [8..15] = S(register part r, new);
+// rows 0 / 1: the plain (unswizzled) initial / seed layouts.
+enum L3Type : uint8_t { L3_U1 = 1, L3_D1 = 2, L3_D2 = 3, L3_X = 4 };
+enum L3Form : uint8_t { L3F_GEN = 0, L3F_REAL = 1, L3F_SWAP = 2 };
+struct alignas(16) L3Op {
+    uint8_t type, j, ck, ci;      // U1: target register slot; control kind (0 none, 1 register slot, 2 thread bit), index
+    uint8_t d0k, d0i, d1k, d1i;   // D1 / D2 bits: kind (1 register slot, 2 thread bit), index (d0 = MSB of the D2 index)
+    uint8_t ngen, form;           // adjoint generators; U1 form (L3Form)
+    uint16_t xi;                  // X: exchange row
+    uint8_t gk[3], pad0;          // GenKind per generator
+    uint16_t acc[3], gi;          // per generator: accumulator; GEN_FULL: gtab row of generator p = gi + p
+    uint32_t pad1[2];
+    double m[8];                  // U1: 2x2 complex row-major (re, im); D1: d0, d1; D2: d00, d01, d10, d11
+};
+
 struct ZTerms {
     int T;
     uint64_t z[64];

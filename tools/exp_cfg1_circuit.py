@@ -16,9 +16,10 @@ torch.cuda.set_device(0)
 ctx = tqd.Context.from_torch()
 wl = W.config(1)
 K = 200
-for cmax in (10, 0):
+for cmax, layout in ((10, 1), (10, 0), (0, 0)):
     st = tqd.State(ctx, wl.n, wl.dtype)
     st.set_option(tqd.OPT_CIRCUIT_MAX, cmax)
+    st.set_option(tqd.OPT_CIRCUIT_LAYOUT, layout)
     st.apply_circuit(wl.gates)
     v, g = st.adjoint_grad(wl.terms)
     for _ in range(10):
@@ -42,7 +43,8 @@ for cmax in (10, 0):
         v, g = st.adjoint_grad(wl.terms)
     m = st.metrics()
     kern_us = (m["fwd_sweep_ms"] + m["bwd_sweep_ms"] + m["other_ms"]) / K * 1e3
-    print(json.dumps({"case": "cfg1", "circuit_max": cmax, "path": "single launch" if cmax else "staged sweeps",
+    print(json.dumps({"case": "cfg1", "circuit_max": cmax, "path": ("single launch, register layout" if layout else "single launch, gate by gate") if cmax
+                      else "staged sweeps", "layout_launches": m["circuit_layout_launches"] / K,
                       "launches_per_call": m["kernel_launches"] / K, "device_us_per_call": round(kern_us, 2),
                       "sweep_us": round((m["fwd_sweep_ms"] + m["bwd_sweep_ms"]) / K * 1e3, 2),
                       "call_ms": round(call_ms, 4), "E": v, "grad0": float(g[0])}), flush=True)
