@@ -12,7 +12,7 @@ python bench.py --config 2 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/
 python tools/bench_brief.py gpurun_out/bench_cfg2_$TAG.log | head -3
 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg4_$TAG.log 2>&1; echo "cfg4 rc=$?"
 python tools/bench_brief.py gpurun_out/bench_cfg4_$TAG.log | head -3
-python tools/bench_configs.py --cases cfg1,cfg2,cfg5_8 > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err; echo "configs rc=$?"
+python tools/bench_configs.py --cases cfg1,cfg2,cfg5_8,cfg5_8_sweep > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err; echo "configs rc=$?"
 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_short_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
