@@ -135,7 +135,7 @@ typedef enum {
                                * gates, a register-layout kernel (8 amplitudes per thread, 4
                                * warps, layout exchanges through swizzled shared memory;
                                * metric circuit_layout_launches).  Same results; measured
-                               * slower (latency-bound at 4 warps, DESIGN.md section 8). */
+                               * slower (latency-bound at 4 warps, DESIGN.md section 6). */
 } tqd_option;
 
 /* Execution metrics, cumulative since tqd_state_init / tqd_state_reset.
