@@ -110,6 +110,22 @@ double orc_normal(uint64_t seed, uint64_t i);
 int  orc_gauss_sample(const double *psi, int n, double shots, uint64_t seed, double *out_y);
 int  orc_gauss_z(const double *psi, int n, double shots, uint64_t seed, double *out_z);
 
+/* ---- Clifford circuits at full size (clifford.c; stabilizer tableau) --------
+ * Gates I X Y Z H S SDG CNOT CZ SWAP and RX / RY / RZ / U3 at multiples of pi/2;
+ * anything else returns -1 (mats are not read).  n <= 63.
+ * orc_clifford_expval: out[t] = c_t <P_t> (each <P_t> in {-1, 0, +1}), c NULL = 1.
+ * orc_clifford_grad:   value = sum_t c_t <P_t>; grad by parameter shift (+-pi/2),
+ *                      slot order as orc_param_shift.                        */
+int  orc_clifford_expval(int n, int G, const int *kinds, const int *wires, const double *params,
+                         int T, const uint64_t *x_mask, const uint64_t *z_mask, const double *coeff,
+                         double *out);
+int  orc_clifford_grad(int n, int G, const int *kinds, const int *wires, const double *params,
+                       const int *trainable, int T, const uint64_t *x_mask, const uint64_t *z_mask,
+                       const double *coeff, double *value, double *grad);
+/* the n stabilizer generators of the final state: sign[k] P_k |psi> = |psi> */
+int  orc_clifford_stabilizers(int n, int G, const int *kinds, const int *wires, const double *params,
+                              uint64_t *x_out, uint64_t *z_out, int *sign_out);
+
 #ifdef __cplusplus
 }
 #endif
