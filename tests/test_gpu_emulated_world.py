@@ -386,3 +386,35 @@ def test_world_product_prefix_qft(tqd, orc, world, n, dtype):
         assert np.max(np.abs(amp - ref)) < TOL[dtype]["amp"]
         assert abs(val - rval) < TOL[dtype]["val"]
         assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]
+
+
+@pytest.mark.parametrize("fused", [1, 0])
+@pytest.mark.parametrize("world,n_loc", [(2, 21), (4, 21), (8, 20)])
+def test_world_clifford_large(tqd, orc, world, n_loc, fused):
+    """Sharded HEA at Clifford angles with local shards large enough that every CTA
+    walks many tiles (2^20-2^21 amplitudes per rank, 23-24 qubits in all), remaps fused
+    and staged, against the stabilizer-tableau oracle: every expectation and gradient."""
+    from test_gpu_clifford_fullsize import quarter_hea, sensitive_terms
+    g = world.bit_length() - 1
+    n = n_loc + g
+    gates = quarter_hea(n, 6, world + n_loc)
+    terms = sensitive_terms(n, gates, 10, world)
+    rev = orc.clifford_expval(n, gates, terms)
+    rval, rgrad = orc.clifford_grad(n, gates, terms)
+    assert np.count_nonzero(rgrad) >= 6
+
+    def fn(r, ctx):
+        st = tqd.State(ctx, n, "c64")
+        st.set_option(tqd.OPT_FUSED_REMAP, fused)
+        st.apply_circuit(gates)
+        ev = st.expval(terms)
+        st.rewind()
+        val, grad = st.adjoint_grad(terms)
+        m = st.metrics()
+        st.free()
+        return ev, val, grad, m
+    for ev, val, grad, m in run_world(tqd, world, fn):
+        assert m["remaps"] > 0
+        assert np.max(np.abs(ev - rev)) < TOL["c64"]["val"]
+        assert abs(val - rval) < TOL["c64"]["val"]
+        assert np.max(np.abs(grad - rgrad)) < TOL["c64"]["val"]
