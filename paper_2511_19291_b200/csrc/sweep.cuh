@@ -581,6 +581,18 @@ __device__ __forceinline__ void run_kop(const uint4 h, const KOp<Real> &op, type
     }
 }
 
+// asynchronous global -> shared 16-byte copies (the next tile's staging, TQD_SWEEP_STAGE:
+// an experiment, off: measured slower, profiles/r02_experiments.md)
+#ifndef TQD_SWEEP_STAGE
+#define TQD_SWEEP_STAGE 0
+#endif
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // evict-first global accesses of the streamed shards (cache-streaming hints)
 __device__ __forceinline__ float2 ldcs_c(const float2 *p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ldcs_c(const double2 *p) { return __ldcs(p); }
@@ -768,11 +780,64 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
     const uint64_t tmask = deposit(~0ull) & (S.n_tiles > 1 ? ~0ull : 0ull);
     const uint64_t step = deposit((uint64_t)gsz);
     uint64_t base = deposit((uint64_t)gid);
+#if TQD_SWEEP_STAGE
+    // Staged tile loads: the next tile's psi (and lambda) are copied into the exchange
+    // buffers by cp.async while this tile's last segment computes and stores (the
+    // buffers are idle after the last exchange); the tile starts with shared-memory
+    // reads instead of exposed global-load latency.  Staging layout: tile-local index
+    // order (16-byte chunk ch = tile bits [cb, k) of its first amplitude); the thread
+    // index covers the low chunk bits (consecutive threads: consecutive 16 bytes of a
+    // 128-byte run), passes j the high ones.
+    constexpr int cb = sizeof(C) == 8 ? 1 : 0;  // tile bits inside one 16-byte chunk
+    const bool stage_ok = cb == 0 || S.ld_phys[0] == 0;
+    const int lgT = __ffs((int)blockDim.x) - 1;
+    const int tb = min(k - cb, lgT), jb = k - cb - tb;
+    const bool st_act = (threadIdx.x >> tb) == 0u;
+    uint64_t stg_thr = 0;
+    for (int i = 0; i < tb; i++)
+        if ((threadIdx.x >> i) & 1u) stg_thr |= 1ull << S.ld_phys[cb + i];
+    auto stage_issue = [&](uint64_t nb) {
+        if (st_act) {
+            for (int j = 0; j < (1 << jb); j++) {
+                uint64_t off = nb | stg_thr;
+                for (int i = 0; i < jb; i++)
+                    if ((j >> i) & 1) off |= 1ull << S.ld_phys[cb + tb + i];
+                const uint32_t ch = threadIdx.x | ((uint32_t)j << tb);
+                cp_async16(reinterpret_cast<char *>(sm_a) + (size_t)ch * 16, psi + off);
+                if (BWD) cp_async16(reinterpret_cast<char *>(sm_l) + (size_t)ch * 16, lam + off);
+            }
+        }
+        cp_async_commit();
+    };
+    if (stage_ok && gid < S.n_tiles) stage_issue(base);
+#endif
     for (int64_t tile = gid; tile < S.n_tiles; tile += gsz, base = ((base | ~tmask) + step) & tmask) {
         const uint64_t basefull = base | rank_hi;
+        const bool has_next = tile + gsz < S.n_tiles;
+        const uint64_t next_base = ((base | ~tmask) + step) & tmask;
 
         C a[NR];
         C l[BWD ? NR : 1];
+#if TQD_SWEEP_STAGE
+        if (stage_ok) {
+            cp_async_wait_all();
+            __syncthreads();
+            // layout 0 from the staged tile (tile-local index order)
+            uint32_t o[NR], c[SWEEP_R];
+#pragma unroll
+            for (int i = 0; i < SWEEP_R; i++) c[i] = (1u << S.lay[0].reg[i]) * (uint32_t)sizeof(C);
+            o[0] = s_tix[threadIdx.x] * (uint32_t)sizeof(C);
+#pragma unroll
+            for (int r = 1; r < NR; r++) o[r] = o[r & (r - 1)] ^ c[ctz4(r)];
+#pragma unroll
+            for (int r = 0; r < NR; r++) {
+                a[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_a) + o[r]);
+                if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_l) + o[r]);
+            }
+            __syncthreads();  // every warp holds its amplitudes: the buffers are free
+            if (nseg == 1 && has_next) stage_issue(next_base);
+        } else
+#endif
         {
             // Gray-code walk over the register offsets: one 64-bit add per address
             const uint64_t b0 = base | ld_thr;
@@ -814,8 +879,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
             }
             __syncthreads();
         }
-        if (tile + gsz < S.n_tiles) {
-            const uint64_t nb = ((base | ~tmask) + step) & tmask;
+        if (has_next) {
+            const uint64_t nb = next_base;
             for (int i = 0; i < n_pf; i++) {
                 const uint64_t e = nb + s_pf[i * blockDim.x + threadIdx.x];
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(psi + e));
@@ -872,7 +937,30 @@ __global__ void __launch_bounds__(SWEEP_THREADS, sizeof(Real) == 4 ? (BWD ? TQD_
                         a[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_a) + o[r]);
                         if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_l) + o[r]);
                     }
+#ifdef TQD_EXP_DOUBLE_EXCH
+                    // timing experiment (variant builds only): a second, identity exchange
+                    // (same addresses, CTA barriers) to measure the marginal exchange cost
+                    __syncthreads();
+#pragma unroll
+                    for (int r = 0; r < NR; r++) {
+                        *reinterpret_cast<C *>(reinterpret_cast<char *>(sm_a) + o[r]) = a[r];
+                        if (BWD) *reinterpret_cast<C *>(reinterpret_cast<char *>(sm_l) + o[r]) = l[r];
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int r = 0; r < NR; r++) {
+                        a[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_a) + o[r]);
+                        if (BWD) l[r] = *reinterpret_cast<const C *>(reinterpret_cast<const char *>(sm_l) + o[r]);
+                    }
+#endif
                 }
+#if TQD_SWEEP_STAGE
+                if (stage_ok && s == nseg - 1) {
+                    // last exchange: every warp has read it; stage the next tile
+                    __syncthreads();
+                    if (has_next) stage_issue(next_base);
+                } else
+#endif
                 if (S.xsync[x] & 0x80) __syncwarp();  // the next writes stay in this warp's region
                 else __syncthreads();
             }
