@@ -255,7 +255,8 @@ __device__ __forceinline__ double2 pmul(double2 x, double2 y) { return make_doub
 //   2 Re <lam|G|psi> = sum_pairs Re(conj l1 a0) - Re(conj l0 a1)
 // two packed accumulators (independent FFMA2 chains), one final add
 #ifndef TQD_GRAD_CHAINS
-#define TQD_GRAD_CHAINS 2  // independent FFMA2 accumulator chains per RY gradient (4 measured 0.4 % slower)
+#define TQD_GRAD_CHAINS 1  // FFMA2 accumulator chains per RY gradient (1: fewer live registers; 1 / 2 / 4 measured
+                           // 10.53 / 10.66 / 10.70 ms per adjoint sweep at 30 q)
 #endif
 template <int T, typename C, typename Real>
 __device__ __forceinline__ Real grad_y(const C *a, const C *l) {
