@@ -820,3 +820,32 @@ def test_product_prefix_two_qubit_rules(tqd, ctx, orc, seed, dtype):
         assert abs(val - rval) < TOL[dtype]["val"] and np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"], pf
         out[pf] = grad
     assert np.max(np.abs(out[1] - out[0])) < TOL[dtype]["val"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_product_prefix_whole_circuit(tqd, ctx, orc, dtype):
+    """Edge case: EVERY gate is in the product prefix (no sweep at all): 1-qubit gates,
+    SWAPs and the QFT of a basis state; the adjoint seed lambda = H psi is contracted
+    directly.  Against the oracle; the tail absorption may take the trailing gates."""
+    n = 13
+    rng = np.random.default_rng(5)
+    gates = [W.Gate("X", (q,)) for q in range(n) if rng.random() < 0.5] + W.qft(n)
+    gates += [W.Gate("RY", (q,), (float(rng.uniform(0, 6.3)),)) for q in range(n)]
+    gates += [W.Gate("SWAP", (0, n - 1)), W.Gate("RX", (3,), (0.7,)), W.Gate("U3", (5,), (0.3, 1.1, -0.4))]
+    terms = W.random_pauli_terms(n, 5, 2) + W.sum_z(n)
+    rval, rgrad = orc.adjoint(n, gates, terms)
+    ref = orc.run(n, gates)
+    st = make_state(tqd, ctx, n, dtype, small_max=0)
+    st.apply_circuit(gates)
+    amps = st.amplitudes()
+    m = st.metrics()
+    st.reset()
+    st.apply_circuit(gates)
+    val, grad = st.adjoint_grad(terms)
+    m2 = st.metrics()
+    st.free()
+    assert m["gates_prefix"] == len(gates) and m["fwd_sweeps"] == 0, m
+    assert m2["bwd_sweeps"] == 0
+    assert np.max(np.abs(amps - ref)) < TOL[dtype]["amp"]
+    assert abs(val - rval) < TOL[dtype]["val"] and np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"]
