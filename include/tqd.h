@@ -116,15 +116,17 @@ typedef enum {
                                * halves; remap blocks and X/Y partner shards move through it
                                * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
                                * force a few KiB so the chunk loop iterates.               */
-    TQD_OPT_PRODUCT_PREFIX = 9, /* 1 (default): every qubit's leading 1-qubit gates (before its
-                               * first entangling gate) act on |0>; fixed 2-qubit gates that
-                               * keep the product (SWAP; diagonal or controlled gates with one
+    TQD_OPT_PRODUCT_PREFIX = 9, /* 2 (default): auto = 1 from 22 local qubits, else 0;
+                               * 1: every qubit's leading 1-qubit gates (before its first
+                               * entangling gate) act on |0>; fixed 2-qubit gates that keep
+                               * the product (SWAP; diagonal or controlled gates with one
                                * qubit in a parameter-independent basis state) join them.  A
-                               * single state (batch 1, >= 11 local qubits, any world size)
-                               * starts from that product state (one write pass instead of
-                               * their sweeps) and the adjoint finishes their gradients from
+                               * state (>= 11 local qubits, any batch and world size) starts
+                               * from that product state (one write pass instead of their
+                               * sweeps) and the adjoint finishes their gradients from
                                * lambda's environments at the prefix boundary (one read pass);
-                               * same values and gradients.  0: sweep every gate.          */
+                               * same values and gradients.  0: sweep every gate.
+                               * Other values: TQD_ERR_ARG.                                  */
     TQD_OPT_CIRCUIT_MAX = 8,   /* single-GPU states of <= this many qubits (0..12; default 10)
                                * run tqd_adjoint_grad with Z-string terms as ONE kernel launch:
                                * forward gates, lambda = H psi and the reverse sweep in one

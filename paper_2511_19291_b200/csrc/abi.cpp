@@ -126,12 +126,13 @@ struct tqd_state {
     int l3_nf = 0, l3_nb = 0, l3_rows = 0, l3_nacc = 0, l3_ngt = 0;
     size_t l3_off_x = 0, l3_off_r = 0, l3_off_a = 0, l3_off_g = 0;
     // product-state prefix of the current execution (prefix_build)
-    int opt_prefix = 1;            // TQD_OPT_PRODUCT_PREFIX
+    int opt_prefix = 2;            // TQD_OPT_PRODUCT_PREFIX: 0 off, 1 on, 2 auto (on from 22 local qubits)
     int opt_layout = 0;            // TQD_OPT_CIRCUIT_LAYOUT (experiment, measured slower)
     bool pf_on = false;
     std::vector<char> pf_in;       // per gate: in the prefix
-    std::vector<cd> pf_s;          // per qubit: s_q (2 entries) at the prefix boundary
-    std::vector<PfOp> pf_ops;      // the prefix as 1-qubit ops on product factors, in gate order
+    std::vector<std::vector<cd>> pf_s;    // per batch element, per qubit: s_q (2 entries) at the boundary
+    std::vector<std::vector<PfOp>> pf_ops; // per batch element: the prefix as 1-qubit ops on product
+                                           // factors, in gate order (same structure for every element)
     std::vector<int> pf_slot_of;   // per qubit: its product factor at the boundary
     int pf_ng = 0;
     void *pf_dev = nullptr;        // group tables (device, state dtype) + M environments (fp64)
@@ -477,6 +478,12 @@ static const std::vector<GateRec> &gates_for(tqd_state *st, int b, std::vector<G
     for (size_t i = 0; i < tmp.size() && i < st->brec.size(); i++)
         if (!st->brec[i].empty()) tmp[i] = st->brec[i][b];
     return tmp;
+}
+
+// gate i as seen by batch element b (no copy of the tape)
+static const GateRec &gate_of(const tqd_state *st, size_t i, int b) {
+    if (b > 0 && i < st->brec.size() && !st->brec[i].empty()) return st->brec[i][b];
+    return st->gates[i];
 }
 
 // Encoded launch list: descriptors of a stage list, uploaded once to the device.
@@ -826,10 +833,14 @@ static uint64_t tape_values_hash(const tqd_state *st) {
 constexpr int PF_BITS_H = 10;
 static bool prefix_build(tqd_state *st, size_t end) {
     st->pf_on = false;
-    if (!st->opt_prefix || st->batch != 1 || st->executed != 0 || st->n_loc < 11 || st->n_loc > 40) return false;
+    if (!st->opt_prefix || st->executed != 0 || st->n_loc < 11 || st->n_loc > 40) return false;
+    // auto: below ~4 M amplitudes per state the host work of the tables and of the
+    // environments' contraction costs more than the sweeps it saves (tools/bench_batch.py:
+    // batch 16 at 20 q 9.2 -> 10.7 ms per step with it, at 24 q 161 -> 143 ms)
+    if (st->opt_prefix == 2 && st->n_loc < 22) return false;
     const int n = st->n;
     st->pf_in.assign(st->gates.size(), 0);
-    st->pf_ops.clear();
+    std::vector<PfOp> ops0;  // element 0 (the structure; batched gates' values per element below)
     // product factors ("slots"): slot f starts as qubit f in |0>; a SWAP of two
     // untouched qubits exchanges their slots
     std::vector<cd> sv(2 * n, cd(0.0));
@@ -849,7 +860,7 @@ static bool prefix_build(tqd_state *st, size_t end) {
         o.gate = (int)i;
         o.slot = f;
         for (int j = 0; j < 4; j++) o.M[j] = M[j];
-        st->pf_ops.push_back(o);
+        ops0.push_back(o);
         const cd a = sv[2 * f], b = sv[2 * f + 1];
         sv[2 * f] = M[0] * a + M[1] * b;
         sv[2 * f + 1] = M[2] * a + M[3] * b;
@@ -858,13 +869,14 @@ static bool prefix_build(tqd_state *st, size_t end) {
     bool any = false;
     for (size_t i = 0; i < end; i++) {
         const GateRec &g = st->gates[i];
-        bool free_ = !g.batched;
+        bool free_ = !(g.batched && g.nw != 1);
         for (int j = 0; j < g.nw; j++) free_ = free_ && !touched[g.w[j]];
         bool take = false;
         if (free_ && g.nw == 1) {
+            // (a batched gate: per-element values, element 0's here; never a basis control)
             const int f = slot_of[g.w[0]];
             apply(i, f, g.M);
-            if (g.ngen) fixed[f] = 0;
+            if (g.ngen || g.batched) fixed[f] = 0;
             take = true;
         } else if (free_ && g.nw == 2) {
             // a fixed 2-qubit gate keeps the product when it is a relabeling or one of
@@ -899,25 +911,40 @@ static bool prefix_build(tqd_state *st, size_t end) {
             for (int j = 0; j < g.nw; j++) touched[g.w[j]] = 1;
         }
     }
-    // per qubit: its slot's factor
-    st->pf_s.assign(2 * n, cd(0.0));
+    // per batch element: its ops (1-qubit gates with the element's values; the 2-qubit
+    // rules only ever read parameter-independent, hence common, factors) and factors
     st->pf_slot_of = slot_of;
-    for (int q = 0; q < n; q++) {
-        st->pf_s[2 * q] = sv[2 * slot_of[q]];
-        st->pf_s[2 * q + 1] = sv[2 * slot_of[q] + 1];
+    st->pf_ops.assign(st->batch, ops0);
+    st->pf_s.assign(st->batch, std::vector<cd>(2 * n, cd(0.0)));
+    for (int b = 0; b < st->batch; b++) {
+        std::vector<cd> fv(2 * n, cd(0.0));
+        for (int f = 0; f < n; f++) fv[2 * f] = cd(1.0);
+        for (PfOp &o : st->pf_ops[b]) {
+            const GateRec &gr = gate_of(st, o.gate, b);
+            if (gr.nw == 1)
+                for (int j = 0; j < 4; j++) o.M[j] = gr.M[j];
+            const cd a = fv[2 * o.slot], c1 = fv[2 * o.slot + 1];
+            fv[2 * o.slot] = o.M[0] * a + o.M[1] * c1;
+            fv[2 * o.slot + 1] = o.M[2] * a + o.M[3] * c1;
+        }
+        for (int q = 0; q < n; q++) {
+            st->pf_s[b][2 * q] = fv[2 * slot_of[q]];
+            st->pf_s[b][2 * q + 1] = fv[2 * slot_of[q] + 1];
+        }
     }
+    (void)sv;
     st->pf_on = any;
     return any;
 }
 
 // the global (sharded) qubits' factor of rank r: prod over the rank bits of s_q(bit)
 // (physical position n_loc + i = qubit n-1-n_loc-i at the start), skipping qubit `skip`
-static cd prefix_rank_factor(const tqd_state *st, int r, int skip) {
+static cd prefix_rank_factor(const tqd_state *st, const std::vector<cd> &S, int r, int skip) {
     cd v(1.0);
     for (int i = 0; i < st->g; i++) {
         const int q = st->n - 1 - (st->n_loc + i);
         if (q == skip) continue;
-        v *= st->pf_s[2 * q + ((r >> i) & 1)];
+        v *= S[2 * q + ((r >> i) & 1)];
     }
     return v;
 }
@@ -925,32 +952,45 @@ static cd prefix_rank_factor(const tqd_state *st, int r, int skip) {
 // the group tables tab_g[i] = prod over the group's physical bits of s_q(bit), q the
 // qubit at that bit (pi = identity at the start: physical bit p = qubit n-1-p)
 static int prefix_init(tqd_state *st) {
-    const int nl = st->n_loc, n = st->n;
+    const int nl = st->n_loc, n = st->n, B = st->batch;
     const int ng = (nl + PF_BITS_H - 1) / PF_BITS_H;
     st->pf_ng = ng;
     const size_t tab_elems = (size_t)ng << PF_BITS_H;
+    // device: [B element tables (state dtype)][B M environments (fp64)]
     const size_t tab_bytes = tab_elems * st->esz, m_bytes = tab_elems * 2 * sizeof(double);
-    if (tab_bytes + m_bytes > st->pf_cap) {
+    const size_t need = (size_t)B * (tab_bytes + m_bytes);
+    if (need > st->pf_cap) {
         if (st->pf_dev) { CUDA_TRY(st, cudaStreamSynchronize(st->ctx->stream)); cudaFree(st->pf_dev); }
         st->pf_dev = nullptr;
         st->pf_cap = 0;
-        if (cudaMalloc(&st->pf_dev, tab_bytes + m_bytes) != cudaSuccess) {
+        if (cudaMalloc(&st->pf_dev, need) != cudaSuccess) {
             cudaGetLastError();
             return fail(TQD_ERR_OOM, "cannot allocate the product-prefix tables");
         }
-        st->pf_cap = tab_bytes + m_bytes;
+        st->pf_cap = need;
     }
-    std::vector<double> h(tab_elems * 2, 0.0);
-    for (int g = 0; g < ng; g++) {
-        const int bits = std::min(PF_BITS_H, nl - PF_BITS_H * g);
-        for (int i = 0; i < (1 << bits); i++) {
-            cd v(1.0);
+    tqd_ctx *c = st->ctx;
+    std::vector<double> h((size_t)B * tab_elems * 2, 0.0);
+    for (int b = 0; b < B; b++) {
+        const std::vector<cd> &S = st->pf_s[b];
+        double *hb = h.data() + (size_t)b * tab_elems * 2;
+        for (int g = 0; g < ng; g++) {
+            // tab[i] = prod_j s_{q_j}(bit j of i), built bit by bit (tab[i | 2^j] = tab[i] s(1) / ... )
+            const int bits = std::min(PF_BITS_H, nl - PF_BITS_H * g);
+            std::vector<cd> t(1, cd(1.0));
             for (int j = 0; j < bits; j++) {
                 const int q = n - 1 - (PF_BITS_H * g + j);
-                v *= st->pf_s[2 * q + ((i >> j) & 1)];
+                const size_t half = t.size();
+                t.resize(2 * half);
+                for (size_t i = 0; i < half; i++) {
+                    t[half + i] = t[i] * S[2 * q + 1];
+                    t[i] = t[i] * S[2 * q];
+                }
             }
-            h[2 * (((size_t)g << PF_BITS_H) + i)] = v.real();
-            h[2 * (((size_t)g << PF_BITS_H) + i) + 1] = v.imag();
+            for (size_t i = 0; i < t.size(); i++) {
+                hb[2 * (((size_t)g << PF_BITS_H) + i)] = t[i].real();
+                hb[2 * (((size_t)g << PF_BITS_H) + i) + 1] = t[i].imag();
+            }
         }
     }
     std::vector<float> hf;
@@ -959,19 +999,22 @@ static int prefix_init(tqd_state *st) {
         hf.assign(h.begin(), h.end());
         src = hf.data();
     }
-    tqd_ctx *c = st->ctx;
-    CUDA_TRY(st, cudaMemcpyAsync(st->pf_dev, src, tab_bytes, cudaMemcpyHostToDevice, c->stream));
-    st->met.h2d_bytes += tab_bytes;
-    const cd cr = prefix_rank_factor(st, c->rank, -1);
+    CUDA_TRY(st, cudaMemcpyAsync(st->pf_dev, src, (size_t)B * tab_bytes, cudaMemcpyHostToDevice, c->stream));
+    st->met.h2d_bytes += (size_t)B * tab_bytes;
     const int ev = ev_begin(st, CAT_OTHER);
-    CUDA_TRY(st, launch_prefix_init(st->dbl, st->psi, 1ull << nl, ng, st->pf_dev, cr.real(), cr.imag(), c->stream));
+    for (int b = 0; b < B; b++) {
+        const cd cr = prefix_rank_factor(st, st->pf_s[b], c->rank, -1);
+        CUDA_TRY(st, launch_prefix_init(st->dbl, (char *)st->psi + (size_t)b * shard_bytes(st), 1ull << nl, ng,
+                                        (const char *)st->pf_dev + (size_t)b * tab_bytes, cr.real(), cr.imag(),
+                                        c->stream));
+        st->met.kernel_launches++;
+    }
     ev_end(st, ev);
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));  // host tables go out of scope
-    st->met.kernel_launches++;
-    st->met.hbm_bytes += shard_bytes(st);
+    st->met.hbm_bytes += (uint64_t)B * shard_bytes(st);
     for (char in : st->pf_in) {
-        st->met.gates_applied += in ? 1 : 0;
-        st->met.gates_prefix += in ? 1 : 0;
+        st->met.gates_applied += in ? (uint64_t)B : 0;
+        st->met.gates_prefix += in ? (uint64_t)B : 0;
     }
     return TQD_OK;
 }
@@ -981,104 +1024,126 @@ static int allreduce_sum(tqd_state *st, double *d, size_t count);
 
 static int prefix_grads(tqd_state *st, std::vector<double> &grad) {
     tqd_ctx *c = st->ctx;
-    const int nl = st->n_loc, n = st->n, ng = st->pf_ng;
+    const int nl = st->n_loc, n = st->n, ng = st->pf_ng, B = st->batch;
     const size_t tab_elems = (size_t)ng << PF_BITS_H;
-    double *dM = (double *)((char *)st->pf_dev + tab_elems * st->esz);
-    CUDA_TRY(st, cudaMemsetAsync(dM, 0, tab_elems * 2 * sizeof(double), c->stream));
-    const int ev = ev_begin(st, CAT_OTHER);
-    CUDA_TRY(st, launch_prefix_contract(st->dbl, st->lam, 1ull << nl, ng, st->pf_dev, dM, c->sms, c->stream));
-    ev_end(st, ev);
-    std::vector<double> M(tab_elems * 2);
-    CUDA_TRY(st, cudaMemcpyAsync(M.data(), dM, M.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    const size_t tab_bytes = tab_elems * st->esz;
+    // every element's environments M_g in one pass each, one readback
+    double *dM = (double *)((char *)st->pf_dev + (size_t)B * tab_bytes);
+    CUDA_TRY(st, cudaMemsetAsync(dM, 0, (size_t)B * tab_elems * 2 * sizeof(double), c->stream));
+    {
+        const int ev = ev_begin(st, CAT_OTHER);
+        for (int be = 0; be < B; be++) {
+            CUDA_TRY(st, launch_prefix_contract(st->dbl, (const char *)st->lam + (size_t)be * shard_bytes(st),
+                                                1ull << nl, ng, (const char *)st->pf_dev + (size_t)be * tab_bytes,
+                                                dM + (size_t)be * tab_elems * 2, c->sms, c->stream));
+            st->met.kernel_launches++;
+        }
+        ev_end(st, ev);
+    }
+    std::vector<double> Mall((size_t)B * tab_elems * 2);
+    CUDA_TRY(st, cudaMemcpyAsync(Mall.data(), dM, Mall.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(st, cudaStreamSynchronize(c->stream));
-    st->met.kernel_launches++;
-    st->met.hbm_bytes += shard_bytes(st);
-    st->met.d2h_bytes += M.size() * sizeof(double);
-    // world > 1: this rank's total contraction Z_r (M_0 . tab_0), then M scaled by the
-    // rank factor c_r and summed over the ranks together with every rank's Z_r
-    std::vector<cd> Zr(c->world, cd(0.0));
-    if (c->world > 1) {
-        std::vector<cd> t0(1 << PF_BITS_H, cd(0.0));
-        {
-            const int bits = std::min(PF_BITS_H, nl);
-            for (int i = 0; i < (1 << bits); i++) {
-                cd v(1.0);
-                for (int j = 0; j < bits; j++) v *= st->pf_s[2 * (n - 1 - j) + ((i >> j) & 1)];
-                t0[i] = v;
-            }
-        }
-        cd z(0.0);
-        for (int i = 0; i < (1 << PF_BITS_H); i++) z += cd(M[2 * i], M[2 * i + 1]) * t0[i];
-        const cd cr = prefix_rank_factor(st, c->rank, -1);
-        for (size_t i = 0; i < tab_elems; i++) {
-            const cd v = cd(M[2 * i], M[2 * i + 1]) * cr;
-            M[2 * i] = v.real();
-            M[2 * i + 1] = v.imag();
-        }
-        std::vector<double> buf(M);
-        buf.resize(M.size() + 2 * c->world, 0.0);
-        buf[M.size() + 2 * c->rank] = z.real();
-        buf[M.size() + 2 * c->rank + 1] = z.imag();
-        const size_t bytes = buf.size() * sizeof(double);
-        int rc = ensure_red(st, buf.size());  // (the gradients are already on the host)
-        if (rc) return rc;
-        dM = st->d_red;
-        CUDA_TRY(st, cudaMemcpyAsync(dM, buf.data(), bytes, cudaMemcpyHostToDevice, c->stream));
-        rc = allreduce_sum(st, dM, buf.size());
-        if (rc) return rc;
-        CUDA_TRY(st, cudaMemcpyAsync(buf.data(), dM, bytes, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_TRY(st, cudaStreamSynchronize(c->stream));
-        for (size_t i = 0; i < M.size(); i++) M[i] = buf[i];
-        for (int r = 0; r < c->world; r++) Zr[r] = cd(buf[M.size() + 2 * r], buf[M.size() + 2 * r + 1]);
-    }
-    // T_q(v) = sum_{i: bit j of i = v} M_g[i] prod_{j' != j in group g} s_{q'}(bit j')
-    std::vector<cd> T(2 * n, cd(0.0));
-    for (int g = 0; g < ng; g++) {
-        const int bits = std::min(PF_BITS_H, nl - PF_BITS_H * g);
-        for (int j = 0; j < bits; j++) {
-            const int q = n - 1 - (PF_BITS_H * g + j);
-            for (int i = 0; i < (1 << bits); i++) {
-                cd e(1.0);
-                for (int jj = 0; jj < bits; jj++) {
-                    if (jj == j) continue;
-                    e *= st->pf_s[2 * (n - 1 - (PF_BITS_H * g + jj)) + ((i >> jj) & 1)];
-                }
-                const cd m(M[2 * (((size_t)g << PF_BITS_H) + i)], M[2 * (((size_t)g << PF_BITS_H) + i) + 1]);
-                T[2 * q + ((i >> j) & 1)] += m * e;
-            }
-        }
-    }
-    // sharded qubits: T_q(v) = sum over the ranks whose bit of q is v of Z_r times the
-    // other sharded qubits' factors
-    for (int i = 0; i < st->g && c->world > 1; i++) {
-        const int q = n - 1 - (nl + i);
-        for (int r = 0; r < c->world; r++) T[2 * q + ((r >> i) & 1)] += Zr[r] * prefix_rank_factor(st, r, q);
-    }
-    // d s_f / d theta for every generator of every prefix gate: replay the gate's
-    // slot chain from |0> with dU = G U inserted at that gate; T of the qubit holding
-    // the slot at the boundary
+    st->met.hbm_bytes += (uint64_t)B * shard_bytes(st);
+    st->met.d2h_bytes += Mall.size() * sizeof(double);
     std::vector<int> q_of_slot(n);
     for (int q = 0; q < n; q++) q_of_slot[st->pf_slot_of[q]] = q;
-    for (size_t oi = 0; oi < st->pf_ops.size(); oi++) {
-        const PfOp &oi_ = st->pf_ops[oi];
-        const GateRec &gi = st->gates[oi_.gate];
-        if (!gi.ngen) continue;
-        const int f = oi_.slot, q = q_of_slot[f];
-        for (int p = 0; p < gi.ngen; p++) {
-            cd a(1.0), b(0.0);
-            for (size_t k = 0; k < st->pf_ops.size(); k++) {
-                const PfOp &o = st->pf_ops[k];
-                if (o.slot != f) continue;
-                cd na = o.M[0] * a + o.M[1] * b, nb = o.M[2] * a + o.M[3] * b;
-                if (k == oi) {
-                    const cd ga = gi.G[p][0] * na + gi.G[p][1] * nb, gb = gi.G[p][2] * na + gi.G[p][3] * nb;
-                    na = ga;
-                    nb = gb;
+    for (int be = 0; be < B; be++) {
+        const std::vector<cd> &S = st->pf_s[be];
+        const std::vector<PfOp> &ops = st->pf_ops[be];
+        std::vector<double> M(Mall.begin() + (size_t)be * tab_elems * 2, Mall.begin() + (size_t)(be + 1) * tab_elems * 2);
+        // world > 1: this rank's total contraction Z_r (M_0 . tab_0), then M scaled by the
+        // rank factor c_r and summed over the ranks together with every rank's Z_r
+        std::vector<cd> Zr(c->world, cd(0.0));
+        if (c->world > 1) {
+            std::vector<cd> t0(1 << PF_BITS_H, cd(0.0));
+            {
+                const int bits = std::min(PF_BITS_H, nl);
+                for (int i = 0; i < (1 << bits); i++) {
+                    cd v(1.0);
+                    for (int j = 0; j < bits; j++) v *= S[2 * (n - 1 - j) + ((i >> j) & 1)];
+                    t0[i] = v;
                 }
-                a = na;
-                b = nb;
             }
-            grad[gi.slot0 + p] += 2.0 * (T[2 * q] * a + T[2 * q + 1] * b).real();
+            cd z(0.0);
+            for (int i = 0; i < (1 << PF_BITS_H); i++) z += cd(M[2 * i], M[2 * i + 1]) * t0[i];
+            const cd cr = prefix_rank_factor(st, S, c->rank, -1);
+            for (size_t i = 0; i < tab_elems; i++) {
+                const cd v = cd(M[2 * i], M[2 * i + 1]) * cr;
+                M[2 * i] = v.real();
+                M[2 * i + 1] = v.imag();
+            }
+            std::vector<double> buf(M);
+            buf.resize(M.size() + 2 * c->world, 0.0);
+            buf[M.size() + 2 * c->rank] = z.real();
+            buf[M.size() + 2 * c->rank + 1] = z.imag();
+            const size_t bytes = buf.size() * sizeof(double);
+            int rc = ensure_red(st, buf.size());  // (the gradients are already on the host)
+            if (rc) return rc;
+            double *dr = st->d_red;
+            CUDA_TRY(st, cudaMemcpyAsync(dr, buf.data(), bytes, cudaMemcpyHostToDevice, c->stream));
+            rc = allreduce_sum(st, dr, buf.size());
+            if (rc) return rc;
+            CUDA_TRY(st, cudaMemcpyAsync(buf.data(), dr, bytes, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(st, cudaStreamSynchronize(c->stream));
+            for (size_t i = 0; i < M.size(); i++) M[i] = buf[i];
+            for (int r = 0; r < c->world; r++) Zr[r] = cd(buf[M.size() + 2 * r], buf[M.size() + 2 * r + 1]);
+        }
+        // T_q(v) = sum_{i: bit j of i = v} M_g[i] prod_{j' != j in group g} s_{q'}(bit j'):
+        // contract M_g with every factor of the group but j (top bits by halving, then
+        // the bits below j by pairing), O(bits 2^bits) per group
+        std::vector<cd> T(2 * n, cd(0.0));
+        for (int g = 0; g < ng; g++) {
+            const int bits = std::min(PF_BITS_H, nl - PF_BITS_H * g);
+            auto sf = [&](int jj, int v) { return S[2 * (n - 1 - (PF_BITS_H * g + jj)) + v]; };
+            for (int j = 0; j < bits; j++) {
+                std::vector<cd> W(1u << bits);
+                for (size_t i = 0; i < W.size(); i++)
+                    W[i] = cd(M[2 * (((size_t)g << PF_BITS_H) + i)], M[2 * (((size_t)g << PF_BITS_H) + i) + 1]);
+                for (int jj = bits - 1; jj > j; jj--) {  // top bit jj: W'[i] = W[i] s(0) + W[i + half] s(1)
+                    const size_t half = W.size() / 2;
+                    for (size_t i = 0; i < half; i++) W[i] = W[i] * sf(jj, 0) + W[i + half] * sf(jj, 1);
+                    W.resize(half);
+                }
+                for (int jj = 0; jj < j; jj++) {  // lowest remaining bit: W'[i] = W[2i] s(0) + W[2i+1] s(1)
+                    const size_t half = W.size() / 2;
+                    for (size_t i = 0; i < half; i++) W[i] = W[2 * i] * sf(jj, 0) + W[2 * i + 1] * sf(jj, 1);
+                    W.resize(half);
+                }
+                const int q = n - 1 - (PF_BITS_H * g + j);
+                T[2 * q] += W[0];
+                T[2 * q + 1] += W[1];
+            }
+        }
+        // sharded qubits: T_q(v) = sum over the ranks whose bit of q is v of Z_r times the
+        // other sharded qubits' factors
+        for (int i = 0; i < st->g && c->world > 1; i++) {
+            const int q = n - 1 - (nl + i);
+            for (int r = 0; r < c->world; r++) T[2 * q + ((r >> i) & 1)] += Zr[r] * prefix_rank_factor(st, S, r, q);
+        }
+        // d s_f / d theta for every generator of every prefix gate: replay the gate's
+        // slot chain from |0> with dU = G U inserted at that gate; T of the qubit holding
+        // the slot at the boundary; the element's own gradient slots (batched gates)
+        for (size_t oi = 0; oi < ops.size(); oi++) {
+            const PfOp &oi_ = ops[oi];
+            const GateRec &gi = gate_of(st, oi_.gate, be);
+            if (!gi.ngen) continue;
+            const int f = oi_.slot, q = q_of_slot[f];
+            for (int p = 0; p < gi.ngen; p++) {
+                cd a(1.0), bb(0.0);
+                for (size_t k = 0; k < ops.size(); k++) {
+                    const PfOp &o = ops[k];
+                    if (o.slot != f) continue;
+                    cd na = o.M[0] * a + o.M[1] * bb, nb = o.M[2] * a + o.M[3] * bb;
+                    if (k == oi) {
+                        const cd ga = gi.G[p][0] * na + gi.G[p][1] * nb, gb2 = gi.G[p][2] * na + gi.G[p][3] * nb;
+                        na = ga;
+                        nb = gb2;
+                    }
+                    a = na;
+                    bb = nb;
+                }
+                grad[gi.slot0 + p] += 2.0 * (T[2 * q] * a + T[2 * q + 1] * bb).real();
+            }
         }
     }
     return TQD_OK;
@@ -1420,7 +1485,10 @@ int tqd_state_set_option(tqd_state *st, int option, int64_t v) {
     case TQD_OPT_USE_GRAPH: st->opt_graph = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_FUSED_REMAP: st->opt_fused = v ? 1 : 0; return TQD_OK;
     case TQD_OPT_ABSORB_TAIL: st->opt_absorb = v ? 1 : 0; return TQD_OK;
-    case TQD_OPT_PRODUCT_PREFIX: st->opt_prefix = v ? 1 : 0; return TQD_OK;
+    case TQD_OPT_PRODUCT_PREFIX:
+        if (v < 0 || v > 2) return fail(TQD_ERR_ARG, "TQD_OPT_PRODUCT_PREFIX: 0, 1 or 2");
+        st->opt_prefix = (int)v;
+        return TQD_OK;
     case TQD_OPT_CIRCUIT_LAYOUT:
         if (st->opt_layout != (v ? 1 : 0)) st->circ_key = 0;  // re-encode the cached circuit
         st->opt_layout = v ? 1 : 0;

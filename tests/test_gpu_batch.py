@@ -261,3 +261,38 @@ def test_batch_diagonal_runs_with_zero_inputs(tqd, ctx, orc, dtype):
         enc = [W.Gate("RZ", (q,), (float(x[q, b, 0]),), None, True) for q in range(n)]
         psi = orc.run(n, pre + enc + post)
         assert np.max(np.abs(amp[b << n:(b + 1) << n] - psi)) < TOL[dtype]["amp"], b
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("kind", ["RY", "U3"])
+def test_batch_product_prefix(tqd, ctx, orc, dtype, kind):
+    """A batch of states with per-state encoder inputs: the encoder (batched gates,
+    per-element values and gradient slots), the fixed gates after it and the first
+    ansatz layer form each element's product prefix.  Against the per-element oracle,
+    prefix on == off, and the prefix gate count (B x per-element prefix)."""
+    n, B = 12, 3
+    x = encoder_inputs(B, n, 77, kind)
+    ansatz = [W.Gate("H", (0,)), W.Gate("S", (1,))] + W.hea(n, 3, seed=5, small=True)
+    terms = W.random_z_terms(n, 3, 4) + W.sum_z(n) + [(1, 2, 0.3)]
+    coeff = np.random.default_rng(9).standard_normal((B, len(terms)))
+    rval, rgrad = expected(orc, n, x, ansatz, terms, coeff, kind)
+    out = {}
+    for pf in (1, 0):
+        st = make(tqd, ctx, n, dtype, B, small_max=0)
+        st.set_option(tqd.OPT_PRODUCT_PREFIX, pf)
+        record_batch(st, x, ansatz, kind)
+        amp = st.amplitudes()
+        m = st.metrics()
+        st.reset()
+        record_batch(st, x, ansatz, kind)
+        val, grad = st.adjoint_grad(terms, coeff=coeff)
+        st.free()
+        # encoder (n) + H + S + the first RY / RZ layer (2n), per element
+        assert m["gates_prefix"] == (B * (n + 2 + 2 * n) if pf else 0), m["gates_prefix"]
+        for b in range(B):
+            psi = orc.run(n, per_element_gates(x, b, ansatz, kind))
+            assert np.max(np.abs(amp[b << n:(b + 1) << n] - psi)) < TOL[dtype]["amp"], (pf, b)
+        assert abs(val - rval) < TOL[dtype]["val"], pf
+        assert np.max(np.abs(grad - rgrad)) < TOL[dtype]["val"], pf
+        out[pf] = grad
+    assert np.max(np.abs(out[1] - out[0])) < TOL[dtype]["val"]

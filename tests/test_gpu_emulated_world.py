@@ -373,6 +373,7 @@ def test_world_product_prefix_qft(tqd, orc, world, n, dtype):
         st = tqd.State(ctx, n, dtype)
         st.set_option(tqd.OPT_TILE_QUBITS, 9)
         st.set_option(tqd.OPT_SMALL_MAX, 0)
+        st.set_option(tqd.OPT_PRODUCT_PREFIX, 1)
         st.apply_circuit(wl.gates)
         amp = st.amplitudes()
         npre = st.metrics()["gates_prefix"]

@@ -837,6 +837,7 @@ def test_product_prefix_whole_circuit(tqd, ctx, orc, dtype):
     rval, rgrad = orc.adjoint(n, gates, terms)
     ref = orc.run(n, gates)
     st = make_state(tqd, ctx, n, dtype, small_max=0)
+    st.set_option(tqd.OPT_PRODUCT_PREFIX, 1)
     st.apply_circuit(gates)
     amps = st.amplitudes()
     m = st.metrics()

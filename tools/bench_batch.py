@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--layers", type=int, default=10)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--prefix", type=int, default=1, help="TQD_OPT_PRODUCT_PREFIX (1: encoder as the product state)")
     a = ap.parse_args()
     import torch
     n, B = a.qubits, a.batch
@@ -51,6 +52,8 @@ def main():
     # (new inputs in a real Adam loop) -> the plan is reused, values re-encoded
     stb = tqd.State(ctx, n, "c64", batch=B)
     sts = [tqd.State(ctx, n, "c64") for _ in range(B)]
+    for s_ in [stb] + sts:
+        s_.set_option(tqd.OPT_PRODUCT_PREFIX, a.prefix)
 
     def run_batched():
         stb.reset()
