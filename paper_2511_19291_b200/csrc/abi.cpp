@@ -128,6 +128,8 @@ struct tqd_state {
     // product-state prefix of the current execution (prefix_build)
     int opt_prefix = 2;            // TQD_OPT_PRODUCT_PREFIX: 0 off, 1 on, 2 auto (on from 22 local qubits)
     int opt_layout = 0;            // TQD_OPT_CIRCUIT_LAYOUT (experiment, measured slower)
+    uint64_t pf_dec_sig = 0;       // auto prefix: circuit structure of the cached decision
+    bool pf_dec = false;           // auto prefix: keep it (cheaper plan)
     bool pf_on = false;
     std::vector<char> pf_in;       // per gate: in the prefix
     std::vector<std::vector<cd>> pf_s;    // per batch element, per qubit: s_q (2 entries) at the boundary
@@ -1162,7 +1164,28 @@ static int execute_pending(tqd_state *st, size_t end = SIZE_MAX, bool keep_tail 
         return TQD_OK;
     }
     uint64_t tmix = (uint64_t)(st->gates.size() - end) * 0x9E3779B97F4A7C15ull;
-    if (prefix_build(st, end)) {
+    if (prefix_build(st, end) && st->opt_prefix == 2) {
+        // auto: keep the prefix only if the plan without its gates is cheaper by more
+        // than the extra read pass of the environments (~0.17 of a sweep pair); the
+        // decision is cached per circuit structure
+        const uint64_t dsig = plan_signature(st->gates, plan_cfg(st)) ^ tmix;
+        if (st->pf_dec_sig != dsig) {
+            std::vector<int> pa, pb;
+            for (size_t i = 0; i < end; i++) {
+                pb.push_back((int)i);
+                if (!st->pf_in[i]) pa.push_back((int)i);
+            }
+            std::vector<int> posa = st->pos, posb = st->pos;
+            std::vector<Stage> sa, sb;
+            std::string e2;
+            const bool ok = plan_circuit(st->gates, pa, posa, plan_cfg(st), sa, e2) == TQD_OK &&
+                            plan_circuit(st->gates, pb, posb, plan_cfg(st), sb, e2) == TQD_OK;
+            st->pf_dec = ok && plan_cost(sa) + 0.17 < plan_cost(sb);
+            st->pf_dec_sig = dsig;
+        }
+        if (!st->pf_dec) st->pf_on = false;
+    }
+    if (st->pf_on) {
         // the prefix replaces |0..0> + its gates' sweeps; it is part of the plan's structure
         for (size_t i = 0; i < st->pf_in.size(); i++)
             if (st->pf_in[i]) tmix = (tmix ^ (i + 1)) * 1099511628211ull;

@@ -579,10 +579,11 @@ static bool plan_sweep(const std::vector<GateRec> &gates, std::vector<int> &pend
     // fewer than seg_min_gates gates is cheaper as part of the next stage.  Its items
     // are last in dependency order, so handing them back keeps the rest closed.
     {
-        static const int seg_min_gates = [] {  // measured: 6 -> 1029 vs 1058 ms per cfg-3 step
+        static const int seg_min_default = [] {  // measured: 6 -> 1029 vs 1058 ms per cfg-3 step
             const char *e = getenv("TQD_PLAN_SEG_MIN_GATES");
             return e ? atoi(e) : 6;
         }();
+        const int seg_min_gates = cfg.seg_min_gates >= 0 ? cfg.seg_min_gates : seg_min_default;
         static const int seg_keep = [] {  // segments always kept (experiment knob)
             const char *e = getenv("TQD_PLAN_SEG_KEEP");
             return e ? std::max(1, atoi(e)) : 3;
@@ -986,8 +987,8 @@ void refresh_plan_values(std::vector<Stage> &stages, const std::vector<GateRec> 
     }
 }
 
-int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,
-                 const PlanConfig &cfg, std::vector<Stage> &out, std::string &err) {
+static int plan_circuit_once(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,
+                             const PlanConfig &cfg, std::vector<Stage> &out, std::string &err) {
     int guard = 0;
     while (!pending.empty()) {
         if (++guard > 1000000) { err = "planner did not converge"; return TQD_ERR_STATE; }
@@ -1011,6 +1012,51 @@ int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, st
         if (rs.rm.m == 0) { err = "planner made no progress"; return TQD_ERR_STATE; }
         out.push_back(std::move(rs));
     }
+    return TQD_OK;
+}
+
+// The trailing-segment trim of plan_sweep (fewer layout exchanges) helps layered
+// circuits (HEA: 65 sweeps / 149 exchanges vs 65 / 157 untrimmed) but can cascade on
+// sequential chains (the paper's CNOT + RY ladder at 24 q: 66 sweeps vs 23).  Plan
+// both ways and keep the cheaper one: cost in sweep pairs = sweeps + 0.24 exchanges
+// (an exchange pair measured at ~0.24 of a 30-q sweep pair) + 2 per
+// remap.
+double plan_cost(const std::vector<Stage> &v) {
+    double c = 0.0;
+    for (const Stage &s : v) {
+        if (s.type == ST_SWEEP) c += 1.0 + 0.24 * (double)(s.sw.lays.size() - 1);
+        else if (s.type == ST_REMAP) c += 2.0;
+        else c += 1.0;
+    }
+    return c;
+}
+
+int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,
+                 const PlanConfig &cfg, std::vector<Stage> &out, std::string &err) {
+    if (cfg.seg_min_gates >= 0 || cfg.n_loc <= cfg.small_max)
+        return plan_circuit_once(gates, pending, pos, cfg, out, err);
+    auto cost = [](const std::vector<Stage> &v) { return plan_cost(v); };
+    static const int seg_min_default = [] {  // (TQD_PLAN_SEG_MIN_GATES: experiment knob)
+        const char *e = getenv("TQD_PLAN_SEG_MIN_GATES");
+        return e ? std::max(0, atoi(e)) : 6;
+    }();
+    PlanConfig ca = cfg, cb = cfg;
+    ca.seg_min_gates = seg_min_default;
+    cb.seg_min_gates = 0;
+    std::vector<int> pa = pos, pb = pos;
+    std::vector<Stage> sa, sb;
+    int rc = plan_circuit_once(gates, pending, pa, ca, sa, err);
+    if (rc) return rc;
+    if (ca.seg_min_gates == 0) {
+        pos = pa;
+        for (auto &s : sa) out.push_back(std::move(s));
+        return TQD_OK;
+    }
+    rc = plan_circuit_once(gates, pending, pb, cb, sb, err);
+    if (rc) return rc;
+    const bool use_b = cost(sb) < cost(sa);
+    pos = use_b ? pb : pa;
+    for (auto &s : (use_b ? sb : sa)) out.push_back(std::move(s));
     return TQD_OK;
 }
 

@@ -130,6 +130,7 @@ struct PlanConfig {
     int c_low = 4;     // physical bits 0..c_low-1 pinned in every tile (2^c_low-amplitude runs)
     int max_ops = MAX_STAGE_OPS;      // per sweep stage (shared-memory budget of the kernel)
     int max_slots = MAX_STAGE_SLOTS;  // gradient slots per sweep stage
+    int seg_min_gates = -1;  // trailing-segment trim (plan_sweep); -1: plan_circuit tries the default and 0
 };
 
 // Plan the gates `pending` (indices into gates, in recording order) starting
@@ -138,6 +139,9 @@ uint64_t plan_signature(const std::vector<GateRec> &gates, const PlanConfig &cfg
 void refresh_plan_values(std::vector<Stage> &stages, const std::vector<GateRec> &gates);
 int plan_circuit(const std::vector<GateRec> &gates, std::vector<int> pending, std::vector<int> &pos,
                  const PlanConfig &cfg, std::vector<Stage> &out, std::string &err);
+// estimated cost of a stage list in 30-q sweep pairs (sweeps + 0.24 per layout
+// exchange + 2 per remap)
+double plan_cost(const std::vector<Stage> &stages);
 
 // Encode a sweep stage into device descriptors (forward or backward order).
 template <typename Real>

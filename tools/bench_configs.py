@@ -43,7 +43,7 @@ def peak_gbs():
 GRAPH = 0
 
 
-def run_case(ctx, name, wl, steps, warmup, tile=0, note="", prefix=1):
+def run_case(ctx, name, wl, steps, warmup, tile=0, note="", prefix=2):
     stream = torch.cuda.current_stream()
     n, gates, terms = wl.n, wl.gates, wl.terms
     st = tqd.State(ctx, n, wl.dtype)
