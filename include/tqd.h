@@ -116,7 +116,8 @@ typedef enum {
                                * halves; remap blocks and X/Y partner shards move through it
                                * in chunks).  0 (default) = min(1 GiB, 2 x shard).  Tests
                                * force a few KiB so the chunk loop iterates.               */
-    TQD_OPT_PRODUCT_PREFIX = 9, /* 2 (default): auto = 1 from 22 local qubits, else 0;
+    TQD_OPT_PRODUCT_PREFIX = 9, /* 2 (default): auto = 1 from 22 local qubits when the plan of
+                               * the remaining gates is cheaper (planner cost model), else 0;
                                * 1: every qubit's leading 1-qubit gates (before its first
                                * entangling gate) act on |0>; fixed 2-qubit gates that keep
                                * the product (SWAP; diagonal or controlled gates with one

@@ -14,6 +14,7 @@ torch.cuda.set_device(0)
 ctx = tqd.Context.from_torch()
 st = tqd.State(ctx, n, "c64")
 st.set_option(tqd.OPT_PROFILE, 1)
+st.set_option(tqd.OPT_PRODUCT_PREFIX, 0)  # sweep the QFT (its basis-state input would make it a product prefix)
 st.apply_circuit(W.basis_prep(n, 12345 % (1 << n)) + W.qft(n))
 print(st.expval(W.sum_z(n))[:2], st.metrics()["fwd_sweeps"], st.metrics()["fwd_sweep_ms"])
 st.free()
