@@ -63,7 +63,13 @@ def case(rng):
             gates += W.qft(n)[: int(rng.integers(5, 40))]
     gates += W.random_circuit(n, int(rng.integers(20, 120)), seed, small=small) + W.hea(n, int(rng.integers(1, 4)), seed, small=small)
     terms = W.random_z_terms(n, 3, seed) + (W.random_pauli_terms(n, 3, seed) if rng.random() < 0.5 else []) + W.sum_z(n)
-    return dict(world=world, n=n, dtype=dtype, prefix=prefix, k=k, fused=fused, grid=grid), gates, terms
+    batch = int(rng.choice([1, 1, 2, 3]))
+    enc = None
+    if batch > 1:  # per-element encoder inputs (batched RY / U3 / RZ, trainable or frozen)
+        kind = str(rng.choice(["RY", "U3", "RZ"]))
+        npar = 3 if kind == "U3" else 1
+        enc = (kind, rng.uniform(0, np.pi, size=(n, batch, npar)), bool(rng.integers(0, 2)))
+    return dict(world=world, n=n, dtype=dtype, prefix=prefix, k=k, fused=fused, grid=grid, batch=batch), gates, terms, enc
 
 
 def main():
@@ -71,22 +77,45 @@ def main():
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
     t0, ncase, nfail = time.time(), 0, 0
     while time.time() - t0 < secs:
-        cfg, gates, terms = case(rng)
-        ref = orc.run(cfg["n"], gates)
-        rval, rgrad = orc.adjoint(cfg["n"], gates, terms)
+        cfg, gates, terms, enc = case(rng)
+        B, n = cfg["batch"], cfg["n"]
+        coeff = None
+        if enc is None:
+            refs = [orc.run(n, gates)]
+            rval, rgrad = orc.adjoint(n, gates, terms)
+        else:
+            # per-element circuits: encoder gates first; batched slots per element, shared summed
+            kind, x, trn = enc
+            coeff = rng.standard_normal((B, len(terms)))
+            refs, rval, encg, shared = [], 0.0, [], None
+            for b in range(B):
+                eg = [W.Gate(kind, (q,), tuple(float(v) for v in x[q, b]), None, trn) for q in range(n)]
+                refs.append(orc.run(n, eg + gates))
+                v, g = orc.adjoint(n, eg + gates, [(t[0], t[1], float(coeff[b, i])) for i, t in enumerate(terms)])
+                rval += v
+                ne = n * x.shape[2] if trn else 0
+                if trn:
+                    encg.append(g[:ne].reshape(n, x.shape[2]))
+                shared = g[ne:] if shared is None else shared + g[ne:]
+            rgrad = np.concatenate([np.stack(encg, 1).reshape(-1) if trn else np.zeros(0), shared])
 
         def fn(r, ctx):
-            st = tqd.State(ctx, cfg["n"], cfg["dtype"])
+            st = tqd.State(ctx, n, cfg["dtype"], batch=B) if B > 1 else tqd.State(ctx, n, cfg["dtype"])
             st.set_option(tqd.OPT_PRODUCT_PREFIX, cfg["prefix"])
             st.set_option(tqd.OPT_TILE_QUBITS, cfg["k"])
             st.set_option(tqd.OPT_SMALL_MAX, 0)
             st.set_option(tqd.OPT_FUSED_REMAP, cfg["fused"])
             st.set_option(tqd.OPT_GRID_CTAS, cfg["grid"])
-            st.apply_circuit(gates)
+            def record():
+                if enc is not None:
+                    for q in range(n):
+                        st.apply_batch(enc[0], [q], enc[1][q], trainable=enc[2])
+                st.apply_circuit(gates)
+            record()
             amp = st.amplitudes()
             st.reset()
-            st.apply_circuit(gates)
-            val, grad = st.adjoint_grad(terms)
+            record()
+            val, grad = st.adjoint_grad(terms, coeff=coeff) if coeff is not None else st.adjoint_grad(terms)
             st.free()
             return amp, val, grad
         try:
@@ -99,6 +128,7 @@ def main():
             else:
                 outs = run_world(cfg["world"], fn)
             ta, tv = TOL[cfg["dtype"]]
+            ref = np.concatenate(refs)
             for amp, val, grad in outs:
                 ea = float(np.max(np.abs(amp - ref)))
                 eg = float(np.max(np.abs(grad - rgrad))) if len(grad) else 0.0
