@@ -1,8 +1,8 @@
 """Randomised parity sweep on the GPU (a robustness check, not a test): random circuits of
 every gate kind, random observables and random options (product prefix 0/1/2, tile
 qubits, grid, small-state threshold, batch, loopback world size, fused remaps) against
-the float64 oracle.  python tools/fuzz_parity.py [seconds] [seed]; prints one line per
-failure and a summary."""
+the float64 oracle.  python tools/fuzz_parity.py [seconds] [seed] (FUZZ_N=lo,hi: local-qubit range);
+prints one line per failure and a summary."""
 import os
 import sys
 import threading
@@ -19,6 +19,7 @@ import paper_2511_19291_b200 as tqd  # noqa: E402
 import workloads as W  # noqa: E402
 
 TOL = {"c64": (1e-5, 1e-4), "c128": (1e-12, 1e-10)}
+NMIN, NMAX = (int(v) for v in os.environ.get("FUZZ_N", "11,17").split(","))  # local qubits [NMIN, NMAX)
 
 
 def run_world(world, fn):
@@ -48,7 +49,7 @@ def run_world(world, fn):
 def case(rng):
     world = int(rng.choice([1, 1, 2, 4]))
     g = world.bit_length() - 1
-    n = int(rng.integers(11 + g, 17 + g))
+    n = int(rng.integers(NMIN + g, NMAX + g))
     dtype = str(rng.choice(["c64", "c128"]))
     prefix = int(rng.choice([0, 1, 2]))
     k = int(rng.choice([9, 10, 11, 12])) if dtype == "c64" else int(rng.choice([9, 10, 11]))
